@@ -109,7 +109,7 @@ class _Lib:
 
     def _check(self, rc: int) -> None:
         if rc != 0:
-            raise SpecdecError(rc, self.lib[self.prefix + "last_error"]().decode())
+            raise SpecdecError(rc, getattr(self.lib, self.prefix + "last_error")().decode())
 
 
 class Oracle(_Lib):
@@ -149,6 +149,8 @@ class Oracle(_Lib):
         L.so_retrieval_predict.argtypes = [I32P, C.c_int, C.c_int, C.c_int, I32P, C.POINTER(C.c_int32)]
         L.so_mix_seed.argtypes = [C.c_uint64] * 3
         L.so_mix_seed.restype = C.c_uint64
+        L.so_fnv1a.argtypes = [C.c_void_p, C.c_int64]
+        L.so_fnv1a.restype = C.c_uint64
         L.so_decode.argtypes = [C.POINTER(EngineConfigT), C.c_void_p, C.c_void_p, I32P, I32P, I32P, I32P,
                                 I32P, C.c_int64, C.POINTER(C.c_int64), np.ctypeslib.ndpointer(np.int64)]
         self.lib = L
@@ -238,6 +240,24 @@ class Oracle(_Lib):
                                        C.byref(nrec), ledger))
         tokens = [gen[s * mx: s * mx + cnt[s]].tolist() for s in range(b)]
         return tokens, rec[: nrec.value * 6].reshape(-1, 6), ledger
+
+
+def fnv_rows(logits) -> np.ndarray:
+    """FNV-1a of each fp32 row's bytes (fast path through the C oracle)."""
+    lib = _fnv_lib()
+    a = np.ascontiguousarray(logits, dtype=np.float32)
+    a = a.reshape(a.shape[0], -1) if a.ndim > 1 else a.reshape(1, -1)
+    return np.array([lib.so_fnv1a(r.ctypes.data, r.nbytes) for r in a], dtype=np.uint64)
+
+
+_FNV = None
+
+
+def _fnv_lib():
+    global _FNV
+    if _FNV is None:
+        _FNV = Oracle().lib
+    return _FNV
 
 
 class Reference(_Lib):

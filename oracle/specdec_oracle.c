@@ -36,6 +36,16 @@ static int fail(int code, const char* fmt, ...) {
 
 const char* so_last_error(void) { return g_err; }
 
+uint64_t so_fnv1a(const void* data, int64_t nbytes) {
+    uint64_t hash = 14695981039346656037ULL;
+    const unsigned char* b = (const unsigned char*)data;
+    for (int64_t i = 0; i < nbytes; ++i) {
+        hash ^= b[i];
+        hash *= 1099511628211ULL;
+    }
+    return hash;
+}
+
 /* ---------------------------------------------------------------- rng.hpp:15-46 */
 uint64_t so_splitmix_next(uint64_t* state) {
     uint64_t z = (*state += 0x9E3779B97F4A7C15ULL);
@@ -739,7 +749,6 @@ static int decode_greedy(const so_engine_config* e, const so_model* target, stat
         CHECK(st[s].len + e->max_new_tokens <= tc->max_positions, E_CAPACITY,
               "prompt plus generation budget exceeds max_positions");
     if (e->max_new_tokens == 0) return OK;
-    int V = tc->vocab_size;
     float* rows = NULL;
     for (int s = 0; s < e->batch_size; ++s) {
         state_t* S = &st[s];

@@ -29,6 +29,9 @@ typedef struct so_cache so_cache;
 
 const char* so_last_error(void);
 
+/* FNV-1a 64 over raw bytes (model.cpp:223-233 hash, reused to fingerprint logits rows) */
+uint64_t so_fnv1a(const void* data, int64_t nbytes);
+
 /* rng.hpp:11-46 */
 uint64_t so_splitmix_next(uint64_t* state);
 uint64_t so_mix_seed(uint64_t a, uint64_t b, uint64_t c);

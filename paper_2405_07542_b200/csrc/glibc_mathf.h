@@ -96,21 +96,19 @@ SDM_FN double sdm_u2d(uint64_t u) {
 
 // tab[i] = bits(RN(2^(i/32))) - (i << 47)   (e_exp2f_data.c).  Recomputed
 // independently from 2^(i/32) with 60-digit decimal arithmetic.
+#define SDM_EXP2F_TAB                                                                           \
+    {0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, 0x3fef9301d0125b51ull,     \
+     0x3fef72b83c7d517bull, 0x3fef54873168b9aaull, 0x3fef387a6e756238ull, 0x3fef1e9df51fdee1ull,     \
+     0x3fef06fe0a31b715ull, 0x3feef1a7373aa9cbull, 0x3feedea64c123422ull, 0x3feece086061892dull,     \
+     0x3feebfdad5362a27ull, 0x3feeb42b569d4f82ull, 0x3feeab07dd485429ull, 0x3feea47eb03a5585ull,     \
+     0x3feea09e667f3bcdull, 0x3fee9f75e8ec5f74ull, 0x3feea11473eb0187ull, 0x3feea589994cce13ull,     \
+     0x3feeace5422aa0dbull, 0x3feeb737b0cdc5e5ull, 0x3feec49182a3f090ull, 0x3feed503b23e255dull,     \
+     0x3feee89f995ad3adull, 0x3feeff76f2fb5e47ull, 0x3fef199bdd85529cull, 0x3fef3720dcef9069ull,     \
+     0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull}
+static const uint64_t sdm_exp2f_tab_host[32] = SDM_EXP2F_TAB;
 #ifdef __CUDACC__
-__device__ __constant__
-#else
-static const
+__device__ __constant__ uint64_t sdm_exp2f_tab_dev[32] = SDM_EXP2F_TAB;
 #endif
-uint64_t sdm_exp2f_tab[32] = {
-    0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, 0x3fef9301d0125b51ull,
-    0x3fef72b83c7d517bull, 0x3fef54873168b9aaull, 0x3fef387a6e756238ull, 0x3fef1e9df51fdee1ull,
-    0x3fef06fe0a31b715ull, 0x3feef1a7373aa9cbull, 0x3feedea64c123422ull, 0x3feece086061892dull,
-    0x3feebfdad5362a27ull, 0x3feeb42b569d4f82ull, 0x3feeab07dd485429ull, 0x3feea47eb03a5585ull,
-    0x3feea09e667f3bcdull, 0x3fee9f75e8ec5f74ull, 0x3feea11473eb0187ull, 0x3feea589994cce13ull,
-    0x3feeace5422aa0dbull, 0x3feeb737b0cdc5e5ull, 0x3feec49182a3f090ull, 0x3feed503b23e255dull,
-    0x3feee89f995ad3adull, 0x3feeff76f2fb5e47ull, 0x3fef199bdd85529cull, 0x3fef3720dcef9069ull,
-    0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull,
-};
 
 // glibc e_expf.c, __expf_fma variant.
 SDM_FN float sd_expf(float x) {
@@ -133,7 +131,11 @@ SDM_FN float sd_expf(float x) {
     uint64_t ki = sdm_d2u(kd);
     kd = SDM_DSUB(kd, kShift);
     double r = SDM_DFMA(kInvLn2N, xd, -kd);
-    uint64_t t = sdm_exp2f_tab[ki % 32];
+#ifdef __CUDA_ARCH__
+    uint64_t t = sdm_exp2f_tab_dev[ki % 32];
+#else
+    uint64_t t = sdm_exp2f_tab_host[ki % 32];
+#endif
     t += ki << 47;
     double s = sdm_u2d(t);
     double z = SDM_DFMA(C0, r, C1);
