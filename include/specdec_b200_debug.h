@@ -1,0 +1,16 @@
+/* specdec_b200_debug.h — kernel-level test hooks (not part of the drop-in
+ * boundary).  Used by tests/ to check the tcgen05 GEMM in isolation. */
+#ifndef SPECDEC_B200_DEBUG_H
+#define SPECDEC_B200_DEBUG_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* Y[T][M] = X[T][K] . W[M][K]^T with bf16 inputs (raw bits) and fp32 output,
+ * through the stream-K tcgen05 kernel on `grid` CTAs (0 = one per SM).
+ * Returns the kernel time in microseconds in *usec (CUDA events). */
+int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K, int T, int grid, float* Y, float* usec);
+#ifdef __cplusplus
+}
+#endif
+#endif

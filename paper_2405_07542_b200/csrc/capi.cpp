@@ -50,6 +50,8 @@ Workspace::~Workspace() {
     dfree(d_argmax);
     dfree(d_flag);
     dfree(d_scores);
+    free_fast_workspace(fast);
+    fast = nullptr;
     cap_tokens = 0;
 }
 
@@ -115,6 +117,7 @@ sd_model* create_model(const Config& cfg, int device, int precision, const float
             }
             if (host_weights) upload_weights_bf16(m, host_weights, h->st);
             else init_weights_bf16(m, h->st);
+            build_fast_model(m);
             note_launches(host_weights ? 0 : 2 + 14 * cfg.num_layers + 3);
         }
         CUDA_OK(cudaStreamSynchronize(h->st));

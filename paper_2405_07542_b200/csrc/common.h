@@ -79,8 +79,14 @@ struct Model {
     std::vector<FastLayer> layers;
     std::vector<void*> allocations;
     int64_t weight_bytes = 0;
+    struct FastModelState* fast = nullptr;  // TMA descriptors of the bf16 weights
     ~Model();
 };
+struct FastModelState;
+struct FastWorkspace;
+void free_fast_model(FastModelState* f);
+void free_fast_workspace(FastWorkspace* f);
+void build_fast_model(Model& m);
 
 // Per-sample KV arena.  K and V live in [L][2][B][heads][cap][head_dim]
 // (head-major per sample so the attention kernel streams one contiguous
@@ -130,6 +136,7 @@ struct Workspace {
     int32_t* d_argmax = nullptr;  // [T]
     int32_t* d_flag = nullptr;    // non-finite logit flag
     float* d_scores = nullptr;    // check-mode attention scratch [T, heads, cap]
+    FastWorkspace* fast = nullptr;  // bf16-mode buffers and TMA descriptors
     void ensure(const Model& m, const Cache& c, int T);
     ~Workspace();
 };

@@ -1,8 +1,640 @@
-// bf16 performance-mode forward (placeholder until the tcgen05 path lands).
+// bf16 PERFORMANCE mode forward of the verify step.
+//
+// Per layer (model.cpp:303-359, restructured for the GPU):
+//   LN1 (fp32 residual -> bf16)          k_layernorm
+//   QKV  tcgen05 GEMM + scatter epilogue  Q -> q16, K/V -> unpadded arena
+//   ragged multi-query attention          k_attention (+ k_attn_combine)
+//   O    tcgen05 GEMM + residual epilogue
+//   LN2                                   k_layernorm
+//   FC   tcgen05 GEMM + GELU epilogue
+//   PROJ tcgen05 GEMM + residual epilogue
+// then final LN, LM-head GEMM with the (max, lowest id) argmax epilogue, and
+// k_argmax_reduce over the vocab tiles.  Weights and KV are bf16; the
+// residual stream, accumulators and softmax are fp32.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "gemm.h"
 #include "handles.h"
 
 namespace sdb {
-void forward_fast(const Model&, Cache&, Workspace&, int, bool, cudaStream_t) {
-    throw Error(INTERNAL, "bf16 performance path not built yet");
+
+constexpr int kChunkTokens = 256;  // tokens per forward chunk (GEMM N <= 256)
+constexpr int kKeysPerCta = 256;   // attention split size (4 warps x 64 keys)
+
+struct FastModelState {
+    std::vector<GemmMaps> qkv, o, fc, proj;  // per layer (A map only used)
+    GemmMaps lm;
+};
+
+struct SampleSeg {
+    int q_start, n_q, kv_len, pad;
+};
+
+struct FastWorkspace {
+    int cap_tokens = 0, B = 0, cap = 0, max_splits = 0;
+    __nv_bfloat16 *xb = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr;
+    float* part_o = nullptr;   // [T][heads][max_splits][hd]
+    float* part_ml = nullptr;  // [T][heads][max_splits][2]
+    SampleSeg* segs = nullptr; // [B]
+    int32_t* qidx = nullptr;   // [T]
+    int32_t* dT = nullptr;
+    float* gemm_ws = nullptr;
+    int* counters = nullptr;
+    float* part_val = nullptr;
+    int* part_idx = nullptr;
+    GemmMaps map_xb, map_ctx, map_act;
+    std::vector<void*> allocs;
+};
+
+void free_fast_model(FastModelState* f) { delete f; }
+void free_fast_workspace(FastWorkspace* f) {
+    if (!f) return;
+    for (void* p : f->allocs) dfree(p);
+    delete f;
 }
+
+void build_fast_model(Model& m) {
+    const Config& c = m.cfg;
+    int64_t h = c.hidden(), mm = c.mlp();
+    SD_CHECK(h % 64 == 0, CONFIG, "bf16 mode needs hidden % 64 == 0");
+    SD_CHECK(c.head_dim == 64 || c.head_dim == 128, CONFIG, "bf16 mode supports head_dim 64 or 128");
+    auto* f = new FastModelState();
+    for (const FastLayer& L : m.layers) {
+        GemmMaps g;
+        g.A = make_tmap_2d(L.wqkv, 3 * h, h, 256);
+        f->qkv.push_back(g);
+        g.A = make_tmap_2d(L.wo, h, h, 256);
+        f->o.push_back(g);
+        g.A = make_tmap_2d(L.wfc, mm, h, 256);
+        f->fc.push_back(g);
+        g.A = make_tmap_2d(L.wproj, h, mm, 256);
+        f->proj.push_back(g);
+    }
+    f->lm.A = make_tmap_2d(m.lm16, m.vocab_pad, h, 256);
+    m.fast = f;
+}
+
+namespace {
+
+// ------------------------------------------------------------- row kernels
+template <typename F>
+__device__ __forceinline__ float block_sum(float v, F* scratch) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    int w = threadIdx.x / 32, l = threadIdx.x % 32;
+    __syncthreads();
+    if (l == 0) scratch[w] = v;
+    __syncthreads();
+    float t = 0.0f;
+    for (int i = 0; i < (int)(blockDim.x / 32); ++i) t += scratch[i];
+    return t;
+}
+
+constexpr int kRowThreads = 256, kMaxPerThread = 32;  // hidden <= 8192
+
+// LayerNorm of fp32 rows into bf16 (two-pass mean / variance, eps 1e-5).
+__device__ __forceinline__ void ln_row(const float* x, const float* g, const float* b, int h,
+                                       __nv_bfloat16* y, float* scratch) {
+    float v[kMaxPerThread];
+    int n = 0;
+    float s = 0.0f;
+    for (int i = threadIdx.x; i < h; i += kRowThreads) s += (v[n++] = x[i]);
+    float mean = block_sum(s, scratch) / h;
+    float q = 0.0f;
+    for (int k = 0; k < n; ++k) {
+        float d = v[k] - mean;
+        q += d * d;
+    }
+    float inv = rsqrtf(block_sum(q, scratch) / h + 1e-5f);
+    n = 0;
+    for (int i = threadIdx.x; i < h; i += kRowThreads, ++n) y[i] = __float2bfloat16_rn((v[n] - mean) * inv * g[i] + b[i]);
+}
+
+__global__ void __launch_bounds__(kRowThreads) k_layernorm(const float* __restrict__ x, const float* __restrict__ g,
+                                                           const float* __restrict__ b, int h,
+                                                           __nv_bfloat16* __restrict__ y, const int* __restrict__ dT) {
+    __shared__ float scratch[32];
+    int t = blockIdx.x;
+    if (t >= *dT) return;
+    ln_row(x + (size_t)t * h, g, b, h, y + (size_t)t * h, scratch);
+}
+
+// embedding (model.cpp:287-294) fused with layer 0's LN1
+__global__ void __launch_bounds__(kRowThreads) k_embed_ln(const __nv_bfloat16* __restrict__ tok,
+                                                          const __nv_bfloat16* __restrict__ pos,
+                                                          const int32_t* __restrict__ tokens,
+                                                          const Plan* __restrict__ plans, int h,
+                                                          float* __restrict__ resid, const float* __restrict__ g,
+                                                          const float* __restrict__ b, __nv_bfloat16* __restrict__ y,
+                                                          const int* __restrict__ dT) {
+    __shared__ float scratch[32];
+    int t = blockIdx.x;
+    if (t >= *dT) return;
+    const __nv_bfloat16* e = tok + (size_t)tokens[t] * h;
+    const __nv_bfloat16* p = pos + (size_t)plans[t].logical_pos * h;
+    float* r = resid + (size_t)t * h;
+    for (int i = threadIdx.x; i < h; i += kRowThreads) r[i] = __bfloat162float(e[i]) + __bfloat162float(p[i]);
+    __syncthreads();
+    ln_row(r, g, b, h, y + (size_t)t * h, scratch);
+}
+
+// per-token argmax over the LM-head tile partials (lowest id on ties)
+__global__ void k_argmax_reduce(const float* __restrict__ pv, const int* __restrict__ pi, int m_tiles, int ld,
+                                int32_t* __restrict__ out, const int* __restrict__ dT) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= *dT) return;
+    float bv = pv[t];
+    int bi = pi[t];
+    for (int k = 1; k < m_tiles; ++k) {
+        float v = pv[(size_t)k * ld + t];
+        int i = pi[(size_t)k * ld + t];
+        if (v > bv || (v == bv && i < bi)) {
+            bv = v;
+            bi = i;
+        }
+    }
+    out[t] = bi;
+}
+
+// ------------------------------------------------------------- attention
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// smem tile [rows][HD] bf16 with the 16-byte chunk index XOR-swizzled by row%8
+template <int HD>
+__device__ __forceinline__ uint32_t swz(int row, int col) {  // byte offset of element (row, col)
+    constexpr int kChunks = HD / 8;
+    int chunk = (col >> 3) ^ (row & 7);
+    return (uint32_t)(row * kChunks + chunk) * 16 + (col & 7) * 2;
+}
+
+struct AttnArgs {
+    const __nv_bfloat16* q;    // [T][h]
+    const __nv_bfloat16* kv;   // arena
+    const Plan* plans;
+    const SampleSeg* segs;
+    const int32_t* qidx;
+    const uint8_t* pad;        // padded grid flags or null
+    __nv_bfloat16* ctx;        // [T][h]
+    float* part_o;
+    float* part_ml;
+    int h, heads, B, cap, layer, max_splits;
+    float scale_log2;          // log2(e) / sqrt(hd)
+};
+
+// One CTA = (sample, head) x 256-key split x 16-query tile; 4 warps each own
+// 64 keys.  S = Q K^T and O = P V run on mma.sync m16n8k16 (bf16 in, fp32
+// accumulate); the 4 warps' partial softmax states merge through smem.  A
+// sample's K/V extent is read once per split, not once per query token (the
+// paper's per-token grid, re-reads it n_s times).
+template <int HD>
+__global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
+    constexpr int kKeys = 64;
+    const int sh = blockIdx.x, split = blockIdx.y, qt = blockIdx.z;
+    const int s = sh / a.heads, head = sh % a.heads;
+    const SampleSeg seg = a.segs[s];
+    const int k_begin = split * kKeysPerCta;
+    if (seg.n_q == 0 || qt * 16 >= seg.n_q || k_begin >= seg.kv_len) return;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int nq = min(16, seg.n_q - qt * 16);
+
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint8_t* sQ = sm;                                   // [16][HD]
+    uint8_t* sK = sm + 16 * HD * 2 + warp * 2 * kKeys * HD * 2;
+    uint8_t* sV = sK + kKeys * HD * 2;
+    float* sMerge = (float*)(sm + 16 * HD * 2 + 4 * 2 * kKeys * HD * 2);  // [4][16][HD] + [4][16][2]
+    __shared__ int sWslot[16];
+    __shared__ int sTok[16];
+
+    // Q tile (rows >= nq zero-filled)
+    for (int i = threadIdx.x; i < 16 * HD / 8; i += 128) {
+        int r = i / (HD / 8), c8 = i % (HD / 8);
+        int tok = r < nq ? a.qidx[seg.q_start + qt * 16 + r] : 0;
+        const __nv_bfloat16* src = a.q + (size_t)tok * a.h + head * HD + c8 * 8;
+        cp_async16(sQ + swz<HD>(r, c8 * 8), src, r < nq);
+    }
+    if (threadIdx.x < 16) {
+        int r = threadIdx.x;
+        int tok = r < nq ? a.qidx[seg.q_start + qt * 16 + r] : -1;
+        sTok[r] = tok;
+        sWslot[r] = tok >= 0 ? a.plans[tok].write_slot : -1;
+    }
+    // this warp's K / V rows
+    const int kw0 = k_begin + warp * kKeys;
+    const size_t kbase = ((((size_t)a.layer * 2 + 0) * a.B + s) * a.heads + head) * (size_t)a.cap * HD;
+    const size_t vbase = ((((size_t)a.layer * 2 + 1) * a.B + s) * a.heads + head) * (size_t)a.cap * HD;
+    const int kv_end = min(seg.kv_len, k_begin + kKeysPerCta);
+    for (int i = lane; i < kKeys * HD / 8; i += 32) {
+        int r = i / (HD / 8), c8 = i % (HD / 8);
+        int key = kw0 + r;
+        bool ok = key < kv_end;
+        size_t off = (size_t)(ok ? key : 0) * HD + c8 * 8;
+        cp_async16(sK + swz<HD>(r, c8 * 8), a.kv + kbase + off, ok);
+        cp_async16(sV + swz<HD>(r, c8 * 8), a.kv + vbase + off, ok);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    const int g = lane / 4, c = lane % 4;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
+    float o[HD / 8][4];
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.0f;
+
+    if (kw0 < kv_end) {
+        const uint32_t qa = (uint32_t)__cvta_generic_to_shared(sQ);
+        const uint32_t ka = (uint32_t)__cvta_generic_to_shared(sK);
+        const uint32_t va = (uint32_t)__cvta_generic_to_shared(sV);
+        // S = Q K^T : 16 x 64
+        float sacc[8][4];
+#pragma unroll
+        for (int n = 0; n < 8; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.0f;
+#pragma unroll
+        for (int kk = 0; kk < HD; kk += 16) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4(qa + swz<HD>(lane % 16, kk + (lane / 16) * 8), a0, a1, a2, a3);
+#pragma unroll
+            for (int n = 0; n < 8; n += 2) {
+                // matrices: (keys n*8.., cols kk), (keys n*8.., kk+8), (keys n*8+8.., kk), (keys n*8+8.., kk+8)
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(ka + swz<HD>(n * 8 + (lane % 8) + (lane / 16) * 8, kk + ((lane / 8) % 2) * 8), b0, b1, b2,
+                        b3);
+                mma_bf16(sacc[n], a0, a1, a2, a3, b0, b1);
+                mma_bf16(sacc[n + 1], a0, a1, a2, a3, b2, b3);
+            }
+        }
+        // mask + local max
+        float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                int row = g + (e >= 2 ? 8 : 0);
+                int key = kw0 + n * 8 + 2 * c + (e & 1);
+                bool vis = key < kv_end && key <= sWslot[row] && !(a.pad && a.pad[(size_t)s * a.cap + key]);
+                float x = vis ? sacc[n][e] * a.scale_log2 : -INFINITY;
+                sacc[n][e] = x;
+                mx[e >> 1] = fmaxf(mx[e >> 1], x);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+            mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+            m_run[r] = mx[r];
+        }
+        float sum[2] = {0.0f, 0.0f};
+        uint32_t p[8][2];
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+            float e0 = m_run[0] == -INFINITY ? 0.0f : exp2f(sacc[n][0] - m_run[0]);
+            float e1 = m_run[0] == -INFINITY ? 0.0f : exp2f(sacc[n][1] - m_run[0]);
+            float e2 = m_run[1] == -INFINITY ? 0.0f : exp2f(sacc[n][2] - m_run[1]);
+            float e3 = m_run[1] == -INFINITY ? 0.0f : exp2f(sacc[n][3] - m_run[1]);
+            sum[0] += e0 + e1;
+            sum[1] += e2 + e3;
+            p[n][0] = pack_bf16(e0, e1);
+            p[n][1] = pack_bf16(e2, e3);
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            sum[r] += __shfl_xor_sync(0xffffffffu, sum[r], 1);
+            sum[r] += __shfl_xor_sync(0xffffffffu, sum[r], 2);
+            l_run[r] = sum[r];
+        }
+        // O = P V : 16 x HD, k = 64 keys in 4 steps
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+            uint32_t a0 = p[2 * ks][0], a1 = p[2 * ks][1], a2 = p[2 * ks + 1][0], a3 = p[2 * ks + 1][1];
+#pragma unroll
+            for (int n = 0; n < HD / 8; n += 2) {
+                uint32_t b0, b1, b2, b3;
+                int key = ks * 16 + (lane % 8) + ((lane / 8) % 2) * 8;
+                int col = n * 8 + (lane / 16) * 8;
+                ldsm_x4_t(va + swz<HD>(key, col), b0, b1, b2, b3);
+                mma_bf16(o[n], a0, a1, a2, a3, b0, b1);
+                mma_bf16(o[n + 1], a0, a1, a2, a3, b2, b3);
+            }
+        }
+    }
+    // merge the 4 warps' (m, l, O) in smem
+    float* mO = sMerge + (size_t)warp * 16 * HD;
+    float* mML = sMerge + 4 * 16 * HD + warp * 32;
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n) {
+        mO[g * HD + n * 8 + 2 * c] = o[n][0];
+        mO[g * HD + n * 8 + 2 * c + 1] = o[n][1];
+        mO[(g + 8) * HD + n * 8 + 2 * c] = o[n][2];
+        mO[(g + 8) * HD + n * 8 + 2 * c + 1] = o[n][3];
+    }
+    if (c == 0) {
+        mML[g * 2] = m_run[0];
+        mML[g * 2 + 1] = l_run[0];
+        mML[(g + 8) * 2] = m_run[1];
+        mML[(g + 8) * 2 + 1] = l_run[1];
+    }
+    __syncthreads();
+    const int nsplit = (seg.kv_len + kKeysPerCta - 1) / kKeysPerCta;
+    for (int i = threadIdx.x; i < 16 * HD; i += 128) {
+        int r = i / HD, d = i % HD;
+        if (r >= nq) continue;
+        float M = -INFINITY;
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, sMerge[4 * 16 * HD + w * 32 + r * 2]);
+        float L = 0.0f, O = 0.0f;
+        for (int w = 0; w < 4; ++w) {
+            float mw = sMerge[4 * 16 * HD + w * 32 + r * 2];
+            if (mw == -INFINITY) continue;
+            float f = exp2f(mw - M);
+            L += sMerge[4 * 16 * HD + w * 32 + r * 2 + 1] * f;
+            O += sMerge[(size_t)w * 16 * HD + r * HD + d] * f;
+        }
+        int tok = sTok[r];
+        if (nsplit == 1) {
+            a.ctx[(size_t)tok * a.h + head * HD + d] = __float2bfloat16_rn(O / L);
+        } else {
+            size_t base = ((size_t)tok * a.heads + head) * a.max_splits + split;
+            a.part_o[base * HD + d] = O;
+            if (d == 0) {
+                a.part_ml[base * 2] = M;
+                a.part_ml[base * 2 + 1] = L;
+            }
+        }
+    }
+}
+
+// merge split-KV partials: grid (T, heads), block HD
+__global__ void k_attn_combine(AttnArgs a, int hd, const int* __restrict__ dT) {
+    int t = blockIdx.x, head = blockIdx.y, d = threadIdx.x;
+    if (t >= *dT) return;
+    int s = a.plans[t].sample;
+    int nsplit = (a.segs[s].kv_len + kKeysPerCta - 1) / kKeysPerCta;
+    if (nsplit <= 1) return;
+    size_t base = ((size_t)t * a.heads + head) * a.max_splits;
+    float M = -INFINITY;
+    for (int k = 0; k < nsplit; ++k) M = fmaxf(M, a.part_ml[(base + k) * 2]);
+    float L = 0.0f, O = 0.0f;
+    for (int k = 0; k < nsplit; ++k) {
+        float mk = a.part_ml[(base + k) * 2];
+        if (mk == -INFINITY) continue;
+        float f = exp2f(mk - M);
+        L += a.part_ml[(base + k) * 2 + 1] * f;
+        O += a.part_o[(base + k) * hd + d] * f;
+    }
+    a.ctx[(size_t)t * a.h + head * hd + d] = __float2bfloat16_rn(O / L);
+}
+
+template <typename T>
+T* walloc(FastWorkspace* f, size_t n) {
+    T* p = (T*)dmalloc(sizeof(T) * (n ? n : 1));
+    f->allocs.push_back(p);
+    return p;
+}
+
+FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
+    FastWorkspace* f = ws.fast;
+    int max_splits = (c.cap + kKeysPerCta - 1) / kKeysPerCta;
+    if (f && f->B >= c.B && f->cap >= c.cap && f->max_splits >= max_splits) return f;
+    free_fast_workspace(f);
+    f = new FastWorkspace();
+    const Config& cfg = m.cfg;
+    size_t h = cfg.hidden(), mm = cfg.mlp(), T = kChunkTokens;
+    f->cap_tokens = (int)T;
+    f->B = c.B;
+    f->cap = c.cap;
+    f->max_splits = max_splits;
+    f->xb = walloc<__nv_bfloat16>(f, T * h);
+    f->q = walloc<__nv_bfloat16>(f, T * h);
+    f->ctx = walloc<__nv_bfloat16>(f, T * h);
+    f->act = walloc<__nv_bfloat16>(f, T * mm);
+    f->part_o = walloc<float>(f, T * cfg.num_heads * max_splits * cfg.head_dim);
+    f->part_ml = walloc<float>(f, T * cfg.num_heads * max_splits * 2);
+    f->segs = walloc<SampleSeg>(f, c.B);
+    f->qidx = walloc<int32_t>(f, T);
+    f->dT = walloc<int32_t>(f, 4);
+    f->gemm_ws = walloc<float>(f, (size_t)2 * 148 * 256 * 256);
+    f->counters = walloc<int>(f, 65536);
+    CUDA_OK(cudaMemset(f->counters, 0, sizeof(int) * 65536));
+    int m_tiles_lm = m.vocab_pad / 256;
+    f->part_val = walloc<float>(f, (size_t)m_tiles_lm * T);
+    f->part_idx = walloc<int>(f, (size_t)m_tiles_lm * T);
+    make_b_maps(f->map_xb, f->xb, T, h);
+    make_b_maps(f->map_ctx, f->ctx, T, h);
+    make_b_maps(f->map_act, f->act, T, mm);
+    ws.fast = f;
+    return f;
+}
+
+}  // namespace
+
+// Host-side ragged descriptors for one chunk of planned tokens: per sample the
+// list of its query tokens (in stream order) and its visible KV extent.
+static void build_segments(const std::vector<Plan>& plans, int t0, int n, int B, std::vector<SampleSeg>& segs,
+                           std::vector<int32_t>& qidx) {
+    segs.assign(B, SampleSeg{0, 0, 0, 0});
+    std::vector<std::vector<int>> per(B);
+    for (int i = 0; i < n; ++i) per[plans[t0 + i].sample].push_back(i);
+    qidx.clear();
+    for (int s = 0; s < B; ++s) {
+        segs[s].q_start = (int)qidx.size();
+        segs[s].n_q = (int)per[s].size();
+        int kv = 0;
+        for (int i : per[s]) {
+            qidx.push_back(i);
+            kv = std::max(kv, plans[t0 + i].write_slot + 1);
+        }
+        segs[s].kv_len = kv;
+    }
+}
+
+void forward_fast_chunk(const Model& m, Cache& c, Workspace& ws, FastWorkspace* f, int t0, int n,
+                        const std::vector<Plan>& plans, bool want_logits, cudaStream_t st) {
+    const Config& cfg = m.cfg;
+    const int h = cfg.hidden(), mm = cfg.mlp(), heads = cfg.num_heads, hd = cfg.head_dim;
+    std::vector<SampleSeg> segs;
+    std::vector<int32_t> qidx;
+    build_segments(plans, t0, n, c.B, segs, qidx);
+    CUDA_OK(cudaMemcpyAsync(f->segs, segs.data(), sizeof(SampleSeg) * c.B, cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(f->qidx, qidx.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(f->dT, &n, sizeof(int), cudaMemcpyHostToDevice, st));
+    int max_kv = 0, max_q = 0;
+    for (auto& sg : segs) {
+        max_kv = std::max(max_kv, sg.kv_len);
+        max_q = std::max(max_q, sg.n_q);
+    }
+    const int32_t* tokens = ws.d_tokens + t0;
+    const Plan* dplans = ws.d_plans + t0;
+    float* resid = ws.d_resid + (size_t)t0 * h;
+    const int sms = 148;
+    int64_t launches = 0;
+
+    GemmArgs base{};
+    base.T = n;
+    base.dT = f->dT;
+    base.ws = f->gemm_ws;
+    base.counters = f->counters;
+    base.h = h;
+    base.hd = hd;
+    base.heads = heads;
+    base.B = c.B;
+    base.cap = c.cap;
+    base.plans = dplans;
+    base.kv = (__nv_bfloat16*)c.kv;
+
+    k_embed_ln<<<n, kRowThreads, 0, st>>>((const __nv_bfloat16*)m.tok16, (const __nv_bfloat16*)m.pos16, tokens,
+                                          dplans, h, resid, m.layers[0].ln1_g, m.layers[0].ln1_b, f->xb, f->dT);
+    launches++;
+    AttnArgs at{};
+    at.q = f->q;
+    at.kv = (const __nv_bfloat16*)c.kv;
+    at.plans = dplans;
+    at.segs = f->segs;
+    at.qidx = f->qidx;
+    at.pad = c.layout == PADDED ? c.d_pad : nullptr;
+    at.ctx = f->ctx;
+    at.part_o = f->part_o;
+    at.part_ml = f->part_ml;
+    at.h = h;
+    at.heads = heads;
+    at.B = c.B;
+    at.cap = c.cap;
+    at.max_splits = f->max_splits;
+    at.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+    const int splits = (max_kv + kKeysPerCta - 1) / kKeysPerCta;
+    const int qtiles = (max_q + 15) / 16;
+    const size_t attn_smem = (size_t)16 * hd * 2 + 4 * 2 * 64 * hd * 2 + (4 * 16 * hd + 4 * 32) * 4;
+
+    for (int l = 0; l < cfg.num_layers; ++l) {
+        const FastLayer& L = m.layers[l];
+        const FastModelState* fm = m.fast;
+        // QKV + scatter
+        GemmArgs g = base;
+        g.M = 3 * h;
+        g.K = h;
+        g.m_tiles = (3 * h + 255) / 256;
+        g.bias = L.bqkv;
+        g.out_bf16 = f->q;
+        g.layer = l;
+        GemmMaps mp = f->map_xb;
+        mp.A = fm->qkv[l].A;
+        gemm_launch(EPI_QKV, g, mp, gemm_grid(g, n, sms), st);
+        // attention
+        at.layer = l;
+        if (hd == 128) {
+            static bool cfg128 = false;
+            if (!cfg128) {
+                CUDA_OK(cudaFuncSetAttribute(k_attention<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                cfg128 = true;
+            }
+            k_attention<128><<<dim3(c.B * heads, splits, qtiles), 128, attn_smem, st>>>(at);
+        } else {
+            static bool cfg64 = false;
+            if (!cfg64) {
+                CUDA_OK(cudaFuncSetAttribute(k_attention<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                cfg64 = true;
+            }
+            k_attention<64><<<dim3(c.B * heads, splits, qtiles), 128, attn_smem, st>>>(at);
+        }
+        launches++;
+        if (splits > 1) {
+            k_attn_combine<<<dim3(n, heads), hd, 0, st>>>(at, hd, f->dT);
+            launches++;
+        }
+        // O projection + residual
+        g = base;
+        g.M = h;
+        g.K = h;
+        g.m_tiles = (h + 255) / 256;
+        g.bias = L.bo;
+        g.out_f32 = resid;
+        g.ld_out = h;
+        mp = f->map_ctx;
+        mp.A = fm->o[l].A;
+        gemm_launch(EPI_RESID, g, mp, gemm_grid(g, n, sms), st);
+        k_layernorm<<<n, kRowThreads, 0, st>>>(resid, L.ln2_g, L.ln2_b, h, f->xb, f->dT);
+        // FC + GELU
+        g = base;
+        g.M = mm;
+        g.K = h;
+        g.m_tiles = (mm + 255) / 256;
+        g.bias = L.bfc;
+        g.out_bf16 = f->act;
+        g.ld_out = mm;
+        mp = f->map_xb;
+        mp.A = fm->fc[l].A;
+        gemm_launch(EPI_GELU, g, mp, gemm_grid(g, n, sms), st);
+        // PROJ + residual
+        g = base;
+        g.M = h;
+        g.K = mm;
+        g.m_tiles = (h + 255) / 256;
+        g.bias = L.bproj;
+        g.out_f32 = resid;
+        g.ld_out = h;
+        mp = f->map_act;
+        mp.A = fm->proj[l].A;
+        gemm_launch(EPI_RESID, g, mp, gemm_grid(g, n, sms), st);
+        // next LN1 or the final LN
+        const float* lg = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_g : m.lnf_g;
+        const float* lb = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_b : m.lnf_b;
+        k_layernorm<<<n, kRowThreads, 0, st>>>(resid, lg, lb, h, f->xb, f->dT);
+        launches += 6;
+    }
+    // LM head + argmax
+    GemmArgs g = base;
+    g.M = m.vocab_pad;
+    g.K = h;
+    g.m_tiles = m.vocab_pad / 256;
+    g.vocab = cfg.vocab_size;
+    g.ld_part = kChunkTokens;
+    g.part_val = f->part_val;
+    g.part_idx = f->part_idx;
+    g.logits = want_logits ? ws.d_logits + (size_t)t0 * cfg.vocab_size : nullptr;
+    g.flag = ws.d_flag;
+    GemmMaps mp = f->map_xb;
+    mp.A = m.fast->lm.A;
+    gemm_launch(EPI_ARGMAX, g, mp, gemm_grid(g, n, sms), st);
+    k_argmax_reduce<<<(n + 127) / 128, 128, 0, st>>>(f->part_val, f->part_idx, g.m_tiles, kChunkTokens,
+                                                     ws.d_argmax + t0, f->dT);
+    launches += 2;
+    note_launches(launches);
+    CUDA_OK(cudaGetLastError());
+}
+
+void forward_fast(const Model& m, Cache& c, Workspace& ws, int T, bool want_logits, cudaStream_t st) {
+    FastWorkspace* f = ensure_fast(m, c, ws);
+    // the plans are needed on the host for the ragged descriptors
+    std::vector<Plan> plans(T);
+    CUDA_OK(cudaMemcpyAsync(plans.data(), ws.d_plans, sizeof(Plan) * T, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    for (int t0 = 0; t0 < T; t0 += kChunkTokens)
+        forward_fast_chunk(m, c, ws, f, t0, std::min(kChunkTokens, T - t0), plans, want_logits, st);
+}
+
 }  // namespace sdb

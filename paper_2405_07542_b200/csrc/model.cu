@@ -49,6 +49,7 @@ void WeightLayout::build(const Config& c) {
 }
 
 Model::~Model() {
+    free_fast_model(fast);
     for (void* p : allocations) dfree(p);
 }
 
