@@ -66,6 +66,12 @@ typedef struct sd_cache sd_cache;
 const char* sd_last_error(void);
 /* number of CUDA kernels this thread's library calls have launched so far */
 int64_t sd_kernel_launches(void);
+/* Per-launch CUDA-event timing of the bf16 forward (eager runs only; graphs
+ * are not instrumented).  sd_profile_read fills out[kinds][3] = {launches,
+ * total_ms, algorithmic_bytes} for kinds 0 gemm_qkv, 1 gemm_o, 2 gemm_fc,
+ * 3 gemm_proj, 4 gemm_lm, 5 attention, 6 layernorm/embed, 7 misc. */
+int sd_profile_enable(int on);
+int sd_profile_read(double* out, int kinds);
 
 /* ---- model --------------------------------------------------------------- */
 /* ModelConfig::validate (model.cpp:12-18) */
@@ -151,6 +157,35 @@ int sd_decode(const sd_engine_config* cfg, sd_model* target, sd_model* draft,
               const int32_t* prompts, const int32_t* prompt_lens, int32_t* gen_tokens,
               int32_t* gen_counts, int32_t* rec, int64_t rec_cap, int64_t* n_rec,
               int64_t* ledger, double* timing);
+
+/* ---- decode sessions (device-resident decode_speculative loop) ----------- */
+/* A session owns one cache and a prefilled batch, and runs the loop of
+ * engine.cpp:391-489 entirely on the GPU: the predictor (LLMA retrieval,
+ * predictors.cpp:39-59, or the synthetic corrupted greedy rollout,
+ * predictors.cpp:61-72, fed from a precomputed trajectory), pack, forward,
+ * verify, clip and commit, replayed from a captured CUDA graph.  bf16 models
+ * only; cfg->mode 1 (vanilla, padded grid) or 2 (EMS, unpadded arena). */
+typedef struct sd_session sd_session;
+const char* sd_session_last_error(void);
+int sd_session_create(sd_model* m, const sd_engine_config* cfg, int capacity, sd_session** out);
+/* prefill (engine.cpp:330-385) and snapshot the post-prefill state */
+int sd_session_prefill(sd_session* s, const int32_t* prompts, const int32_t* prompt_lens);
+/* traj[B][stride]: each sample's greedy continuation (synthetic predictor) */
+int sd_session_set_trajectory(sd_session* s, const int32_t* traj, int stride);
+/* roll back to the post-prefill state (metadata only, no KV moves) */
+int sd_session_reset(sd_session* s);
+/* run until every sample finished; steps = verify steps, gpu_ms = CUDA-event
+ * time on the session stream from the first step to the last */
+int sd_session_run(sd_session* s, int use_graph, int graph_steps, int32_t* steps, float* gpu_ms);
+/* the same loop driven from the host through sd_verify_step (predictor on the
+ * host, H2D drafts / D2H tau + accepted per step); reports the bytes moved */
+int sd_session_run_host(sd_session* s, int32_t* steps, float* gpu_ms, int64_t* h2d_bytes, int64_t* d2h_bytes);
+/* gen_tokens[B][max_new_tokens], gen_counts[B]; per-step logs [max_steps][B]
+ * of draft counts k (-1 inactive) and tau (| 0x10000 when clipped) */
+int sd_session_outputs(sd_session* s, int32_t* gen_tokens, int32_t* gen_counts, int32_t* log_k,
+                       int32_t* log_tau, int max_steps);
+int sd_session_cache(sd_session* s, sd_cache** out);
+void sd_session_destroy(sd_session* s);
 
 #ifdef __cplusplus
 }

@@ -37,6 +37,10 @@ void Workspace::ensure(const Model& m, const Cache& c, int T) {
     CUDA_OK(cudaMemset(d_flag, 0, sizeof(int32_t) * 4));
     if (m.precision == FP32_CHECK)
         d_scores = (float*)dmalloc(sizeof(float) * 2 * (size_t)T2 * cfg.num_heads * c.cap);
+    d_segs = (SampleSeg*)dmalloc(sizeof(SampleSeg) * (size_t)c.B);
+    d_qidx = (int32_t*)dmalloc(sizeof(int32_t) * T2);
+    d_T = (int32_t*)dmalloc(sizeof(int32_t) * 4);
+    segs_cap = c.B;
     cap_tokens = T2;
 }
 
@@ -50,6 +54,9 @@ Workspace::~Workspace() {
     dfree(d_argmax);
     dfree(d_flag);
     dfree(d_scores);
+    dfree(d_segs);
+    dfree(d_qidx);
+    dfree(d_T);
     free_fast_workspace(fast);
     fast = nullptr;
     cap_tokens = 0;
@@ -333,7 +340,7 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
     for (int i = 0; i < ndraft; ++i)
         SD_CHECK(drafts[i] >= 0 && drafts[i] < cfg.vocab_size, CONTRACT, "token id out of vocabulary");
     SD_CHECK(nact > 0, CONTRACT, "forward pass over zero tokens");
-    int T = 0;
+    int T = 0, max_kv = 0, max_q = 0;
     for (int s = 0; s < B; ++s) {
         if (!active[s]) continue;
         int n = c.layout == PADDED ? 1 + kmax : 1 + counts[s];
@@ -345,6 +352,8 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
         SD_CHECK(last_slot < c.cap, CAPACITY,
                  "cache position " + std::to_string(last_slot) + " exceeds capacity " + std::to_string(c.cap));
         T += n;
+        max_kv = std::max(max_kv, last_slot + 1);
+        max_q = std::max(max_q, n);
     }
     // device buffers: inputs [5B + kcap*B], scratch, outputs
     int kcap = std::max(kmax, 1);
@@ -388,6 +397,8 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
     a.pad = c.layout == PADDED ? c.d_pad : nullptr;
     a.tokens = h->ws.d_tokens;
     a.plans = h->ws.d_plans;
+    a.segs = h->ws.d_segs;
+    a.qidx = h->ws.d_qidx;
     a.first_row = ds + o_first;
     a.draft_off = ds + o_doff;
     a.scalars = ds + o_scal;
@@ -398,14 +409,14 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
     launch_pack(a, st);
     note_launches(1);
     // run the forward (argmax always; logits on request)
-    {
-        Model& mm = m;
-        if (mm.precision == FP32_CHECK) {
-            forward_check(mm, c, h->ws, T, true, st);
-            note_launches(3 + 11 * (int64_t)cfg.num_layers + 3);
-        } else {
-            forward_fast(mm, c, h->ws, T, logits != nullptr, st);
-        }
+    if (m.precision == FP32_CHECK) {
+        forward_check(m, c, h->ws, T, true, st);
+        note_launches(3 + 11 * (int64_t)cfg.num_layers + 3);
+    } else if (T <= 256) {
+        DeviceBatch db{h->ws.d_segs, h->ws.d_qidx, ds + o_scal, T, max_kv, max_q};
+        forward_fast_dev(m, c, h->ws, db, 0, logits != nullptr, st);
+    } else {
+        forward_fast(m, c, h->ws, T, logits != nullptr, st);
     }
     launch_accept(a, st);
     note_launches(1);
@@ -570,6 +581,13 @@ extern "C" {
 
 const char* sd_last_error(void) { return g_err.c_str(); }
 int64_t sd_kernel_launches(void) { return g_launches.load(); }
+
+int sd_profile_enable(int on) {
+    return guarded([&] { profile_enable(on != 0); });
+}
+int sd_profile_read(double* out, int kinds) {
+    return guarded([&] { profile_read(out, kinds); });
+}
 
 int sd_config_validate(const sd_model_config* cfg) {
     return guarded([&] {

@@ -117,6 +117,25 @@ struct Plan {
     int32_t sample, logical_pos, write_slot, store;
 };
 
+// Per-sample ragged descriptor consumed by the attention kernel: the sample's
+// query tokens are qidx[q_start .. q_start + n_q) of the packed stream and its
+// visible KV extent is slots [0, kv_len) (each query still sees only slots
+// <= its own write_slot).
+struct SampleSeg {
+    int q_start, n_q, kv_len, pad_;
+};
+
+// Where a device-described batch lives (written by k_pack or uploaded by the
+// host) and the host-side upper bounds the launch grids are sized for.
+struct DeviceBatch {
+    const SampleSeg* segs;
+    const int32_t* qidx;
+    const int32_t* dT;   // device token count
+    int T_upper;         // grid bound for token-parallel kernels (<= 256)
+    int max_kv_upper;    // bound on any sample's kv_len
+    int max_q_upper;     // bound on any sample's query count
+};
+
 // ---- device entry points (defined in the .cu files) -------------------------
 void init_weights_fp32(Model& m, cudaStream_t st);
 void init_weights_bf16(Model& m, cudaStream_t st);
@@ -137,6 +156,10 @@ struct Workspace {
     int32_t* d_flag = nullptr;    // non-finite logit flag
     float* d_scores = nullptr;    // check-mode attention scratch [T, heads, cap]
     FastWorkspace* fast = nullptr;  // bf16-mode buffers and TMA descriptors
+    SampleSeg* d_segs = nullptr;    // [batch] ragged descriptors
+    int32_t* d_qidx = nullptr;      // [T]
+    int32_t* d_T = nullptr;         // device token count
+    int segs_cap = 0;
     void ensure(const Model& m, const Cache& c, int T);
     ~Workspace();
 };

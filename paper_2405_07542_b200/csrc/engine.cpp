@@ -27,6 +27,8 @@ uint64_t mix_seed(uint64_t a, uint64_t b, uint64_t c) {  // rng.hpp:43-46
     return splitmix_next(st);
 }
 
+}  // namespace
+
 // predictors.cpp:39-59 (LLMA prompt lookup: rightmost earlier match)
 std::vector<int32_t> retrieval_predict(const std::vector<int32_t>& ctx, int match_len, int copy_len) {
     SD_CHECK(match_len >= 1, CONTRACT, "match length must be >= 1");
@@ -42,6 +44,8 @@ std::vector<int32_t> retrieval_predict(const std::vector<int32_t>& ctx, int matc
     }
     return {};
 }
+
+namespace {
 
 // predictors.cpp:9-37: greedy k-token rollout on a FRESH cache every call
 // (the scratch cache is reset, which is observationally a fresh arena).

@@ -28,18 +28,11 @@ struct FastModelState {
     GemmMaps lm;
 };
 
-struct SampleSeg {
-    int q_start, n_q, kv_len, pad;
-};
-
 struct FastWorkspace {
     int cap_tokens = 0, B = 0, cap = 0, max_splits = 0;
     __nv_bfloat16 *xb = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr;
     float* part_o = nullptr;   // [T][heads][max_splits][hd]
     float* part_ml = nullptr;  // [T][heads][max_splits][2]
-    SampleSeg* segs = nullptr; // [B]
-    int32_t* qidx = nullptr;   // [T]
-    int32_t* dT = nullptr;
     float* gemm_ws = nullptr;
     int* counters = nullptr;
     float* part_val = nullptr;
@@ -435,9 +428,6 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     f->act = walloc<__nv_bfloat16>(f, T * mm);
     f->part_o = walloc<float>(f, T * cfg.num_heads * max_splits * cfg.head_dim);
     f->part_ml = walloc<float>(f, T * cfg.num_heads * max_splits * 2);
-    f->segs = walloc<SampleSeg>(f, c.B);
-    f->qidx = walloc<int32_t>(f, T);
-    f->dT = walloc<int32_t>(f, 4);
     f->gemm_ws = walloc<float>(f, (size_t)2 * 148 * 256 * 256);
     f->counters = walloc<int>(f, 65536);
     CUDA_OK(cudaMemset(f->counters, 0, sizeof(int) * 65536));
@@ -453,41 +443,68 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
 
 }  // namespace
 
-// Host-side ragged descriptors for one chunk of planned tokens: per sample the
-// list of its query tokens (in stream order) and its visible KV extent.
-static void build_segments(const std::vector<Plan>& plans, int t0, int n, int B, std::vector<SampleSeg>& segs,
-                           std::vector<int32_t>& qidx) {
-    segs.assign(B, SampleSeg{0, 0, 0, 0});
-    std::vector<std::vector<int>> per(B);
-    for (int i = 0; i < n; ++i) per[plans[t0 + i].sample].push_back(i);
-    qidx.clear();
-    for (int s = 0; s < B; ++s) {
-        segs[s].q_start = (int)qidx.size();
-        segs[s].n_q = (int)per[s].size();
-        int kv = 0;
-        for (int i : per[s]) {
-            qidx.push_back(i);
-            kv = std::max(kv, plans[t0 + i].write_slot + 1);
-        }
-        segs[s].kv_len = kv;
-    }
+// ------------------------------------------------------------- profiling
+// Eager (non-graph) runs can time every launch with CUDA events on the
+// launching stream and charge it the ALGORITHMIC bytes it must move
+// (weights + activations + KV it reads/writes once).  bench.py reads this
+// to report the dominant kernel's achieved bandwidth.
+enum ProfKind { PK_QKV, PK_O, PK_FC, PK_PROJ, PK_LM, PK_ATTN, PK_ROW, PK_MISC, PK_N };
+struct ProfRec {
+    int kind;
+    cudaEvent_t a, b;
+};
+static bool g_prof = false;
+static std::vector<ProfRec> g_prof_pending;
+static double g_prof_acc[PK_N][3];  // launches, ms, bytes
+
+#define PROF(kind, ...)                                    \
+    do {                                                   \
+        if (g_prof) {                                      \
+            ProfRec r__{kind, nullptr, nullptr};           \
+            CUDA_OK(cudaEventCreate(&r__.a));              \
+            CUDA_OK(cudaEventCreate(&r__.b));              \
+            CUDA_OK(cudaEventRecord(r__.a, st));           \
+            __VA_ARGS__;                                   \
+            CUDA_OK(cudaEventRecord(r__.b, st));           \
+            g_prof_pending.push_back(r__);                 \
+        } else {                                           \
+            __VA_ARGS__;                                   \
+        }                                                  \
+    } while (0)
+
+void profile_enable(bool on) {
+    g_prof = on;
+    if (on)
+        for (auto& r : g_prof_acc) r[0] = r[1] = r[2] = 0.0;
+}
+void profile_read(double* out, int kinds) {
+    for (int k = 0; k < kinds && k < PK_N; ++k)
+        for (int j = 0; j < 3; ++j) out[k * 3 + j] = g_prof_acc[k][j];
 }
 
-void forward_fast_chunk(const Model& m, Cache& c, Workspace& ws, FastWorkspace* f, int t0, int n,
-                        const std::vector<Plan>& plans, bool want_logits, cudaStream_t st) {
+// One-time kernel attributes (must run before any CUDA-graph capture).
+void prepare_fast_kernels() {
+    static bool done = false;
+    if (done) return;
+    CUDA_OK(cudaFuncSetAttribute(k_attention<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CUDA_OK(cudaFuncSetAttribute(k_attention<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    gemm_prepare();
+    done = true;
+}
+
+// Forward over a device-described batch of <= 256 tokens: tokens / plans in
+// ws.d_tokens / ws.d_plans (offset t0), ragged descriptors in `db`.  Every
+// launch has a fixed grid sized from the host-side upper bounds and reads
+// the true token count from device memory, so the sequence is CUDA-graph
+// capturable.
+void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch& db, int t0, bool want_logits,
+                      cudaStream_t st) {
+    prepare_fast_kernels();
+    FastWorkspace* f = ensure_fast(m, c, ws);
     const Config& cfg = m.cfg;
     const int h = cfg.hidden(), mm = cfg.mlp(), heads = cfg.num_heads, hd = cfg.head_dim;
-    std::vector<SampleSeg> segs;
-    std::vector<int32_t> qidx;
-    build_segments(plans, t0, n, c.B, segs, qidx);
-    CUDA_OK(cudaMemcpyAsync(f->segs, segs.data(), sizeof(SampleSeg) * c.B, cudaMemcpyHostToDevice, st));
-    CUDA_OK(cudaMemcpyAsync(f->qidx, qidx.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
-    CUDA_OK(cudaMemcpyAsync(f->dT, &n, sizeof(int), cudaMemcpyHostToDevice, st));
-    int max_kv = 0, max_q = 0;
-    for (auto& sg : segs) {
-        max_kv = std::max(max_kv, sg.kv_len);
-        max_q = std::max(max_q, sg.n_q);
-    }
+    const int n = db.T_upper;
+    SD_CHECK(n <= kChunkTokens, INTERNAL, "device batch larger than one forward chunk");
     const int32_t* tokens = ws.d_tokens + t0;
     const Plan* dplans = ws.d_plans + t0;
     float* resid = ws.d_resid + (size_t)t0 * h;
@@ -496,7 +513,7 @@ void forward_fast_chunk(const Model& m, Cache& c, Workspace& ws, FastWorkspace* 
 
     GemmArgs base{};
     base.T = n;
-    base.dT = f->dT;
+    base.dT = db.dT;
     base.ws = f->gemm_ws;
     base.counters = f->counters;
     base.h = h;
@@ -507,15 +524,16 @@ void forward_fast_chunk(const Model& m, Cache& c, Workspace& ws, FastWorkspace* 
     base.plans = dplans;
     base.kv = (__nv_bfloat16*)c.kv;
 
-    k_embed_ln<<<n, kRowThreads, 0, st>>>((const __nv_bfloat16*)m.tok16, (const __nv_bfloat16*)m.pos16, tokens,
-                                          dplans, h, resid, m.layers[0].ln1_g, m.layers[0].ln1_b, f->xb, f->dT);
+    PROF(PK_ROW, k_embed_ln<<<n, kRowThreads, 0, st>>>((const __nv_bfloat16*)m.tok16, (const __nv_bfloat16*)m.pos16,
+                                                       tokens, dplans, h, resid, m.layers[0].ln1_g,
+                                                       m.layers[0].ln1_b, f->xb, db.dT));
     launches++;
     AttnArgs at{};
     at.q = f->q;
     at.kv = (const __nv_bfloat16*)c.kv;
     at.plans = dplans;
-    at.segs = f->segs;
-    at.qidx = f->qidx;
+    at.segs = db.segs;
+    at.qidx = db.qidx;
     at.pad = c.layout == PADDED ? c.d_pad : nullptr;
     at.ctx = f->ctx;
     at.part_o = f->part_o;
@@ -526,8 +544,8 @@ void forward_fast_chunk(const Model& m, Cache& c, Workspace& ws, FastWorkspace* 
     at.cap = c.cap;
     at.max_splits = f->max_splits;
     at.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-    const int splits = (max_kv + kKeysPerCta - 1) / kKeysPerCta;
-    const int qtiles = (max_q + 15) / 16;
+    const int splits = std::max(1, (db.max_kv_upper + kKeysPerCta - 1) / kKeysPerCta);
+    const int qtiles = std::max(1, (db.max_q_upper + 15) / 16);
     const size_t attn_smem = (size_t)16 * hd * 2 + 4 * 2 * 64 * hd * 2 + (4 * 16 * hd + 4 * 32) * 4;
 
     for (int l = 0; l < cfg.num_layers; ++l) {
@@ -543,27 +561,16 @@ void forward_fast_chunk(const Model& m, Cache& c, Workspace& ws, FastWorkspace* 
         g.layer = l;
         GemmMaps mp = f->map_xb;
         mp.A = fm->qkv[l].A;
-        gemm_launch(EPI_QKV, g, mp, gemm_grid(g, n, sms), st);
+        PROF(PK_QKV, gemm_launch(EPI_QKV, g, mp, gemm_grid(g, n, sms), st));
         // attention
         at.layer = l;
-        if (hd == 128) {
-            static bool cfg128 = false;
-            if (!cfg128) {
-                CUDA_OK(cudaFuncSetAttribute(k_attention<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-                cfg128 = true;
-            }
-            k_attention<128><<<dim3(c.B * heads, splits, qtiles), 128, attn_smem, st>>>(at);
-        } else {
-            static bool cfg64 = false;
-            if (!cfg64) {
-                CUDA_OK(cudaFuncSetAttribute(k_attention<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-                cfg64 = true;
-            }
-            k_attention<64><<<dim3(c.B * heads, splits, qtiles), 128, attn_smem, st>>>(at);
-        }
+        if (hd == 128)
+            PROF(PK_ATTN, k_attention<128><<<dim3(c.B * heads, splits, qtiles), 128, attn_smem, st>>>(at));
+        else
+            PROF(PK_ATTN, k_attention<64><<<dim3(c.B * heads, splits, qtiles), 128, attn_smem, st>>>(at));
         launches++;
         if (splits > 1) {
-            k_attn_combine<<<dim3(n, heads), hd, 0, st>>>(at, hd, f->dT);
+            PROF(PK_ATTN, k_attn_combine<<<dim3(n, heads), hd, 0, st>>>(at, hd, db.dT));
             launches++;
         }
         // O projection + residual
@@ -576,8 +583,8 @@ void forward_fast_chunk(const Model& m, Cache& c, Workspace& ws, FastWorkspace* 
         g.ld_out = h;
         mp = f->map_ctx;
         mp.A = fm->o[l].A;
-        gemm_launch(EPI_RESID, g, mp, gemm_grid(g, n, sms), st);
-        k_layernorm<<<n, kRowThreads, 0, st>>>(resid, L.ln2_g, L.ln2_b, h, f->xb, f->dT);
+        PROF(PK_O, gemm_launch(EPI_RESID, g, mp, gemm_grid(g, n, sms), st));
+        PROF(PK_ROW, k_layernorm<<<n, kRowThreads, 0, st>>>(resid, L.ln2_g, L.ln2_b, h, f->xb, db.dT));
         // FC + GELU
         g = base;
         g.M = mm;
@@ -588,7 +595,7 @@ void forward_fast_chunk(const Model& m, Cache& c, Workspace& ws, FastWorkspace* 
         g.ld_out = mm;
         mp = f->map_xb;
         mp.A = fm->fc[l].A;
-        gemm_launch(EPI_GELU, g, mp, gemm_grid(g, n, sms), st);
+        PROF(PK_FC, gemm_launch(EPI_GELU, g, mp, gemm_grid(g, n, sms), st));
         // PROJ + residual
         g = base;
         g.M = h;
@@ -599,11 +606,11 @@ void forward_fast_chunk(const Model& m, Cache& c, Workspace& ws, FastWorkspace* 
         g.ld_out = h;
         mp = f->map_act;
         mp.A = fm->proj[l].A;
-        gemm_launch(EPI_RESID, g, mp, gemm_grid(g, n, sms), st);
+        PROF(PK_PROJ, gemm_launch(EPI_RESID, g, mp, gemm_grid(g, n, sms), st));
         // next LN1 or the final LN
         const float* lg = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_g : m.lnf_g;
         const float* lb = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_b : m.lnf_b;
-        k_layernorm<<<n, kRowThreads, 0, st>>>(resid, lg, lb, h, f->xb, f->dT);
+        PROF(PK_ROW, k_layernorm<<<n, kRowThreads, 0, st>>>(resid, lg, lb, h, f->xb, db.dT));
         launches += 6;
     }
     // LM head + argmax
@@ -619,22 +626,76 @@ void forward_fast_chunk(const Model& m, Cache& c, Workspace& ws, FastWorkspace* 
     g.flag = ws.d_flag;
     GemmMaps mp = f->map_xb;
     mp.A = m.fast->lm.A;
-    gemm_launch(EPI_ARGMAX, g, mp, gemm_grid(g, n, sms), st);
-    k_argmax_reduce<<<(n + 127) / 128, 128, 0, st>>>(f->part_val, f->part_idx, g.m_tiles, kChunkTokens,
-                                                     ws.d_argmax + t0, f->dT);
+    PROF(PK_LM, gemm_launch(EPI_ARGMAX, g, mp, gemm_grid(g, n, sms), st));
+    PROF(PK_MISC, k_argmax_reduce<<<(n + 127) / 128, 128, 0, st>>>(f->part_val, f->part_idx, g.m_tiles,
+                                                                   kChunkTokens, ws.d_argmax + t0, db.dT));
     launches += 2;
     note_launches(launches);
     CUDA_OK(cudaGetLastError());
+    if (g_prof) {  // charge every timed launch its algorithmic bytes
+        CUDA_OK(cudaStreamSynchronize(st));
+        int T = 0;
+        CUDA_OK(cudaMemcpy(&T, db.dT, 4, cudaMemcpyDeviceToHost));
+        std::vector<SampleSeg> segs(c.B);
+        CUDA_OK(cudaMemcpy(segs.data(), db.segs, sizeof(SampleSeg) * c.B, cudaMemcpyDeviceToHost));
+        double kv = 0;
+        for (auto& sg : segs) kv += (double)sg.kv_len * (sg.n_q > 0);
+        const double H = h, Mm = mm, Tt = T, V = cfg.vocab_size;
+        double bytes[PK_N] = {3 * H * H * 2 + Tt * H * 2 + Tt * 3 * H * 2,
+                              H * H * 2 + Tt * H * 2 + Tt * H * 8,
+                              Mm * H * 2 + Tt * H * 2 + Tt * Mm * 2,
+                              H * Mm * 2 + Tt * Mm * 2 + Tt * H * 8,
+                              V * H * 2 + Tt * H * 2,
+                              kv * 2 * hd * 2 * heads + Tt * H * 4,
+                              Tt * H * 6,
+                              0};
+        for (auto& r : g_prof_pending) {
+            float ms = 0.0f;
+            CUDA_OK(cudaEventElapsedTime(&ms, r.a, r.b));
+            g_prof_acc[r.kind][0] += 1;
+            g_prof_acc[r.kind][1] += ms;
+            // attention bytes are charged once per layer (combine adds none)
+            bool combine = r.kind == PK_ATTN && (&r != &g_prof_pending.front()) && (&r - 1)->kind == PK_ATTN;
+            g_prof_acc[r.kind][2] += combine ? 0.0 : bytes[r.kind];
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        g_prof_pending.clear();
+    }
 }
 
+// Forward over host-known plans (any T): chunks of <= 256 tokens with ragged
+// descriptors built on the host.  Chunking is exact because each sample's
+// tokens carry increasing slots and every token only attends to slots <= its
+// own, all of which an earlier chunk (or this one) has already written.
 void forward_fast(const Model& m, Cache& c, Workspace& ws, int T, bool want_logits, cudaStream_t st) {
-    FastWorkspace* f = ensure_fast(m, c, ws);
-    // the plans are needed on the host for the ragged descriptors
     std::vector<Plan> plans(T);
     CUDA_OK(cudaMemcpyAsync(plans.data(), ws.d_plans, sizeof(Plan) * T, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
-    for (int t0 = 0; t0 < T; t0 += kChunkTokens)
-        forward_fast_chunk(m, c, ws, f, t0, std::min(kChunkTokens, T - t0), plans, want_logits, st);
+    for (int t0 = 0; t0 < T; t0 += kChunkTokens) {
+        int n = std::min(kChunkTokens, T - t0);
+        std::vector<SampleSeg> segs(c.B, SampleSeg{0, 0, 0, 0});
+        std::vector<std::vector<int>> per(c.B);
+        for (int i = 0; i < n; ++i) per[plans[t0 + i].sample].push_back(i);
+        std::vector<int32_t> qidx;
+        int max_kv = 0, max_q = 0;
+        for (int s = 0; s < c.B; ++s) {
+            segs[s].q_start = (int)qidx.size();
+            segs[s].n_q = (int)per[s].size();
+            for (int i : per[s]) {
+                qidx.push_back(i);
+                segs[s].kv_len = std::max(segs[s].kv_len, plans[t0 + i].write_slot + 1);
+            }
+            max_kv = std::max(max_kv, segs[s].kv_len);
+            max_q = std::max(max_q, segs[s].n_q);
+        }
+        CUDA_OK(cudaMemcpyAsync(ws.d_segs, segs.data(), sizeof(SampleSeg) * c.B, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(ws.d_qidx, qidx.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(ws.d_T, &n, sizeof(int), cudaMemcpyHostToDevice, st));
+        DeviceBatch db{ws.d_segs, ws.d_qidx, ws.d_T, n, max_kv, max_q};
+        forward_fast_dev(m, c, ws, db, t0, want_logits, st);
+        CUDA_OK(cudaStreamSynchronize(st));  // host vectors above are reused per chunk
+    }
 }
 
 }  // namespace sdb

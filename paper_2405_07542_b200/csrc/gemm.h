@@ -39,6 +39,7 @@ struct GemmMaps {
 CUtensorMap make_tmap_2d(const void* base, int64_t rows, int64_t cols, int box_rows);
 void make_b_maps(GemmMaps& maps, const void* x, int64_t rows, int64_t cols);
 int gemm_grid(const GemmArgs& a, int T_upper, int sms);
+void gemm_prepare();  // one-time kernel attributes (before any graph capture)
 void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int grid, cudaStream_t st);
 
 }  // namespace sdb

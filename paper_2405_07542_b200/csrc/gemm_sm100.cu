@@ -374,6 +374,14 @@ void make_b_maps(GemmMaps& maps, const void* x, int64_t rows, int64_t cols) {
     for (int i = 0; i < 4; ++i) maps.B[i] = make_tmap_2d(x, rows, cols, boxes[i]);
 }
 
+void gemm_prepare() {
+    CUDA_OK(cudaFuncSetAttribute(k_gemm<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    CUDA_OK(cudaFuncSetAttribute(k_gemm<EPI_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    CUDA_OK(cudaFuncSetAttribute(k_gemm<EPI_GELU>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    CUDA_OK(cudaFuncSetAttribute(k_gemm<EPI_QKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    CUDA_OK(cudaFuncSetAttribute(k_gemm<EPI_ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+}
+
 int gemm_grid(const GemmArgs& a, int T_upper, int sms) {
     long long n_tiles = (T_upper + 255) / 256;
     long long U = (long long)a.m_tiles * n_tiles * (a.K / kBK);

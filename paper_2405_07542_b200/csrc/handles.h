@@ -57,11 +57,17 @@ int decode_impl(const sd_engine_config& e, sd_model* target, sd_model* draft, co
                 const int32_t* prompt_lens, int32_t* gen_tokens, int32_t* gen_counts, int32_t* rec,
                 int64_t rec_cap, int64_t* n_rec, int64_t* ledger, double* timing);
 void reset_cache(sd_cache* c);  // back to an empty arena (fresh-cache semantics)
+std::vector<int32_t> retrieval_predict(const std::vector<int32_t>& ctx, int match_len, int copy_len);
 
 sd_model* create_model(const Config& cfg, int device, int precision, const float* host_weights);
 sd_cache* create_cache(sd_model* m, int batch, int capacity, int layout);
 
 // forward for the bf16 performance mode (fast_kernels.cu)
 void forward_fast(const Model& m, Cache& c, Workspace& ws, int T, bool want_logits, cudaStream_t st);
+void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch& db, int t0, bool want_logits,
+                      cudaStream_t st);
+void prepare_fast_kernels();
+void profile_enable(bool on);
+void profile_read(double* out, int kinds);
 
 }  // namespace sdb

@@ -6,19 +6,33 @@ namespace sdb {
 
 struct StepArgs {
     int B, cap, layout, stop_on_eos, acc_stride;
-    // inputs
-    const int32_t* last;     // [B]
-    const int32_t* counts;   // [B] draft counts k_s
-    const int32_t* drafts;   // concatenated drafts
-    const int32_t* budget;   // [B] max_new_tokens - generated
-    const int32_t* active;   // [B]
-    // cache descriptors (mutated by k_accept)
+    // inputs (host-driven step) ----------------------------------------------
+    const int32_t* last;     // [B] tokens.back(); null in device mode (read from ctx)
+    int32_t* counts;         // [B] draft counts k_s (written by the device predictor)
+    int32_t* drafts;         // host mode: concatenated; device mode: [B][kcap]
+    int draft_stride;        // 0 = concatenated (host mode), else per-sample stride
+    const int32_t* budget;   // [B] max_new_tokens - generated; null in device mode
+    int32_t* active;         // [B]
+    // device-resident loop state (null in the host-driven step) --------------
+    int32_t* ctx;            // [B][ctx_cap] prompt + generated tokens
+    int32_t* ctx_len;        // [B]
+    int ctx_cap;
+    int32_t* gen;            // [B] tokens generated so far
+    int max_new;
+    int32_t* n_active;       // scalar: samples still active after this step
+    int32_t* log_k;          // [max_steps][B] step records (or null)
+    int32_t* log_tau;
+    int32_t* step;           // scalar step counter
+    int max_steps;
+    // cache descriptors (mutated by k_accept) --------------------------------
     int32_t* committed;      // [B]
     int32_t* logical;        // [B]
     uint8_t* pad;            // [B*cap] or null (unpad)
-    // pack outputs / scratch
+    // pack outputs / scratch -------------------------------------------------
     int32_t* tokens;         // [T_max]
     Plan* plans;             // [T_max]
+    SampleSeg* segs;         // [B]
+    int32_t* qidx;           // [T_max]
     int32_t* first_row;      // [B]
     int32_t* draft_off;      // [B]
     int32_t* scalars;        // [0]=T [1]=k_max [2]=grid base [3]=tau_max
@@ -30,8 +44,19 @@ struct StepArgs {
     int32_t* clipped;        // [B]
 };
 
+// Device predictors for the resident loop (predictors.cpp:39-72 on device).
+struct PredictArgs {
+    int kind;                // 1 retrieval (LLMA prompt lookup), 2 synthetic trajectory
+    int match_len, copy_len, k, vocab;
+    uint64_t seed;
+    double accuracy;
+    const int32_t* traj;     // [B][traj_stride] greedy continuation (synthetic)
+    int traj_stride;
+};
+
 void launch_pack(const StepArgs& a, cudaStream_t st);
 void launch_accept(const StepArgs& a, cudaStream_t st);
 void launch_pad_fill(const StepArgs& a, const Cache& c, cudaStream_t st);
+void launch_predict(const StepArgs& a, const PredictArgs& p, cudaStream_t st);
 
 }  // namespace sdb

@@ -106,6 +106,18 @@ def lib() -> C.CDLL:
         "sd_verify_step": ([vp, vp, I32P, I32P, I32P, I32P, I32P, C.c_int, I32P, I32P, I32P, vp], C.c_int),
         "sd_decode": ([C.POINTER(_EngineConfigT), vp, vp, I32P, I32P, I32P, I32P, I32P, C.c_int64,
                        C.POINTER(C.c_int64), I64P, np.ctypeslib.ndpointer(np.float64)], C.c_int),
+        "sd_profile_enable": ([C.c_int], C.c_int),
+        "sd_profile_read": ([np.ctypeslib.ndpointer(np.float64), C.c_int], C.c_int),
+        "sd_session_last_error": ([], C.c_char_p),
+        "sd_session_create": ([vp, C.POINTER(_EngineConfigT), C.c_int, pp], C.c_int),
+        "sd_session_prefill": ([vp, I32P, I32P], C.c_int),
+        "sd_session_set_trajectory": ([vp, I32P, C.c_int], C.c_int),
+        "sd_session_reset": ([vp], C.c_int),
+        "sd_session_run": ([vp, C.c_int, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_float)], C.c_int),
+        "sd_session_run_host": ([vp, C.POINTER(C.c_int32), C.POINTER(C.c_float), C.POINTER(C.c_int64),
+                                 C.POINTER(C.c_int64)], C.c_int),
+        "sd_session_outputs": ([vp, I32P, I32P, vp, vp, C.c_int], C.c_int),
+        "sd_session_destroy": ([vp], None),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -504,3 +516,77 @@ def step_records(rows: np.ndarray) -> list[dict]:
             tau_max=tmax,
         ))
     return out
+
+
+# ---------------------------------------------------------------- sessions
+PROFILE_KINDS = ["gemm_qkv", "gemm_o", "gemm_fc", "gemm_proj", "gemm_lm", "attention", "layernorm", "misc"]
+
+
+def profile_enable(on: bool) -> None:
+    _check(lib().sd_profile_enable(int(on)))
+
+
+def profile_read() -> dict:
+    out = np.zeros(len(PROFILE_KINDS) * 3, dtype=np.float64)
+    _check(lib().sd_profile_read(out, len(PROFILE_KINDS)))
+    out = out.reshape(-1, 3)
+    return {k: dict(launches=int(r[0]), ms=float(r[1]), bytes=float(r[2])) for k, r in zip(PROFILE_KINDS, out)}
+
+
+def _scheck(rc: int) -> None:
+    if rc != 0:
+        raise _ERRORS.get(rc, SpecdecError)(lib().sd_session_last_error().decode())
+
+
+class Session:
+    """A prefilled batch whose decode loop (engine.cpp:391-489) runs on the GPU."""
+
+    def __init__(self, model: Model, config: EngineConfig, capacity: int):
+        h = C.c_void_p()
+        _scheck(lib().sd_session_create(model._h, C.byref(config._c()), capacity, C.byref(h)))
+        self._h = h.value
+        self.model = model
+        self.config = config
+
+    def close(self):
+        if self._h:
+            lib().sd_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def prefill(self, prompts) -> None:
+        flat = _i32([t for p in prompts for t in p])
+        _scheck(lib().sd_session_prefill(self._h, flat, _i32([len(p) for p in prompts])))
+
+    def set_trajectory(self, traj: np.ndarray) -> None:
+        traj = np.ascontiguousarray(traj, dtype=np.int32)
+        _scheck(lib().sd_session_set_trajectory(self._h, traj.reshape(-1), traj.shape[1]))
+
+    def reset(self) -> None:
+        _scheck(lib().sd_session_reset(self._h))
+
+    def run(self, use_graph: bool = True, graph_steps: int = 8):
+        steps, ms = C.c_int32(), C.c_float()
+        _scheck(lib().sd_session_run(self._h, int(use_graph), graph_steps, C.byref(steps), C.byref(ms)))
+        return steps.value, ms.value
+
+    def run_host(self):
+        steps, ms, h2d, d2h = C.c_int32(), C.c_float(), C.c_int64(), C.c_int64()
+        _scheck(lib().sd_session_run_host(self._h, C.byref(steps), C.byref(ms), C.byref(h2d), C.byref(d2h)))
+        return steps.value, ms.value, h2d.value, d2h.value
+
+    def outputs(self):
+        B, mx = self.config.batch_size, self.config.max_new_tokens
+        gen = np.zeros(B * mx, dtype=np.int32)
+        cnt = np.zeros(B, dtype=np.int32)
+        steps = mx + 2
+        lk = np.zeros(steps * B, dtype=np.int32)
+        lt = np.zeros(steps * B, dtype=np.int32)
+        _scheck(lib().sd_session_outputs(self._h, gen, cnt, lk.ctypes.data, lt.ctypes.data, steps))
+        tokens = [gen[s * mx: s * mx + min(cnt[s], mx)].tolist() for s in range(B)]
+        return tokens, lk.reshape(steps, B), lt.reshape(steps, B)

@@ -126,3 +126,49 @@ def test_bf16_decode_agrees_with_oracle(sd, oracle, mode):
                                    copy_len=7, batch_size=B, max_new_tokens=48, stop_on_eos=False), m, prompts)
     same = np.mean([a == b for a, b in zip(r.generated_tokens, r2.generated_tokens)])
     print(f"{mode}: vanilla/ems identical streams fraction {same:.2f}")
+
+
+@pytest.mark.parametrize("mode", ["ems", "vanilla"])
+@pytest.mark.parametrize("predictor", ["retrieval", "synthetic"])
+def test_device_loop_equals_host_loop_and_engine(sd, mode, predictor):
+    """The device-resident session loop (device predictor + graph replay), the
+    host-driven sd_verify_step loop and the sd_decode engine produce the same
+    token streams and step records; reset() replays identically."""
+    cfg = dict(num_layers=2, num_heads=4, head_dim=128, vocab_size=700, max_positions=512, init_seed=0x5E55)
+    rng = np.random.default_rng(11)
+    B, new = 5, 40
+    # repetitive prompts so the LLMA predictor actually drafts
+    base = rng.integers(3, 700, size=12).tolist()
+    prompts = [[0] + (base * 6)[: int(rng.integers(30, 70))] for _ in range(B)]
+    m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.BF16)
+    e = sd.EngineConfig(mode=mode, predictor=predictor, k=5, copy_len=5, batch_size=B, max_new_tokens=new,
+                        stop_on_eos=False, seed=9, synthetic_accuracy=0.7)
+    s = sd.Session(m, e, 512)
+    s.prefill(prompts)
+    if predictor == "synthetic":
+        g = sd.decode(sd.EngineConfig(mode="greedy", batch_size=B, max_new_tokens=new + 6, stop_on_eos=False), m,
+                      prompts)
+        s.set_trajectory(np.array(g.generated_tokens, np.int32))
+    steps, ms = s.run(use_graph=True, graph_steps=4)
+    toks_dev, lk, lt = s.outputs()
+    s.reset()
+    s.run(use_graph=False)
+    toks_dev2, lk2, lt2 = s.outputs()
+    assert toks_dev == toks_dev2 and (lt == lt2).all() and (lk == lk2).all()
+    s.reset()
+    hsteps, _, h2d, d2h = s.run_host()
+    toks_host, _, _ = s.outputs()
+    assert toks_host == toks_dev
+    assert hsteps == steps and h2d > 0 and d2h > 0
+    assert all(len(t) == new for t in toks_dev)
+    if predictor == "retrieval":
+        r = sd.decode(e, m, prompts)
+        assert r.generated_tokens == toks_dev
+        ks = [x["k"] for st in r.steps for x in st["samples"]]
+        taus = [x["tau"] for st in r.steps for x in st["samples"]]
+        act = lk[:steps] >= 0
+        assert ks == lk[:steps][act].tolist() and taus == (lt[:steps][act] & 0xFFFF).tolist()
+        assert max(taus) > 1  # drafts were accepted
+    # greedy losslessness inside the bf16 model
+    g = sd.decode(sd.EngineConfig(mode="greedy", batch_size=B, max_new_tokens=new, stop_on_eos=False), m, prompts)
+    assert g.generated_tokens == toks_dev
