@@ -22,6 +22,7 @@ namespace sdb {
 
 constexpr int kChunkTokens = 256;  // tokens per forward chunk (GEMM N <= 256)
 constexpr int kKeysPerCta = 256;   // attention split size (4 warps x 64 keys)
+constexpr int kSms = 148;          // B200 SM count (stream-K GEMM grid)
 
 struct FastModelState {
     std::vector<GemmMaps> qkv, o, fc, proj;  // per layer (A map only used)
@@ -33,10 +34,7 @@ struct FastWorkspace {
     __nv_bfloat16 *xb = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr;
     float* part_o = nullptr;   // [T][heads][max_splits][hd]
     float* part_ml = nullptr;  // [T][heads][max_splits][2]
-    float* gemm_ws = nullptr;
-    int* counters = nullptr;
-    float* part_val = nullptr;
-    int* part_idx = nullptr;
+    float* part = nullptr;     // stream-K partial sums (largest GEMM of the model)
     GemmMaps map_xb, map_ctx, map_act;
     std::vector<void*> allocs;
 };
@@ -428,12 +426,12 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     f->act = walloc<__nv_bfloat16>(f, T * mm);
     f->part_o = walloc<float>(f, T * cfg.num_heads * max_splits * cfg.head_dim);
     f->part_ml = walloc<float>(f, T * cfg.num_heads * max_splits * 2);
-    f->gemm_ws = walloc<float>(f, (size_t)2 * 148 * 256 * 256);
-    f->counters = walloc<int>(f, 65536);
-    CUDA_OK(cudaMemset(f->counters, 0, sizeof(int) * 65536));
-    int m_tiles_lm = m.vocab_pad / 256;
-    f->part_val = walloc<float>(f, (size_t)m_tiles_lm * T);
-    f->part_idx = walloc<int>(f, (size_t)m_tiles_lm * T);
+    size_t part = 0;
+    for (auto mk : {std::make_pair((int)(3 * h), (int)h), std::make_pair((int)h, (int)h),
+                    std::make_pair((int)mm, (int)h), std::make_pair((int)h, (int)mm),
+                    std::make_pair(m.vocab_pad, (int)h)})
+        part = std::max(part, gemm_part_floats(mk.first, mk.second, kSms));
+    f->part = walloc<float>(f, part);
     make_b_maps(f->map_xb, f->xb, T, h);
     make_b_maps(f->map_ctx, f->ctx, T, h);
     make_b_maps(f->map_act, f->act, T, mm);
@@ -508,14 +506,12 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     const int32_t* tokens = ws.d_tokens + t0;
     const Plan* dplans = ws.d_plans + t0;
     float* resid = ws.d_resid + (size_t)t0 * h;
-    const int sms = 148;
     int64_t launches = 0;
 
     GemmArgs base{};
     base.T = n;
     base.dT = db.dT;
-    base.ws = f->gemm_ws;
-    base.counters = f->counters;
+    base.part = f->part;
     base.h = h;
     base.hd = hd;
     base.heads = heads;
@@ -551,7 +547,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     for (int l = 0; l < cfg.num_layers; ++l) {
         const FastLayer& L = m.layers[l];
         const FastModelState* fm = m.fast;
-        // QKV + scatter
+        // QKV + scatter (Q -> q16, K/V -> the arena at each token's write slot)
         GemmArgs g = base;
         g.M = 3 * h;
         g.K = h;
@@ -559,9 +555,10 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         g.bias = L.bqkv;
         g.out_bf16 = f->q;
         g.layer = l;
+        gemm_plan(g, kSms);
         GemmMaps mp = f->map_xb;
         mp.A = fm->qkv[l].A;
-        PROF(PK_QKV, gemm_launch(EPI_QKV, g, mp, gemm_grid(g, n, sms), st));
+        PROF(PK_QKV, gemm_launch(EPI_QKV, g, mp, n, st));
         // attention
         at.layer = l;
         if (hd == 128)
@@ -573,7 +570,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
             PROF(PK_ATTN, k_attn_combine<<<dim3(n, heads), hd, 0, st>>>(at, hd, db.dT));
             launches++;
         }
-        // O projection + residual
+        // O projection + residual, fused with LN2 -> xb
         g = base;
         g.M = h;
         g.K = h;
@@ -581,10 +578,13 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         g.bias = L.bo;
         g.out_f32 = resid;
         g.ld_out = h;
+        g.ln_g = L.ln2_g;
+        g.ln_b = L.ln2_b;
+        g.ln_out = f->xb;
+        gemm_plan(g, kSms);
         mp = f->map_ctx;
         mp.A = fm->o[l].A;
-        PROF(PK_O, gemm_launch(EPI_RESID, g, mp, gemm_grid(g, n, sms), st));
-        PROF(PK_ROW, k_layernorm<<<n, kRowThreads, 0, st>>>(resid, L.ln2_g, L.ln2_b, h, f->xb, db.dT));
+        PROF(PK_O, gemm_launch(EPI_RESID_LN, g, mp, n, st));
         // FC + GELU
         g = base;
         g.M = mm;
@@ -593,10 +593,11 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         g.bias = L.bfc;
         g.out_bf16 = f->act;
         g.ld_out = mm;
+        gemm_plan(g, kSms);
         mp = f->map_xb;
         mp.A = fm->fc[l].A;
-        PROF(PK_FC, gemm_launch(EPI_GELU, g, mp, gemm_grid(g, n, sms), st));
-        // PROJ + residual
+        PROF(PK_FC, gemm_launch(EPI_GELU, g, mp, n, st));
+        // PROJ + residual, fused with the next LN1 (or the final LN) -> xb
         g = base;
         g.M = h;
         g.K = mm;
@@ -604,31 +605,28 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         g.bias = L.bproj;
         g.out_f32 = resid;
         g.ld_out = h;
+        g.ln_g = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_g : m.lnf_g;
+        g.ln_b = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_b : m.lnf_b;
+        g.ln_out = f->xb;
+        gemm_plan(g, kSms);
         mp = f->map_act;
         mp.A = fm->proj[l].A;
-        PROF(PK_PROJ, gemm_launch(EPI_RESID, g, mp, gemm_grid(g, n, sms), st));
-        // next LN1 or the final LN
-        const float* lg = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_g : m.lnf_g;
-        const float* lb = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_b : m.lnf_b;
-        PROF(PK_ROW, k_layernorm<<<n, kRowThreads, 0, st>>>(resid, lg, lb, h, f->xb, db.dT));
-        launches += 6;
+        PROF(PK_PROJ, gemm_launch(EPI_RESID_LN, g, mp, n, st));
+        launches += 8;
     }
-    // LM head + argmax
+    // LM head + greedy argmax
     GemmArgs g = base;
     g.M = m.vocab_pad;
     g.K = h;
     g.m_tiles = m.vocab_pad / 256;
     g.vocab = cfg.vocab_size;
-    g.ld_part = kChunkTokens;
-    g.part_val = f->part_val;
-    g.part_idx = f->part_idx;
+    g.argmax = ws.d_argmax + t0;
     g.logits = want_logits ? ws.d_logits + (size_t)t0 * cfg.vocab_size : nullptr;
     g.flag = ws.d_flag;
+    gemm_plan(g, kSms);
     GemmMaps mp = f->map_xb;
     mp.A = m.fast->lm.A;
-    PROF(PK_LM, gemm_launch(EPI_ARGMAX, g, mp, gemm_grid(g, n, sms), st));
-    PROF(PK_MISC, k_argmax_reduce<<<(n + 127) / 128, 128, 0, st>>>(f->part_val, f->part_idx, g.m_tiles,
-                                                                   kChunkTokens, ws.d_argmax + t0, db.dT));
+    PROF(PK_LM, gemm_launch(EPI_ARGMAX, g, mp, n, st));
     launches += 2;
     note_launches(launches);
     CUDA_OK(cudaGetLastError());

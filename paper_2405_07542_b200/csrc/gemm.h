@@ -7,26 +7,34 @@
 
 namespace sdb {
 
-enum Epilogue { EPI_STORE = 0, EPI_RESID = 1, EPI_GELU = 2, EPI_QKV = 3, EPI_ARGMAX = 4 };
+// What the split-K reduction kernel does with the finished sums.
+enum Epilogue {
+    EPI_STORE = 0,    // out_f32[t][m] = y
+    EPI_RESID_LN = 1, // resid[t][m] += y + b; then LayerNorm(resid[t]) -> ln_out (bf16)
+    EPI_GELU = 2,     // out_bf16[t][m] = gelu(y + b)
+    EPI_QKV = 3,      // Q -> out_bf16, K/V -> KV arena at each token's write slot
+    EPI_ARGMAX = 4,   // argmax over the vocab (lowest id on ties) -> argmax[t]
+};
 
 struct GemmArgs {
-    int M, K, m_tiles;        // W is [M_pad][K] bf16, m_tiles = ceil(M / 256)
-    int T;                    // token count when dT == nullptr
+    int M, K, m_tiles;        // W is [m_tiles * 256][K] bf16 (zero-padded rows)
+    int T;                    // token count when dT == nullptr (must be <= 256)
     const int* dT;            // device token count (graph-capturable), or nullptr
-    float* ws;                // split-K partials: [2 * grid][256 cols][256 rows] fp32
-    int* counters;            // per-tile arrival counters (zeroed, self-resetting)
+    int grid, max_contrib;    // stream-K schedule (set by gemm_plan)
+    float* part;              // fp32 partial sums [m_tiles * max_contrib][256 tok][256 rows]
     const float* bias;        // [M] or nullptr
-    float* out_f32;           // EPI_STORE out / EPI_RESID residual stream
+    float* out_f32;           // EPI_STORE output / EPI_RESID_LN residual stream
     __nv_bfloat16* out_bf16;  // EPI_GELU activations / EPI_QKV queries
     int ld_out;
+    const float *ln_g, *ln_b; // EPI_RESID_LN
+    __nv_bfloat16* ln_out;
     // EPI_QKV scatter into the KV arena [L][2][B][heads][cap][hd]
     __nv_bfloat16* kv;
     const Plan* plans;
     int h, hd, heads, B, cap, layer;
     // EPI_ARGMAX (LM head)
-    int vocab, ld_part;
-    float* part_val;          // [m_tiles][ld_part]
-    int* part_idx;
+    int vocab;
+    int32_t* argmax;
     float* logits;            // optional [T][vocab]
     int* flag;                // non-finite flag
 };
@@ -38,8 +46,12 @@ struct GemmMaps {
 
 CUtensorMap make_tmap_2d(const void* base, int64_t rows, int64_t cols, int box_rows);
 void make_b_maps(GemmMaps& maps, const void* x, int64_t rows, int64_t cols);
-int gemm_grid(const GemmArgs& a, int T_upper, int sms);
+// fill a.grid / a.max_contrib for this shape on `sms` SMs
+void gemm_plan(GemmArgs& a, int sms);
+// floats the partial buffer needs for a shape (max over the model's GEMMs)
+size_t gemm_part_floats(int M, int K, int sms);
+// stream the weights (tcgen05 mainloop -> fp32 partials), then reduce + epilogue
+void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, cudaStream_t st);
 void gemm_prepare();  // one-time kernel attributes (before any graph capture)
-void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int grid, cudaStream_t st);
 
 }  // namespace sdb

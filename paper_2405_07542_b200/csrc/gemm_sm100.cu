@@ -3,22 +3,29 @@
 //   Y[t][m] = sum_k W[m][k] * X[t][k]       (W = weights [M][K], X = tokens [T][K])
 //
 // "Swap-AB": the weights are the 128-row UMMA A operand (M = output features)
-// and the T <= 256 packed tokens are the UMMA N dimension, so one CTA tile is
+// and the T <= 256 packed tokens are the UMMA N dimension, so a CTA tile is
 // 256 output features x N tokens held in TMEM as two 128-lane fp32
-// accumulators (512 columns).  Operands are staged by TMA with the 128-byte
-// swizzle into a multi-stage mbarrier ring; one thread issues tcgen05.mma.
+// accumulators.  Operands are staged by TMA with the 128-byte swizzle into a
+// multi-stage mbarrier ring and one thread issues tcgen05.mma.
 //
-// The problem is HBM-bound (every weight byte is read once per step), so the
-// schedule is stream-K: the m_tiles x n_tiles x (K/64) k-block units are split
-// evenly over the 148 SMs; a tile cut by a CTA boundary is reduced by its last
-// finishing contributor, in contributor order (deterministic), which then runs
-// the fused epilogue: bias, GELU, residual add, Q/K/V scatter into the
-// unpadded KV arena, or the LM-head (max, lowest id) argmax partials.
+// The GEMM is HBM-bound (every weight byte is read once per step), so the
+// schedule is stream-K: the m_tiles x (K/64) k-block units are split evenly
+// over the SMs and every CTA streams one contiguous range of weights.  Each
+// (tile, contributor) segment dumps its raw fp32 accumulator into a partial
+// buffer; a separate, fully parallel reduction kernel sums a tile's
+// contributors in fixed order (deterministic) and applies the fused epilogue:
+// bias + Q/K/V scatter into the unpadded KV arena, bias + GELU, bias +
+// residual + the NEXT LayerNorm, or the LM-head argmax (lowest id on ties).
+// No CTA ever waits for another one, and TMEM is double-buffered for N <= 128
+// so a segment's epilogue overlaps the next segment's MMAs.
 //
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer, w2 TMEM
 // allocator, w4-7 epilogue (TMEM lanes 0-127).
 #include <cuda_bf16.h>
 
+#include <string>
+
+#include "../../include/specdec_b200_debug.h"
 #include "gemm.h"
 #include "sm100_ptx.cuh"
 
@@ -27,15 +34,10 @@ namespace {
 
 constexpr int kBM = 256, kBK = 64, kThreads = 256;
 constexpr int kABytes = kBM * kBK * 2;  // 32 KB per stage
-constexpr int kRedBytes = 8 * 256 * 8;  // argmax cross-warp scratch
 constexpr int kSmemBytes = 226 * 1024;  // + static smem stays under the 227 KB opt-in limit
 constexpr int kMaxStages = 8;
 
-struct Seg {
-    int tile, kb0, kb1;
-};
-
-__device__ __forceinline__ int cta_of(long long x, long long G, long long U) {
+__host__ __device__ __forceinline__ int cta_of(long long x, long long G, long long U) {
     return (int)(((x + 1) * G - 1) / U);
 }
 
@@ -48,83 +50,6 @@ __device__ __forceinline__ float gelu_fast(float x) {
     return 0.5f * x * (1.0f + t);
 }
 
-template <int EPI>
-__device__ __forceinline__ void finalize_chunk(const GemmArgs& a, int T, int m_base, int n0, int j0, int acc,
-                                               int lane, int w, float (&v)[16], float* red_val, int* red_idx) {
-    const int m = m_base + acc * 128 + w * 32 + lane;
-    if constexpr (EPI == EPI_STORE) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            int j = n0 + j0 + i;
-            if (j < T && m < a.M) a.out_f32[(size_t)j * a.ld_out + m] = v[i];
-        }
-    } else if constexpr (EPI == EPI_RESID) {
-        float b = (m < a.M && a.bias) ? a.bias[m] : 0.0f;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            int j = n0 + j0 + i;
-            if (j < T && m < a.M) a.out_f32[(size_t)j * a.ld_out + m] += v[i] + b;
-        }
-    } else if constexpr (EPI == EPI_GELU) {
-        float b = (m < a.M && a.bias) ? a.bias[m] : 0.0f;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            int j = n0 + j0 + i;
-            if (j < T && m < a.M) a.out_bf16[(size_t)j * a.ld_out + m] = __float2bfloat16_rn(gelu_fast(v[i] + b));
-        }
-    } else if constexpr (EPI == EPI_QKV) {
-        if (m < a.M) {
-            float b = a.bias ? a.bias[m] : 0.0f;
-            int which = m / a.h, hm = m - which * a.h;
-            int head = hm / a.hd, d = hm - head * a.hd;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                int j = n0 + j0 + i;
-                if (j >= T) break;
-                __nv_bfloat16 x = __float2bfloat16_rn(v[i] + b);
-                if (which == 0) {
-                    a.out_bf16[(size_t)j * a.h + hm] = x;
-                } else {
-                    Plan pl = a.plans[j];
-                    if (pl.store) {
-                        size_t off = ((((size_t)a.layer * 2 + (which - 1)) * a.B + pl.sample) * a.heads + head) *
-                                         (size_t)a.cap * a.hd +
-                                     (size_t)pl.write_slot * a.hd + d;
-                        a.kv[off] = x;
-                    }
-                }
-            }
-        }
-    } else if constexpr (EPI == EPI_ARGMAX) {
-        const bool valid = m < a.vocab;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            int j = n0 + j0 + i;
-            float x = v[i];
-            if (valid && j < T) {
-                if (a.logits) a.logits[(size_t)j * a.vocab + m] = x;
-                if (!isfinite(x)) atomicExch(a.flag, 1);
-            }
-            float bv = valid ? x : -INFINITY;
-            int bi = valid ? m : 0x7fffffff;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-                int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-                if (ov > bv || (ov == bv && oi < bi)) {
-                    bv = ov;
-                    bi = oi;
-                }
-            }
-            if (lane == 0) {
-                red_val[(w * 2 + acc) * 256 + j0 + i] = bv;
-                red_idx[(w * 2 + acc) * 256 + j0 + i] = bi;
-            }
-        }
-    }
-}
-
-template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB32,
            const __grid_constant__ CUtensorMap tmB64, const __grid_constant__ CUtensorMap tmB128,
@@ -134,28 +59,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int T = a.dT ? *a.dT : a.T;
     if (T <= 0) return;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int n_tiles = (T + 255) / 256;
-    int BN = n_tiles > 1 ? 256 : ((T + 15) / 16) * 16;
+    const int BN = T <= 16 ? 16 : ((T + 15) / 16) * 16;
     const int box = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-    if (n_tiles == 1 && BN < 16) BN = 16;
     const CUtensorMap* tmB = box == 32 ? &tmB32 : box == 64 ? &tmB64 : box == 128 ? &tmB128 : &tmB256;
+    const int nbuf = BN <= 128 ? 2 : 1;  // TMEM accumulator buffers
     const int stage_bytes = kABytes + box * 128;
-    const int avail = kSmemBytes - 1024 - kRedBytes - 1024;
-    int S = avail / stage_bytes;
+    int S = (kSmemBytes - 2048) / stage_bytes;
     if (S > kMaxStages) S = kMaxStages;
     uint8_t* stage_base = smem;
-    float* red_val = (float*)(smem + S * stage_bytes);
-    int* red_idx = (int*)((uint8_t*)red_val + 8 * 256 * 4);  // [8][256] floats, then [8][256] ints
-    uint64_t* bars = (uint64_t*)((uint8_t*)red_val + kRedBytes);
+    uint64_t* bars = (uint64_t*)(smem + S * stage_bytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + kMaxStages;
-    uint64_t* tmem_full = bars + 2 * kMaxStages;
-    uint64_t* tmem_empty = tmem_full + 1;
-    uint32_t* tmem_slot = (uint32_t*)(tmem_empty + 1);
-    __shared__ int s_last;
+    uint64_t* tmem_full = bars + 2 * kMaxStages;  // [2]
+    uint64_t* tmem_empty = tmem_full + 2;          // [2]
+    uint32_t* tmem_slot = (uint32_t*)(tmem_empty + 2);
 
     const long long KB = a.K / kBK;
-    const long long U = (long long)a.m_tiles * n_tiles * KB;
+    const long long U = (long long)a.m_tiles * KB;
     const long long G = gridDim.x;
     const long long u0 = (long long)blockIdx.x * U / G, u1 = (long long)(blockIdx.x + 1) * U / G;
 
@@ -166,8 +86,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
         }
-        ptx::mbar_init(tmem_full, 1);
-        ptx::mbar_init(tmem_empty, 128);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&tmem_full[b], 1);
+            ptx::mbar_init(&tmem_empty[b], 128);
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
@@ -177,27 +99,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer
+        if (lane == 0) {  // ---------------- TMA producer: one contiguous weight range
             const uint64_t pol_w = ptx::policy_evict_first();  // weights: streamed once
             const uint64_t pol_x = ptx::policy_evict_last();   // tokens: re-read by every tile
             int stage = 0;
             uint32_t phase = 0;
-            for (long long u = u0; u < u1;) {
-                int tile = (int)(u / KB), kb0 = (int)(u % KB);
-                int kb1 = (int)min((long long)KB, kb0 + (u1 - u));
-                int m0 = (tile % a.m_tiles) * kBM, n0 = (tile / a.m_tiles) * 256;
-                for (int kb = kb0; kb < kb1; ++kb) {
-                    ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* sa = stage_base + stage * stage_bytes;
-                    ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes);
-                    ptx::tma_load_2d(sa, &tmA, &full[stage], kb * kBK, m0, pol_w);
-                    ptx::tma_load_2d(sa + kABytes, tmB, &full[stage], kb * kBK, n0, pol_x);
-                    if (++stage == S) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+            for (long long u = u0; u < u1; ++u) {
+                int tile = (int)(u / KB), kb = (int)(u % KB);
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* sa = stage_base + stage * stage_bytes;
+                ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes);
+                ptx::tma_load_2d(sa, &tmA, &full[stage], kb * kBK, tile * kBM, pol_w);
+                ptx::tma_load_2d(sa + kABytes, tmB, &full[stage], kb * kBK, 0, pol_x);
+                if (++stage == S) {
+                    stage = 0;
+                    phase ^= 1;
                 }
-                u += kb1 - kb0;
             }
         }
     } else if (warp == 1) {
@@ -208,8 +125,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (long long u = u0; u < u1; ++seg) {
                 int kb0 = (int)(u % KB);
                 int kb1 = (int)min((long long)KB, kb0 + (u1 - u));
-                ptx::mbar_wait(tmem_empty, (seg & 1) ^ 1);
+                const int buf = nbuf == 2 ? (int)(seg & 1) : 0;
+                const uint32_t use = nbuf == 2 ? seg >> 1 : seg;
+                ptx::mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);
                 ptx::tc_fence_after();
+                const uint32_t d0 = tmem + (nbuf == 2 ? buf * 256 : 0);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
@@ -221,7 +141,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int acc = 0; acc < 2; ++acc) {
                             uint64_t adesc = ptx::umma_desc_kmajor_sw128(sa + acc * (128 * 128) + k * 32);
-                            ptx::umma_bf16(tmem + acc * 256, adesc, bdesc, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                            ptx::umma_bf16(d0 + acc * (nbuf == 2 ? 128 : 256), adesc, bdesc, idesc,
+                                           (kb > kb0 || k > 0) ? 1u : 0u);
                         }
                     }
                     ptx::umma_commit(&empty[stage]);
@@ -230,101 +151,181 @@ __global__ void __launch_bounds__(kThreads, 1)
                         phase ^= 1;
                     }
                 }
-                ptx::umma_commit(tmem_full);
+                ptx::umma_commit(&tmem_full[buf]);
                 u += kb1 - kb0;
             }
         }
-    } else if (warp >= 4) {  // ---------------- epilogue
+    } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> fp32 partials
         const int w = warp - 4;
-        const int et = threadIdx.x - 128;  // 0..127
+        const int row_in_acc = w * 32 + lane;
+        const int ncols = BN;
         uint32_t seg = 0;
         for (long long u = u0; u < u1; ++seg) {
             int tile = (int)(u / KB), kb0 = (int)(u % KB);
             int kb1 = (int)min((long long)KB, kb0 + (u1 - u));
-            int m_tile = tile % a.m_tiles, n_tile = tile / a.m_tiles;
-            int m_base = m_tile * kBM, n0 = n_tile * 256;
-            int ncols = min(BN, ((T - n0 + 15) / 16) * 16);
-            bool whole = kb0 == 0 && kb1 == KB;
-            ptx::mbar_wait(tmem_full, seg & 1);
+            const int buf = nbuf == 2 ? (int)(seg & 1) : 0;
+            const uint32_t use = nbuf == 2 ? seg >> 1 : seg;
+            const int ci = (int)blockIdx.x - cta_of((long long)tile * KB, G, U);
+            float* dst = a.part + (size_t)(tile * a.max_contrib + ci) * 256 * 256;
+            ptx::mbar_wait(&tmem_full[buf], use & 1);
             ptx::tc_fence_after();
-            const uint32_t trow = tmem + ((uint32_t)(w * 32) << 16);
-            if (whole) {
-                for (int acc = 0; acc < 2; ++acc)
-                    for (int j0 = 0; j0 < ncols; j0 += 16) {
-                        float v[16];
-                        ptx::tmem_ld16(trow + acc * 256 + j0, v);
-                        finalize_chunk<EPI>(a, T, m_base, n0, j0, acc, lane, w, v, red_val, red_idx);
-                    }
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(tmem_empty);
-            } else {
-                // split tile: publish this contributor's partial, the last one reduces
-                long long tk0 = (long long)tile * KB;
-                int cf = cta_of(tk0, G, U), cl = cta_of(tk0 + KB - 1, G, U);
-                int me = blockIdx.x;
-                int slot = me == cf ? 2 * me + 1 : 2 * me;
-                float* mine = a.ws + (size_t)slot * 256 * 256;
-                for (int acc = 0; acc < 2; ++acc)
-                    for (int j0 = 0; j0 < ncols; j0 += 16) {
-                        float v[16];
-                        ptx::tmem_ld16(trow + acc * 256 + j0, v);
+            const uint32_t trow = tmem + ((uint32_t)(w * 32) << 16) + (nbuf == 2 ? buf * 256 : 0);
+            for (int acc = 0; acc < 2; ++acc) {
+                const int row = acc * 128 + row_in_acc;
+                for (int j0 = 0; j0 < ncols; j0 += 16) {
+                    float v[16];
+                    ptx::tmem_ld16(trow + acc * (nbuf == 2 ? 128 : 256) + j0, v);
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) mine[(size_t)(j0 + i) * 256 + acc * 128 + et] = v[i];
-                    }
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(tmem_empty);
-                __threadfence();
-                ptx::named_bar_sync(1, 128);
-                if (et == 0) {
-                    int old = atomicAdd(&a.counters[tile], 1);
-                    s_last = (old == cl - cf);
-                    if (s_last) atomicExch(&a.counters[tile], 0);
-                }
-                ptx::named_bar_sync(1, 128);
-                if (s_last) {
-                    __threadfence();
-                    for (int acc = 0; acc < 2; ++acc)
-                        for (int j0 = 0; j0 < ncols; j0 += 16) {
-                            float v[16];
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) v[i] = 0.0f;
-                            for (int c = cf; c <= cl; ++c) {
-                                const float* p = a.ws + (size_t)(c == cf ? 2 * c + 1 : 2 * c) * 256 * 256;
-#pragma unroll
-                                for (int i = 0; i < 16; ++i) v[i] += __ldcg(p + (size_t)(j0 + i) * 256 + acc * 128 + et);
-                            }
-                            finalize_chunk<EPI>(a, T, m_base, n0, j0, acc, lane, w, v, red_val, red_idx);
-                        }
+                    for (int i = 0; i < 16; ++i) dst[(size_t)(j0 + i) * 256 + row] = v[i];
                 }
             }
-            if constexpr (EPI == EPI_ARGMAX) {
-                ptx::named_bar_sync(1, 128);
-                bool fin = whole || s_last;
-                if (fin) {
-                    for (int j = et; j < ncols; j += 128) {
-                        float bv = red_val[j];
-                        int bi = red_idx[j];
-                        for (int g = 1; g < 8; ++g) {
-                            float ov = red_val[g * 256 + j];
-                            int oi = red_idx[g * 256 + j];
-                            if (ov > bv || (ov == bv && oi < bi)) {
-                                bv = ov;
-                                bi = oi;
-                            }
-                        }
-                        if (n0 + j < T) {
-                            a.part_val[(size_t)m_tile * a.ld_part + n0 + j] = bv;
-                            a.part_idx[(size_t)m_tile * a.ld_part + n0 + j] = bi;
-                        }
-                    }
-                }
-                ptx::named_bar_sync(1, 128);
-            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tmem_empty[buf]);
             u += kb1 - kb0;
         }
     }
     __syncthreads();
     if (warp == 2) ptx::tmem_dealloc<512>(tmem);
+}
+
+// ------------------------------------------------------------- reductions
+struct RedInfo {
+    int KB, G;
+    long long U;
+};
+
+// sum of tile contributors in contributor order (deterministic)
+__device__ __forceinline__ float tile_sum(const GemmArgs& a, const RedInfo& r, int tile, int t, int row) {
+    long long tk0 = (long long)tile * r.KB;
+    int cf = cta_of(tk0, r.G, r.U), cl = cta_of(tk0 + r.KB - 1, r.G, r.U);
+    const float* p = a.part + ((size_t)tile * a.max_contrib * 256 + t) * 256 + row;
+    float v = 0.0f;
+    for (int c = 0; c <= cl - cf; ++c) v += __ldcg(p + (size_t)c * 256 * 256);
+    return v;
+}
+
+// grid (T_upper, m_tiles), block 256: one output feature per thread
+template <int EPI>
+__global__ void __launch_bounds__(256) k_reduce_tile(GemmArgs a, RedInfo r) {
+    const int t = blockIdx.x, tile = blockIdx.y, row = threadIdx.x;
+    const int T = a.dT ? *a.dT : a.T;
+    const int m = tile * 256 + row;
+    if (t >= T || m >= a.M) return;
+    float v = tile_sum(a, r, tile, t, row);
+    if constexpr (EPI == EPI_STORE) {
+        a.out_f32[(size_t)t * a.ld_out + m] = v;
+    } else if constexpr (EPI == EPI_GELU) {
+        a.out_bf16[(size_t)t * a.ld_out + m] = __float2bfloat16_rn(gelu_fast(v + a.bias[m]));
+    } else if constexpr (EPI == EPI_QKV) {
+        __nv_bfloat16 x = __float2bfloat16_rn(v + a.bias[m]);
+        int which = m / a.h, hm = m - which * a.h;
+        if (which == 0) {
+            a.out_bf16[(size_t)t * a.h + hm] = x;
+        } else {
+            Plan pl = a.plans[t];
+            if (pl.store) {
+                int head = hm / a.hd, d = hm - head * a.hd;
+                size_t off = ((((size_t)a.layer * 2 + (which - 1)) * a.B + pl.sample) * a.heads + head) *
+                                 (size_t)a.cap * a.hd +
+                             (size_t)pl.write_slot * a.hd + d;
+                a.kv[off] = x;
+            }
+        }
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* scratch) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (threadIdx.x % 32 == 0) scratch[threadIdx.x / 32] = v;
+    __syncthreads();
+    float s = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) s += scratch[i];
+    return s;
+}
+
+// grid T_upper, block 512: residual add of one token row, then the next
+// LayerNorm of that row (two-pass mean / variance, eps 1e-5) -> bf16
+constexpr int kLnThreads = 512, kLnPer = 16;  // hidden <= 8192
+__global__ void __launch_bounds__(kLnThreads) k_reduce_resid_ln(GemmArgs a, RedInfo r) {
+    __shared__ float scratch[32];
+    const int t = blockIdx.x;
+    const int T = a.dT ? *a.dT : a.T;
+    if (t >= T) return;
+    float x[kLnPer];
+    float s = 0.0f;
+    float* res = a.out_f32 + (size_t)t * a.ld_out;
+#pragma unroll
+    for (int k = 0; k < kLnPer; ++k) {
+        int m = threadIdx.x + k * kLnThreads;
+        x[k] = 0.0f;
+        if (m < a.M) {
+            float v = tile_sum(a, r, m >> 8, t, m & 255) + a.bias[m];
+            x[k] = res[m] + v;
+            res[m] = x[k];
+            s += x[k];
+        }
+    }
+    const float mean = block_sum<kLnThreads>(s, scratch) / a.M;
+    float q = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kLnPer; ++k) {
+        int m = threadIdx.x + k * kLnThreads;
+        if (m < a.M) q += (x[k] - mean) * (x[k] - mean);
+    }
+    const float inv = rsqrtf(block_sum<kLnThreads>(q, scratch) / a.M + 1e-5f);
+    __nv_bfloat16* y = a.ln_out + (size_t)t * a.M;
+#pragma unroll
+    for (int k = 0; k < kLnPer; ++k) {
+        int m = threadIdx.x + k * kLnThreads;
+        if (m < a.M) y[m] = __float2bfloat16_rn((x[k] - mean) * inv * a.ln_g[m] + a.ln_b[m]);
+    }
+}
+
+// grid T_upper, block 1024: greedy_next over the vocab (model.cpp:34-41)
+__global__ void __launch_bounds__(1024) k_reduce_argmax(GemmArgs a, RedInfo r) {
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    const int t = blockIdx.x;
+    const int T = a.dT ? *a.dT : a.T;
+    if (t >= T) return;
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    bool bad = false;
+    for (int m = threadIdx.x; m < a.vocab; m += 1024) {
+        float v = tile_sum(a, r, m >> 8, t, m & 255);
+        if (a.logits) a.logits[(size_t)t * a.vocab + m] = v;
+        if (!isfinite(v)) bad = true;
+        if (v > bv) {  // ascending m per thread: strict > keeps the lowest id
+            bv = v;
+            bi = m;
+        }
+    }
+    if (bad) atomicExch(a.flag, 1);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    if (threadIdx.x % 32 == 0) {
+        sv[threadIdx.x / 32] = bv;
+        si[threadIdx.x / 32] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 32; ++w)
+            if (sv[w] > bv || (sv[w] == bv && si[w] < bi)) {
+                bv = sv[w];
+                bi = si[w];
+            }
+        a.argmax[t] = bi == 0x7fffffff ? 0 : bi;
+    }
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -344,14 +345,14 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-template <int EPI>
-void launch_impl(const GemmArgs& a, const GemmMaps& maps, int grid, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        CUDA_OK(cudaFuncSetAttribute(k_gemm<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-        configured = true;
+int max_contrib_for(int m_tiles, int KB, int G) {
+    long long U = (long long)m_tiles * KB;
+    int mx = 1;
+    for (int t = 0; t < m_tiles; ++t) {
+        long long tk0 = (long long)t * KB;
+        mx = std::max(mx, cta_of(tk0 + KB - 1, G, U) - cta_of(tk0, G, U) + 1);
     }
-    k_gemm<EPI><<<grid, kThreads, kSmemBytes, st>>>(maps.A, maps.B[0], maps.B[1], maps.B[2], maps.B[3], a);
+    return mx;
 }
 
 }  // namespace
@@ -374,28 +375,41 @@ void make_b_maps(GemmMaps& maps, const void* x, int64_t rows, int64_t cols) {
     for (int i = 0; i < 4; ++i) maps.B[i] = make_tmap_2d(x, rows, cols, boxes[i]);
 }
 
-void gemm_prepare() {
-    CUDA_OK(cudaFuncSetAttribute(k_gemm<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    CUDA_OK(cudaFuncSetAttribute(k_gemm<EPI_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    CUDA_OK(cudaFuncSetAttribute(k_gemm<EPI_GELU>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    CUDA_OK(cudaFuncSetAttribute(k_gemm<EPI_QKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    CUDA_OK(cudaFuncSetAttribute(k_gemm<EPI_ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-}
-
-int gemm_grid(const GemmArgs& a, int T_upper, int sms) {
-    long long n_tiles = (T_upper + 255) / 256;
-    long long U = (long long)a.m_tiles * n_tiles * (a.K / kBK);
-    return (int)(U < sms ? U : sms);
-}
-
-void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int grid, cudaStream_t st) {
+void gemm_plan(GemmArgs& a, int sms) {
     SD_CHECK(a.K % kBK == 0, CONFIG, "bf16 mode needs K % 64 == 0");
+    long long U = (long long)a.m_tiles * (a.K / kBK);
+    a.grid = (int)std::min<long long>(U, sms);
+    a.max_contrib = max_contrib_for(a.m_tiles, a.K / kBK, a.grid);
+}
+
+size_t gemm_part_floats(int M, int K, int sms) {
+    GemmArgs a{};
+    a.M = M;
+    a.K = K;
+    a.m_tiles = (M + 255) / 256;
+    gemm_plan(a, sms);
+    return (size_t)a.m_tiles * a.max_contrib * 256 * 256;
+}
+
+void gemm_prepare() {
+    CUDA_OK(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+}
+
+void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, cudaStream_t st) {
+    static bool prepared = false;
+    if (!prepared) {
+        gemm_prepare();
+        prepared = true;
+    }
+    SD_CHECK(T_upper <= 256, INTERNAL, "GEMM token tile is at most 256");
+    k_gemm<<<a.grid, kThreads, kSmemBytes, st>>>(maps.A, maps.B[0], maps.B[1], maps.B[2], maps.B[3], a);
+    RedInfo r{a.K / kBK, a.grid, (long long)a.m_tiles * (a.K / kBK)};
     switch (epi) {
-        case EPI_STORE: launch_impl<EPI_STORE>(a, maps, grid, st); break;
-        case EPI_RESID: launch_impl<EPI_RESID>(a, maps, grid, st); break;
-        case EPI_GELU: launch_impl<EPI_GELU>(a, maps, grid, st); break;
-        case EPI_QKV: launch_impl<EPI_QKV>(a, maps, grid, st); break;
-        case EPI_ARGMAX: launch_impl<EPI_ARGMAX>(a, maps, grid, st); break;
+        case EPI_STORE: k_reduce_tile<EPI_STORE><<<dim3(T_upper, a.m_tiles), 256, 0, st>>>(a, r); break;
+        case EPI_GELU: k_reduce_tile<EPI_GELU><<<dim3(T_upper, a.m_tiles), 256, 0, st>>>(a, r); break;
+        case EPI_QKV: k_reduce_tile<EPI_QKV><<<dim3(T_upper, a.m_tiles), 256, 0, st>>>(a, r); break;
+        case EPI_RESID_LN: k_reduce_resid_ln<<<T_upper, kLnThreads, 0, st>>>(a, r); break;
+        case EPI_ARGMAX: k_reduce_argmax<<<T_upper, 1024, 0, st>>>(a, r); break;
         default: throw Error(INTERNAL, "unknown GEMM epilogue");
     }
     CUDA_OK(cudaGetLastError());
@@ -404,8 +418,6 @@ void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int grid, cud
 }  // namespace sdb
 
 // --------------------------------------------------------------- test hook
-#include "../../include/specdec_b200_debug.h"
-#include <string>
 namespace {
 thread_local std::string g_dbg_err;
 }
@@ -416,39 +428,39 @@ extern "C" int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K,
         int m_tiles = (M + 255) / 256;
         size_t wbytes = (size_t)m_tiles * 256 * K * 2, xbytes = (size_t)T * K * 2;
         void *dW = dmalloc(wbytes), *dX = dmalloc(xbytes), *dY = dmalloc((size_t)T * M * 4);
-        void* dws = dmalloc((size_t)2 * 148 * 256 * 256 * 4);
-        int* dcnt = (int*)dmalloc(65536 * 4);
-        CUDA_OK(cudaMemset(dW, 0, wbytes));
-        CUDA_OK(cudaMemset(dcnt, 0, 65536 * 4));
-        CUDA_OK(cudaMemcpy(dW, W, (size_t)M * K * 2, cudaMemcpyHostToDevice));
-        CUDA_OK(cudaMemcpy(dX, X, xbytes, cudaMemcpyHostToDevice));
-        GemmMaps maps;
-        maps.A = make_tmap_2d(dW, (int64_t)m_tiles * 256, K, 256);
-        make_b_maps(maps, dX, T, K);
         GemmArgs a{};
         a.M = M;
         a.K = K;
         a.m_tiles = m_tiles;
         a.T = T;
-        a.ws = (float*)dws;
-        a.counters = dcnt;
+        gemm_plan(a, grid > 0 ? grid : 148);
+        void* dpart = dmalloc(sizeof(float) * (size_t)m_tiles * a.max_contrib * 256 * 256);
+        CUDA_OK(cudaMemset(dW, 0, wbytes));
+        CUDA_OK(cudaMemcpy(dW, W, (size_t)M * K * 2, cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMemcpy(dX, X, xbytes, cudaMemcpyHostToDevice));
+        GemmMaps maps;
+        maps.A = make_tmap_2d(dW, (int64_t)m_tiles * 256, K, 256);
+        make_b_maps(maps, dX, T, K);
+        a.part = (float*)dpart;
         a.out_f32 = (float*)dY;
         a.ld_out = M;
-        int g = grid > 0 ? grid : gemm_grid(a, T, 148);
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
-        gemm_launch(EPI_STORE, a, maps, g, 0);  // warm-up / configure
+        gemm_launch(EPI_STORE, a, maps, T, 0);  // warm-up / configure
         CUDA_OK(cudaDeviceSynchronize());
         cudaEventRecord(e0);
-        gemm_launch(EPI_STORE, a, maps, g, 0);
+        gemm_launch(EPI_STORE, a, maps, T, 0);
         cudaEventRecord(e1);
         CUDA_OK(cudaDeviceSynchronize());
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
         if (usec) *usec = ms * 1000.0f;
         CUDA_OK(cudaMemcpy(Y, dY, (size_t)T * M * 4, cudaMemcpyDeviceToHost));
-        dfree(dW); dfree(dX); dfree(dY); dfree(dws); dfree(dcnt);
+        dfree(dW);
+        dfree(dX);
+        dfree(dY);
+        dfree(dpart);
         return 0;
     } catch (const Error& e) {
         g_dbg_err = e.what();

@@ -170,7 +170,9 @@ __global__ void k_accept(StepArgs a) {
     }
     if (threadIdx.x == 0) {
         if (a.n_active) *a.n_active = s_active;
-        if (a.step) *a.step = s_step + 1;
+        // count only steps that verified something (graph replays may run
+        // trailing no-op steps after every sample finished)
+        if (a.step && s_taumax > 0) *a.step = s_step + 1;
     }
 }
 
