@@ -9,7 +9,10 @@ extern "C" {
 /* Y[T][M] = X[T][K] . W[M][K]^T with bf16 inputs (raw bits) and fp32 output,
  * through the stream-K tcgen05 kernel on `grid` CTAs (0 = one per SM).
  * Returns the kernel time in microseconds in *usec (CUDA events). */
-int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K, int T, int grid, float* Y, float* usec);
+/* flags bit 0: store W tile-major ([m_tile][K/64][256][64], one contiguous 32 KB
+ * TMA box per k-block) instead of row-major */
+int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K, int T, int grid, int flags, float* Y,
+                  float* usec);
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,7 @@
 namespace sdb {
 
 constexpr int kChunkTokens = 256;  // tokens per forward chunk (GEMM N <= 256)
-constexpr int kKeysPerCta = 256;   // attention split size (4 warps x 64 keys)
+constexpr int kKeysPerCta = 128;   // attention split size (4 warps x 32 keys)
 constexpr int kSms = 148;          // B200 SM count (stream-K GEMM grid)
 
 struct FastModelState {
@@ -200,14 +200,16 @@ struct AttnArgs {
     float scale_log2;          // log2(e) / sqrt(hd)
 };
 
-// One CTA = (sample, head) x 256-key split x 16-query tile; 4 warps each own
-// 64 keys.  S = Q K^T and O = P V run on mma.sync m16n8k16 (bf16 in, fp32
-// accumulate); the 4 warps' partial softmax states merge through smem.  A
-// sample's K/V extent is read once per split, not once per query token (the
-// paper's per-token grid, re-reads it n_s times).
+// One CTA = (sample, head) x 128-key split x 16-query tile; 4 warps each own
+// 32 keys.  S = Q K^T and O = P V run on mma.sync m16n8k16 (bf16 in, fp32
+// accumulate); the 4 warps' partial softmax states merge through smem (reusing
+// the K/V staging area).  68 KB of smem per CTA keeps 3 CTAs (12 warps, 192 KB
+// of K/V loads) in flight per SM.  A sample's K/V extent is read once per
+// split, not once per query token (the paper's per-token grid,
+// PAPER.md:872-876, re-reads it n_s times).
 template <int HD>
 __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
-    constexpr int kKeys = 64;
+    constexpr int kKeys = kKeysPerCta / 4;  // keys per warp
     const int sh = blockIdx.x, split = blockIdx.y, qt = blockIdx.z;
     const int s = sh / a.heads, head = sh % a.heads;
     const SampleSeg seg = a.segs[s];
@@ -217,10 +219,11 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
     const int nq = min(16, seg.n_q - qt * 16);
 
     extern __shared__ __align__(128) uint8_t sm[];
-    uint8_t* sQ = sm;                                   // [16][HD]
-    uint8_t* sK = sm + 16 * HD * 2 + warp * 2 * kKeys * HD * 2;
+    uint8_t* sQ = sm;                                                   // [16][HD]
+    uint8_t* sKV = sm + 16 * HD * 2;                                    // per warp: K[kKeys][HD], V[kKeys][HD]
+    uint8_t* sK = sKV + warp * 2 * kKeys * HD * 2;
     uint8_t* sV = sK + kKeys * HD * 2;
-    float* sMerge = (float*)(sm + 16 * HD * 2 + 4 * 2 * kKeys * HD * 2);  // [4][16][HD] + [4][16][2]
+    float* sMerge = (float*)sKV;  // reused after compute: [4][16][HD] + [4][16][2]
     __shared__ int sWslot[16];
     __shared__ int sTok[16];
 
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
         sTok[r] = tok;
         sWslot[r] = tok >= 0 ? a.plans[tok].write_slot : -1;
     }
-    // this warp's K / V rows
+    // this warp's K / V rows (rows past the extent are zero-filled)
     const int kw0 = k_begin + warp * kKeys;
     const size_t kbase = ((((size_t)a.layer * 2 + 0) * a.B + s) * a.heads + head) * (size_t)a.cap * HD;
     const size_t vbase = ((((size_t)a.layer * 2 + 1) * a.B + s) * a.heads + head) * (size_t)a.cap * HD;
@@ -263,16 +266,16 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
         const uint32_t qa = (uint32_t)__cvta_generic_to_shared(sQ);
         const uint32_t ka = (uint32_t)__cvta_generic_to_shared(sK);
         const uint32_t va = (uint32_t)__cvta_generic_to_shared(sV);
-        // S = Q K^T : 16 x 64
-        float sacc[8][4];
+        // S = Q K^T : 16 x kKeys
+        float sacc[kKeys / 8][4];
 #pragma unroll
-        for (int n = 0; n < 8; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.0f;
+        for (int n = 0; n < kKeys / 8; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.0f;
 #pragma unroll
         for (int kk = 0; kk < HD; kk += 16) {
             uint32_t a0, a1, a2, a3;
             ldsm_x4(qa + swz<HD>(lane % 16, kk + (lane / 16) * 8), a0, a1, a2, a3);
 #pragma unroll
-            for (int n = 0; n < 8; n += 2) {
+            for (int n = 0; n < kKeys / 8; n += 2) {
                 // matrices: (keys n*8.., cols kk), (keys n*8.., kk+8), (keys n*8+8.., kk), (keys n*8+8.., kk+8)
                 uint32_t b0, b1, b2, b3;
                 ldsm_x4(ka + swz<HD>(n * 8 + (lane % 8) + (lane / 16) * 8, kk + ((lane / 8) % 2) * 8), b0, b1, b2,
@@ -281,10 +284,10 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
                 mma_bf16(sacc[n + 1], a0, a1, a2, a3, b2, b3);
             }
         }
-        // mask + local max
+        // mask (own extent, causal write slot, padded-grid holes) + local max
         float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-        for (int n = 0; n < 8; ++n) {
+        for (int n = 0; n < kKeys / 8; ++n) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 int row = g + (e >= 2 ? 8 : 0);
@@ -302,9 +305,9 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
             m_run[r] = mx[r];
         }
         float sum[2] = {0.0f, 0.0f};
-        uint32_t p[8][2];
+        uint32_t p[kKeys / 8][2];
 #pragma unroll
-        for (int n = 0; n < 8; ++n) {
+        for (int n = 0; n < kKeys / 8; ++n) {
             float e0 = m_run[0] == -INFINITY ? 0.0f : exp2f(sacc[n][0] - m_run[0]);
             float e1 = m_run[0] == -INFINITY ? 0.0f : exp2f(sacc[n][1] - m_run[0]);
             float e2 = m_run[1] == -INFINITY ? 0.0f : exp2f(sacc[n][2] - m_run[1]);
@@ -320,9 +323,9 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
             sum[r] += __shfl_xor_sync(0xffffffffu, sum[r], 2);
             l_run[r] = sum[r];
         }
-        // O = P V : 16 x HD, k = 64 keys in 4 steps
+        // O = P V : 16 x HD, k = kKeys keys in steps of 16
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
+        for (int ks = 0; ks < kKeys / 16; ++ks) {
             uint32_t a0 = p[2 * ks][0], a1 = p[2 * ks][1], a2 = p[2 * ks + 1][0], a3 = p[2 * ks + 1][1];
 #pragma unroll
             for (int n = 0; n < HD / 8; n += 2) {
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
             }
         }
     }
-    // merge the 4 warps' (m, l, O) in smem
+    __syncthreads();  // every warp is done with K/V: reuse the area for the merge
     float* mO = sMerge + (size_t)warp * 16 * HD;
     float* mML = sMerge + 4 * 16 * HD + warp * 32;
 #pragma unroll
@@ -542,7 +545,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     at.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
     const int splits = std::max(1, (db.max_kv_upper + kKeysPerCta - 1) / kKeysPerCta);
     const int qtiles = std::max(1, (db.max_q_upper + 15) / 16);
-    const size_t attn_smem = (size_t)16 * hd * 2 + 4 * 2 * 64 * hd * 2 + (4 * 16 * hd + 4 * 32) * 4;
+    const size_t attn_smem = (size_t)16 * hd * 2 + 4 * 2 * (kKeysPerCta / 4) * hd * 2;
 
     for (int l = 0; l < cfg.num_layers; ++l) {
         const FastLayer& L = m.layers[l];

@@ -21,6 +21,7 @@ struct GemmArgs {
     int T;                    // token count when dT == nullptr (must be <= 256)
     const int* dT;            // device token count (graph-capturable), or nullptr
     int grid, max_contrib;    // stream-K schedule (set by gemm_plan)
+    int a_tiled;              // W stored tile-major: [m_tile][K/64][256][64] (contiguous 32 KB boxes)
     float* part;              // fp32 partial sums [m_tiles * max_contrib][256 tok][256 rows]
     const float* bias;        // [M] or nullptr
     float* out_f32;           // EPI_STORE output / EPI_RESID_LN residual stream

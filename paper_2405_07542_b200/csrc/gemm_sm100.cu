@@ -23,7 +23,9 @@
 // allocator, w4-7 epilogue (TMEM lanes 0-127).
 #include <cuda_bf16.h>
 
+#include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/specdec_b200_debug.h"
 #include "gemm.h"
@@ -63,14 +65,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int box = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
     const CUtensorMap* tmB = box == 32 ? &tmB32 : box == 64 ? &tmB64 : box == 128 ? &tmB128 : &tmB256;
     const int nbuf = BN <= 128 ? 2 : 1;  // TMEM accumulator buffers
-    const int stage_bytes = kABytes + box * 128;
-    int S = (kSmemBytes - 2048) / stage_bytes;
-    if (S > kMaxStages) S = kMaxStages;
-    uint8_t* stage_base = smem;
-    uint64_t* bars = (uint64_t*)(smem + S * stage_bytes);
-    uint64_t* full = bars;
-    uint64_t* empty = bars + kMaxStages;
-    uint64_t* tmem_full = bars + 2 * kMaxStages;  // [2]
+    // Decoupled rings: the weight (A) ring is as deep as smem allows so enough
+    // HBM bytes stay in flight to cover DRAM latency; the token (B) ring is
+    // shallow because B is L2-resident (re-read by every tile).
+    const int b_bytes = box * 128;
+    const int SB = 2;
+    int SA = (kSmemBytes - 2048 - SB * b_bytes) / kABytes;
+    if (SA > kMaxStages) SA = kMaxStages;
+    uint8_t* a_base = smem;
+    uint8_t* b_base = smem + SA * kABytes;
+    uint64_t* bars = (uint64_t*)(b_base + SB * b_bytes);
+    uint64_t* fullA = bars;
+    uint64_t* emptyA = bars + kMaxStages;
+    uint64_t* fullB = bars + 2 * kMaxStages;       // [SB]
+    uint64_t* emptyB = fullB + 4;                  // [SB]
+    uint64_t* tmem_full = emptyB + 4;              // [2]
     uint64_t* tmem_empty = tmem_full + 2;          // [2]
     uint32_t* tmem_slot = (uint32_t*)(tmem_empty + 2);
 
@@ -82,9 +91,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(tmB);
-        for (int s = 0; s < S; ++s) {
-            ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], 1);
+        for (int s = 0; s < SA; ++s) {
+            ptx::mbar_init(&fullA[s], 1);
+            ptx::mbar_init(&emptyA[s], 1);
+        }
+        for (int s = 0; s < SB; ++s) {
+            ptx::mbar_init(&fullB[s], 1);
+            ptx::mbar_init(&emptyB[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&tmem_full[b], 1);
@@ -99,19 +112,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer: one contiguous weight range
+        if (lane == 0) {  // ---------------- TMA producer A: one contiguous weight range
             const uint64_t pol_w = ptx::policy_evict_first();  // weights: streamed once
-            const uint64_t pol_x = ptx::policy_evict_last();   // tokens: re-read by every tile
             int stage = 0;
             uint32_t phase = 0;
             for (long long u = u0; u < u1; ++u) {
-                int tile = (int)(u / KB), kb = (int)(u % KB);
-                ptx::mbar_wait(&empty[stage], phase ^ 1);
-                uint8_t* sa = stage_base + stage * stage_bytes;
-                ptx::mbar_arrive_expect_tx(&full[stage], stage_bytes);
-                ptx::tma_load_2d(sa, &tmA, &full[stage], kb * kBK, tile * kBM, pol_w);
-                ptx::tma_load_2d(sa + kABytes, tmB, &full[stage], kb * kBK, 0, pol_x);
-                if (++stage == S) {
+                ptx::mbar_wait(&emptyA[stage], phase ^ 1);
+                uint8_t* sa = a_base + stage * kABytes;
+                ptx::mbar_arrive_expect_tx(&fullA[stage], kABytes);
+                if (a.a_tiled)
+                    ptx::tma_load_2d(sa, &tmA, &fullA[stage], 0, (int)(u * kBM), pol_w);
+                else
+                    ptx::tma_load_2d(sa, &tmA, &fullA[stage], (int)(u % KB) * kBK, (int)(u / KB) * kBM, pol_w);
+                if (++stage == SA) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 3) {
+        if (lane == 0) {  // ---------------- TMA producer B: the token tile of each k-block
+            const uint64_t pol_x = ptx::policy_evict_last();  // tokens: re-read by every tile
+            int stage = 0;
+            uint32_t phase = 0;
+            for (long long u = u0; u < u1; ++u) {
+                ptx::mbar_wait(&emptyB[stage], phase ^ 1);
+                ptx::mbar_arrive_expect_tx(&fullB[stage], b_bytes);
+                ptx::tma_load_2d(b_base + stage * b_bytes, tmB, &fullB[stage], (int)(u % KB) * kBK, 0, pol_x);
+                if (++stage == SB) {
                     stage = 0;
                     phase ^= 1;
                 }
@@ -120,8 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
             const uint32_t idesc = ptx::umma_idesc_bf16(128, BN);
-            int stage = 0;
-            uint32_t phase = 0, seg = 0;
+            int sa_i = 0, sb_i = 0;
+            uint32_t pa = 0, pb = 0, seg = 0;
             for (long long u = u0; u < u1; ++seg) {
                 int kb0 = (int)(u % KB);
                 int kb1 = (int)min((long long)KB, kb0 + (u1 - u));
@@ -131,10 +159,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 const uint32_t d0 = tmem + (nbuf == 2 ? buf * 256 : 0);
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::mbar_wait(&fullA[sa_i], pa);
+                    ptx::mbar_wait(&fullB[sb_i], pb);
                     ptx::tc_fence_after();
-                    uint32_t sa = ptx::smem_u32(stage_base + stage * stage_bytes);
-                    uint32_t sb = sa + kABytes;
+                    uint32_t sa = ptx::smem_u32(a_base + sa_i * kABytes);
+                    uint32_t sb = ptx::smem_u32(b_base + sb_i * b_bytes);
 #pragma unroll
                     for (int k = 0; k < kBK / 16; ++k) {
                         uint64_t bdesc = ptx::umma_desc_kmajor_sw128(sb + k * 32);
@@ -145,10 +174,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                                            (kb > kb0 || k > 0) ? 1u : 0u);
                         }
                     }
-                    ptx::umma_commit(&empty[stage]);
-                    if (++stage == S) {
-                        stage = 0;
-                        phase ^= 1;
+                    ptx::umma_commit(&emptyA[sa_i]);
+                    ptx::umma_commit(&emptyB[sb_i]);
+                    if (++sa_i == SA) {
+                        sa_i = 0;
+                        pa ^= 1;
+                    }
+                    if (++sb_i == SB) {
+                        sb_i = 0;
+                        pb ^= 1;
                     }
                 }
                 ptx::umma_commit(&tmem_full[buf]);
@@ -158,6 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> fp32 partials
         const int w = warp - 4;
         const int row_in_acc = w * 32 + lane;
+        const uint64_t pol_keep = ptx::policy_evict_last();  // partials are re-read from L2
         const int ncols = BN;
         uint32_t seg = 0;
         for (long long u = u0; u < u1; ++seg) {
@@ -176,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float v[16];
                     ptx::tmem_ld16(trow + acc * (nbuf == 2 ? 128 : 256) + j0, v);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) dst[(size_t)(j0 + i) * 256 + row] = v[i];
+                    for (int i = 0; i < 16; ++i) ptx::st_f32_hint(dst + (size_t)(j0 + i) * 256 + row, v[i], pol_keep);
                 }
             }
             ptx::tc_fence_before();
@@ -194,42 +229,60 @@ struct RedInfo {
     long long U;
 };
 
-// sum of tile contributors in contributor order (deterministic)
-__device__ __forceinline__ float tile_sum(const GemmArgs& a, const RedInfo& r, int tile, int t, int row) {
+__device__ __forceinline__ void tile_contrib(const RedInfo& r, int tile, int& n) {
     long long tk0 = (long long)tile * r.KB;
-    int cf = cta_of(tk0, r.G, r.U), cl = cta_of(tk0 + r.KB - 1, r.G, r.U);
-    const float* p = a.part + ((size_t)tile * a.max_contrib * 256 + t) * 256 + row;
-    float v = 0.0f;
-    for (int c = 0; c <= cl - cf; ++c) v += __ldcg(p + (size_t)c * 256 * 256);
-    return v;
+    n = cta_of(tk0 + r.KB - 1, r.G, r.U) - cta_of(tk0, r.G, r.U) + 1;
 }
 
-// grid (T_upper, m_tiles), block 256: one output feature per thread
+// grid (m_tiles, ceil(T_upper / kRT)), block 256: thread = one output feature
+// of the tile for kRT tokens; all kRT x contributors loads issue before use.
+constexpr int kRT = 16;
 template <int EPI>
-__global__ void __launch_bounds__(256) k_reduce_tile(GemmArgs a, RedInfo r) {
-    const int t = blockIdx.x, tile = blockIdx.y, row = threadIdx.x;
+__global__ void __launch_bounds__(256) k_reduce_tile(const GemmArgs a, const RedInfo r) {
+    const int tile = blockIdx.x, t0 = blockIdx.y * kRT, row = threadIdx.x;
     const int T = a.dT ? *a.dT : a.T;
     const int m = tile * 256 + row;
-    if (t >= T || m >= a.M) return;
-    float v = tile_sum(a, r, tile, t, row);
-    if constexpr (EPI == EPI_STORE) {
-        a.out_f32[(size_t)t * a.ld_out + m] = v;
-    } else if constexpr (EPI == EPI_GELU) {
-        a.out_bf16[(size_t)t * a.ld_out + m] = __float2bfloat16_rn(gelu_fast(v + a.bias[m]));
-    } else if constexpr (EPI == EPI_QKV) {
-        __nv_bfloat16 x = __float2bfloat16_rn(v + a.bias[m]);
-        int which = m / a.h, hm = m - which * a.h;
-        if (which == 0) {
-            a.out_bf16[(size_t)t * a.h + hm] = x;
-        } else {
-            Plan pl = a.plans[t];
-            if (pl.store) {
-                int head = hm / a.hd, d = hm - head * a.hd;
-                size_t off = ((((size_t)a.layer * 2 + (which - 1)) * a.B + pl.sample) * a.heads + head) *
-                                 (size_t)a.cap * a.hd +
-                             (size_t)pl.write_slot * a.hd + d;
-                a.kv[off] = x;
+    if (t0 >= T || m >= a.M) return;
+    int nc;
+    tile_contrib(r, tile, nc);
+    const float* __restrict__ p = a.part + ((size_t)tile * a.max_contrib * 256 + t0) * 256 + row;
+    float v[kRT];
+#pragma unroll
+    for (int i = 0; i < kRT; ++i) v[i] = 0.0f;
+    for (int c = 0; c < nc; ++c) {
+#pragma unroll
+        for (int i = 0; i < kRT; ++i) v[i] += __ldcg(p + ((size_t)c * 256 + i) * 256);
+    }
+    const float b = a.bias ? a.bias[m] : 0.0f;
+    const int nt = min(kRT, T - t0);
+    if constexpr (EPI == EPI_QKV) {
+        const int which = m / a.h, hm = m - which * a.h;
+        const int head = hm / a.hd, d = hm - head * a.hd;
+#pragma unroll
+        for (int i = 0; i < kRT; ++i) {
+            if (i >= nt) break;
+            const int t = t0 + i;
+            __nv_bfloat16 x = __float2bfloat16_rn(v[i] + b);
+            if (which == 0) {
+                a.out_bf16[(size_t)t * a.h + hm] = x;
+            } else {
+                Plan pl = a.plans[t];
+                if (pl.store) {
+                    size_t off = ((((size_t)a.layer * 2 + (which - 1)) * a.B + pl.sample) * a.heads + head) *
+                                     (size_t)a.cap * a.hd +
+                                 (size_t)pl.write_slot * a.hd + d;
+                    a.kv[off] = x;
+                }
             }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < kRT; ++i) {
+            if (i >= nt) break;
+            const int t = t0 + i;
+            if constexpr (EPI == EPI_STORE) a.out_f32[(size_t)t * a.ld_out + m] = v[i];
+            if constexpr (EPI == EPI_GELU)
+                a.out_bf16[(size_t)t * a.ld_out + m] = __float2bfloat16_rn(gelu_fast(v[i] + b));
         }
     }
 }
@@ -247,60 +300,110 @@ __device__ __forceinline__ float block_sum(float v, float* scratch) {
 }
 
 // grid T_upper, block 512: residual add of one token row, then the next
-// LayerNorm of that row (two-pass mean / variance, eps 1e-5) -> bf16
+// LayerNorm of that row (two-pass mean / variance, eps 1e-5) -> bf16.
+// All partial loads of the row are issued before any store.
 constexpr int kLnThreads = 512, kLnPer = 16;  // hidden <= 8192
-__global__ void __launch_bounds__(kLnThreads) k_reduce_resid_ln(GemmArgs a, RedInfo r) {
+__global__ void __launch_bounds__(kLnThreads) k_reduce_resid_ln(const GemmArgs a, const RedInfo r) {
     __shared__ float scratch[32];
     const int t = blockIdx.x;
     const int T = a.dT ? *a.dT : a.T;
     if (t >= T) return;
     float x[kLnPer];
-    float s = 0.0f;
-    float* res = a.out_f32 + (size_t)t * a.ld_out;
+    int ncs[kLnPer];
+    const float* __restrict__ part = a.part;
 #pragma unroll
     for (int k = 0; k < kLnPer; ++k) {
-        int m = threadIdx.x + k * kLnThreads;
+        const int m = threadIdx.x + k * kLnThreads;
         x[k] = 0.0f;
+        ncs[k] = 0;
+        if (m < a.M) tile_contrib(r, m >> 8, ncs[k]);
+    }
+    int ncmax = 0;
+#pragma unroll
+    for (int k = 0; k < kLnPer; ++k) ncmax = max(ncmax, ncs[k]);
+    for (int c = 0; c < ncmax; ++c) {
+#pragma unroll
+        for (int k = 0; k < kLnPer; ++k) {
+            const int m = threadIdx.x + k * kLnThreads;
+            if (c < ncs[k])
+                x[k] += __ldcg(part + (((size_t)(m >> 8) * a.max_contrib + c) * 256 + t) * 256 + (m & 255));
+        }
+    }
+    float* __restrict__ res = a.out_f32 + (size_t)t * a.ld_out;
+    float s = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kLnPer; ++k) {
+        const int m = threadIdx.x + k * kLnThreads;
         if (m < a.M) {
-            float v = tile_sum(a, r, m >> 8, t, m & 255) + a.bias[m];
-            x[k] = res[m] + v;
-            res[m] = x[k];
+            x[k] += res[m] + a.bias[m];
             s += x[k];
         }
+    }
+#pragma unroll
+    for (int k = 0; k < kLnPer; ++k) {
+        const int m = threadIdx.x + k * kLnThreads;
+        if (m < a.M) res[m] = x[k];
     }
     const float mean = block_sum<kLnThreads>(s, scratch) / a.M;
     float q = 0.0f;
 #pragma unroll
     for (int k = 0; k < kLnPer; ++k) {
-        int m = threadIdx.x + k * kLnThreads;
+        const int m = threadIdx.x + k * kLnThreads;
         if (m < a.M) q += (x[k] - mean) * (x[k] - mean);
     }
     const float inv = rsqrtf(block_sum<kLnThreads>(q, scratch) / a.M + 1e-5f);
     __nv_bfloat16* y = a.ln_out + (size_t)t * a.M;
 #pragma unroll
     for (int k = 0; k < kLnPer; ++k) {
-        int m = threadIdx.x + k * kLnThreads;
+        const int m = threadIdx.x + k * kLnThreads;
         if (m < a.M) y[m] = __float2bfloat16_rn((x[k] - mean) * inv * a.ln_g[m] + a.ln_b[m]);
     }
 }
 
-// grid T_upper, block 1024: greedy_next over the vocab (model.cpp:34-41)
-__global__ void __launch_bounds__(1024) k_reduce_argmax(GemmArgs a, RedInfo r) {
-    __shared__ float sv[32];
-    __shared__ int si[32];
-    const int t = blockIdx.x;
+// grid (T_upper, ceil(m_tiles / 8)), block 256: LM-head logits of one token
+// for 8 vocab tiles, reduced to a (max, lowest id) partial; the last block of
+// a token (arrival counter) folds the partials into greedy_next
+// (model.cpp:34-41).
+constexpr int kArgTiles = 8;
+__global__ void __launch_bounds__(256) k_reduce_argmax(const GemmArgs a, const RedInfo r, float* __restrict__ pv,
+                                                       int* __restrict__ pi, int* __restrict__ cnt) {
+    __shared__ float sv[8];
+    __shared__ int si[8];
+    __shared__ int s_last;
+    const int t = blockIdx.x, g = blockIdx.y;
     const int T = a.dT ? *a.dT : a.T;
     if (t >= T) return;
     float bv = -INFINITY;
     int bi = 0x7fffffff;
     bool bad = false;
-    for (int m = threadIdx.x; m < a.vocab; m += 1024) {
-        float v = tile_sum(a, r, m >> 8, t, m & 255);
-        if (a.logits) a.logits[(size_t)t * a.vocab + m] = v;
-        if (!isfinite(v)) bad = true;
-        if (v > bv) {  // ascending m per thread: strict > keeps the lowest id
-            bv = v;
-            bi = m;
+    const int tile0 = g * kArgTiles;
+    float v[kArgTiles];
+    int nc[kArgTiles];
+#pragma unroll
+    for (int k = 0; k < kArgTiles; ++k) {
+        v[k] = 0.0f;
+        nc[k] = 0;
+        if (tile0 + k < a.m_tiles) tile_contrib(r, tile0 + k, nc[k]);
+    }
+    int ncmax = 0;
+#pragma unroll
+    for (int k = 0; k < kArgTiles; ++k) ncmax = max(ncmax, nc[k]);
+    for (int c = 0; c < ncmax; ++c) {
+#pragma unroll
+        for (int k = 0; k < kArgTiles; ++k)
+            if (c < nc[k])
+                v[k] += __ldcg(a.part + ((((size_t)(tile0 + k) * a.max_contrib + c) * 256 + t) * 256) + threadIdx.x);
+    }
+#pragma unroll
+    for (int k = 0; k < kArgTiles; ++k) {  // ascending ids per thread: strict > keeps the lowest
+        const int m = (tile0 + k) * 256 + threadIdx.x;
+        if (tile0 + k < a.m_tiles && m < a.vocab) {
+            if (a.logits) a.logits[(size_t)t * a.vocab + m] = v[k];
+            if (!isfinite(v[k])) bad = true;
+            if (v[k] > bv) {
+                bv = v[k];
+                bi = m;
+            }
         }
     }
     if (bad) atomicExch(a.flag, 1);
@@ -319,12 +422,32 @@ __global__ void __launch_bounds__(1024) k_reduce_argmax(GemmArgs a, RedInfo r) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < 32; ++w)
+        for (int w = 1; w < 8; ++w)
             if (sv[w] > bv || (sv[w] == bv && si[w] < bi)) {
                 bv = sv[w];
                 bi = si[w];
             }
-        a.argmax[t] = bi == 0x7fffffff ? 0 : bi;
+        pv[(size_t)t * gridDim.y + g] = bv;
+        pi[(size_t)t * gridDim.y + g] = bi;
+        __threadfence();
+        const int old = atomicAdd(&cnt[t], 1);
+        s_last = old == (int)gridDim.y - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        float best = __ldcg(pv + (size_t)t * gridDim.y);
+        int bidx = __ldcg(pi + (size_t)t * gridDim.y);
+        for (int k = 1; k < (int)gridDim.y; ++k) {
+            float ov = __ldcg(pv + (size_t)t * gridDim.y + k);
+            int oi = __ldcg(pi + (size_t)t * gridDim.y + k);
+            if (ov > best || (ov == best && oi < bidx)) {
+                best = ov;
+                bidx = oi;
+            }
+        }
+        a.argmax[t] = bidx == 0x7fffffff ? 0 : bidx;
+        cnt[t] = 0;  // self-resetting for the next launch / graph replay
     }
 }
 
@@ -404,12 +527,26 @@ void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, 
     SD_CHECK(T_upper <= 256, INTERNAL, "GEMM token tile is at most 256");
     k_gemm<<<a.grid, kThreads, kSmemBytes, st>>>(maps.A, maps.B[0], maps.B[1], maps.B[2], maps.B[3], a);
     RedInfo r{a.K / kBK, a.grid, (long long)a.m_tiles * (a.K / kBK)};
+    const dim3 tg(a.m_tiles, (T_upper + kRT - 1) / kRT);
     switch (epi) {
-        case EPI_STORE: k_reduce_tile<EPI_STORE><<<dim3(T_upper, a.m_tiles), 256, 0, st>>>(a, r); break;
-        case EPI_GELU: k_reduce_tile<EPI_GELU><<<dim3(T_upper, a.m_tiles), 256, 0, st>>>(a, r); break;
-        case EPI_QKV: k_reduce_tile<EPI_QKV><<<dim3(T_upper, a.m_tiles), 256, 0, st>>>(a, r); break;
+        case EPI_STORE: k_reduce_tile<EPI_STORE><<<tg, 256, 0, st>>>(a, r); break;
+        case EPI_GELU: k_reduce_tile<EPI_GELU><<<tg, 256, 0, st>>>(a, r); break;
+        case EPI_QKV: k_reduce_tile<EPI_QKV><<<tg, 256, 0, st>>>(a, r); break;
         case EPI_RESID_LN: k_reduce_resid_ln<<<T_upper, kLnThreads, 0, st>>>(a, r); break;
-        case EPI_ARGMAX: k_reduce_argmax<<<T_upper, 1024, 0, st>>>(a, r); break;
+        case EPI_ARGMAX: {
+            static float* pv = nullptr;
+            static int *pi = nullptr, *cnt = nullptr;
+            if (!pv) {  // per-process scratch for the vocab-group partials (<= 256 tokens)
+                pv = (float*)dmalloc(sizeof(float) * 256 * 64);
+                pi = (int*)dmalloc(sizeof(int) * 256 * 64);
+                cnt = (int*)dmalloc(sizeof(int) * 256);
+                CUDA_OK(cudaMemset(cnt, 0, sizeof(int) * 256));
+            }
+            const int groups = (a.m_tiles + kArgTiles - 1) / kArgTiles;
+            SD_CHECK(groups <= 64, INTERNAL, "vocab too large for the argmax scratch");
+            k_reduce_argmax<<<dim3(T_upper, groups), 256, 0, st>>>(a, r, pv, pi, cnt);
+            break;
+        }
         default: throw Error(INTERNAL, "unknown GEMM epilogue");
     }
     CUDA_OK(cudaGetLastError());
@@ -421,8 +558,8 @@ void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, 
 namespace {
 thread_local std::string g_dbg_err;
 }
-extern "C" int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K, int T, int grid, float* Y,
-                             float* usec) {
+extern "C" int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K, int T, int grid, int flags,
+                             float* Y, float* usec) {
     using namespace sdb;
     try {
         int m_tiles = (M + 255) / 256;
@@ -436,10 +573,23 @@ extern "C" int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K,
         gemm_plan(a, grid > 0 ? grid : 148);
         void* dpart = dmalloc(sizeof(float) * (size_t)m_tiles * a.max_contrib * 256 * 256);
         CUDA_OK(cudaMemset(dW, 0, wbytes));
-        CUDA_OK(cudaMemcpy(dW, W, (size_t)M * K * 2, cudaMemcpyHostToDevice));
-        CUDA_OK(cudaMemcpy(dX, X, xbytes, cudaMemcpyHostToDevice));
         GemmMaps maps;
-        maps.A = make_tmap_2d(dW, (int64_t)m_tiles * 256, K, 256);
+        a.a_tiled = flags & 1;
+        if (a.a_tiled) {  // tile-major weights: [m_tile][K/64][256][64]
+            int KB = K / 64;
+            std::vector<uint16_t> wt((size_t)m_tiles * 256 * K, 0);
+            for (int t = 0; t < m_tiles; ++t)
+                for (int kb = 0; kb < KB; ++kb)
+                    for (int r = 0; r < 256 && t * 256 + r < M; ++r)
+                        std::memcpy(&wt[(((size_t)t * KB + kb) * 256 + r) * 64], &W[(size_t)(t * 256 + r) * K + kb * 64],
+                                    128);
+            CUDA_OK(cudaMemcpy(dW, wt.data(), wbytes, cudaMemcpyHostToDevice));
+            maps.A = make_tmap_2d(dW, (int64_t)m_tiles * KB * 256, 64, 256);
+        } else {
+            CUDA_OK(cudaMemcpy(dW, W, (size_t)M * K * 2, cudaMemcpyHostToDevice));
+            maps.A = make_tmap_2d(dW, (int64_t)m_tiles * 256, K, 256);
+        }
+        CUDA_OK(cudaMemcpy(dX, X, xbytes, cudaMemcpyHostToDevice));
         make_b_maps(maps, dX, T, K);
         a.part = (float*)dpart;
         a.out_f32 = (float*)dY;

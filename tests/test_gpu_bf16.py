@@ -29,16 +29,16 @@ def from_bf16_bits(b):
     return (b.astype(np.uint32) << 16).view(np.float32)
 
 
-def run_gemm(sd, W, X, grid=0):
+def run_gemm(sd, W, X, grid=0, flags=0):
     L = sd.lib()
     fn = L.sd_debug_gemm
     fn.argtypes = [np.ctypeslib.ndpointer(np.uint16), np.ctypeslib.ndpointer(np.uint16), C.c_int, C.c_int, C.c_int,
-                   C.c_int, np.ctypeslib.ndpointer(np.float32), C.POINTER(C.c_float)]
+                   C.c_int, C.c_int, np.ctypeslib.ndpointer(np.float32), C.POINTER(C.c_float)]
     M, K = W.shape
     T = X.shape[0]
     Y = np.zeros((T, M), np.float32)
     us = C.c_float()
-    rc = fn(np.ascontiguousarray(W), np.ascontiguousarray(X), M, K, T, grid, Y, C.byref(us))
+    rc = fn(np.ascontiguousarray(W), np.ascontiguousarray(X), M, K, T, grid, flags, Y, C.byref(us))
     assert rc == 0
     return Y, us.value
 
@@ -50,10 +50,12 @@ def test_gemm_matches_fp64(sd, M, K, T, grid):
     rng = np.random.default_rng(M * 7 + K + T)
     W = to_bf16_bits(rng.uniform(-1, 1, (M, K)).astype(np.float32))
     X = to_bf16_bits(rng.uniform(-1, 1, (T, K)).astype(np.float32))
-    Y, _ = run_gemm(sd, W, X, grid)
     ref = from_bf16_bits(X).astype(np.float64) @ from_bf16_bits(W).astype(np.float64).T
+    Y, _ = run_gemm(sd, W, X, grid)
     err = np.abs(Y - ref)
     assert err.max() <= 2e-3 * np.abs(ref).max() + 1e-3, (err.max(), np.abs(ref).max())
+    Yt, _ = run_gemm(sd, W, X, grid, flags=1)  # tile-major weights give the same bits
+    assert np.array_equal(Yt.view(np.uint32), Y.view(np.uint32))
 
 
 def bf16_vs_oracle(sd, oracle, cfg, B, prompt_len, seed):

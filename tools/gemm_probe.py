@@ -10,7 +10,7 @@ from paper_2405_07542_b200 import specdec as sd
 L = sd.lib()
 fn = L.sd_debug_gemm
 fn.argtypes = [np.ctypeslib.ndpointer(np.uint16), np.ctypeslib.ndpointer(np.uint16), C.c_int, C.c_int, C.c_int,
-               C.c_int, np.ctypeslib.ndpointer(np.float32), C.POINTER(C.c_float)]
+               C.c_int, C.c_int, np.ctypeslib.ndpointer(np.float32), C.POINTER(C.c_float)]
 rng = np.random.default_rng(0)
 shapes = {"qkv": (15360, 5120), "o": (5120, 5120), "fc": (20480, 5120), "proj": (5120, 20480), "lm": (50272, 5120)}
 only = sys.argv[1:] or list(shapes)
@@ -21,11 +21,11 @@ for name in only:
         X = rng.integers(0, 1 << 15, size=(T, K), dtype=np.uint16) & 0x3FFF
         Y = np.zeros((T, M), np.float32)
         res = []
-        for grid in (0, 74, 37):
+        for grid, flags in ((0, 0), (0, 1)):
             us = C.c_float()
             best = 1e9
             for _ in range(3):
-                fn(W, X, M, K, T, grid, Y, C.byref(us))
+                fn(W, X, M, K, T, grid, flags, Y, C.byref(us))
                 best = min(best, us.value)
-            res.append(f"g{grid or 148}={best:7.1f}us ({M * K * 2 / best / 1e3:6.0f} GB/s)")
+            res.append(f"{'tiled' if flags else 'rowmj'}={best:7.1f}us ({M * K * 2 / best / 1e3:6.0f} GB/s)")
         print(f"{name:5s} T={T:3d} " + "  ".join(res), flush=True)
