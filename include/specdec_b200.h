@@ -185,6 +185,8 @@ int sd_session_run_host(sd_session* s, int32_t* steps, float* gpu_ms, int64_t* h
 int sd_session_outputs(sd_session* s, int32_t* gen_tokens, int32_t* gen_counts, int32_t* log_k,
                        int32_t* log_tau, int max_steps);
 int sd_session_cache(sd_session* s, sd_cache** out);
+/* run n device steps eagerly (no graph, no completion loop) -- profiling */
+int sd_session_step(sd_session* s, int n);
 void sd_session_destroy(sd_session* s);
 
 #ifdef __cplusplus

@@ -1,6 +1,7 @@
 // C ABI (include/specdec_b200.h) and the host-side validation that mirrors the
 // reference's contracts before any device work is launched.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -17,6 +18,15 @@ static std::atomic<int64_t> g_launches{0};
 void note_launches(int64_t n) { g_launches += n; }
 
 void set_device(int device) { CUDA_OK(cudaSetDevice(device)); }
+
+bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("SD_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on != 0;
+}
 
 // ---------------------------------------------------------------- workspace
 void Workspace::ensure(const Model& m, const Cache& c, int T) {

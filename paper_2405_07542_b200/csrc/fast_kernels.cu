@@ -17,6 +17,7 @@
 
 #include "gemm.h"
 #include "handles.h"
+#include "pdl.cuh"
 
 namespace sdb {
 
@@ -35,6 +36,8 @@ struct FastWorkspace {
     float* part_o = nullptr;   // [T][heads][max_splits][hd]
     float* part_ml = nullptr;  // [T][heads][max_splits][2]
     float* part = nullptr;     // stream-K partial sums (largest GEMM of the model)
+    int* row_cnt = nullptr;    // per-token LayerNorm arrival counters [256]
+    int* attn_cnt = nullptr;   // split-KV arrival counters [B * heads * 16]
     GemmMaps map_xb, map_ctx, map_act;
     std::vector<void*> allocs;
 };
@@ -119,6 +122,8 @@ __global__ void __launch_bounds__(kRowThreads) k_embed_ln(const __nv_bfloat16* _
                                                           float* __restrict__ resid, const float* __restrict__ g,
                                                           const float* __restrict__ b, __nv_bfloat16* __restrict__ y,
                                                           const int* __restrict__ dT) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ float scratch[32];
     int t = blockIdx.x;
     if (t >= *dT) return;
@@ -196,6 +201,7 @@ struct AttnArgs {
     __nv_bfloat16* ctx;        // [T][h]
     float* part_o;
     float* part_ml;
+    int* cnt;                  // [B * heads * q_tiles] split arrival counters (self-resetting)
     int h, heads, B, cap, layer, max_splits;
     float scale_log2;          // log2(e) / sqrt(hd)
 };
@@ -209,6 +215,8 @@ struct AttnArgs {
 // PAPER.md:872-876, re-reads it n_s times).
 template <int HD>
 __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
+    pdl_trigger();
+    pdl_wait();
     constexpr int kKeys = kKeysPerCta / 4;  // keys per warp
     const int sh = blockIdx.x, split = blockIdx.y, qt = blockIdx.z;
     const int s = sh / a.heads, head = sh % a.heads;
@@ -385,6 +393,8 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
 
 // merge split-KV partials: grid (T, heads), block HD
 __global__ void k_attn_combine(AttnArgs a, int hd, const int* __restrict__ dT) {
+    pdl_trigger();
+    pdl_wait();
     int t = blockIdx.x, head = blockIdx.y, d = threadIdx.x;
     if (t >= *dT) return;
     int s = a.plans[t].sample;
@@ -435,6 +445,10 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
                     std::make_pair(m.vocab_pad, (int)h)})
         part = std::max(part, gemm_part_floats(mk.first, mk.second, kSms));
     f->part = walloc<float>(f, part);
+    f->row_cnt = walloc<int>(f, 256);
+    f->attn_cnt = walloc<int>(f, (size_t)c.B * cfg.num_heads * 16);
+    CUDA_OK(cudaMemset(f->row_cnt, 0, sizeof(int) * 256));
+    CUDA_OK(cudaMemset(f->attn_cnt, 0, sizeof(int) * (size_t)c.B * cfg.num_heads * 16));
     make_b_maps(f->map_xb, f->xb, T, h);
     make_b_maps(f->map_ctx, f->ctx, T, h);
     make_b_maps(f->map_act, f->act, T, mm);
@@ -515,6 +529,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     base.T = n;
     base.dT = db.dT;
     base.part = f->part;
+    base.row_cnt = f->row_cnt;
     base.h = h;
     base.hd = hd;
     base.heads = heads;
@@ -523,9 +538,9 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     base.plans = dplans;
     base.kv = (__nv_bfloat16*)c.kv;
 
-    PROF(PK_ROW, k_embed_ln<<<n, kRowThreads, 0, st>>>((const __nv_bfloat16*)m.tok16, (const __nv_bfloat16*)m.pos16,
-                                                       tokens, dplans, h, resid, m.layers[0].ln1_g,
-                                                       m.layers[0].ln1_b, f->xb, db.dT));
+    PROF(PK_ROW, launch_k(k_embed_ln, dim3(n), dim3(kRowThreads), 0, st, (const __nv_bfloat16*)m.tok16,
+                          (const __nv_bfloat16*)m.pos16, tokens, dplans, h, resid, (const float*)m.layers[0].ln1_g,
+                          (const float*)m.layers[0].ln1_b, f->xb, (const int*)db.dT));
     launches++;
     AttnArgs at{};
     at.q = f->q;
@@ -537,6 +552,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     at.ctx = f->ctx;
     at.part_o = f->part_o;
     at.part_ml = f->part_ml;
+    at.cnt = f->attn_cnt;
     at.h = h;
     at.heads = heads;
     at.B = c.B;
@@ -565,12 +581,12 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         // attention
         at.layer = l;
         if (hd == 128)
-            PROF(PK_ATTN, k_attention<128><<<dim3(c.B * heads, splits, qtiles), 128, attn_smem, st>>>(at));
+            PROF(PK_ATTN, launch_k(k_attention<128>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
         else
-            PROF(PK_ATTN, k_attention<64><<<dim3(c.B * heads, splits, qtiles), 128, attn_smem, st>>>(at));
+            PROF(PK_ATTN, launch_k(k_attention<64>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
         launches++;
         if (splits > 1) {
-            PROF(PK_ATTN, k_attn_combine<<<dim3(n, heads), hd, 0, st>>>(at, hd, db.dT));
+            PROF(PK_ATTN, launch_k(k_attn_combine, dim3(n, heads), dim3(hd), 0, st, at, hd, (const int*)db.dT));
             launches++;
         }
         // O projection + residual, fused with LN2 -> xb

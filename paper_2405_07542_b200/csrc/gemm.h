@@ -21,6 +21,7 @@ struct GemmArgs {
     int T;                    // token count when dT == nullptr (must be <= 256)
     const int* dT;            // device token count (graph-capturable), or nullptr
     int grid, max_contrib;    // stream-K schedule (set by gemm_plan)
+    int box;                  // token-tile rows staged per k-block (set by gemm_launch)
     int a_tiled;              // W stored tile-major: [m_tile][K/64][256][64] (contiguous 32 KB boxes)
     float* part;              // fp32 partial sums [m_tiles * max_contrib][256 tok][256 rows]
     const float* bias;        // [M] or nullptr
@@ -29,6 +30,7 @@ struct GemmArgs {
     int ld_out;
     const float *ln_g, *ln_b; // EPI_RESID_LN
     __nv_bfloat16* ln_out;
+    int* row_cnt;             // EPI_RESID_LN: per-token tile arrival counters (zeroed, self-resetting)
     // EPI_QKV scatter into the KV arena [L][2][B][heads][cap][hd]
     __nv_bfloat16* kv;
     const Plan* plans;

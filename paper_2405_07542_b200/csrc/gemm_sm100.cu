@@ -29,6 +29,7 @@
 
 #include "../../include/specdec_b200_debug.h"
 #include "gemm.h"
+#include "pdl.cuh"
 #include "sm100_ptx.cuh"
 
 namespace sdb {
@@ -58,13 +59,12 @@ __global__ void __launch_bounds__(kThreads, 1)
            const __grid_constant__ CUtensorMap tmB256, const GemmArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    const int T = a.dT ? *a.dT : a.T;
-    if (T <= 0) return;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int BN = T <= 16 ? 16 : ((T + 15) / 16) * 16;
-    const int box = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    // smem layout from the host-side token bound (known before the predecessor
+    // finishes); the true token count is read after griddepcontrol.wait
+    const int box = a.box;
     const CUtensorMap* tmB = box == 32 ? &tmB32 : box == 64 ? &tmB64 : box == 128 ? &tmB128 : &tmB256;
-    const int nbuf = BN <= 128 ? 2 : 1;  // TMEM accumulator buffers
+    const int nbuf = box <= 128 ? 2 : 1;  // TMEM accumulator buffers
     // Decoupled rings: the weight (A) ring is as deep as smem allows so enough
     // HBM bytes stay in flight to cover DRAM latency; the token (B) ring is
     // shallow because B is L2-resident (re-read by every tile).
@@ -110,8 +110,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();  // tokens / partial buffer / token count come from earlier kernels
+    const int T = a.dT ? *a.dT : a.T;
+    const int BN = T <= 16 ? 16 : ((T + 15) / 16) * 16;
 
-    if (warp == 0) {
+    if (T <= 0 || BN > box) {
+        // nothing to do (a finished step) -- fall through to teardown
+    } else if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer A: one contiguous weight range
             const uint64_t pol_w = ptx::policy_evict_first();  // weights: streamed once
             int stage = 0;
@@ -234,32 +240,40 @@ __device__ __forceinline__ void tile_contrib(const RedInfo& r, int tile, int& n)
     n = cta_of(tk0 + r.KB - 1, r.G, r.U) - cta_of(tk0, r.G, r.U) + 1;
 }
 
-// grid (m_tiles, ceil(T_upper / kRT)), block 256: thread = one output feature
-// of the tile for kRT tokens; all kRT x contributors loads issue before use.
+// grid (m_tiles, ceil(T_upper / RT)), block 256: thread = one output feature
+// of the tile for RT tokens; all RT x contributors loads issue before use.
 constexpr int kRT = 16;
-template <int EPI>
+template <int EPI, int RT = kRT>
 __global__ void __launch_bounds__(256) k_reduce_tile(const GemmArgs a, const RedInfo r) {
-    const int tile = blockIdx.x, t0 = blockIdx.y * kRT, row = threadIdx.x;
+    pdl_trigger();
+    pdl_wait();
+    const int tile = blockIdx.x, t0 = blockIdx.y * RT, row = threadIdx.x;
     const int T = a.dT ? *a.dT : a.T;
     const int m = tile * 256 + row;
     if (t0 >= T || m >= a.M) return;
     int nc;
     tile_contrib(r, tile, nc);
     const float* __restrict__ p = a.part + ((size_t)tile * a.max_contrib * 256 + t0) * 256 + row;
-    float v[kRT];
+    float v[RT];
 #pragma unroll
-    for (int i = 0; i < kRT; ++i) v[i] = 0.0f;
+    for (int i = 0; i < RT; ++i) v[i] = 0.0f;
     for (int c = 0; c < nc; ++c) {
 #pragma unroll
-        for (int i = 0; i < kRT; ++i) v[i] += __ldcg(p + ((size_t)c * 256 + i) * 256);
+        for (int i = 0; i < RT; ++i) v[i] += __ldcg(p + ((size_t)c * 256 + i) * 256);
     }
     const float b = a.bias ? a.bias[m] : 0.0f;
-    const int nt = min(kRT, T - t0);
-    if constexpr (EPI == EPI_QKV) {
+    const int nt = min(RT, T - t0);
+    if constexpr (EPI == EPI_RESID_LN) {  // residual add; the LayerNorm runs in k_ln_rows
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+            if (i >= nt) break;
+            a.out_f32[(size_t)(t0 + i) * a.ld_out + m] += v[i] + b;
+        }
+    } else if constexpr (EPI == EPI_QKV) {
         const int which = m / a.h, hm = m - which * a.h;
         const int head = hm / a.hd, d = hm - head * a.hd;
 #pragma unroll
-        for (int i = 0; i < kRT; ++i) {
+        for (int i = 0; i < RT; ++i) {
             if (i >= nt) break;
             const int t = t0 + i;
             __nv_bfloat16 x = __float2bfloat16_rn(v[i] + b);
@@ -277,7 +291,7 @@ __global__ void __launch_bounds__(256) k_reduce_tile(const GemmArgs a, const Red
         }
     } else {
 #pragma unroll
-        for (int i = 0; i < kRT; ++i) {
+        for (int i = 0; i < RT; ++i) {
             if (i >= nt) break;
             const int t = t0 + i;
             if constexpr (EPI == EPI_STORE) a.out_f32[(size_t)t * a.ld_out + m] = v[i];
@@ -299,11 +313,129 @@ __device__ __forceinline__ float block_sum(float v, float* scratch) {
     return s;
 }
 
+// grid T_upper, block 256: LayerNorm of the updated residual row -> bf16
+// (two-pass mean / variance, eps 1e-5; hidden <= 8192)
+__global__ void __launch_bounds__(256) k_ln_rows(const GemmArgs a) {
+    pdl_trigger();
+    pdl_wait();
+    __shared__ float scratch[32];
+    const int t = blockIdx.x;
+    const int T = a.dT ? *a.dT : a.T;
+    if (t >= T) return;
+    const float4* __restrict__ row = (const float4*)(a.out_f32 + (size_t)t * a.ld_out);
+    constexpr int kPer = 8;  // float4 per thread
+    float4 x[kPer];
+    float s = 0.0f;
+    const int n4 = a.M / 4;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int i = threadIdx.x + k * 256;
+        x[k] = i < n4 ? row[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        s += x[k].x + x[k].y + x[k].z + x[k].w;
+    }
+    const float mean = block_sum<256>(s, scratch) / a.M;
+    float q = 0.0f;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int i = threadIdx.x + k * 256;
+        if (i < n4) {
+            float dx = x[k].x - mean, dy = x[k].y - mean, dz = x[k].z - mean, dw = x[k].w - mean;
+            q += dx * dx + dy * dy + dz * dz + dw * dw;
+        }
+    }
+    const float inv = rsqrtf(block_sum<256>(q, scratch) / a.M + 1e-5f);
+    __nv_bfloat162* y = (__nv_bfloat162*)(a.ln_out + (size_t)t * a.M);
+    const float4* g4 = (const float4*)a.ln_g;
+    const float4* b4 = (const float4*)a.ln_b;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int i = threadIdx.x + k * 256;
+        if (i < n4) {
+            float4 g = g4[i], b = b4[i];
+            y[2 * i] = __floats2bfloat162_rn((x[k].x - mean) * inv * g.x + b.x, (x[k].y - mean) * inv * g.y + b.y);
+            y[2 * i + 1] =
+                __floats2bfloat162_rn((x[k].z - mean) * inv * g.z + b.z, (x[k].w - mean) * inv * g.w + b.w);
+        }
+    }
+}
+
+// grid (m_tiles, ceil(T_upper / RT)), block 256: split-K sum + bias +
+// residual add for RT tokens of one tile; the block that completes a token
+// row's LAST tile (per-token arrival counter) then runs that row's LayerNorm
+// (two-pass, eps 1e-5) into bf16 -- no separate LN launch.
+template <int RT>
+__global__ void __launch_bounds__(256) k_reduce_resid_ln2(const GemmArgs a, const RedInfo r) {
+    pdl_trigger();
+    pdl_wait();
+    __shared__ float scratch[32];
+    __shared__ int s_last[RT];
+    const int tile = blockIdx.x, t0 = blockIdx.y * RT, row = threadIdx.x;
+    const int T = a.dT ? *a.dT : a.T;
+    if (t0 >= T) return;
+    const int m = tile * 256 + row;
+    const int nt = min(RT, T - t0);
+    if (m < a.M) {
+        int nc;
+        tile_contrib(r, tile, nc);
+        const float* __restrict__ p = a.part + ((size_t)tile * a.max_contrib * 256 + t0) * 256 + row;
+        float v[RT];
+#pragma unroll
+        for (int i = 0; i < RT; ++i) v[i] = 0.0f;
+        for (int c = 0; c < nc; ++c) {
+#pragma unroll
+            for (int i = 0; i < RT; ++i) v[i] += __ldcg(p + ((size_t)c * 256 + i) * 256);
+        }
+        const float b = a.bias[m];
+#pragma unroll
+        for (int i = 0; i < RT; ++i)
+            if (i < nt) a.out_f32[(size_t)(t0 + i) * a.ld_out + m] += v[i] + b;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x < nt) {
+        const int old = atomicAdd(&a.row_cnt[t0 + threadIdx.x], 1);
+        s_last[threadIdx.x] = old == a.m_tiles - 1;
+        if (old == a.m_tiles - 1) a.row_cnt[t0 + threadIdx.x] = 0;  // self-resetting
+    }
+    __syncthreads();
+    for (int i = 0; i < nt; ++i) {
+        if (!s_last[i]) continue;  // block-uniform
+        __threadfence();
+        const int t = t0 + i;
+        const float* rowp = a.out_f32 + (size_t)t * a.ld_out;
+        constexpr int kPer = 32;  // hidden <= 8192
+        float x[kPer];
+        float s = 0.0f;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int j = threadIdx.x + k * 256;
+            x[k] = j < a.M ? __ldcg(rowp + j) : 0.0f;
+            s += x[k];
+        }
+        const float mean = block_sum<256>(s, scratch) / a.M;
+        float q = 0.0f;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int j = threadIdx.x + k * 256;
+            if (j < a.M) q += (x[k] - mean) * (x[k] - mean);
+        }
+        const float inv = rsqrtf(block_sum<256>(q, scratch) / a.M + 1e-5f);
+        __nv_bfloat16* y = a.ln_out + (size_t)t * a.M;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int j = threadIdx.x + k * 256;
+            if (j < a.M) y[j] = __float2bfloat16_rn((x[k] - mean) * inv * a.ln_g[j] + a.ln_b[j]);
+        }
+    }
+}
+
 // grid T_upper, block 512: residual add of one token row, then the next
 // LayerNorm of that row (two-pass mean / variance, eps 1e-5) -> bf16.
 // All partial loads of the row are issued before any store.
 constexpr int kLnThreads = 512, kLnPer = 16;  // hidden <= 8192
 __global__ void __launch_bounds__(kLnThreads) k_reduce_resid_ln(const GemmArgs a, const RedInfo r) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ float scratch[32];
     const int t = blockIdx.x;
     const int T = a.dT ? *a.dT : a.T;
@@ -367,6 +499,8 @@ __global__ void __launch_bounds__(kLnThreads) k_reduce_resid_ln(const GemmArgs a
 constexpr int kArgTiles = 8;
 __global__ void __launch_bounds__(256) k_reduce_argmax(const GemmArgs a, const RedInfo r, float* __restrict__ pv,
                                                        int* __restrict__ pi, int* __restrict__ cnt) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ float sv[8];
     __shared__ int si[8];
     __shared__ int s_last;
@@ -525,14 +659,21 @@ void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, 
         prepared = true;
     }
     SD_CHECK(T_upper <= 256, INTERNAL, "GEMM token tile is at most 256");
-    k_gemm<<<a.grid, kThreads, kSmemBytes, st>>>(maps.A, maps.B[0], maps.B[1], maps.B[2], maps.B[3], a);
+    GemmArgs ab = a;
+    ab.box = T_upper <= 32 ? 32 : T_upper <= 64 ? 64 : T_upper <= 128 ? 128 : 256;
+    launch_k(k_gemm, dim3(a.grid), dim3(kThreads), kSmemBytes, st, maps.A, maps.B[0], maps.B[1], maps.B[2],
+             maps.B[3], ab);
     RedInfo r{a.K / kBK, a.grid, (long long)a.m_tiles * (a.K / kBK)};
     const dim3 tg(a.m_tiles, (T_upper + kRT - 1) / kRT);
     switch (epi) {
-        case EPI_STORE: k_reduce_tile<EPI_STORE><<<tg, 256, 0, st>>>(a, r); break;
-        case EPI_GELU: k_reduce_tile<EPI_GELU><<<tg, 256, 0, st>>>(a, r); break;
-        case EPI_QKV: k_reduce_tile<EPI_QKV><<<tg, 256, 0, st>>>(a, r); break;
-        case EPI_RESID_LN: k_reduce_resid_ln<<<T_upper, kLnThreads, 0, st>>>(a, r); break;
+        case EPI_STORE: launch_k(k_reduce_tile<EPI_STORE>, tg, dim3(256), 0, st, ab, r); break;
+        case EPI_GELU: launch_k(k_reduce_tile<EPI_GELU>, tg, dim3(256), 0, st, ab, r); break;
+        case EPI_QKV: launch_k(k_reduce_tile<EPI_QKV>, tg, dim3(256), 0, st, ab, r); break;
+        case EPI_RESID_LN:  // tile-parallel split-K sum + residual, then the row LayerNorm
+            SD_CHECK(a.M % 4 == 0 && a.M <= 8192, CONFIG, "bf16 mode needs hidden % 4 == 0 and <= 8192");
+            launch_k(k_reduce_tile<EPI_RESID_LN, 4>, dim3(a.m_tiles, (T_upper + 3) / 4), dim3(256), 0, st, ab, r);
+            launch_k(k_ln_rows, dim3(T_upper), dim3(256), 0, st, ab);
+            break;
         case EPI_ARGMAX: {
             static float* pv = nullptr;
             static int *pi = nullptr, *cnt = nullptr;
@@ -544,7 +685,7 @@ void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, 
             }
             const int groups = (a.m_tiles + kArgTiles - 1) / kArgTiles;
             SD_CHECK(groups <= 64, INTERNAL, "vocab too large for the argmax scratch");
-            k_reduce_argmax<<<dim3(T_upper, groups), 256, 0, st>>>(a, r, pv, pi, cnt);
+            launch_k(k_reduce_argmax, dim3(T_upper, groups), dim3(256), 0, st, ab, r, pv, pi, cnt);
             break;
         }
         default: throw Error(INTERNAL, "unknown GEMM epilogue");

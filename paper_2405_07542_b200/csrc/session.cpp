@@ -449,6 +449,16 @@ int sd_session_reset(sd_session* s) {
 int sd_session_run(sd_session* s, int use_graph, int graph_steps, int32_t* steps, float* gpu_ms) {
     return sguard([&] { *steps = session_run(s, use_graph, graph_steps, gpu_ms); });
 }
+// n eager device steps (no graph, no completion check): profiling hook
+int sd_session_step(sd_session* s, int n) {
+    return sguard([&] {
+        SD_CHECK(s->prefilled, CONTRACT, "session has not been prefilled");
+        set_device(s->model->m.device);
+        prepare_fast_kernels();
+        for (int i = 0; i < n; ++i) device_step(s, s->model->st);
+        CUDA_OK(cudaStreamSynchronize(s->model->st));
+    });
+}
 int sd_session_run_host(sd_session* s, int32_t* steps, float* gpu_ms, int64_t* h2d_bytes, int64_t* d2h_bytes) {
     return sguard([&] { *steps = session_run_host(s, gpu_ms, h2d_bytes, d2h_bytes); });
 }

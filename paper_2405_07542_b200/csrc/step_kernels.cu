@@ -12,6 +12,7 @@
 #include <cuda_bf16.h>
 
 #include "common.h"
+#include "pdl.cuh"
 #include "step.h"
 
 namespace sdb {
@@ -26,6 +27,8 @@ __device__ __forceinline__ int32_t draft_at(const StepArgs& a, int s, int doff, 
 // One block.  Thread 0 runs the O(B) prefix sums (B <= a few hundred), then
 // every thread fills token/plan rows in parallel.
 __global__ void k_pack(StepArgs a) {
+    pdl_trigger();
+    pdl_wait();
     const int B = a.B;
     if (threadIdx.x == 0) {
         int t = 0, d = 0, kmax = 0;
@@ -98,6 +101,8 @@ __global__ void k_pack(StepArgs a) {
 
 // One block, one thread per sample.
 __global__ void k_accept(StepArgs a) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ int s_taumax, s_active, s_step;
     if (threadIdx.x == 0) {
         s_taumax = 0;
@@ -181,6 +186,8 @@ __global__ void k_accept(StepArgs a) {
 // base + tau_max.  grid = (L * 2, B), block 256.
 template <typename T>
 __global__ void k_pad_fill(StepArgs a, T* kv, int heads, int hd) {
+    pdl_trigger();
+    pdl_wait();
     int lw = blockIdx.x, s = blockIdx.y;
     if (!a.tau[s]) return;
     int tmax = a.scalars[3];
@@ -203,6 +210,8 @@ __device__ __forceinline__ uint64_t splitmix_next(uint64_t& st) {  // rng.hpp:15
 
 // grid = B, block 128
 __global__ void k_predict(StepArgs a, PredictArgs p) {
+    pdl_trigger();
+    pdl_wait();
     const int s = blockIdx.x;
     __shared__ int s_best;
     if (!a.active[s]) {
@@ -251,17 +260,17 @@ __global__ void k_predict(StepArgs a, PredictArgs p) {
     }
 }
 
-void launch_pack(const StepArgs& a, cudaStream_t st) { k_pack<<<1, 256, 0, st>>>(a); }
-void launch_accept(const StepArgs& a, cudaStream_t st) { k_accept<<<1, 256, 0, st>>>(a); }
+void launch_pack(const StepArgs& a, cudaStream_t st) { launch_k(k_pack, dim3(1), dim3(256), 0, st, a); }
+void launch_accept(const StepArgs& a, cudaStream_t st) { launch_k(k_accept, dim3(1), dim3(256), 0, st, a); }
 void launch_pad_fill(const StepArgs& a, const Cache& c, cudaStream_t st) {
     dim3 grid(c.L * 2, c.B);
     if (c.elem_bytes == 4)
-        k_pad_fill<float><<<grid, 256, 0, st>>>(a, (float*)c.kv, c.heads, c.hd);
+        launch_k(k_pad_fill<float>, grid, dim3(256), 0, st, a, (float*)c.kv, c.heads, c.hd);
     else
-        k_pad_fill<__nv_bfloat16><<<grid, 256, 0, st>>>(a, (__nv_bfloat16*)c.kv, c.heads, c.hd);
+        launch_k(k_pad_fill<__nv_bfloat16>, grid, dim3(256), 0, st, a, (__nv_bfloat16*)c.kv, c.heads, c.hd);
 }
 void launch_predict(const StepArgs& a, const PredictArgs& p, cudaStream_t st) {
-    k_predict<<<a.B, 128, 0, st>>>(a, p);
+    launch_k(k_predict, dim3(a.B), dim3(128), 0, st, a, p);
 }
 
 }  // namespace sdb
