@@ -22,7 +22,8 @@
 namespace sdb {
 
 constexpr int kChunkTokens = 256;  // tokens per forward chunk (GEMM N <= 256)
-constexpr int kKeysPerCta = 128;   // attention split size (4 warps x 32 keys)
+constexpr int kSplit = 128;        // attention keys per CTA (4 warps x 32)
+constexpr int kQT = 8;             // queries per attention CTA (the mma N side)
 constexpr int kSms = 148;          // B200 SM count (stream-K GEMM grid)
 
 struct FastModelState {
@@ -206,182 +207,194 @@ struct AttnArgs {
     float scale_log2;          // log2(e) / sqrt(hd)
 };
 
-// One CTA = (sample, head) x 128-key split x 16-query tile; 4 warps each own
-// 32 keys.  S = Q K^T and O = P V run on mma.sync m16n8k16 (bf16 in, fp32
-// accumulate); the 4 warps' partial softmax states merge through smem (reusing
-// the K/V staging area).  68 KB of smem per CTA keeps 3 CTAs (12 warps, 192 KB
-// of K/V loads) in flight per SM.  A sample's K/V extent is read once per
-// split, not once per query token (the paper's per-token grid,
-// PAPER.md:872-876, re-reads it n_s times).
+// Ragged multi-query attention, "keys as M" formulation.
+//
+// One CTA = (sample, head) x 128-key split x 8-query tile; 4 warps each own 32
+// keys.  With only n_s <= 8 draft queries per sample, the tensor-core tile is
+// transposed so the KEYS are the 16-row M side and the queries the 8-wide N
+// side of mma.sync m16n8k16:  S^T = K Q^T  and  O^T += V^T P^T.  P^T is
+// re-laid from the S^T accumulator fragments with movmatrix (no smem trip),
+// the softmax reduces over keys with 3 shuffles, and the O^T accumulators are
+// 32 registers per thread.  This halves the MMA count of a 16-query tile and
+// keeps register pressure low enough for several CTAs per SM.  The 4 warps'
+// (max, sum, O) states merge through smem; splits merge in k_attn_combine.
+// A sample's K/V extent is read once per split, not once per query token (the
+// paper's per-token grid, re-reads it n_s times).
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+    uint32_t y;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+
 template <int HD>
 __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
     pdl_trigger();
     pdl_wait();
-    constexpr int kKeys = kKeysPerCta / 4;  // keys per warp
+    constexpr int kKeys = kSplit / 4;  // keys per warp (32)
     const int sh = blockIdx.x, split = blockIdx.y, qt = blockIdx.z;
     const int s = sh / a.heads, head = sh % a.heads;
     const SampleSeg seg = a.segs[s];
-    const int k_begin = split * kKeysPerCta;
-    if (seg.n_q == 0 || qt * 16 >= seg.n_q || k_begin >= seg.kv_len) return;
+    const int k_begin = split * kSplit;
+    if (seg.n_q == 0 || qt * kQT >= seg.n_q || k_begin >= seg.kv_len) return;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int nq = min(16, seg.n_q - qt * 16);
+    const int nq = min(kQT, seg.n_q - qt * kQT);
 
     extern __shared__ __align__(128) uint8_t sm[];
-    uint8_t* sQ = sm;                                                   // [16][HD]
-    uint8_t* sKV = sm + 16 * HD * 2;                                    // per warp: K[kKeys][HD], V[kKeys][HD]
-    uint8_t* sK = sKV + warp * 2 * kKeys * HD * 2;
+    uint8_t* sQ = sm;                                    // [8][HD]
+    uint8_t* sK = sm + kQT * HD * 2 + warp * 2 * kKeys * HD * 2;
     uint8_t* sV = sK + kKeys * HD * 2;
-    float* sMerge = (float*)sKV;  // reused after compute: [4][16][HD] + [4][16][2]
-    __shared__ int sWslot[16];
-    __shared__ int sTok[16];
+    float* sMerge = (float*)(sm + kQT * HD * 2);         // reused: [4][8][HD] + [4][8][2]
+    __shared__ int sWslot[kQT];
+    __shared__ int sTok[kQT];
 
-    // Q tile (rows >= nq zero-filled)
-    for (int i = threadIdx.x; i < 16 * HD / 8; i += 128) {
-        int r = i / (HD / 8), c8 = i % (HD / 8);
-        int tok = r < nq ? a.qidx[seg.q_start + qt * 16 + r] : 0;
-        const __nv_bfloat16* src = a.q + (size_t)tok * a.h + head * HD + c8 * 8;
-        cp_async16(sQ + swz<HD>(r, c8 * 8), src, r < nq);
-    }
-    if (threadIdx.x < 16) {
-        int r = threadIdx.x;
-        int tok = r < nq ? a.qidx[seg.q_start + qt * 16 + r] : -1;
-        sTok[r] = tok;
-        sWslot[r] = tok >= 0 ? a.plans[tok].write_slot : -1;
-    }
-    // this warp's K / V rows (rows past the extent are zero-filled)
     const int kw0 = k_begin + warp * kKeys;
     const size_t kbase = ((((size_t)a.layer * 2 + 0) * a.B + s) * a.heads + head) * (size_t)a.cap * HD;
     const size_t vbase = ((((size_t)a.layer * 2 + 1) * a.B + s) * a.heads + head) * (size_t)a.cap * HD;
-    const int kv_end = min(seg.kv_len, k_begin + kKeysPerCta);
-    for (int i = lane; i < kKeys * HD / 8; i += 32) {
-        int r = i / (HD / 8), c8 = i % (HD / 8);
-        int key = kw0 + r;
-        bool ok = key < kv_end;
-        size_t off = (size_t)(ok ? key : 0) * HD + c8 * 8;
+    const int kv_end = min(seg.kv_len, k_begin + kSplit);
+    for (int i = lane; i < kKeys * HD / 8; i += 32) {  // this warp's K / V rows (zero past the extent)
+        const int r = i / (HD / 8), c8 = i % (HD / 8);
+        const int key = kw0 + r;
+        const bool ok = key < kv_end;
+        const size_t off = (size_t)(ok ? key : 0) * HD + c8 * 8;
         cp_async16(sK + swz<HD>(r, c8 * 8), a.kv + kbase + off, ok);
         cp_async16(sV + swz<HD>(r, c8 * 8), a.kv + vbase + off, ok);
+    }
+    for (int i = threadIdx.x; i < kQT * HD / 8; i += 128) {  // Q tile (rows >= nq zero)
+        const int r = i / (HD / 8), c8 = i % (HD / 8);
+        const int tok = r < nq ? a.qidx[seg.q_start + qt * kQT + r] : 0;
+        cp_async16(sQ + swz<HD>(r, c8 * 8), a.q + (size_t)tok * a.h + head * HD + c8 * 8, r < nq);
+    }
+    if (threadIdx.x < kQT) {
+        const int r = threadIdx.x;
+        const int tok = r < nq ? a.qidx[seg.q_start + qt * kQT + r] : -1;
+        sTok[r] = tok;
+        sWslot[r] = tok >= 0 ? a.plans[tok].write_slot : -1;
     }
     cp_async_wait_all();
     __syncthreads();
 
     const int g = lane / 4, c = lane % 4;
+    // running softmax state for this thread's two query columns q = 2c, 2c+1
     float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
-    float o[HD / 8][4];
+    float o[HD / 16][4];  // O^T fragments: (hd d0+g / d0+g+8) x (q 2c, 2c+1)
 #pragma unroll
-    for (int n = 0; n < HD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.0f;
+    for (int n = 0; n < HD / 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.0f;
 
     if (kw0 < kv_end) {
         const uint32_t qa = (uint32_t)__cvta_generic_to_shared(sQ);
         const uint32_t ka = (uint32_t)__cvta_generic_to_shared(sK);
         const uint32_t va = (uint32_t)__cvta_generic_to_shared(sV);
-        // S = Q K^T : 16 x kKeys
-        float sacc[kKeys / 8][4];
+        // S^T = K Q^T : (kKeys keys) x (8 queries), as kKeys/16 m-tiles
+        float st[kKeys / 16][4];
 #pragma unroll
-        for (int n = 0; n < kKeys / 8; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.0f;
+        for (int t = 0; t < kKeys / 16; ++t) st[t][0] = st[t][1] = st[t][2] = st[t][3] = 0.0f;
 #pragma unroll
-        for (int kk = 0; kk < HD; kk += 16) {
-            uint32_t a0, a1, a2, a3;
-            ldsm_x4(qa + swz<HD>(lane % 16, kk + (lane / 16) * 8), a0, a1, a2, a3);
+        for (int kk = 0; kk < HD; kk += 32) {
+            // B = Q^T for two k-steps: matrices (q 0-7, hd kk), (kk+8), (kk+16), (kk+24)
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(qa + swz<HD>(lane % 8, kk + (lane / 8) * 8), b0, b1, b2, b3);
 #pragma unroll
-            for (int n = 0; n < kKeys / 8; n += 2) {
-                // matrices: (keys n*8.., cols kk), (keys n*8.., kk+8), (keys n*8+8.., kk), (keys n*8+8.., kk+8)
-                uint32_t b0, b1, b2, b3;
-                ldsm_x4(ka + swz<HD>(n * 8 + (lane % 8) + (lane / 16) * 8, kk + ((lane / 8) % 2) * 8), b0, b1, b2,
-                        b3);
-                mma_bf16(sacc[n], a0, a1, a2, a3, b0, b1);
-                mma_bf16(sacc[n + 1], a0, a1, a2, a3, b2, b3);
+            for (int t = 0; t < kKeys / 16; ++t) {
+                uint32_t a0, a1, a2, a3, e0, e1, e2, e3;
+                // A = K rows t*16.. : (keys 0-7, kk), (keys 8-15, kk), (keys 0-7, kk+8), (keys 8-15, kk+8)
+                ldsm_x4(ka + swz<HD>(t * 16 + (lane % 16), kk + (lane / 16) * 8), a0, a1, a2, a3);
+                ldsm_x4(ka + swz<HD>(t * 16 + (lane % 16), kk + 16 + (lane / 16) * 8), e0, e1, e2, e3);
+                mma_bf16(st[t], a0, a1, a2, a3, b0, b1);
+                mma_bf16(st[t], e0, e1, e2, e3, b2, b3);
             }
         }
-        // mask (own extent, causal write slot, padded-grid holes) + local max
+        // mask + max over this warp's keys for each query column
+        const int ws[2] = {sWslot[2 * c], sWslot[2 * c + 1]};
         float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-        for (int n = 0; n < kKeys / 8; ++n) {
+        for (int t = 0; t < kKeys / 16; ++t) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                int row = g + (e >= 2 ? 8 : 0);
-                int key = kw0 + n * 8 + 2 * c + (e & 1);
-                bool vis = key < kv_end && key <= sWslot[row] && !(a.pad && a.pad[(size_t)s * a.cap + key]);
-                float x = vis ? sacc[n][e] * a.scale_log2 : -INFINITY;
-                sacc[n][e] = x;
-                mx[e >> 1] = fmaxf(mx[e >> 1], x);
+                const int key = kw0 + t * 16 + g + (e >= 2 ? 8 : 0);
+                const int qi = e & 1;
+                const bool vis = key < kv_end && key <= ws[qi] && !(a.pad && a.pad[(size_t)s * a.cap + key]);
+                const float x = vis ? st[t][e] * a.scale_log2 : -INFINITY;
+                st[t][e] = x;
+                mx[qi] = fmaxf(mx[qi], x);
             }
         }
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-            mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-            m_run[r] = mx[r];
+        for (int qi = 0; qi < 2; ++qi) {
+            mx[qi] = fmaxf(mx[qi], __shfl_xor_sync(0xffffffffu, mx[qi], 4));
+            mx[qi] = fmaxf(mx[qi], __shfl_xor_sync(0xffffffffu, mx[qi], 8));
+            mx[qi] = fmaxf(mx[qi], __shfl_xor_sync(0xffffffffu, mx[qi], 16));
+            m_run[qi] = mx[qi];
         }
         float sum[2] = {0.0f, 0.0f};
-        uint32_t p[kKeys / 8][2];
+        uint32_t pb[kKeys / 16][2];  // P^T as mma B fragments (keys 2c.. / 2c+8.., q g)
 #pragma unroll
-        for (int n = 0; n < kKeys / 8; ++n) {
-            float e0 = m_run[0] == -INFINITY ? 0.0f : exp2f(sacc[n][0] - m_run[0]);
-            float e1 = m_run[0] == -INFINITY ? 0.0f : exp2f(sacc[n][1] - m_run[0]);
-            float e2 = m_run[1] == -INFINITY ? 0.0f : exp2f(sacc[n][2] - m_run[1]);
-            float e3 = m_run[1] == -INFINITY ? 0.0f : exp2f(sacc[n][3] - m_run[1]);
-            sum[0] += e0 + e1;
-            sum[1] += e2 + e3;
-            p[n][0] = pack_bf16(e0, e1);
-            p[n][1] = pack_bf16(e2, e3);
+        for (int t = 0; t < kKeys / 16; ++t) {
+            const float p0 = m_run[0] == -INFINITY ? 0.0f : exp2f(st[t][0] - m_run[0]);
+            const float p1 = m_run[1] == -INFINITY ? 0.0f : exp2f(st[t][1] - m_run[1]);
+            const float p2 = m_run[0] == -INFINITY ? 0.0f : exp2f(st[t][2] - m_run[0]);
+            const float p3 = m_run[1] == -INFINITY ? 0.0f : exp2f(st[t][3] - m_run[1]);
+            sum[0] += p0 + p2;
+            sum[1] += p1 + p3;
+            pb[t][0] = movmatrix_t(pack_bf16(p0, p1));  // rows = keys 0-7 of the tile
+            pb[t][1] = movmatrix_t(pack_bf16(p2, p3));  // rows = keys 8-15
         }
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            sum[r] += __shfl_xor_sync(0xffffffffu, sum[r], 1);
-            sum[r] += __shfl_xor_sync(0xffffffffu, sum[r], 2);
-            l_run[r] = sum[r];
+        for (int qi = 0; qi < 2; ++qi) {
+            sum[qi] += __shfl_xor_sync(0xffffffffu, sum[qi], 4);
+            sum[qi] += __shfl_xor_sync(0xffffffffu, sum[qi], 8);
+            sum[qi] += __shfl_xor_sync(0xffffffffu, sum[qi], 16);
+            l_run[qi] = sum[qi];
         }
-        // O = P V : 16 x HD, k = kKeys keys in steps of 16
+        // O^T += V^T P^T : per 16 keys (k-step) and 16 hd rows (m-tile)
 #pragma unroll
-        for (int ks = 0; ks < kKeys / 16; ++ks) {
-            uint32_t a0 = p[2 * ks][0], a1 = p[2 * ks][1], a2 = p[2 * ks + 1][0], a3 = p[2 * ks + 1][1];
+        for (int t = 0; t < kKeys / 16; ++t) {
 #pragma unroll
-            for (int n = 0; n < HD / 8; n += 2) {
-                uint32_t b0, b1, b2, b3;
-                int key = ks * 16 + (lane % 8) + ((lane / 8) % 2) * 8;
-                int col = n * 8 + (lane / 16) * 8;
-                ldsm_x4_t(va + swz<HD>(key, col), b0, b1, b2, b3);
-                mma_bf16(o[n], a0, a1, a2, a3, b0, b1);
-                mma_bf16(o[n + 1], a0, a1, a2, a3, b2, b3);
+            for (int n = 0; n < HD / 16; ++n) {
+                uint32_t a0, a1, a2, a3;
+                // A = V^T (hd x keys): trans of V blocks (keys t*16+[0,8)/[8,16), hd n*16+[0,8)/[8,16))
+                const int key = t * 16 + (lane % 8) + ((lane / 16) * 8);
+                const int col = n * 16 + ((lane / 8) % 2) * 8;
+                ldsm_x4_t(va + swz<HD>(key, col), a0, a1, a2, a3);
+                mma_bf16(o[n], a0, a1, a2, a3, pb[t][0], pb[t][1]);
             }
         }
     }
-    __syncthreads();  // every warp is done with K/V: reuse the area for the merge
-    float* mO = sMerge + (size_t)warp * 16 * HD;
-    float* mML = sMerge + 4 * 16 * HD + warp * 32;
+    __syncthreads();  // every warp is done with K / V: reuse the area for the merge
+    float* mO = sMerge + (size_t)warp * kQT * HD;   // [q][hd]
+    float* mML = sMerge + 4 * kQT * HD + warp * 2 * kQT;
 #pragma unroll
-    for (int n = 0; n < HD / 8; ++n) {
-        mO[g * HD + n * 8 + 2 * c] = o[n][0];
-        mO[g * HD + n * 8 + 2 * c + 1] = o[n][1];
-        mO[(g + 8) * HD + n * 8 + 2 * c] = o[n][2];
-        mO[(g + 8) * HD + n * 8 + 2 * c + 1] = o[n][3];
+    for (int n = 0; n < HD / 16; ++n) {
+        mO[(2 * c) * HD + n * 16 + g] = o[n][0];
+        mO[(2 * c + 1) * HD + n * 16 + g] = o[n][1];
+        mO[(2 * c) * HD + n * 16 + g + 8] = o[n][2];
+        mO[(2 * c + 1) * HD + n * 16 + g + 8] = o[n][3];
     }
-    if (c == 0) {
-        mML[g * 2] = m_run[0];
-        mML[g * 2 + 1] = l_run[0];
-        mML[(g + 8) * 2] = m_run[1];
-        mML[(g + 8) * 2 + 1] = l_run[1];
+    if (g == 0) {
+        mML[(2 * c) * 2] = m_run[0];
+        mML[(2 * c) * 2 + 1] = l_run[0];
+        mML[(2 * c + 1) * 2] = m_run[1];
+        mML[(2 * c + 1) * 2 + 1] = l_run[1];
     }
     __syncthreads();
-    const int nsplit = (seg.kv_len + kKeysPerCta - 1) / kKeysPerCta;
-    for (int i = threadIdx.x; i < 16 * HD; i += 128) {
-        int r = i / HD, d = i % HD;
+    const int nsplit = (seg.kv_len + kSplit - 1) / kSplit;
+    for (int i = threadIdx.x; i < kQT * HD; i += 128) {
+        const int r = i / HD, d = i % HD;
         if (r >= nq) continue;
         float M = -INFINITY;
-        for (int w = 0; w < 4; ++w) M = fmaxf(M, sMerge[4 * 16 * HD + w * 32 + r * 2]);
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, sMerge[4 * kQT * HD + w * 2 * kQT + r * 2]);
         float L = 0.0f, O = 0.0f;
         for (int w = 0; w < 4; ++w) {
-            float mw = sMerge[4 * 16 * HD + w * 32 + r * 2];
+            const float mw = sMerge[4 * kQT * HD + w * 2 * kQT + r * 2];
             if (mw == -INFINITY) continue;
-            float f = exp2f(mw - M);
-            L += sMerge[4 * 16 * HD + w * 32 + r * 2 + 1] * f;
-            O += sMerge[(size_t)w * 16 * HD + r * HD + d] * f;
+            const float f = exp2f(mw - M);
+            L += sMerge[4 * kQT * HD + w * 2 * kQT + r * 2 + 1] * f;
+            O += sMerge[(size_t)w * kQT * HD + r * HD + d] * f;
         }
-        int tok = sTok[r];
+        const int tok = sTok[r];
         if (nsplit == 1) {
             a.ctx[(size_t)tok * a.h + head * HD + d] = __float2bfloat16_rn(O / L);
         } else {
-            size_t base = ((size_t)tok * a.heads + head) * a.max_splits + split;
+            const size_t base = ((size_t)tok * a.heads + head) * a.max_splits + split;
             a.part_o[base * HD + d] = O;
             if (d == 0) {
                 a.part_ml[base * 2] = M;
@@ -398,7 +411,7 @@ __global__ void k_attn_combine(AttnArgs a, int hd, const int* __restrict__ dT) {
     int t = blockIdx.x, head = blockIdx.y, d = threadIdx.x;
     if (t >= *dT) return;
     int s = a.plans[t].sample;
-    int nsplit = (a.segs[s].kv_len + kKeysPerCta - 1) / kKeysPerCta;
+    int nsplit = (a.segs[s].kv_len + kSplit - 1) / kSplit;
     if (nsplit <= 1) return;
     size_t base = ((size_t)t * a.heads + head) * a.max_splits;
     float M = -INFINITY;
@@ -423,7 +436,7 @@ T* walloc(FastWorkspace* f, size_t n) {
 
 FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     FastWorkspace* f = ws.fast;
-    int max_splits = (c.cap + kKeysPerCta - 1) / kKeysPerCta;
+    int max_splits = (c.cap + kSplit - 1) / kSplit;
     if (f && f->B >= c.B && f->cap >= c.cap && f->max_splits >= max_splits) return f;
     free_fast_workspace(f);
     f = new FastWorkspace();
@@ -559,9 +572,9 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     at.cap = c.cap;
     at.max_splits = f->max_splits;
     at.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-    const int splits = std::max(1, (db.max_kv_upper + kKeysPerCta - 1) / kKeysPerCta);
-    const int qtiles = std::max(1, (db.max_q_upper + 15) / 16);
-    const size_t attn_smem = (size_t)16 * hd * 2 + 4 * 2 * (kKeysPerCta / 4) * hd * 2;
+    const int splits = std::max(1, (db.max_kv_upper + kSplit - 1) / kSplit);
+    const int qtiles = std::max(1, (db.max_q_upper + kQT - 1) / kQT);
+    const size_t attn_smem = (size_t)kQT * hd * 2 + (size_t)4 * 2 * (kSplit / 4) * hd * 2;
 
     for (int l = 0; l < cfg.num_layers; ++l) {
         const FastLayer& L = m.layers[l];
