@@ -250,6 +250,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2405_07542_b200 import sharding
     from paper_2405_07542_b200 import specdec as sd
 
     V = cfg["vocab_size"]
@@ -281,7 +282,7 @@ def main():
         return ms_tot, acc_tot, steps_tot, stats
 
     B = a.batch
-    gids = list(range(rank * B, (rank + 1) * B))
+    gids = sharding.local_ids(B, rank)
     t_setup = time.time()
     ems, prompts = make_session("ems", B, gids)
     pad, _ = make_session("vanilla", B, gids)
@@ -310,11 +311,8 @@ def main():
         c = torch.tensor([ems_acc, pad_acc], device="cuda", dtype=torch.float64)
         dist.all_reduce(c)
         ems_acc_all, pad_acc_all = c.tolist()
-        # gather per-sample outputs (the run's only collective)
-        toks = torch.tensor([t + [-1] * (a.max_new - len(t)) for t in ems.outputs()[0]], device="cuda",
-                            dtype=torch.int32)
-        gathered = [torch.empty_like(toks) for _ in range(world)]
-        dist.all_gather(gathered, toks)
+        # gather per-sample outputs (the run's only collective, NCCL over NVLink)
+        sharding.gather_outputs(ems.outputs()[0], a.max_new, dist, device="cuda")
     else:
         ems_ms_max, pad_ms_max, ems_acc_all, pad_acc_all = ems_ms, pad_ms, ems_acc, pad_acc
     value = ems_acc_all / (ems_ms_max / 1000.0)
@@ -375,7 +373,7 @@ def main():
             if b == B:
                 sweep[b] = {"ems": value / world, "padded": padded_value / world}
                 continue
-            g = list(range(rank * b, (rank + 1) * b))
+            g = sharding.local_ids(b, rank)
             se, _ = make_session("ems", b, g)
             sp, _ = make_session("vanilla", b, g)
             r_e = timed(se, 2, 1)
