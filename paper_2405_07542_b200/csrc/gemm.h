@@ -22,7 +22,9 @@ struct GemmArgs {
     const int* dT;            // device token count (graph-capturable), or nullptr
     int grid, max_contrib;    // stream-K schedule (set by gemm_plan)
     int box;                  // token-tile rows staged per k-block (set by gemm_launch)
-    int a_tiled;              // W stored tile-major: [m_tile][K/64][256][64] (contiguous 32 KB boxes)
+    int dbg;                  // probe only: bit0 skip MMAs, bit1 skip partial stores
+    int a_tiled;              // 1: W tile-major [m_tile][K/64][256][64] (TMA); 2: same, pre-swizzled (bulk copy)
+    const void* a_ptr;        // a_tiled == 2: base of the pre-swizzled tiles
     float* part;              // fp32 partial sums [m_tiles * max_contrib][256 tok][256 rows]
     const float* bias;        // [M] or nullptr
     float* out_f32;           // EPI_STORE output / EPI_RESID_LN residual stream

@@ -53,6 +53,7 @@ __device__ __forceinline__ float gelu_fast(float x) {
     return 0.5f * x * (1.0f + t);
 }
 
+// Partial-sum buffer layout: [tile * max_contrib + contributor][256 tokens][256 rows] fp32.
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB32,
            const __grid_constant__ CUtensorMap tmB64, const __grid_constant__ CUtensorMap tmB128,
@@ -111,14 +112,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     pdl_trigger();
-    pdl_wait();  // tokens / partial buffer / token count come from earlier kernels
-    const int T = a.dT ? *a.dT : a.T;
-    const int BN = T <= 16 ? 16 : ((T + 15) / 16) * 16;
 
-    if (T <= 0 || BN > box) {
-        // nothing to do (a finished step) -- fall through to teardown
-    } else if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer A: one contiguous weight range
+    if (warp == 0) {
+        // ---------------- TMA producer A: one contiguous weight range.  Weights
+        // do not depend on earlier kernels, so this starts BEFORE
+        // griddepcontrol.wait and the ring fills while the predecessor drains.
+        if (lane == 0) {
             const uint64_t pol_w = ptx::policy_evict_first();  // weights: streamed once
             int stage = 0;
             uint32_t phase = 0;
@@ -126,7 +125,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(&emptyA[stage], phase ^ 1);
                 uint8_t* sa = a_base + stage * kABytes;
                 ptx::mbar_arrive_expect_tx(&fullA[stage], kABytes);
-                if (a.a_tiled)
+                if (a.a_tiled == 2)  // pre-swizzled contiguous 32 KB tile: one bulk copy
+                    ptx::bulk_load(sa, (const uint8_t*)a.a_ptr + (size_t)u * kABytes, kABytes, &fullA[stage], pol_w);
+                else if (a.a_tiled)
                     ptx::tma_load_2d(sa, &tmA, &fullA[stage], 0, (int)(u * kBM), pol_w);
                 else
                     ptx::tma_load_2d(sa, &tmA, &fullA[stage], (int)(u % KB) * kBK, (int)(u / KB) * kBM, pol_w);
@@ -136,93 +137,106 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp == 3) {
-        if (lane == 0) {  // ---------------- TMA producer B: the token tile of each k-block
-            const uint64_t pol_x = ptx::policy_evict_last();  // tokens: re-read by every tile
-            int stage = 0;
-            uint32_t phase = 0;
-            for (long long u = u0; u < u1; ++u) {
-                ptx::mbar_wait(&emptyB[stage], phase ^ 1);
-                ptx::mbar_arrive_expect_tx(&fullB[stage], b_bytes);
-                ptx::tma_load_2d(b_base + stage * b_bytes, tmB, &fullB[stage], (int)(u % KB) * kBK, 0, pol_x);
-                if (++stage == SB) {
-                    stage = 0;
-                    phase ^= 1;
+    } else {
+        pdl_wait();  // tokens, partial buffer and token count come from earlier kernels
+        const int T = a.dT ? *a.dT : a.T;
+        const int BN = T <= 16 ? 16 : ((T + 15) / 16) * 16;
+        const bool idle = T <= 0 || BN > box;  // a finished step: drain the A ring only
+        if (warp == 3) {
+            if (lane == 0 && !idle) {  // ---------------- TMA producer B: the token tile of each k-block
+                const uint64_t pol_x = ptx::policy_evict_last();  // tokens: re-read by every tile
+                int stage = 0;
+                uint32_t phase = 0;
+                for (long long u = u0; u < u1; ++u) {
+                    ptx::mbar_wait(&emptyB[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&fullB[stage], b_bytes);
+                    ptx::tma_load_2d(b_base + stage * b_bytes, tmB, &fullB[stage], (int)(u % KB) * kBK, 0, pol_x);
+                    if (++stage == SB) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
             }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
-            const uint32_t idesc = ptx::umma_idesc_bf16(128, BN);
-            int sa_i = 0, sb_i = 0;
-            uint32_t pa = 0, pb = 0, seg = 0;
+        } else if (warp == 1) {
+            if (lane == 0) {  // ---------------- MMA issuer
+                const uint32_t idesc = ptx::umma_idesc_bf16(128, BN);
+                int sa_i = 0, sb_i = 0;
+                uint32_t pa = 0, pb = 0, seg = 0;
+                for (long long u = u0; u < u1; ++seg) {
+                    int kb0 = (int)(u % KB);
+                    int kb1 = (int)min((long long)KB, kb0 + (u1 - u));
+                    const int buf = nbuf == 2 ? (int)(seg & 1) : 0;
+                    const uint32_t use = nbuf == 2 ? seg >> 1 : seg;
+                    if (!idle) {
+                        ptx::mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);
+                        ptx::tc_fence_after();
+                    }
+                    const uint32_t d0 = tmem + (nbuf == 2 ? buf * 256 : 0);
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        ptx::mbar_wait(&fullA[sa_i], pa);
+                        if (!idle) {
+                            ptx::mbar_wait(&fullB[sb_i], pb);
+                            ptx::tc_fence_after();
+                            uint32_t sa = ptx::smem_u32(a_base + sa_i * kABytes);
+                            uint32_t sb = ptx::smem_u32(b_base + sb_i * b_bytes);
+                            if (!(a.dbg & 1)) {
+#pragma unroll
+                                for (int k = 0; k < kBK / 16; ++k) {
+                                    uint64_t bdesc = ptx::umma_desc_kmajor_sw128(sb + k * 32);
+#pragma unroll
+                                    for (int acc = 0; acc < 2; ++acc) {
+                                        uint64_t adesc = ptx::umma_desc_kmajor_sw128(sa + acc * (128 * 128) + k * 32);
+                                        ptx::umma_bf16(d0 + acc * (nbuf == 2 ? 128 : 256), adesc, bdesc, idesc,
+                                                       (kb > kb0 || k > 0) ? 1u : 0u);
+                                    }
+                                }
+                            }
+                            ptx::umma_commit(&emptyB[sb_i]);
+                            if (++sb_i == SB) {
+                                sb_i = 0;
+                                pb ^= 1;
+                            }
+                        }
+                        ptx::umma_commit(&emptyA[sa_i]);
+                        if (++sa_i == SA) {
+                            sa_i = 0;
+                            pa ^= 1;
+                        }
+                    }
+                    if (!idle) ptx::umma_commit(&tmem_full[buf]);
+                    u += kb1 - kb0;
+                }
+            }
+        } else if (warp >= 4 && !idle) {  // ---------------- epilogue: TMEM -> fp32 partials
+            const int w = warp - 4;
+            const int row_in_acc = w * 32 + lane;
+            const uint64_t pol_keep = ptx::policy_evict_last();  // partials are re-read from L2
+            uint32_t seg = 0;
             for (long long u = u0; u < u1; ++seg) {
-                int kb0 = (int)(u % KB);
+                int tile = (int)(u / KB), kb0 = (int)(u % KB);
                 int kb1 = (int)min((long long)KB, kb0 + (u1 - u));
                 const int buf = nbuf == 2 ? (int)(seg & 1) : 0;
                 const uint32_t use = nbuf == 2 ? seg >> 1 : seg;
-                ptx::mbar_wait(&tmem_empty[buf], (use & 1) ^ 1);
+                const int ci = (int)blockIdx.x - cta_of((long long)tile * KB, G, U);
+                float* dst = a.part + (size_t)(tile * a.max_contrib + ci) * 256 * 256;
+                ptx::mbar_wait(&tmem_full[buf], use & 1);
                 ptx::tc_fence_after();
-                const uint32_t d0 = tmem + (nbuf == 2 ? buf * 256 : 0);
-                for (int kb = kb0; kb < kb1; ++kb) {
-                    ptx::mbar_wait(&fullA[sa_i], pa);
-                    ptx::mbar_wait(&fullB[sb_i], pb);
-                    ptx::tc_fence_after();
-                    uint32_t sa = ptx::smem_u32(a_base + sa_i * kABytes);
-                    uint32_t sb = ptx::smem_u32(b_base + sb_i * b_bytes);
+                const uint32_t trow = tmem + ((uint32_t)(w * 32) << 16) + (nbuf == 2 ? buf * 256 : 0);
+                for (int acc = 0; acc < 2; ++acc) {
+                    float* dcol = dst + acc * 128 + row_in_acc;  // [token][row]: a warp stores 128 B per token
+                    for (int j0 = 0; j0 < BN; j0 += 16) {
+                        float v[16];
+                        ptx::tmem_ld16(trow + acc * (nbuf == 2 ? 128 : 256) + j0, v);
+                        if (!(a.dbg & 2)) {
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k) {
-                        uint64_t bdesc = ptx::umma_desc_kmajor_sw128(sb + k * 32);
-#pragma unroll
-                        for (int acc = 0; acc < 2; ++acc) {
-                            uint64_t adesc = ptx::umma_desc_kmajor_sw128(sa + acc * (128 * 128) + k * 32);
-                            ptx::umma_bf16(d0 + acc * (nbuf == 2 ? 128 : 256), adesc, bdesc, idesc,
-                                           (kb > kb0 || k > 0) ? 1u : 0u);
+                            for (int i = 0; i < 16; ++i) ptx::st_f32_hint(dcol + (size_t)(j0 + i) * 256, v[i], pol_keep);
                         }
                     }
-                    ptx::umma_commit(&emptyA[sa_i]);
-                    ptx::umma_commit(&emptyB[sb_i]);
-                    if (++sa_i == SA) {
-                        sa_i = 0;
-                        pa ^= 1;
-                    }
-                    if (++sb_i == SB) {
-                        sb_i = 0;
-                        pb ^= 1;
-                    }
                 }
-                ptx::umma_commit(&tmem_full[buf]);
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&tmem_empty[buf]);
                 u += kb1 - kb0;
             }
-        }
-    } else if (warp >= 4) {  // ---------------- epilogue: TMEM -> fp32 partials
-        const int w = warp - 4;
-        const int row_in_acc = w * 32 + lane;
-        const uint64_t pol_keep = ptx::policy_evict_last();  // partials are re-read from L2
-        const int ncols = BN;
-        uint32_t seg = 0;
-        for (long long u = u0; u < u1; ++seg) {
-            int tile = (int)(u / KB), kb0 = (int)(u % KB);
-            int kb1 = (int)min((long long)KB, kb0 + (u1 - u));
-            const int buf = nbuf == 2 ? (int)(seg & 1) : 0;
-            const uint32_t use = nbuf == 2 ? seg >> 1 : seg;
-            const int ci = (int)blockIdx.x - cta_of((long long)tile * KB, G, U);
-            float* dst = a.part + (size_t)(tile * a.max_contrib + ci) * 256 * 256;
-            ptx::mbar_wait(&tmem_full[buf], use & 1);
-            ptx::tc_fence_after();
-            const uint32_t trow = tmem + ((uint32_t)(w * 32) << 16) + (nbuf == 2 ? buf * 256 : 0);
-            for (int acc = 0; acc < 2; ++acc) {
-                const int row = acc * 128 + row_in_acc;
-                for (int j0 = 0; j0 < ncols; j0 += 16) {
-                    float v[16];
-                    ptx::tmem_ld16(trow + acc * (nbuf == 2 ? 128 : 256) + j0, v);
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) ptx::st_f32_hint(dst + (size_t)(j0 + i) * 256 + row, v[i], pol_keep);
-                }
-            }
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&tmem_empty[buf]);
-            u += kb1 - kb0;
         }
     }
     __syncthreads();
@@ -241,7 +255,8 @@ __device__ __forceinline__ void tile_contrib(const RedInfo& r, int tile, int& n)
 }
 
 // grid (m_tiles, ceil(T_upper / RT)), block 256: thread = one output feature
-// of the tile for RT tokens; all RT x contributors loads issue before use.
+// (tile row) for RT consecutive tokens, read as float4; contributors summed in
+// order (deterministic).
 constexpr int kRT = 16;
 template <int EPI, int RT = kRT>
 __global__ void __launch_bounds__(256) k_reduce_tile(const GemmArgs a, const RedInfo r) {
@@ -254,21 +269,20 @@ __global__ void __launch_bounds__(256) k_reduce_tile(const GemmArgs a, const Red
     int nc;
     tile_contrib(r, tile, nc);
     const float* __restrict__ p = a.part + ((size_t)tile * a.max_contrib * 256 + t0) * 256 + row;
+    const int nt = min(RT, T - t0);
     float v[RT];
 #pragma unroll
     for (int i = 0; i < RT; ++i) v[i] = 0.0f;
     for (int c = 0; c < nc; ++c) {
 #pragma unroll
-        for (int i = 0; i < RT; ++i) v[i] += __ldcg(p + ((size_t)c * 256 + i) * 256);
+        for (int i = 0; i < RT; ++i)
+            if (i < nt) v[i] += __ldcg(p + ((size_t)c * 256 + i) * 256);
     }
     const float b = a.bias ? a.bias[m] : 0.0f;
-    const int nt = min(RT, T - t0);
     if constexpr (EPI == EPI_RESID_LN) {  // residual add; the LayerNorm runs in k_ln_rows
 #pragma unroll
-        for (int i = 0; i < RT; ++i) {
-            if (i >= nt) break;
-            a.out_f32[(size_t)(t0 + i) * a.ld_out + m] += v[i] + b;
-        }
+        for (int i = 0; i < RT; ++i)
+            if (i < nt) a.out_f32[(size_t)(t0 + i) * a.ld_out + m] += v[i] + b;
     } else if constexpr (EPI == EPI_QKV) {
         const int which = m / a.h, hm = m - which * a.h;
         const int head = hm / a.hd, d = hm - head * a.hd;
@@ -359,216 +373,89 @@ __global__ void __launch_bounds__(256) k_ln_rows(const GemmArgs a) {
     }
 }
 
-// grid (m_tiles, ceil(T_upper / RT)), block 256: split-K sum + bias +
-// residual add for RT tokens of one tile; the block that completes a token
-// row's LAST tile (per-token arrival counter) then runs that row's LayerNorm
-// (two-pass, eps 1e-5) into bf16 -- no separate LN launch.
-template <int RT>
-__global__ void __launch_bounds__(256) k_reduce_resid_ln2(const GemmArgs a, const RedInfo r) {
-    pdl_trigger();
-    pdl_wait();
-    __shared__ float scratch[32];
-    __shared__ int s_last[RT];
-    const int tile = blockIdx.x, t0 = blockIdx.y * RT, row = threadIdx.x;
-    const int T = a.dT ? *a.dT : a.T;
-    if (t0 >= T) return;
-    const int m = tile * 256 + row;
-    const int nt = min(RT, T - t0);
-    if (m < a.M) {
-        int nc;
-        tile_contrib(r, tile, nc);
-        const float* __restrict__ p = a.part + ((size_t)tile * a.max_contrib * 256 + t0) * 256 + row;
-        float v[RT];
-#pragma unroll
-        for (int i = 0; i < RT; ++i) v[i] = 0.0f;
-        for (int c = 0; c < nc; ++c) {
-#pragma unroll
-            for (int i = 0; i < RT; ++i) v[i] += __ldcg(p + ((size_t)c * 256 + i) * 256);
-        }
-        const float b = a.bias[m];
-#pragma unroll
-        for (int i = 0; i < RT; ++i)
-            if (i < nt) a.out_f32[(size_t)(t0 + i) * a.ld_out + m] += v[i] + b;
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x < nt) {
-        const int old = atomicAdd(&a.row_cnt[t0 + threadIdx.x], 1);
-        s_last[threadIdx.x] = old == a.m_tiles - 1;
-        if (old == a.m_tiles - 1) a.row_cnt[t0 + threadIdx.x] = 0;  // self-resetting
-    }
-    __syncthreads();
-    for (int i = 0; i < nt; ++i) {
-        if (!s_last[i]) continue;  // block-uniform
-        __threadfence();
-        const int t = t0 + i;
-        const float* rowp = a.out_f32 + (size_t)t * a.ld_out;
-        constexpr int kPer = 32;  // hidden <= 8192
-        float x[kPer];
-        float s = 0.0f;
-#pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const int j = threadIdx.x + k * 256;
-            x[k] = j < a.M ? __ldcg(rowp + j) : 0.0f;
-            s += x[k];
-        }
-        const float mean = block_sum<256>(s, scratch) / a.M;
-        float q = 0.0f;
-#pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const int j = threadIdx.x + k * 256;
-            if (j < a.M) q += (x[k] - mean) * (x[k] - mean);
-        }
-        const float inv = rsqrtf(block_sum<256>(q, scratch) / a.M + 1e-5f);
-        __nv_bfloat16* y = a.ln_out + (size_t)t * a.M;
-#pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const int j = threadIdx.x + k * 256;
-            if (j < a.M) y[j] = __float2bfloat16_rn((x[k] - mean) * inv * a.ln_g[j] + a.ln_b[j]);
-        }
-    }
-}
-
-// grid T_upper, block 512: residual add of one token row, then the next
-// LayerNorm of that row (two-pass mean / variance, eps 1e-5) -> bf16.
-// All partial loads of the row are issued before any store.
-constexpr int kLnThreads = 512, kLnPer = 16;  // hidden <= 8192
-__global__ void __launch_bounds__(kLnThreads) k_reduce_resid_ln(const GemmArgs a, const RedInfo r) {
-    pdl_trigger();
-    pdl_wait();
-    __shared__ float scratch[32];
-    const int t = blockIdx.x;
-    const int T = a.dT ? *a.dT : a.T;
-    if (t >= T) return;
-    float x[kLnPer];
-    int ncs[kLnPer];
-    const float* __restrict__ part = a.part;
-#pragma unroll
-    for (int k = 0; k < kLnPer; ++k) {
-        const int m = threadIdx.x + k * kLnThreads;
-        x[k] = 0.0f;
-        ncs[k] = 0;
-        if (m < a.M) tile_contrib(r, m >> 8, ncs[k]);
-    }
-    int ncmax = 0;
-#pragma unroll
-    for (int k = 0; k < kLnPer; ++k) ncmax = max(ncmax, ncs[k]);
-    for (int c = 0; c < ncmax; ++c) {
-#pragma unroll
-        for (int k = 0; k < kLnPer; ++k) {
-            const int m = threadIdx.x + k * kLnThreads;
-            if (c < ncs[k])
-                x[k] += __ldcg(part + (((size_t)(m >> 8) * a.max_contrib + c) * 256 + t) * 256 + (m & 255));
-        }
-    }
-    float* __restrict__ res = a.out_f32 + (size_t)t * a.ld_out;
-    float s = 0.0f;
-#pragma unroll
-    for (int k = 0; k < kLnPer; ++k) {
-        const int m = threadIdx.x + k * kLnThreads;
-        if (m < a.M) {
-            x[k] += res[m] + a.bias[m];
-            s += x[k];
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < kLnPer; ++k) {
-        const int m = threadIdx.x + k * kLnThreads;
-        if (m < a.M) res[m] = x[k];
-    }
-    const float mean = block_sum<kLnThreads>(s, scratch) / a.M;
-    float q = 0.0f;
-#pragma unroll
-    for (int k = 0; k < kLnPer; ++k) {
-        const int m = threadIdx.x + k * kLnThreads;
-        if (m < a.M) q += (x[k] - mean) * (x[k] - mean);
-    }
-    const float inv = rsqrtf(block_sum<kLnThreads>(q, scratch) / a.M + 1e-5f);
-    __nv_bfloat16* y = a.ln_out + (size_t)t * a.M;
-#pragma unroll
-    for (int k = 0; k < kLnPer; ++k) {
-        const int m = threadIdx.x + k * kLnThreads;
-        if (m < a.M) y[m] = __float2bfloat16_rn((x[k] - mean) * inv * a.ln_g[m] + a.ln_b[m]);
-    }
-}
-
-// grid (T_upper, ceil(m_tiles / 8)), block 256: LM-head logits of one token
-// for 8 vocab tiles, reduced to a (max, lowest id) partial; the last block of
-// a token (arrival counter) folds the partials into greedy_next
-// (model.cpp:34-41).
+// grid (ceil(T_upper / 4), ceil(m_tiles / kArgTiles)), block 256: LM-head
+// logits of 4 tokens over kArgTiles vocab tiles, reduced to (max, lowest id)
+// partials per token; the last block of a token (arrival counter) folds them
+// into greedy_next (model.cpp:34-41).
 constexpr int kArgTiles = 8;
 __global__ void __launch_bounds__(256) k_reduce_argmax(const GemmArgs a, const RedInfo r, float* __restrict__ pv,
                                                        int* __restrict__ pi, int* __restrict__ cnt) {
     pdl_trigger();
     pdl_wait();
-    __shared__ float sv[8];
-    __shared__ int si[8];
-    __shared__ int s_last;
-    const int t = blockIdx.x, g = blockIdx.y;
+    __shared__ float sv[8][4];
+    __shared__ int si[8][4];
+    __shared__ int s_last[4];
+    const int t0 = blockIdx.x * 4, grp = blockIdx.y, row = threadIdx.x;
     const int T = a.dT ? *a.dT : a.T;
-    if (t >= T) return;
-    float bv = -INFINITY;
-    int bi = 0x7fffffff;
+    if (t0 >= T) return;
+    const int nt = min(4, T - t0);
+    float bv[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
     bool bad = false;
-    const int tile0 = g * kArgTiles;
-    float v[kArgTiles];
-    int nc[kArgTiles];
-#pragma unroll
-    for (int k = 0; k < kArgTiles; ++k) {
-        v[k] = 0.0f;
-        nc[k] = 0;
-        if (tile0 + k < a.m_tiles) tile_contrib(r, tile0 + k, nc[k]);
-    }
-    int ncmax = 0;
-#pragma unroll
-    for (int k = 0; k < kArgTiles; ++k) ncmax = max(ncmax, nc[k]);
-    for (int c = 0; c < ncmax; ++c) {
-#pragma unroll
-        for (int k = 0; k < kArgTiles; ++k)
-            if (c < nc[k])
-                v[k] += __ldcg(a.part + ((((size_t)(tile0 + k) * a.max_contrib + c) * 256 + t) * 256) + threadIdx.x);
-    }
-#pragma unroll
     for (int k = 0; k < kArgTiles; ++k) {  // ascending ids per thread: strict > keeps the lowest
-        const int m = (tile0 + k) * 256 + threadIdx.x;
-        if (tile0 + k < a.m_tiles && m < a.vocab) {
-            if (a.logits) a.logits[(size_t)t * a.vocab + m] = v[k];
-            if (!isfinite(v[k])) bad = true;
-            if (v[k] > bv) {
-                bv = v[k];
-                bi = m;
+        const int tile = grp * kArgTiles + k;
+        const int m = tile * 256 + row;
+        if (tile >= a.m_tiles) break;
+        int nc;
+        tile_contrib(r, tile, nc);
+        const float* p = a.part + ((size_t)tile * a.max_contrib * 256 + t0) * 256 + row;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = 0; c < nc; ++c) {
+            const float* q = p + (size_t)c * 65536;
+            v.x += __ldcg(q);
+            if (nt > 1) v.y += __ldcg(q + 256);
+            if (nt > 2) v.z += __ldcg(q + 512);
+            if (nt > 3) v.w += __ldcg(q + 768);
+        }
+        if (m >= a.vocab) continue;
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (i >= nt) break;
+            if (a.logits) a.logits[(size_t)(t0 + i) * a.vocab + m] = vv[i];
+            if (!isfinite(vv[i])) bad = true;
+            if (vv[i] > bv[i]) {
+                bv[i] = vv[i];
+                bi[i] = m;
             }
         }
     }
     if (bad) atomicExch(a.flag, 1);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (ov > bv || (ov == bv && oi < bi)) {
-            bv = ov;
-            bi = oi;
+    for (int i = 0; i < 4; ++i) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            float ov = __shfl_xor_sync(0xffffffffu, bv[i], off);
+            int oi = __shfl_xor_sync(0xffffffffu, bi[i], off);
+            if (ov > bv[i] || (ov == bv[i] && oi < bi[i])) {
+                bv[i] = ov;
+                bi[i] = oi;
+            }
+        }
+        if (threadIdx.x % 32 == 0) {
+            sv[threadIdx.x / 32][i] = bv[i];
+            si[threadIdx.x / 32][i] = bi[i];
         }
     }
-    if (threadIdx.x % 32 == 0) {
-        sv[threadIdx.x / 32] = bv;
-        si[threadIdx.x / 32] = bi;
-    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < nt) {
+        const int i = threadIdx.x, t = t0 + i;
+        float b = sv[0][i];
+        int idx = si[0][i];
         for (int w = 1; w < 8; ++w)
-            if (sv[w] > bv || (sv[w] == bv && si[w] < bi)) {
-                bv = sv[w];
-                bi = si[w];
+            if (sv[w][i] > b || (sv[w][i] == b && si[w][i] < idx)) {
+                b = sv[w][i];
+                idx = si[w][i];
             }
-        pv[(size_t)t * gridDim.y + g] = bv;
-        pi[(size_t)t * gridDim.y + g] = bi;
+        pv[(size_t)t * gridDim.y + grp] = b;
+        pi[(size_t)t * gridDim.y + grp] = idx;
         __threadfence();
         const int old = atomicAdd(&cnt[t], 1);
-        s_last = old == (int)gridDim.y - 1;
+        s_last[i] = old == (int)gridDim.y - 1;
     }
     __syncthreads();
-    if (s_last && threadIdx.x == 0) {
+    if (threadIdx.x < nt && s_last[threadIdx.x]) {
+        const int t = t0 + threadIdx.x;
         __threadfence();
         float best = __ldcg(pv + (size_t)t * gridDim.y);
         int bidx = __ldcg(pi + (size_t)t * gridDim.y);
@@ -685,9 +572,10 @@ void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, 
             }
             const int groups = (a.m_tiles + kArgTiles - 1) / kArgTiles;
             SD_CHECK(groups <= 64, INTERNAL, "vocab too large for the argmax scratch");
-            launch_k(k_reduce_argmax, dim3(T_upper, groups), dim3(256), 0, st, ab, r, pv, pi, cnt);
+            launch_k(k_reduce_argmax, dim3((T_upper + 3) / 4, groups), dim3(256), 0, st, ab, r, pv, pi, cnt);
             break;
         }
+        case -1: break;  // probe: streaming kernel only
         default: throw Error(INTERNAL, "unknown GEMM epilogue");
     }
     CUDA_OK(cudaGetLastError());
@@ -716,7 +604,22 @@ extern "C" int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K,
         CUDA_OK(cudaMemset(dW, 0, wbytes));
         GemmMaps maps;
         a.a_tiled = flags & 1;
-        if (a.a_tiled) {  // tile-major weights: [m_tile][K/64][256][64]
+        a.dbg = (flags >> 1) & 3;                  // bit1 skip MMAs, bit2 skip partial stores
+        const int epi = (flags & 8) ? -1 : EPI_STORE;  // bit3: time the streaming kernel alone
+        if (flags & 16) {  // tile-major AND pre-swizzled (SW128 K-major smem image): bulk copies
+            a.a_tiled = 2;
+            int KB = K / 64;
+            std::vector<uint16_t> wt((size_t)m_tiles * 256 * K, 0);
+            for (int t = 0; t < m_tiles; ++t)
+                for (int kb = 0; kb < KB; ++kb)
+                    for (int r = 0; r < 256 && t * 256 + r < M; ++r)
+                        for (int j = 0; j < 8; ++j)
+                            std::memcpy(&wt[(((size_t)t * KB + kb) * 256 + r) * 64 + ((j ^ (r & 7)) * 8)],
+                                        &W[(size_t)(t * 256 + r) * K + kb * 64 + j * 8], 16);
+            CUDA_OK(cudaMemcpy(dW, wt.data(), wbytes, cudaMemcpyHostToDevice));
+            a.a_ptr = dW;
+            maps.A = make_tmap_2d(dW, (int64_t)m_tiles * KB * 256, 64, 256);  // unused
+        } else if (a.a_tiled) {  // tile-major weights: [m_tile][K/64][256][64]
             int KB = K / 64;
             std::vector<uint16_t> wt((size_t)m_tiles * 256 * K, 0);
             for (int t = 0; t < m_tiles; ++t)
@@ -738,10 +641,10 @@ extern "C" int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K,
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
-        gemm_launch(EPI_STORE, a, maps, T, 0);  // warm-up / configure
+        gemm_launch(epi, a, maps, T, 0);  // warm-up / configure
         CUDA_OK(cudaDeviceSynchronize());
         cudaEventRecord(e0);
-        gemm_launch(EPI_STORE, a, maps, T, 0);
+        gemm_launch(epi, a, maps, T, 0);
         cudaEventRecord(e1);
         CUDA_OK(cudaDeviceSynchronize());
         float ms = 0;
