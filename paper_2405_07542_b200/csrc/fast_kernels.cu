@@ -14,10 +14,14 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gemm.h"
 #include "handles.h"
 #include "pdl.cuh"
+#include "trace.cuh"
+
+SD_TRACE_TU(fast)
 
 namespace sdb {
 
@@ -36,10 +40,16 @@ struct FastWorkspace {
     __nv_bfloat16 *xb = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr;
     float* part_o = nullptr;   // [T][heads][max_splits][hd]
     float* part_ml = nullptr;  // [T][heads][max_splits][2]
-    float* part = nullptr;     // stream-K partial sums (largest GEMM of the model)
-    int* row_cnt = nullptr;    // per-token LayerNorm arrival counters [256]
+    float* part[2] = {nullptr, nullptr};  // stream-K partial sums, alternating between chained GEMMs
+    int* gemm_cnt = nullptr;   // per GEMM call site: kGemmCntInts counters, zeroed per forward
+    int n_sites = 0;
+    float* arg_v = nullptr;    // LM-head per-tile argmax partials [256][kGemmMaxTiles]
+    int* arg_i = nullptr;
     int* attn_cnt = nullptr;   // split-KV arrival counters [B * heads * 16]
     GemmMaps map_xb, map_ctx, map_act;
+    // per GEMM call site: the model's weight map + this workspace's token maps
+    std::vector<GemmMaps> map_qkv, map_o, map_fc, map_proj;
+    GemmMaps map_lm;
     std::vector<void*> allocs;
 };
 
@@ -58,16 +68,16 @@ void build_fast_model(Model& m) {
     auto* f = new FastModelState();
     for (const FastLayer& L : m.layers) {
         GemmMaps g;
-        g.A = make_tmap_2d(L.wqkv, 3 * h, h, 256);
+        g.A = make_tmap_2d(L.wqkv, 3 * h, h, kGemmTile);
         f->qkv.push_back(g);
-        g.A = make_tmap_2d(L.wo, h, h, 256);
+        g.A = make_tmap_2d(L.wo, h, h, kGemmTile);
         f->o.push_back(g);
-        g.A = make_tmap_2d(L.wfc, mm, h, 256);
+        g.A = make_tmap_2d(L.wfc, mm, h, kGemmTile);
         f->fc.push_back(g);
-        g.A = make_tmap_2d(L.wproj, h, mm, 256);
+        g.A = make_tmap_2d(L.wproj, h, mm, kGemmTile);
         f->proj.push_back(g);
     }
-    f->lm.A = make_tmap_2d(m.lm16, m.vocab_pad, h, 256);
+    f->lm.A = make_tmap_2d(m.lm16, m.vocab_pad, h, kGemmTile);
     m.fast = f;
 }
 
@@ -123,6 +133,7 @@ __global__ void __launch_bounds__(kRowThreads) k_embed_ln(const __nv_bfloat16* _
                                                           float* __restrict__ resid, const float* __restrict__ g,
                                                           const float* __restrict__ b, __nv_bfloat16* __restrict__ y,
                                                           const int* __restrict__ dT) {
+    CtaTrace trace__(TK_EMBED_LN);
     pdl_trigger();
     pdl_wait();
     __shared__ float scratch[32];
@@ -228,6 +239,7 @@ __device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
 
 template <int HD>
 __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
+    CtaTrace trace__(TK_ATTN);
     pdl_trigger();
     pdl_wait();
     constexpr int kKeys = kSplit / 4;  // keys per warp (32)
@@ -406,6 +418,7 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
 
 // merge split-KV partials: grid (T, heads), block HD
 __global__ void k_attn_combine(AttnArgs a, int hd, const int* __restrict__ dT) {
+    CtaTrace trace__(TK_ATTN_COMBINE);
     pdl_trigger();
     pdl_wait();
     int t = blockIdx.x, head = blockIdx.y, d = threadIdx.x;
@@ -457,14 +470,34 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
                     std::make_pair((int)mm, (int)h), std::make_pair((int)h, (int)mm),
                     std::make_pair(m.vocab_pad, (int)h)})
         part = std::max(part, gemm_part_floats(mk.first, mk.second, kSms));
-    f->part = walloc<float>(f, part);
-    f->row_cnt = walloc<int>(f, 256);
+    f->part[0] = walloc<float>(f, part);
+    f->part[1] = walloc<float>(f, part);
+    f->n_sites = cfg.num_layers * 4 + 1;
+    f->gemm_cnt = walloc<int>(f, (size_t)f->n_sites * kGemmCntInts);
+    f->arg_v = walloc<float>(f, (size_t)256 * kGemmMaxTiles);
+    f->arg_i = walloc<int>(f, (size_t)256 * kGemmMaxTiles);
     f->attn_cnt = walloc<int>(f, (size_t)c.B * cfg.num_heads * 16);
-    CUDA_OK(cudaMemset(f->row_cnt, 0, sizeof(int) * 256));
     CUDA_OK(cudaMemset(f->attn_cnt, 0, sizeof(int) * (size_t)c.B * cfg.num_heads * 16));
     make_b_maps(f->map_xb, f->xb, T, h);
     make_b_maps(f->map_ctx, f->ctx, T, h);
     make_b_maps(f->map_act, f->act, T, mm);
+    const FastModelState* fm = m.fast;
+    for (int l = 0; l < cfg.num_layers; ++l) {
+        GemmMaps g = f->map_xb;
+        g.A = fm->qkv[l].A;
+        f->map_qkv.push_back(g);
+        g = f->map_ctx;
+        g.A = fm->o[l].A;
+        f->map_o.push_back(g);
+        g = f->map_xb;
+        g.A = fm->fc[l].A;
+        f->map_fc.push_back(g);
+        g = f->map_act;
+        g.A = fm->proj[l].A;
+        f->map_proj.push_back(g);
+    }
+    f->map_lm = f->map_xb;
+    f->map_lm.A = fm->lm.A;
     ws.fast = f;
     return f;
 }
@@ -476,19 +509,20 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
 // launching stream and charge it the ALGORITHMIC bytes it must move
 // (weights + activations + KV it reads/writes once).  bench.py reads this
 // to report the dominant kernel's achieved bandwidth.
-enum ProfKind { PK_QKV, PK_O, PK_FC, PK_PROJ, PK_LM, PK_ATTN, PK_ROW, PK_MISC, PK_N };
+enum ProfKind { PK_GEMM, PK_ATTN, PK_ROW, PK_MISC, PK_N };
 struct ProfRec {
     int kind;
+    double wb, tc;  // algorithmic bytes = wb + T * tc (attention: from the KV extents; wb < 0: combine)
     cudaEvent_t a, b;
 };
 static bool g_prof = false;
 static std::vector<ProfRec> g_prof_pending;
 static double g_prof_acc[PK_N][3];  // launches, ms, bytes
 
-#define PROF(kind, ...)                                    \
+#define PROF(kind, wb, tc, ...)                            \
     do {                                                   \
         if (g_prof) {                                      \
-            ProfRec r__{kind, nullptr, nullptr};           \
+            ProfRec r__{kind, wb, tc, nullptr, nullptr};   \
             CUDA_OK(cudaEventCreate(&r__.a));              \
             CUDA_OK(cudaEventCreate(&r__.b));              \
             CUDA_OK(cudaEventRecord(r__.a, st));           \
@@ -539,10 +573,11 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     int64_t launches = 0;
 
     GemmArgs base{};
-    base.T = n;
-    base.dT = db.dT;
-    base.part = f->part;
-    base.row_cnt = f->row_cnt;
+    base.arg_v = f->arg_v;
+    base.arg_i = f->arg_i;
+    // every GEMM call site owns a counter region, zeroed once per forward
+    CUDA_OK(cudaMemsetAsync(f->gemm_cnt, 0, sizeof(int) * (size_t)f->n_sites * kGemmCntInts, st));
+    auto site = [&](int l, int k) { return f->gemm_cnt + (size_t)(l * 4 + k) * kGemmCntInts; };
     base.h = h;
     base.hd = hd;
     base.heads = heads;
@@ -551,7 +586,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     base.plans = dplans;
     base.kv = (__nv_bfloat16*)c.kv;
 
-    PROF(PK_ROW, launch_k(k_embed_ln, dim3(n), dim3(kRowThreads), 0, st, (const __nv_bfloat16*)m.tok16,
+    PROF(PK_ROW, 0.0, 6.0 * h, launch_k(k_embed_ln, dim3(n), dim3(kRowThreads), 0, st, (const __nv_bfloat16*)m.tok16,
                           (const __nv_bfloat16*)m.pos16, tokens, dplans, h, resid, (const float*)m.layers[0].ln1_g,
                           (const float*)m.layers[0].ln1_b, f->xb, (const int*)db.dT));
     launches++;
@@ -576,90 +611,140 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     const int qtiles = std::max(1, (db.max_q_upper + kQT - 1) / kQT);
     const size_t attn_smem = (size_t)kQT * hd * 2 + (size_t)4 * 2 * (kSplit / 4) * hd * 2;
 
-    for (int l = 0; l < cfg.num_layers; ++l) {
-        const FastLayer& L = m.layers[l];
-        const FastModelState* fm = m.fast;
-        // QKV + scatter (Q -> q16, K/V -> the arena at each token's write slot)
-        GemmArgs g = base;
+    // the four GEMMs of a layer and the LM head, as chain links
+    auto qkv = [&](int l, GemmChain& ch, const GemmMaps*& mp) {
+        GemmArgs& g = ch.g[ch.n];
+        g = base;
+        g.epi = EPI_QKV;
         g.M = 3 * h;
         g.K = h;
-        g.m_tiles = (3 * h + 255) / 256;
-        g.bias = L.bqkv;
+        g.m_tiles = (3 * h + kGemmTile - 1) / kGemmTile;
+        g.cnt = site(l, 0);
+        g.bias = m.layers[l].bqkv;
         g.out_bf16 = f->q;
         g.layer = l;
-        gemm_plan(g, kSms);
-        GemmMaps mp = f->map_xb;
-        mp.A = fm->qkv[l].A;
-        PROF(PK_QKV, gemm_launch(EPI_QKV, g, mp, n, st));
-        // attention
-        at.layer = l;
-        if (hd == 128)
-            PROF(PK_ATTN, launch_k(k_attention<128>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
-        else
-            PROF(PK_ATTN, launch_k(k_attention<64>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
-        launches++;
-        if (splits > 1) {
-            PROF(PK_ATTN, launch_k(k_attn_combine, dim3(n, heads), dim3(hd), 0, st, at, hd, (const int*)db.dT));
-            launches++;
-        }
-        // O projection + residual, fused with LN2 -> xb
+        mp = &f->map_qkv[l];
+    };
+    auto o_proj = [&](int l, GemmChain& ch, const GemmMaps*& mp) {
+        GemmArgs& g = ch.g[ch.n];
         g = base;
+        g.epi = EPI_RESID_LN;  // residual, fused with LN2 -> xb
         g.M = h;
         g.K = h;
-        g.m_tiles = (h + 255) / 256;
-        g.bias = L.bo;
+        g.m_tiles = (h + kGemmTile - 1) / kGemmTile;
+        g.cnt = site(l, 1);
+        g.bias = m.layers[l].bo;
         g.out_f32 = resid;
         g.ld_out = h;
-        g.ln_g = L.ln2_g;
-        g.ln_b = L.ln2_b;
+        g.ln_g = m.layers[l].ln2_g;
+        g.ln_b = m.layers[l].ln2_b;
         g.ln_out = f->xb;
-        gemm_plan(g, kSms);
-        mp = f->map_ctx;
-        mp.A = fm->o[l].A;
-        PROF(PK_O, gemm_launch(EPI_RESID_LN, g, mp, n, st));
-        // FC + GELU
+        mp = &f->map_o[l];
+    };
+    auto fc = [&](int l, GemmChain& ch, const GemmMaps*& mp) {
+        GemmArgs& g = ch.g[ch.n];
         g = base;
+        g.epi = EPI_GELU;
         g.M = mm;
         g.K = h;
-        g.m_tiles = (mm + 255) / 256;
-        g.bias = L.bfc;
+        g.m_tiles = (mm + kGemmTile - 1) / kGemmTile;
+        g.cnt = site(l, 2);
+        g.bias = m.layers[l].bfc;
         g.out_bf16 = f->act;
         g.ld_out = mm;
-        gemm_plan(g, kSms);
-        mp = f->map_xb;
-        mp.A = fm->fc[l].A;
-        PROF(PK_FC, gemm_launch(EPI_GELU, g, mp, n, st));
-        // PROJ + residual, fused with the next LN1 (or the final LN) -> xb
+        mp = &f->map_fc[l];
+    };
+    auto proj = [&](int l, GemmChain& ch, const GemmMaps*& mp) {
+        GemmArgs& g = ch.g[ch.n];
         g = base;
+        g.epi = EPI_RESID_LN;  // residual, fused with the next LN1 (or the final LN) -> xb
         g.M = h;
         g.K = mm;
-        g.m_tiles = (h + 255) / 256;
-        g.bias = L.bproj;
+        g.m_tiles = (h + kGemmTile - 1) / kGemmTile;
+        g.cnt = site(l, 3);
+        g.bias = m.layers[l].bproj;
         g.out_f32 = resid;
         g.ld_out = h;
         g.ln_g = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_g : m.lnf_g;
         g.ln_b = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_b : m.lnf_b;
         g.ln_out = f->xb;
-        gemm_plan(g, kSms);
-        mp = f->map_act;
-        mp.A = fm->proj[l].A;
-        PROF(PK_PROJ, gemm_launch(EPI_RESID_LN, g, mp, n, st));
-        launches += 8;
+        mp = &f->map_proj[l];
+    };
+    auto lm = [&](GemmChain& ch, const GemmMaps*& mp) {
+        GemmArgs& g = ch.g[ch.n];
+        g = base;
+        g.epi = EPI_ARGMAX;
+        g.M = m.vocab_pad;
+        g.K = h;
+        g.m_tiles = m.vocab_pad / kGemmTile;
+        g.cnt = site(cfg.num_layers, 0);
+        g.vocab = cfg.vocab_size;
+        g.argmax = ws.d_argmax + t0;
+        g.logits = want_logits ? ws.d_logits + (size_t)t0 * cfg.vocab_size : nullptr;
+        g.flag = ws.d_flag;
+        mp = &f->map_lm;
+    };
+    // algorithmic bytes of a link: weights once + token operand + outputs
+    auto link_bytes = [&](const GemmArgs& g, double& wb, double& tc) {
+        wb += (double)g.M * g.K * 2;
+        double out = g.epi == EPI_QKV ? 3.0 * h * 2 : g.epi == EPI_GELU ? mm * 2.0 : g.epi == EPI_ARGMAX ? 4.0 : h * 10.0;
+        tc += g.K * 2.0 + out;
+    };
+    auto run_chain = [&](GemmChain& ch, const GemmMaps* const* mps) {
+        ch.T = n;
+        ch.dT = db.dT;
+        ch.T_upper = n;
+        static const int dbg = getenv("SD_GEMM_DBG") ? atoi(getenv("SD_GEMM_DBG")) : 0;
+        ch.dbg = dbg;
+        static const int pf = getenv("SD_GEMM_PREFETCH") ? atoi(getenv("SD_GEMM_PREFETCH")) : 0;
+        ch.prefetch = pf;
+        double wb = 0, tc = 0;
+        for (int i = 0; i < ch.n; ++i) {
+            ch.g[i].part = f->part[i & 1];
+            gemm_plan(ch.g[i], kSms);
+            link_bytes(ch.g[i], wb, tc);
+        }
+        PROF(PK_GEMM, wb, tc, chain_launch(ch, mps, st));
+        launches++;
+    };
+
+    {  // layer 0's QKV (+ scatter into the arena) on its own
+        GemmChain ch{};
+        const GemmMaps* mps[kMaxChain];
+        qkv(0, ch, mps[0]);
+        ch.n = 1;
+        run_chain(ch, mps);
     }
-    // LM head + greedy argmax
-    GemmArgs g = base;
-    g.M = m.vocab_pad;
-    g.K = h;
-    g.m_tiles = m.vocab_pad / 256;
-    g.vocab = cfg.vocab_size;
-    g.argmax = ws.d_argmax + t0;
-    g.logits = want_logits ? ws.d_logits + (size_t)t0 * cfg.vocab_size : nullptr;
-    g.flag = ws.d_flag;
-    gemm_plan(g, kSms);
-    GemmMaps mp = f->map_xb;
-    mp.A = m.fast->lm.A;
-    PROF(PK_LM, gemm_launch(EPI_ARGMAX, g, mp, n, st));
-    launches += 2;
+    for (int l = 0; l < cfg.num_layers; ++l) {
+        // ragged attention of layer l
+        at.layer = l;
+        if (hd == 128)
+            PROF(PK_ATTN, 0.0, 0.0,
+                 launch_k(k_attention<128>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
+        else
+            PROF(PK_ATTN, 0.0, 0.0,
+                 launch_k(k_attention<64>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
+        launches++;
+        if (splits > 1) {
+            PROF(PK_ATTN, -1.0, 0.0, launch_k(k_attn_combine, dim3(n, heads), dim3(hd), 0, st, at, hd, (const int*)db.dT));
+            launches++;
+        }
+        // one persistent launch: O -> FC -> PROJ -> next layer's QKV (or the LM head)
+        GemmChain ch{};
+        const GemmMaps* mps[kMaxChain];
+        o_proj(l, ch, mps[ch.n]);
+        ch.n++;
+        fc(l, ch, mps[ch.n]);
+        ch.n++;
+        proj(l, ch, mps[ch.n]);
+        ch.n++;
+        if (l + 1 < cfg.num_layers)
+            qkv(l + 1, ch, mps[ch.n]);
+        else
+            lm(ch, mps[ch.n]);
+        ch.n++;
+        run_chain(ch, mps);
+    }
     note_launches(launches);
     CUDA_OK(cudaGetLastError());
     if (g_prof) {  // charge every timed launch its algorithmic bytes
@@ -670,23 +755,14 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         CUDA_OK(cudaMemcpy(segs.data(), db.segs, sizeof(SampleSeg) * c.B, cudaMemcpyDeviceToHost));
         double kv = 0;
         for (auto& sg : segs) kv += (double)sg.kv_len * (sg.n_q > 0);
-        const double H = h, Mm = mm, Tt = T, V = cfg.vocab_size;
-        double bytes[PK_N] = {3 * H * H * 2 + Tt * H * 2 + Tt * 3 * H * 2,
-                              H * H * 2 + Tt * H * 2 + Tt * H * 8,
-                              Mm * H * 2 + Tt * H * 2 + Tt * Mm * 2,
-                              H * Mm * 2 + Tt * Mm * 2 + Tt * H * 8,
-                              V * H * 2 + Tt * H * 2,
-                              kv * 2 * hd * 2 * heads + Tt * H * 4,
-                              Tt * H * 6,
-                              0};
+        const double attn_bytes = kv * 2 * hd * 2 * heads + (double)T * h * 4;
         for (auto& r : g_prof_pending) {
             float ms = 0.0f;
             CUDA_OK(cudaEventElapsedTime(&ms, r.a, r.b));
             g_prof_acc[r.kind][0] += 1;
             g_prof_acc[r.kind][1] += ms;
-            // attention bytes are charged once per layer (combine adds none)
-            bool combine = r.kind == PK_ATTN && (&r != &g_prof_pending.front()) && (&r - 1)->kind == PK_ATTN;
-            g_prof_acc[r.kind][2] += combine ? 0.0 : bytes[r.kind];
+            // attention bytes are charged once per layer (the combine adds none)
+            g_prof_acc[r.kind][2] += r.kind == PK_ATTN ? (r.wb < 0 ? 0.0 : attn_bytes) : r.wb + (double)T * r.tc;
             cudaEventDestroy(r.a);
             cudaEventDestroy(r.b);
         }

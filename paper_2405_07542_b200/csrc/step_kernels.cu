@@ -14,6 +14,9 @@
 #include "common.h"
 #include "pdl.cuh"
 #include "step.h"
+#include "trace.cuh"
+
+SD_TRACE_TU(step)
 
 namespace sdb {
 
@@ -27,6 +30,7 @@ __device__ __forceinline__ int32_t draft_at(const StepArgs& a, int s, int doff, 
 // One block.  Thread 0 runs the O(B) prefix sums (B <= a few hundred), then
 // every thread fills token/plan rows in parallel.
 __global__ void k_pack(StepArgs a) {
+    CtaTrace trace__(TK_PACK);
     pdl_trigger();
     pdl_wait();
     const int B = a.B;
@@ -101,6 +105,7 @@ __global__ void k_pack(StepArgs a) {
 
 // One block, one thread per sample.
 __global__ void k_accept(StepArgs a) {
+    CtaTrace trace__(TK_ACCEPT);
     pdl_trigger();
     pdl_wait();
     __shared__ int s_taumax, s_active, s_step;
@@ -186,6 +191,7 @@ __global__ void k_accept(StepArgs a) {
 // base + tau_max.  grid = (L * 2, B), block 256.
 template <typename T>
 __global__ void k_pad_fill(StepArgs a, T* kv, int heads, int hd) {
+    CtaTrace trace__(TK_PAD_FILL);
     pdl_trigger();
     pdl_wait();
     int lw = blockIdx.x, s = blockIdx.y;
@@ -210,6 +216,7 @@ __device__ __forceinline__ uint64_t splitmix_next(uint64_t& st) {  // rng.hpp:15
 
 // grid = B, block 128
 __global__ void k_predict(StepArgs a, PredictArgs p) {
+    CtaTrace trace__(TK_PREDICT);
     pdl_trigger();
     pdl_wait();
     const int s = blockIdx.x;
