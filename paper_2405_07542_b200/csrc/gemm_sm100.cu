@@ -873,6 +873,8 @@ extern "C" int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K,
 namespace sdb {
 void trace_set_fast(const TraceBuf& b);
 void trace_set_step(const TraceBuf& b);
+void trace_set_attn(const TraceBuf& b);
+void trace_set_attn1(const TraceBuf& b);
 }  // namespace sdb
 namespace {
 sdb::TraceBuf g_host_trace{nullptr, nullptr, 0};
@@ -891,6 +893,8 @@ extern "C" int sd_debug_trace_begin(int cap) {
         trace_set_gemm(g_host_trace);
         trace_set_fast(g_host_trace);
         trace_set_step(g_host_trace);
+        trace_set_attn(g_host_trace);
+        trace_set_attn1(g_host_trace);
         CUDA_OK(cudaDeviceSynchronize());
         return 0;
     } catch (const Error& e) {
@@ -911,6 +915,8 @@ extern "C" int sd_debug_trace_end(void* out, int cap, int* n) {
         trace_set_gemm(off);
         trace_set_fast(off);
         trace_set_step(off);
+        trace_set_attn(off);
+        trace_set_attn1(off);
         return 0;
     } catch (const Error& e) {
         g_dbg_err = e.what();
