@@ -26,6 +26,8 @@ struct GemmArgs {
     int M, K, m_tiles;        // W is [m_tiles * 128][K] bf16 (rows >= M are zero or ignored)
     int max_contrib;          // stream-K schedule (set by gemm_plan)
     int n_slices;             // sum over tiles of their contributor counts (set by gemm_plan)
+    int owner_mode;           // 1: each tile's k-block-0 CTA reduces it (few contributors per tile);
+                              // 0: every CTA reduces an equal share of all tiles (set by gemm_plan)
     float* part;              // fp32 partial sums [m_tiles * max_contrib][256 tok][128 rows]
     int* cnt;                 // this call site's kGemmCntInts counters, zero before the launch
     const float* bias;        // [M] or nullptr

@@ -43,6 +43,7 @@
 // LayerNorm rows, argmax folds.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -247,11 +248,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ch
     const int b_stride = max(b_bytes, 16384);
     const int SB = P.sb > 0 ? min(P.sb, kMaxStagesB) : 3;
     const uint32_t stg_half = (uint32_t)(SB * b_stride / 2) & ~15u;
-    int SA = (kSmemBytes - 2048 - SB * b_stride) / kABytes;
+    bool has_arg = false;
+    for (int i = 0; i < P.n; ++i) has_arg |= P.g[i].epi == EPI_ARGMAX;
+    const int scratch_bytes = has_arg ? 2 * 16 * kBM * 4 : 0;  // argmax: [half][16 tokens][128 rows] fp32
+    int SA = (kSmemBytes - 2048 - SB * b_stride - scratch_bytes) / kABytes;
     if (SA > kMaxStagesA) SA = kMaxStagesA;
     uint8_t* a_base = smem;
     uint8_t* b_base = smem + SA * kABytes;
-    uint64_t* bars = (uint64_t*)(b_base + SB * b_stride);
+    float* arg_scratch = (float*)(b_base + SB * b_stride);
+    uint64_t* bars = (uint64_t*)(b_base + SB * b_stride + scratch_bytes);
     uint64_t* fullA = bars;
     uint64_t* emptyA = fullA + kMaxStagesA;
     uint64_t* fullB = emptyA + kMaxStagesA;
@@ -415,236 +420,459 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ch
                 }
             }
         } else if (warp >= 4 && !idle) {
-            // ---------------- epilogue warps: per GEMM, TMEM -> fp32 partials,
-            // then this CTA's reduction slices (+ LayerNorm rows / argmax folds)
-            // warps 4-11: TMEM lane quadrant warp % 4 (= tile rows), column half (warp - 4) / 4
-            const int row = (warp % 4) * 32 + lane, half = (warp - 4) / 4, etid = threadIdx.x - 128;
-            const uint64_t pol_keep = ptx::policy_evict_last();  // partials are re-read from L2
+            // ---------------- epilogue warps (4-11): TMEM lane quadrant warp % 4 =
+            // tile rows, column half (warp - 4) / 4 = alternate 16-token chunks.
+            // Per segment:
+            //   * not the tile's owner (it does not hold k-block 0): drain the
+            //     accumulator into the partial buffer and publish it;
+            //   * owner, sole contributor: the epilogue straight from TMEM;
+            //   * owner of a split tile -- always its CTA's LAST segment, and in
+            //     stream-K order every other contributor but the middle ones has
+            //     published long before -- add the others' partials (bulk-copied
+            //     into the then idle token ring, two token chunks in flight) to
+            //     the accumulator and apply the epilogue.
+            // The owner's own accumulator never leaves the SM.
+            const int q4 = warp % 4, half = (warp - 4) / 4;
+            const int row = q4 * 32 + lane, etid = threadIdx.x - 128;
+            const uint64_t pol_keep = ptx::policy_evict_last();    // partials are re-read from L2
+            const uint64_t pol_part = ptx::policy_evict_first();   // ... once
             uint32_t seg = 0;
             uint32_t red_ph[2] = {0u, 0u};  // staging-buffer mbarrier phases
+            float* scr = arg_scratch + half * 16 * kBM;            // argmax: this half's [16 tok][128 rows]
             for (int gi = 0; gi < P.n; ++gi) {
                 const GemmArgs& a = P.g[gi];
                 const Range r = range_of(a, G);
+                const int extra = a.epi == EPI_RESID_LN ? 1 : 0;    // residual rows staged after the partials
+                if (a.epi == EPI_ARGMAX && etid == 0) s_nlast = 0;
+                ptx::named_bar_sync(1, kEpiThreads);
                 for (long long u = r.u0; u < r.u1; ++seg) {
                     const Seg s = seg_at(u, r.u1, r.KB, G, r.U);
+                    u += s.kb1 - s.kb0;
                     const int buf = (int)(seg & 1);
-                    float* dst = a.part + (size_t)(s.tile * a.max_contrib + s.ci) * kSlot + row;  // [token][row]
                     ptx::mbar_wait(&tmem_full[buf], (seg >> 1) & 1);
                     ptx::tc_fence_after();
-                    const uint32_t trow = tmem + ((uint32_t)((warp % 4) * 32) << 16) + buf * 256;
-                    for (int j0 = half * 16; j0 < BN; j0 += 32) {
-                        float v[16];
-                        ptx::tmem_ld16(trow + j0, v);
-                        if (!(P.dbg & 2)) {
+                    const uint32_t trow = tmem + ((uint32_t)(q4 * 32) << 16) + buf * 256;
+                    const bool owner = a.owner_mode && s.ci == 0 && a.epi >= 0;
+                    if (!owner) {
+                        // ---- contributor: accumulator -> partial slot, publish
+                        float* dst = a.part + (size_t)(s.tile * a.max_contrib + s.ci) * kSlot + row;  // [token][row]
+                        for (int j0 = half * 16; j0 < BN; j0 += 32) {
+                            float v[16];
+                            ptx::tmem_ld16(trow + j0, v);
+                            if (!(P.dbg & 2)) {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    ptx::st_f32_hint(dst + (size_t)(j0 + i) * kBM, v[i], pol_keep);
+                            }
+                        }
+                        ptx::tc_fence_before();
+                        ptx::mbar_arrive(&tmem_empty[buf]);
+                        if (a.epi >= 0) {
+                            ptx::named_bar_sync(1, kEpiThreads);
+                            if (etid == 0) {
+                                __threadfence();
+                                atomicAdd(a.cnt + s.tile, 1);
+                            }
+                            __syncwarp();
+                        }
+                        continue;
+                    }
+                    // ---- owner: per-row epilogue constants
+                    const int m = s.tile * kBM + row;
+                    const bool mv = m < a.M;
+                    const float bias = (a.bias && mv) ? __ldg(a.bias + m) : 0.0f;
+                    int which = 0, hm = m;
+                    size_t kv_base = 0, kv_sample = 0;
+                    if (a.epi == EPI_QKV && mv) {
+                        which = m / a.h;
+                        hm = m - which * a.h;
+                        const int head = hm / a.hd, d = hm - head * a.hd;
+                        kv_sample = (size_t)a.heads * a.cap * a.hd;
+                        kv_base = ((size_t)a.layer * 2 + (which > 0 ? which - 1 : 0)) * a.B * kv_sample +
+                                  (size_t)head * a.cap * a.hd + d;
+                    }
+                    // one 16-token chunk [t0, t0+16) of this row: v = accumulator (+ others),
+                    // rres = staged residual row values (or null: read from global)
+                    auto out16 = [&](int t0, float (&v)[16], const float* rres) {
+                        if (a.epi == EPI_ARGMAX) {
+                            // rows -> per-token (max, lowest id) through this half's scratch
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) scr[i * kBM + row] = v[i] + bias;
+                            ptx::named_bar_sync(2 + half, 128);
+                            const int ht = (etid & 127) / 8, hq = (etid & 127) % 8;  // 8 threads per token
+                            const int t = t0 + ht;
+                            float bv = -INFINITY;
+                            int bi = 0x7fffffff;
+                            bool bad = false;
+                            if (t < T) {
+                                for (int k = 0; k < 16; ++k) {
+                                    const int rr = hq * 16 + ((k + ht) & 15);
+                                    const int mm = s.tile * kBM + rr;
+                                    const float x = scr[ht * kBM + rr];
+                                    if (mm < a.vocab) {
+                                        if (a.logits) a.logits[(size_t)t * a.vocab + mm] = x;
+                                        if (!isfinite(x)) bad = true;
+                                        if (arg_better(x, mm, bv, bi)) {
+                                            bv = x;
+                                            bi = mm;
+                                        }
+                                    }
+                                }
+                            }
+#pragma unroll
+                            for (int off = 1; off < 8; off <<= 1) {
+                                const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                                const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                                if (arg_better(ov, oi, bv, bi)) {
+                                    bv = ov;
+                                    bi = oi;
+                                }
+                            }
+                            if (bad) atomicExch(a.flag, 1);
+                            if (hq == 0 && t < T) {
+                                a.arg_v[(size_t)t * kGemmMaxTiles + s.tile] = bv;
+                                a.arg_i[(size_t)t * kGemmMaxTiles + s.tile] = bi;
+                                __threadfence();
+                                if (atomicAdd(a.cnt + kTokCnt + t, 1) == a.m_tiles - 1) s_last[atomicAdd(&s_nlast, 1)] = t;
+                            }
+                            ptx::named_bar_sync(2 + half, 128);  // scratch reuse
+                            return;
+                        }
+                        if (!mv) return;
+                        if (a.epi == EPI_RESID_LN) {
+                            float rv[16];
 #pragma unroll
                             for (int i = 0; i < 16; ++i)
-                                ptx::st_f32_hint(dst + (size_t)(j0 + i) * kBM, v[i], pol_keep);
+                                if (t0 + i < T)
+                                    rv[i] = rres ? rres[i * kBM] : __ldcg(a.out_f32 + (size_t)(t0 + i) * a.ld_out + m);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (t0 + i < T) a.out_f32[(size_t)(t0 + i) * a.ld_out + m] = rv[i] + v[i] + bias;
+                        } else if (a.epi == EPI_GELU) {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (t0 + i < T)
+                                    a.out_bf16[(size_t)(t0 + i) * a.ld_out + m] = __float2bfloat16_rn(gelu_fast(v[i] + bias));
+                        } else if (a.epi == EPI_QKV) {
+                            if (which == 0) {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    if (t0 + i < T) a.out_bf16[(size_t)(t0 + i) * a.h + hm] = __float2bfloat16_rn(v[i] + bias);
+                            } else {
+                                int slot[16];
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) {
+                                    slot[i] = -1;
+                                    if (t0 + i < T) {
+                                        const Plan pl = a.plans[t0 + i];
+                                        slot[i] = pl.store ? pl.sample * a.cap + pl.write_slot : -1;
+                                    }
+                                }
+#pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    if (slot[i] >= 0) {
+                                        const int smp = slot[i] / a.cap, ws = slot[i] - smp * a.cap;
+                                        a.kv[kv_base + (size_t)smp * kv_sample + (size_t)ws * a.hd] =
+                                            __float2bfloat16_rn(v[i] + bias);
+                                    }
+                            }
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (t0 + i < T) a.out_f32[(size_t)(t0 + i) * a.ld_out + m] = v[i] + bias;
+                        }
+                    };
+                    if (s.nc == 1) {
+                        // ---- sole contributor: epilogue straight from TMEM
+                        for (int j0 = half * 16; j0 < BN; j0 += 32) {
+                            float v[16];
+                            ptx::tmem_ld16(trow + j0, v);
+                            out16(j0, v, nullptr);
+                        }
+                        if (a.epi == EPI_ARGMAX && (BN / 16) % 2 == 1 && half == 1) {
+                            // keep the two halves' argmax barriers paired: half 1 has one chunk fewer
+                            float v[16];
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) v[i] = -INFINITY;
+                            out16(BN, v, nullptr);
+                        }
+                    } else {
+                        // ---- owner of a split tile: others' partials (slots 1..nc-1) staged per
+                        // token chunk into the idle token ring, two chunks in flight
+                        const int nothers = s.nc - 1;
+                        int cap = (int)(stg_half / (uint32_t)((nothers + extra) * kBM * 4)) & ~15;
+                        const bool staged = cap >= 16 && !(P.dbg & 4);
+                        if (!staged) cap = 32;
+                        const int njobs = (T + cap - 1) / cap;
+                        auto issue = [&](int jn) {  // etid 0: job jn into staging buffer jn & 1
+                            const int b2 = jn & 1;
+                            if (jn >= njobs) return;
+                            if (jn == 0) {
+                                trace_point(109, blockIdx.x | (gi << 16));
+                                wait_count(a.cnt + s.tile, nothers);
+                                asm volatile("fence.proxy.async.global;" ::: "memory");
+                                trace_point(110, blockIdx.x | (gi << 16));
+                            }
+                            const int t0 = jn * cap, nt = min(cap, T - t0);
+                            if (!staged) {
+                                ptx::mbar_arrive_expect_tx(&red_full[b2], 0);
+                                return;
+                            }
+                            ptx::mbar_arrive_expect_tx(&red_full[b2], (uint32_t)((nothers + extra) * nt * kBM * 4));
+                            uint8_t* dstb = b_base + b2 * stg_half;
+                            for (int c = 0; c < nothers; ++c)
+                                ptx::bulk_load(dstb + (size_t)c * cap * kBM * 4,
+                                               a.part + ((size_t)s.tile * a.max_contrib + 1 + c) * kSlot + (size_t)t0 * kBM,
+                                               (uint32_t)(nt * kBM * 4), &red_full[b2], pol_part);
+                            if (extra)
+                                for (int i = 0; i < nt; ++i)
+                                    ptx::bulk_load(dstb + ((size_t)nothers * cap + i) * kBM * 4,
+                                                   a.out_f32 + (size_t)(t0 + i) * a.ld_out + (size_t)s.tile * kBM,
+                                                   kBM * 4, &red_full[b2], pol_part);
+                        };
+                        if (etid == 0) {
+                            issue(0);
+                            issue(1);
+                        }
+                        // warp 4's other lanes must not spin on the staging barrier while
+                        // lane 0 is still issuing (a suspended spinning warp starves it)
+                        __syncwarp();
+                        for (int jn = 0; jn < njobs; ++jn) {
+                            const int b2 = jn & 1;
+                            ptx::mbar_wait(&red_full[b2], red_ph[b2]);
+                            red_ph[b2] ^= 1u;
+                            if (etid == 0) trace_point(107, blockIdx.x | (gi << 16) | (jn << 24));
+                            const int t0 = jn * cap, nt = min(cap, T - t0);
+                            const float* sm = (const float*)(b_base + b2 * stg_half);  // [c][cap tok][row]
+                            const float* gp = a.part + (size_t)s.tile * a.max_contrib * kSlot + row;
+                            const int nch = (nt + 15) / 16;
+                            // both halves run the same number of chunks (argmax barriers pair up)
+                            for (int jj = half; jj < nch + (nch & 1); jj += 2) {
+                                const int tt = t0 + jj * 16;
+                                float v[16];
+                                if (jj < nch) {
+                                    ptx::tmem_ld16(trow + tt, v);
+                                    for (int c = 0; c < nothers; ++c) {
+#pragma unroll
+                                        for (int i = 0; i < 16; ++i) {
+                                            if (jj * 16 + i >= nt) break;
+                                            v[i] += staged ? sm[((size_t)c * cap + jj * 16 + i) * kBM + row]
+                                                           : __ldcg(gp + (size_t)(1 + c) * kSlot + (size_t)(tt + i) * kBM);
+                                        }
+                                    }
+                                    out16(tt, v, staged && extra ? sm + ((size_t)nothers * cap + jj * 16) * kBM + row
+                                                                 : nullptr);
+                                } else if (a.epi == EPI_ARGMAX) {
+#pragma unroll
+                                    for (int i = 0; i < 16; ++i) v[i] = -INFINITY;
+                                    out16(T, v, nullptr);  // no tokens: barrier pairing only
+                                }
+                            }
+                            ptx::named_bar_sync(1, kEpiThreads);  // staging buffer consumed
+                            if (etid == 0) {
+                                trace_point(108, blockIdx.x | (gi << 16) | (jn << 24));
+                                issue(jn + 2);
+                            }
+                            __syncwarp();
                         }
                     }
                     ptx::tc_fence_before();
                     ptx::mbar_arrive(&tmem_empty[buf]);
-                    if (a.epi >= 0) {  // publish this contributor's partial
-                        ptx::named_bar_sync(1, kEpiThreads);
-                        if (etid == 0) {
-                            __threadfence();
-                            atomicAdd(a.cnt + s.tile, 1);
-                        }
-                    }
-                    u += s.kb1 - s.kb0;
                 }
                 if (etid == 0) trace_point(104, blockIdx.x | (gi << 16));
                 if (a.epi < 0) continue;
-
+                ptx::named_bar_sync(1, kEpiThreads);  // this CTA's owned tiles are written
+                if (!a.owner_mode) {
                 // ------------------------------------ reduction + epilogue of GEMM gi
-                // Jobs = (tile slice, token chunk).  Each job's nc contributor
-                // chunks are contiguous in the partial buffer ([slot][token][row])
-                // and are bulk-copied into the B ring -- idle until every CTA
-                // has finished this GEMM -- two jobs in flight, so the L2
-                // latency is paid once per job, not once per load.
-                if (a.epi == EPI_ARGMAX && etid == 0) s_nlast = 0;
-                {
-                    const uint64_t pol_part = ptx::policy_evict_first();  // partials: read once
-                    // this CTA's share of the GEMM's (tile, token) outputs
-                    const long long W = (long long)a.m_tiles * T;
-                    long long ix = (long long)blockIdx.x * W / G;
-                    const long long ix_end = (long long)(blockIdx.x + 1) * W / G;
-                    int prev_tile = -1;
-                    RJob q[2];
-                    const int extra = a.epi == EPI_RESID_LN ? 1 : 0;  // residual rows staged after the partials
-                    auto issue = [&](int buf) {  // etid 0 only: next job into staging buffer `buf`
-                        RJob j;
-                        if (!rjob_next(r, ix, ix_end, prev_tile, j, G, T, stg_half, extra, P.dbg)) {
-                            q[buf].nt = 0;
-                            return;
-                        }
-                        q[buf] = j;
-                        if (j.first) {
-                            wait_count(a.cnt + j.tile, j.nc);
-                            asm volatile("fence.proxy.async.global;" ::: "memory");
-                        }
-                        const uint32_t bytes = j.staged ? (uint32_t)((j.nc + extra) * j.nt * kBM * 4) : 0u;
-                        ptx::mbar_arrive_expect_tx(&red_full[buf], bytes);
-                        if (j.staged) {
-                            uint8_t* dst = b_base + buf * stg_half;
-                            for (int c = 0; c < j.nc; ++c)
-                                ptx::bulk_load(dst + (size_t)c * j.nt * kBM * 4,
-                                               a.part + ((size_t)j.tile * a.max_contrib + c) * kSlot + (size_t)j.t0 * kBM,
-                                               (uint32_t)(j.nt * kBM * 4), &red_full[buf], pol_part);
-                            if (extra)  // this tile's 128 residual columns of each token
-                                for (int i = 0; i < j.nt; ++i)
-                                    ptx::bulk_load(dst + ((size_t)j.nc * j.nt + i) * kBM * 4,
-                                                   a.out_f32 + (size_t)(j.t0 + i) * a.ld_out + (size_t)j.tile * kBM,
-                                                   kBM * 4, &red_full[buf], pol_part);
-                        }
-                    };
-                    if (etid == 0) {
-                        issue(0);
-                        issue(1);
-                        s_job[0] = q[0];
-                        s_job[1] = q[1];
-                    }
-                    ptx::named_bar_sync(1, kEpiThreads);
-                    for (int jn = 0;; ++jn) {
-                        const int buf = jn & 1;
-                        const RJob j = s_job[buf];
-                        if (j.nt == 0) break;
-                        ptx::mbar_wait(&red_full[buf], red_ph[buf]);
-                        red_ph[buf] ^= 1u;
-                        if (etid == 0) trace_point(107, blockIdx.x | (gi << 16) | (jn << 24));
-                        float* sm = (float*)(b_base + buf * stg_half);  // [c][tok][row]
-                        if (a.epi == EPI_ARGMAX) {
-                            // sums back into contributor 0's chunk, then (max, lowest id) over
-                            // the tile's rows per token: 4 threads per token, 32 rows each
-                            // (skewed: no bank conflicts)
-                            for (int i = half; i < j.nt; i += 2) {
-                                float v = 0.0f;
-                                for (int c = 0; c < j.nc; ++c) v += sm[((size_t)c * j.nt + i) * kBM + row];
-                                sm[(size_t)i * kBM + row] = v;
+                    // Jobs = (tile slice, token chunk).  Each job's nc contributor
+                    // chunks are contiguous in the partial buffer ([slot][token][row])
+                    // and are bulk-copied into the B ring -- idle until every CTA
+                    // has finished this GEMM -- two jobs in flight, so the L2
+                    // latency is paid once per job, not once per load.
+                    {
+                        const uint64_t pol_part = ptx::policy_evict_first();  // partials: read once
+                        // this CTA's share of the GEMM's (tile, token) outputs
+                        const long long W = (long long)a.m_tiles * T;
+                        long long ix = (long long)blockIdx.x * W / G;
+                        const long long ix_end = (long long)(blockIdx.x + 1) * W / G;
+                        int prev_tile = -1;
+                        RJob q[2];
+                        auto issue = [&](int buf) {  // etid 0 only: next job into staging buffer `buf`
+                            RJob j;
+                            if (!rjob_next(r, ix, ix_end, prev_tile, j, G, T, stg_half, extra, P.dbg)) {
+                                q[buf].nt = 0;
+                                return;
                             }
-                            ptx::named_bar_sync(1, kEpiThreads);
-                            bool bad = false;
-                            for (int i0 = 0; i0 < j.nt; i0 += kEpiThreads / 4) {
-                                const int i = i0 + etid / 4, qq = etid % 4;
-                                float bv = -INFINITY;
-                                int bi = 0x7fffffff;
-                                if (i < j.nt) {
-                                    for (int k = 0; k < 32; ++k) {
-                                        const int rr = qq * 32 + ((k + i) & 31);
-                                        const int mm = j.tile * kBM + rr;
-                                        const float v = sm[(size_t)i * kBM + rr];
-                                        if (mm < a.vocab) {
-                                            if (a.logits) a.logits[(size_t)(j.t0 + i) * a.vocab + mm] = v;
-                                            if (!isfinite(v)) bad = true;
-                                            if (arg_better(v, mm, bv, bi)) {
-                                                bv = v;
-                                                bi = mm;
-                                            }
-                                        }
-                                    }
-                                }
-#pragma unroll
-                                for (int off = 1; off < 4; off <<= 1) {
-                                    const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-                                    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-                                    if (arg_better(ov, oi, bv, bi)) {
-                                        bv = ov;
-                                        bi = oi;
-                                    }
-                                }
-                                if (qq == 0 && i < j.nt) {
-                                    const int t = j.t0 + i;
-                                    a.arg_v[(size_t)t * kGemmMaxTiles + j.tile] = bv;
-                                    a.arg_i[(size_t)t * kGemmMaxTiles + j.tile] = bi;
-                                    __threadfence();
-                                    if (atomicAdd(a.cnt + kTokCnt + t, 1) == a.m_tiles - 1)
-                                        s_last[atomicAdd(&s_nlast, 1)] = t;
-                                }
+                            q[buf] = j;
+                            if (j.first) {
+                                wait_count(a.cnt + j.tile, j.nc);
+                                asm volatile("fence.proxy.async.global;" ::: "memory");
                             }
-                            if (bad) atomicExch(a.flag, 1);
-                        } else {
-                            // thread = 2 adjacent rows (float2 / bf16x2 accesses) x tokens
-                            // q4, q4 + 4, ... of the job, two tokens in flight
-                            const int r2 = (etid & 63) * 2, q4 = etid >> 6;
-                            const int m2 = j.tile * kBM + r2;
-                            if (m2 < a.M) {  // M is even: both rows valid
-                                const float2 bias = a.bias ? __ldg((const float2*)(a.bias + m2)) : make_float2(0.f, 0.f);
-                                // per-thread constants of the QKV scatter (the row pair fixes Q/K/V, head, d)
-                                int which = 0, hm = m2;
-                                size_t kv_base = 0, kv_sample = 0;
-                                if (a.epi == EPI_QKV) {
-                                    which = m2 / a.h;
-                                    hm = m2 - which * a.h;
-                                    const int head = hm / a.hd, d = hm - head * a.hd;
-                                    kv_sample = (size_t)a.heads * a.cap * a.hd;
-                                    kv_base = ((size_t)a.layer * 2 + (which > 0 ? which - 1 : 0)) * a.B * kv_sample +
-                                              (size_t)head * a.cap * a.hd + d;
-                                }
-                                const float* gp2 = a.part + (size_t)j.tile * a.max_contrib * kSlot + r2;
-                                for (int i0 = q4; i0 < j.nt; i0 += 8) {
-                                    float2 v[2];
-#pragma unroll
-                                    for (int k = 0; k < 2; ++k) {
-                                        const int i = i0 + 4 * k;
-                                        v[k] = bias;
-                                        if (i < j.nt) {
-                                            if (j.staged) {
-#pragma unroll 4
-                                                for (int c = 0; c < j.nc; ++c) {
-                                                    const float2 x = *(const float2*)(sm + ((size_t)c * j.nt + i) * kBM + r2);
-                                                    v[k].x += x.x;
-                                                    v[k].y += x.y;
-                                                }
-                                            } else {
-                                                for (int c = 0; c < j.nc; ++c) {
-                                                    const float2 x = __ldcg((const float2*)(gp2 + c * kSlot + (size_t)(j.t0 + i) * kBM));
-                                                    v[k].x += x.x;
-                                                    v[k].y += x.y;
-                                                }
-                                            }
-                                        }
-                                    }
-#pragma unroll
-                                    for (int k = 0; k < 2; ++k) {
-                                        const int i = i0 + 4 * k;
-                                        if (i >= j.nt) break;
-                                        const int t = j.t0 + i;
-                                        if (a.epi == EPI_RESID_LN) {
-                                            float2* rp = (float2*)(a.out_f32 + (size_t)t * a.ld_out + m2);
-                                            const float2 rv = j.staged ? *(const float2*)(sm + ((size_t)j.nc * j.nt + i) * kBM + r2)
-                                                                       : __ldcg(rp);
-                                            *rp = make_float2(rv.x + v[k].x, rv.y + v[k].y);
-                                        } else if (a.epi == EPI_GELU) {
-                                            *(__nv_bfloat162*)(a.out_bf16 + (size_t)t * a.ld_out + m2) =
-                                                __floats2bfloat162_rn(gelu_fast(v[k].x), gelu_fast(v[k].y));
-                                        } else if (a.epi == EPI_QKV) {
-                                            const __nv_bfloat162 x2 = __floats2bfloat162_rn(v[k].x, v[k].y);
-                                            if (which == 0) {
-                                                *(__nv_bfloat162*)(a.out_bf16 + (size_t)t * a.h + hm) = x2;
-                                            } else {
-                                                const Plan pl = a.plans[t];
-                                                if (pl.store)
-                                                    *(__nv_bfloat162*)(a.kv + kv_base + (size_t)pl.sample * kv_sample +
-                                                                       (size_t)pl.write_slot * a.hd) = x2;
-                                            }
-                                        } else {
-                                            *(float2*)(a.out_f32 + (size_t)t * a.ld_out + m2) = v[k];
-                                        }
-                                    }
-                                }
+                            const uint32_t bytes = j.staged ? (uint32_t)((j.nc + extra) * j.nt * kBM * 4) : 0u;
+                            ptx::mbar_arrive_expect_tx(&red_full[buf], bytes);
+                            if (j.staged) {
+                                uint8_t* dst = b_base + buf * stg_half;
+                                for (int c = 0; c < j.nc; ++c)
+                                    ptx::bulk_load(dst + (size_t)c * j.nt * kBM * 4,
+                                                   a.part + ((size_t)j.tile * a.max_contrib + c) * kSlot + (size_t)j.t0 * kBM,
+                                                   (uint32_t)(j.nt * kBM * 4), &red_full[buf], pol_part);
+                                if (extra)  // this tile's 128 residual columns of each token
+                                    for (int i = 0; i < j.nt; ++i)
+                                        ptx::bulk_load(dst + ((size_t)j.nc * j.nt + i) * kBM * 4,
+                                                       a.out_f32 + (size_t)(j.t0 + i) * a.ld_out + (size_t)j.tile * kBM,
+                                                       kBM * 4, &red_full[buf], pol_part);
                             }
-                        }
-                        ptx::named_bar_sync(1, kEpiThreads);  // staging buffer consumed
-                        if (etid == 0) trace_point(108, blockIdx.x | (gi << 16) | (jn << 24));
+                        };
                         if (etid == 0) {
-                            issue(buf);
-                            s_job[buf] = q[buf];
+                            issue(0);
+                            issue(1);
+                            s_job[0] = q[0];
+                            s_job[1] = q[1];
                         }
                         ptx::named_bar_sync(1, kEpiThreads);
+                        for (int jn = 0;; ++jn) {
+                            const int buf = jn & 1;
+                            const RJob j = s_job[buf];
+                            if (j.nt == 0) break;
+                            ptx::mbar_wait(&red_full[buf], red_ph[buf]);
+                            red_ph[buf] ^= 1u;
+                            if (etid == 0) trace_point(107, blockIdx.x | (gi << 16) | (jn << 24));
+                            float* sm = (float*)(b_base + buf * stg_half);  // [c][tok][row]
+                            if (a.epi == EPI_ARGMAX) {
+                                // sums back into contributor 0's chunk, then (max, lowest id) over
+                                // the tile's rows per token: 4 threads per token, 32 rows each
+                                // (skewed: no bank conflicts)
+                                for (int i = half; i < j.nt; i += 2) {
+                                    float v = 0.0f;
+                                    for (int c = 0; c < j.nc; ++c) v += sm[((size_t)c * j.nt + i) * kBM + row];
+                                    sm[(size_t)i * kBM + row] = v;
+                                }
+                                ptx::named_bar_sync(1, kEpiThreads);
+                                bool bad = false;
+                                for (int i0 = 0; i0 < j.nt; i0 += kEpiThreads / 4) {
+                                    const int i = i0 + etid / 4, qq = etid % 4;
+                                    float bv = -INFINITY;
+                                    int bi = 0x7fffffff;
+                                    if (i < j.nt) {
+                                        for (int k = 0; k < 32; ++k) {
+                                            const int rr = qq * 32 + ((k + i) & 31);
+                                            const int mm = j.tile * kBM + rr;
+                                            const float v = sm[(size_t)i * kBM + rr];
+                                            if (mm < a.vocab) {
+                                                if (a.logits) a.logits[(size_t)(j.t0 + i) * a.vocab + mm] = v;
+                                                if (!isfinite(v)) bad = true;
+                                                if (arg_better(v, mm, bv, bi)) {
+                                                    bv = v;
+                                                    bi = mm;
+                                                }
+                                            }
+                                        }
+                                    }
+    #pragma unroll
+                                    for (int off = 1; off < 4; off <<= 1) {
+                                        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                                        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                                        if (arg_better(ov, oi, bv, bi)) {
+                                            bv = ov;
+                                            bi = oi;
+                                        }
+                                    }
+                                    if (qq == 0 && i < j.nt) {
+                                        const int t = j.t0 + i;
+                                        a.arg_v[(size_t)t * kGemmMaxTiles + j.tile] = bv;
+                                        a.arg_i[(size_t)t * kGemmMaxTiles + j.tile] = bi;
+                                        __threadfence();
+                                        if (atomicAdd(a.cnt + kTokCnt + t, 1) == a.m_tiles - 1)
+                                            s_last[atomicAdd(&s_nlast, 1)] = t;
+                                    }
+                                }
+                                if (bad) atomicExch(a.flag, 1);
+                            } else {
+                                // thread = 2 adjacent rows (float2 / bf16x2 accesses) x tokens
+                                // q4, q4 + 4, ... of the job, two tokens in flight
+                                const int r2 = (etid & 63) * 2, q4 = etid >> 6;
+                                const int m2 = j.tile * kBM + r2;
+                                if (m2 < a.M) {  // M is even: both rows valid
+                                    const float2 bias = a.bias ? __ldg((const float2*)(a.bias + m2)) : make_float2(0.f, 0.f);
+                                    // per-thread constants of the QKV scatter (the row pair fixes Q/K/V, head, d)
+                                    int which = 0, hm = m2;
+                                    size_t kv_base = 0, kv_sample = 0;
+                                    if (a.epi == EPI_QKV) {
+                                        which = m2 / a.h;
+                                        hm = m2 - which * a.h;
+                                        const int head = hm / a.hd, d = hm - head * a.hd;
+                                        kv_sample = (size_t)a.heads * a.cap * a.hd;
+                                        kv_base = ((size_t)a.layer * 2 + (which > 0 ? which - 1 : 0)) * a.B * kv_sample +
+                                                  (size_t)head * a.cap * a.hd + d;
+                                    }
+                                    const float* gp2 = a.part + (size_t)j.tile * a.max_contrib * kSlot + r2;
+                                    for (int i0 = q4; i0 < j.nt; i0 += 8) {
+                                        float2 v[2];
+    #pragma unroll
+                                        for (int k = 0; k < 2; ++k) {
+                                            const int i = i0 + 4 * k;
+                                            v[k] = bias;
+                                            if (i < j.nt) {
+                                                if (j.staged) {
+    #pragma unroll 4
+                                                    for (int c = 0; c < j.nc; ++c) {
+                                                        const float2 x = *(const float2*)(sm + ((size_t)c * j.nt + i) * kBM + r2);
+                                                        v[k].x += x.x;
+                                                        v[k].y += x.y;
+                                                    }
+                                                } else {
+                                                    for (int c = 0; c < j.nc; ++c) {
+                                                        const float2 x = __ldcg((const float2*)(gp2 + c * kSlot + (size_t)(j.t0 + i) * kBM));
+                                                        v[k].x += x.x;
+                                                        v[k].y += x.y;
+                                                    }
+                                                }
+                                            }
+                                        }
+    #pragma unroll
+                                        for (int k = 0; k < 2; ++k) {
+                                            const int i = i0 + 4 * k;
+                                            if (i >= j.nt) break;
+                                            const int t = j.t0 + i;
+                                            if (a.epi == EPI_RESID_LN) {
+                                                float2* rp = (float2*)(a.out_f32 + (size_t)t * a.ld_out + m2);
+                                                const float2 rv = j.staged ? *(const float2*)(sm + ((size_t)j.nc * j.nt + i) * kBM + r2)
+                                                                           : __ldcg(rp);
+                                                *rp = make_float2(rv.x + v[k].x, rv.y + v[k].y);
+                                            } else if (a.epi == EPI_GELU) {
+                                                *(__nv_bfloat162*)(a.out_bf16 + (size_t)t * a.ld_out + m2) =
+                                                    __floats2bfloat162_rn(gelu_fast(v[k].x), gelu_fast(v[k].y));
+                                            } else if (a.epi == EPI_QKV) {
+                                                const __nv_bfloat162 x2 = __floats2bfloat162_rn(v[k].x, v[k].y);
+                                                if (which == 0) {
+                                                    *(__nv_bfloat162*)(a.out_bf16 + (size_t)t * a.h + hm) = x2;
+                                                } else {
+                                                    const Plan pl = a.plans[t];
+                                                    if (pl.store)
+                                                        *(__nv_bfloat162*)(a.kv + kv_base + (size_t)pl.sample * kv_sample +
+                                                                           (size_t)pl.write_slot * a.hd) = x2;
+                                                }
+                                            } else {
+                                                *(float2*)(a.out_f32 + (size_t)t * a.ld_out + m2) = v[k];
+                                            }
+                                        }
+                                    }
+                                }
+                            }
+                            ptx::named_bar_sync(1, kEpiThreads);  // staging buffer consumed
+                            if (etid == 0) trace_point(108, blockIdx.x | (gi << 16) | (jn << 24));
+                            if (etid == 0) {
+                                issue(buf);
+                                s_job[buf] = q[buf];
+                            }
+                            ptx::named_bar_sync(1, kEpiThreads);
+                        }
                     }
+    
                 }
                 if (etid == 0) trace_point(105, blockIdx.x | (gi << 16));
                 if (a.epi == EPI_RESID_LN) {
-                    // every CTA's residual slices are final: LayerNorm rows blockIdx.x, +G, ...
+                    // every tile's residual is final: LayerNorm rows blockIdx.x, +G, ...
                     if (etid == 0) {
                         __threadfence();
                         atomicAdd(a.cnt + kLnCnt, 1);
@@ -653,8 +881,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ch
                     ptx::named_bar_sync(1, kEpiThreads);
                     for (int t = blockIdx.x; t < T; t += (int)G) ln_row(a, t, s_red);
                 } else if (a.epi == EPI_ARGMAX) {
-                    // tokens whose last vocab tile this CTA reduced: fold the per-tile partials
-                    ptx::named_bar_sync(1, kEpiThreads);
+                    // tokens whose last vocab tile this CTA wrote: fold the per-tile partials
                     __threadfence();
                     for (int jj = warp - 4; jj < s_nlast; jj += kEpiThreads / 32) {
                         const int t = s_last[jj];
@@ -750,6 +977,11 @@ void gemm_plan(GemmArgs& a, int sms) {
     SD_CHECK(a.K % kBK == 0, CONFIG, "bf16 mode needs K % 64 == 0");
     SD_CHECK(a.m_tiles >= 1 && a.m_tiles <= kGemmMaxTiles, CONFIG, "GEMM has too many 128-row tiles");
     plan_counts(a.m_tiles, a.K / kBK, sms, a.max_contrib, a.n_slices);
+    // owner reduction keeps the owner's accumulator on chip and overlaps the
+    // early contributors with the mainloop, but serialises a tile's whole
+    // epilogue on one CTA: worth it only while tiles have few contributors
+    static const int mode = getenv("SD_GEMM_OWNER") ? atoi(getenv("SD_GEMM_OWNER")) : -1;
+    a.owner_mode = mode >= 0 ? mode : (a.max_contrib <= 3 ? 1 : 0);
 }
 
 size_t gemm_part_floats(int M, int K, int sms) {

@@ -51,8 +51,8 @@ struct TraceBuf {
     [[maybe_unused]] __device__ __forceinline__ void trace_point(uint32_t kid, uint32_t tag) { \
         const TraceBuf& b = g_trace_##name;                                               \
         if (b.rec) {                                                                      \
+            const uint64_t t = globaltimer(); /* before the (contended) slot atomic */   \
             unsigned i = atomicAdd(b.count, 1u);                                          \
-            uint64_t t = globaltimer();                                                   \
             if (i < b.cap) b.rec[i] = TraceRec{kid, tag, smid(), 0, t, t};                \
         }                                                                                 \
     }                                                                                     \
@@ -65,10 +65,11 @@ struct TraceBuf {
         __device__ __forceinline__ ~CtaTrace() {                                          \
             const TraceBuf& b = g_trace_##name;                                           \
             if (b.rec && threadIdx.x == 0) {                                              \
+                const uint64_t t1 = globaltimer();                                        \
                 unsigned i = atomicAdd(b.count, 1u);                                      \
                 if (i < b.cap) {                                                          \
                     uint32_t blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
-                    b.rec[i] = TraceRec{kid, blk, smid(), gridDim.x * gridDim.y * gridDim.z, t0, globaltimer()}; \
+                    b.rec[i] = TraceRec{kid, blk, smid(), gridDim.x * gridDim.y * gridDim.z, t0, t1}; \
                 }                                                                         \
             }                                                                             \
         }                                                                                 \
