@@ -13,11 +13,6 @@ extern "C" {
  * TMA box per k-block) instead of row-major */
 int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K, int T, int grid, int flags, float* Y,
                   float* usec);
-/* Two GEMMs chained in one persistent launch (GELU or residual+LayerNorm
- * epilogue, then a plain store): the chain dependency, the in-kernel
- * split-K reduction and the fused epilogues in isolation. */
-int sd_debug_chain(const uint16_t* X, const uint16_t* W1, const float* b1, const uint16_t* W2, const float* b2,
-                   float* resid, int T, int K, int M1, int M2, int epi1, int flags, uint16_t* act_out, float* Y);
 /* In-graph kernel timeline (tools/timeline.py): while on, every CTA of every
  * verify-step kernel appends {kernel id, block, SM, grid size, t_entry, t_exit}
  * (globaltimer ns, 32 bytes) to a device buffer of `cap` records. */

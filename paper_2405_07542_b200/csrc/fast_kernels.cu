@@ -3,7 +3,7 @@
 // Per layer (model.cpp:303-359, restructured for the GPU):
 //   LN1 (fp32 residual -> bf16)          k_layernorm
 //   QKV  tcgen05 GEMM + scatter epilogue  Q -> q16, K/V -> unpadded arena
-//   ragged multi-query attention          attention_sm100.cu (persistent, in-kernel split combine)
+//   ragged multi-query attention          k_attention (+ k_attn_combine)
 //   O    tcgen05 GEMM + residual epilogue
 //   LN2                                   k_layernorm
 //   FC   tcgen05 GEMM + GELU epilogue
@@ -14,9 +14,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
-#include <cstdlib>
 
-#include "attn.h"
 #include "gemm.h"
 #include "handles.h"
 #include "pdl.cuh"
@@ -27,6 +25,8 @@ SD_TRACE_TU(fast)
 namespace sdb {
 
 constexpr int kChunkTokens = 256;  // tokens per forward chunk (GEMM N <= 256)
+constexpr int kSplit = 128;        // attention keys per CTA (4 warps x 32)
+constexpr int kQT = 8;             // queries per attention CTA (the mma N side)
 constexpr int kSms = 148;          // B200 SM count (stream-K GEMM grid)
 
 struct FastModelState {
@@ -39,17 +39,10 @@ struct FastWorkspace {
     __nv_bfloat16 *xb = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr;
     float* part_o = nullptr;   // [T][heads][max_splits][hd]
     float* part_ml = nullptr;  // [T][heads][max_splits][2]
-    float* part[2] = {nullptr, nullptr};  // stream-K partial sums, alternating between chained GEMMs
-    int* gemm_cnt = nullptr;   // per GEMM call site: kGemmCntInts counters, zeroed per forward
-    int n_sites = 0;
-    float* arg_v = nullptr;    // LM-head per-tile argmax partials [256][kGemmMaxTiles]
-    int* arg_i = nullptr;
-    int* attn_cnt = nullptr;   // split-KV arrival counters [B * heads * kMaxQTiles]
-    CUtensorMap kv_map;        // TMA view of the cache's KV arena
+    float* part = nullptr;     // stream-K partial sums (largest GEMM of the model)
+    int* row_cnt = nullptr;    // per-token LayerNorm arrival counters [256]
+    int* attn_cnt = nullptr;   // split-KV arrival counters [B * heads * 16]
     GemmMaps map_xb, map_ctx, map_act;
-    // per GEMM call site: the model's weight map + this workspace's token maps
-    std::vector<GemmMaps> map_qkv, map_o, map_fc, map_proj;
-    GemmMaps map_lm;
     std::vector<void*> allocs;
 };
 
@@ -65,20 +58,19 @@ void build_fast_model(Model& m) {
     int64_t h = c.hidden(), mm = c.mlp();
     SD_CHECK(h % 64 == 0, CONFIG, "bf16 mode needs hidden % 64 == 0");
     SD_CHECK(c.head_dim == 64 || c.head_dim == 128, CONFIG, "bf16 mode supports head_dim 64 or 128");
-    SD_CHECK(c.num_layers <= 256, CONFIG, "bf16 mode supports up to 256 layers");
     auto* f = new FastModelState();
     for (const FastLayer& L : m.layers) {
         GemmMaps g;
-        g.A = make_tmap_2d(L.wqkv, 3 * h, h, kGemmTile);
+        g.A = make_tmap_2d(L.wqkv, 3 * h, h, 256);
         f->qkv.push_back(g);
-        g.A = make_tmap_2d(L.wo, h, h, kGemmTile);
+        g.A = make_tmap_2d(L.wo, h, h, 256);
         f->o.push_back(g);
-        g.A = make_tmap_2d(L.wfc, mm, h, kGemmTile);
+        g.A = make_tmap_2d(L.wfc, mm, h, 256);
         f->fc.push_back(g);
-        g.A = make_tmap_2d(L.wproj, h, mm, kGemmTile);
+        g.A = make_tmap_2d(L.wproj, h, mm, 256);
         f->proj.push_back(g);
     }
-    f->lm.A = make_tmap_2d(m.lm16, m.vocab_pad, h, kGemmTile);
+    f->lm.A = make_tmap_2d(m.lm16, m.vocab_pad, h, 256);
     m.fast = f;
 }
 
@@ -166,6 +158,281 @@ __global__ void k_argmax_reduce(const float* __restrict__ pv, const int* __restr
     out[t] = bi;
 }
 
+// ------------------------------------------------------------- attention
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// smem tile [rows][HD] bf16 with the 16-byte chunk index XOR-swizzled by row%8
+template <int HD>
+__device__ __forceinline__ uint32_t swz(int row, int col) {  // byte offset of element (row, col)
+    constexpr int kChunks = HD / 8;
+    int chunk = (col >> 3) ^ (row & 7);
+    return (uint32_t)(row * kChunks + chunk) * 16 + (col & 7) * 2;
+}
+
+struct AttnArgs {
+    const __nv_bfloat16* q;    // [T][h]
+    const __nv_bfloat16* kv;   // arena
+    const Plan* plans;
+    const SampleSeg* segs;
+    const int32_t* qidx;
+    const uint8_t* pad;        // padded grid flags or null
+    __nv_bfloat16* ctx;        // [T][h]
+    float* part_o;
+    float* part_ml;
+    int* cnt;                  // [B * heads * q_tiles] split arrival counters (self-resetting)
+    int h, heads, B, cap, layer, max_splits;
+    float scale_log2;          // log2(e) / sqrt(hd)
+};
+
+// Ragged multi-query attention, "keys as M" formulation.
+//
+// One CTA = (sample, head) x 128-key split x 8-query tile; 4 warps each own 32
+// keys.  With only n_s <= 8 draft queries per sample, the tensor-core tile is
+// transposed so the KEYS are the 16-row M side and the queries the 8-wide N
+// side of mma.sync m16n8k16:  S^T = K Q^T  and  O^T += V^T P^T.  P^T is
+// re-laid from the S^T accumulator fragments with movmatrix (no smem trip),
+// the softmax reduces over keys with 3 shuffles, and the O^T accumulators are
+// 32 registers per thread.  This halves the MMA count of a 16-query tile and
+// keeps register pressure low enough for several CTAs per SM.  The 4 warps'
+// (max, sum, O) states merge through smem; splits merge in k_attn_combine.
+// A sample's K/V extent is read once per split, not once per query token (the
+// paper's per-token grid, re-reads it n_s times).
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+    uint32_t y;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+
+template <int HD>
+__global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
+    CtaTrace trace__(TK_ATTN);
+    pdl_trigger();
+    pdl_wait();
+    constexpr int kKeys = kSplit / 4;  // keys per warp (32)
+    const int sh = blockIdx.x, split = blockIdx.y, qt = blockIdx.z;
+    const int s = sh / a.heads, head = sh % a.heads;
+    const SampleSeg seg = a.segs[s];
+    const int k_begin = split * kSplit;
+    if (seg.n_q == 0 || qt * kQT >= seg.n_q || k_begin >= seg.kv_len) return;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int nq = min(kQT, seg.n_q - qt * kQT);
+
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint8_t* sQ = sm;                                    // [8][HD]
+    uint8_t* sK = sm + kQT * HD * 2 + warp * 2 * kKeys * HD * 2;
+    uint8_t* sV = sK + kKeys * HD * 2;
+    float* sMerge = (float*)(sm + kQT * HD * 2);         // reused: [4][8][HD] + [4][8][2]
+    __shared__ int sWslot[kQT];
+    __shared__ int sTok[kQT];
+
+    const int kw0 = k_begin + warp * kKeys;
+    const size_t kbase = ((((size_t)a.layer * 2 + 0) * a.B + s) * a.heads + head) * (size_t)a.cap * HD;
+    const size_t vbase = ((((size_t)a.layer * 2 + 1) * a.B + s) * a.heads + head) * (size_t)a.cap * HD;
+    const int kv_end = min(seg.kv_len, k_begin + kSplit);
+    for (int i = lane; i < kKeys * HD / 8; i += 32) {  // this warp's K / V rows (zero past the extent)
+        const int r = i / (HD / 8), c8 = i % (HD / 8);
+        const int key = kw0 + r;
+        const bool ok = key < kv_end;
+        const size_t off = (size_t)(ok ? key : 0) * HD + c8 * 8;
+        cp_async16(sK + swz<HD>(r, c8 * 8), a.kv + kbase + off, ok);
+        cp_async16(sV + swz<HD>(r, c8 * 8), a.kv + vbase + off, ok);
+    }
+    for (int i = threadIdx.x; i < kQT * HD / 8; i += 128) {  // Q tile (rows >= nq zero)
+        const int r = i / (HD / 8), c8 = i % (HD / 8);
+        const int tok = r < nq ? a.qidx[seg.q_start + qt * kQT + r] : 0;
+        cp_async16(sQ + swz<HD>(r, c8 * 8), a.q + (size_t)tok * a.h + head * HD + c8 * 8, r < nq);
+    }
+    if (threadIdx.x < kQT) {
+        const int r = threadIdx.x;
+        const int tok = r < nq ? a.qidx[seg.q_start + qt * kQT + r] : -1;
+        sTok[r] = tok;
+        sWslot[r] = tok >= 0 ? a.plans[tok].write_slot : -1;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    const int g = lane / 4, c = lane % 4;
+    // running softmax state for this thread's two query columns q = 2c, 2c+1
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
+    float o[HD / 16][4];  // O^T fragments: (hd d0+g / d0+g+8) x (q 2c, 2c+1)
+#pragma unroll
+    for (int n = 0; n < HD / 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.0f;
+
+    if (kw0 < kv_end) {
+        const uint32_t qa = (uint32_t)__cvta_generic_to_shared(sQ);
+        const uint32_t ka = (uint32_t)__cvta_generic_to_shared(sK);
+        const uint32_t va = (uint32_t)__cvta_generic_to_shared(sV);
+        // S^T = K Q^T : (kKeys keys) x (8 queries), as kKeys/16 m-tiles
+        float st[kKeys / 16][4];
+#pragma unroll
+        for (int t = 0; t < kKeys / 16; ++t) st[t][0] = st[t][1] = st[t][2] = st[t][3] = 0.0f;
+#pragma unroll
+        for (int kk = 0; kk < HD; kk += 32) {
+            // B = Q^T for two k-steps: matrices (q 0-7, hd kk), (kk+8), (kk+16), (kk+24)
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(qa + swz<HD>(lane % 8, kk + (lane / 8) * 8), b0, b1, b2, b3);
+#pragma unroll
+            for (int t = 0; t < kKeys / 16; ++t) {
+                uint32_t a0, a1, a2, a3, e0, e1, e2, e3;
+                // A = K rows t*16.. : (keys 0-7, kk), (keys 8-15, kk), (keys 0-7, kk+8), (keys 8-15, kk+8)
+                ldsm_x4(ka + swz<HD>(t * 16 + (lane % 16), kk + (lane / 16) * 8), a0, a1, a2, a3);
+                ldsm_x4(ka + swz<HD>(t * 16 + (lane % 16), kk + 16 + (lane / 16) * 8), e0, e1, e2, e3);
+                mma_bf16(st[t], a0, a1, a2, a3, b0, b1);
+                mma_bf16(st[t], e0, e1, e2, e3, b2, b3);
+            }
+        }
+        // mask + max over this warp's keys for each query column
+        const int ws[2] = {sWslot[2 * c], sWslot[2 * c + 1]};
+        float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+        for (int t = 0; t < kKeys / 16; ++t) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int key = kw0 + t * 16 + g + (e >= 2 ? 8 : 0);
+                const int qi = e & 1;
+                const bool vis = key < kv_end && key <= ws[qi] && !(a.pad && a.pad[(size_t)s * a.cap + key]);
+                const float x = vis ? st[t][e] * a.scale_log2 : -INFINITY;
+                st[t][e] = x;
+                mx[qi] = fmaxf(mx[qi], x);
+            }
+        }
+#pragma unroll
+        for (int qi = 0; qi < 2; ++qi) {
+            mx[qi] = fmaxf(mx[qi], __shfl_xor_sync(0xffffffffu, mx[qi], 4));
+            mx[qi] = fmaxf(mx[qi], __shfl_xor_sync(0xffffffffu, mx[qi], 8));
+            mx[qi] = fmaxf(mx[qi], __shfl_xor_sync(0xffffffffu, mx[qi], 16));
+            m_run[qi] = mx[qi];
+        }
+        float sum[2] = {0.0f, 0.0f};
+        uint32_t pb[kKeys / 16][2];  // P^T as mma B fragments (keys 2c.. / 2c+8.., q g)
+#pragma unroll
+        for (int t = 0; t < kKeys / 16; ++t) {
+            const float p0 = m_run[0] == -INFINITY ? 0.0f : exp2f(st[t][0] - m_run[0]);
+            const float p1 = m_run[1] == -INFINITY ? 0.0f : exp2f(st[t][1] - m_run[1]);
+            const float p2 = m_run[0] == -INFINITY ? 0.0f : exp2f(st[t][2] - m_run[0]);
+            const float p3 = m_run[1] == -INFINITY ? 0.0f : exp2f(st[t][3] - m_run[1]);
+            sum[0] += p0 + p2;
+            sum[1] += p1 + p3;
+            pb[t][0] = movmatrix_t(pack_bf16(p0, p1));  // rows = keys 0-7 of the tile
+            pb[t][1] = movmatrix_t(pack_bf16(p2, p3));  // rows = keys 8-15
+        }
+#pragma unroll
+        for (int qi = 0; qi < 2; ++qi) {
+            sum[qi] += __shfl_xor_sync(0xffffffffu, sum[qi], 4);
+            sum[qi] += __shfl_xor_sync(0xffffffffu, sum[qi], 8);
+            sum[qi] += __shfl_xor_sync(0xffffffffu, sum[qi], 16);
+            l_run[qi] = sum[qi];
+        }
+        // O^T += V^T P^T : per 16 keys (k-step) and 16 hd rows (m-tile)
+#pragma unroll
+        for (int t = 0; t < kKeys / 16; ++t) {
+#pragma unroll
+            for (int n = 0; n < HD / 16; ++n) {
+                uint32_t a0, a1, a2, a3;
+                // A = V^T (hd x keys): trans of V blocks (keys t*16+[0,8)/[8,16), hd n*16+[0,8)/[8,16))
+                const int key = t * 16 + (lane % 8) + ((lane / 16) * 8);
+                const int col = n * 16 + ((lane / 8) % 2) * 8;
+                ldsm_x4_t(va + swz<HD>(key, col), a0, a1, a2, a3);
+                mma_bf16(o[n], a0, a1, a2, a3, pb[t][0], pb[t][1]);
+            }
+        }
+    }
+    __syncthreads();  // every warp is done with K / V: reuse the area for the merge
+    float* mO = sMerge + (size_t)warp * kQT * HD;   // [q][hd]
+    float* mML = sMerge + 4 * kQT * HD + warp * 2 * kQT;
+#pragma unroll
+    for (int n = 0; n < HD / 16; ++n) {
+        mO[(2 * c) * HD + n * 16 + g] = o[n][0];
+        mO[(2 * c + 1) * HD + n * 16 + g] = o[n][1];
+        mO[(2 * c) * HD + n * 16 + g + 8] = o[n][2];
+        mO[(2 * c + 1) * HD + n * 16 + g + 8] = o[n][3];
+    }
+    if (g == 0) {
+        mML[(2 * c) * 2] = m_run[0];
+        mML[(2 * c) * 2 + 1] = l_run[0];
+        mML[(2 * c + 1) * 2] = m_run[1];
+        mML[(2 * c + 1) * 2 + 1] = l_run[1];
+    }
+    __syncthreads();
+    const int nsplit = (seg.kv_len + kSplit - 1) / kSplit;
+    for (int i = threadIdx.x; i < kQT * HD; i += 128) {
+        const int r = i / HD, d = i % HD;
+        if (r >= nq) continue;
+        float M = -INFINITY;
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, sMerge[4 * kQT * HD + w * 2 * kQT + r * 2]);
+        float L = 0.0f, O = 0.0f;
+        for (int w = 0; w < 4; ++w) {
+            const float mw = sMerge[4 * kQT * HD + w * 2 * kQT + r * 2];
+            if (mw == -INFINITY) continue;
+            const float f = exp2f(mw - M);
+            L += sMerge[4 * kQT * HD + w * 2 * kQT + r * 2 + 1] * f;
+            O += sMerge[(size_t)w * kQT * HD + r * HD + d] * f;
+        }
+        const int tok = sTok[r];
+        if (nsplit == 1) {
+            a.ctx[(size_t)tok * a.h + head * HD + d] = __float2bfloat16_rn(O / L);
+        } else {
+            const size_t base = ((size_t)tok * a.heads + head) * a.max_splits + split;
+            a.part_o[base * HD + d] = O;
+            if (d == 0) {
+                a.part_ml[base * 2] = M;
+                a.part_ml[base * 2 + 1] = L;
+            }
+        }
+    }
+}
+
+// merge split-KV partials: grid (T, heads), block HD
+__global__ void k_attn_combine(AttnArgs a, int hd, const int* __restrict__ dT) {
+    CtaTrace trace__(TK_ATTN_COMBINE);
+    pdl_trigger();
+    pdl_wait();
+    int t = blockIdx.x, head = blockIdx.y, d = threadIdx.x;
+    if (t >= *dT) return;
+    int s = a.plans[t].sample;
+    int nsplit = (a.segs[s].kv_len + kSplit - 1) / kSplit;
+    if (nsplit <= 1) return;
+    size_t base = ((size_t)t * a.heads + head) * a.max_splits;
+    float M = -INFINITY;
+    for (int k = 0; k < nsplit; ++k) M = fmaxf(M, a.part_ml[(base + k) * 2]);
+    float L = 0.0f, O = 0.0f;
+    for (int k = 0; k < nsplit; ++k) {
+        float mk = a.part_ml[(base + k) * 2];
+        if (mk == -INFINITY) continue;
+        float f = exp2f(mk - M);
+        L += a.part_ml[(base + k) * 2 + 1] * f;
+        O += a.part_o[(base + k) * hd + d] * f;
+    }
+    a.ctx[(size_t)t * a.h + head * hd + d] = __float2bfloat16_rn(O / L);
+}
+
 template <typename T>
 T* walloc(FastWorkspace* f, size_t n) {
     T* p = (T*)dmalloc(sizeof(T) * (n ? n : 1));
@@ -175,7 +442,7 @@ T* walloc(FastWorkspace* f, size_t n) {
 
 FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     FastWorkspace* f = ws.fast;
-    int max_splits = (c.cap + kAttnSplit - 1) / kAttnSplit;
+    int max_splits = (c.cap + kSplit - 1) / kSplit;
     if (f && f->B >= c.B && f->cap >= c.cap && f->max_splits >= max_splits) return f;
     free_fast_workspace(f);
     f = new FastWorkspace();
@@ -189,42 +456,21 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     f->q = walloc<__nv_bfloat16>(f, T * h);
     f->ctx = walloc<__nv_bfloat16>(f, T * h);
     f->act = walloc<__nv_bfloat16>(f, T * mm);
-    f->part_o = walloc<float>(f, T * cfg.num_heads * max_splits * 4 * cfg.head_dim);  // 4 warp contributors per split
-    f->part_ml = walloc<float>(f, T * cfg.num_heads * max_splits * 4 * 2);
+    f->part_o = walloc<float>(f, T * cfg.num_heads * max_splits * cfg.head_dim);
+    f->part_ml = walloc<float>(f, T * cfg.num_heads * max_splits * 2);
     size_t part = 0;
     for (auto mk : {std::make_pair((int)(3 * h), (int)h), std::make_pair((int)h, (int)h),
                     std::make_pair((int)mm, (int)h), std::make_pair((int)h, (int)mm),
                     std::make_pair(m.vocab_pad, (int)h)})
         part = std::max(part, gemm_part_floats(mk.first, mk.second, kSms));
-    f->part[0] = walloc<float>(f, part);
-    f->part[1] = walloc<float>(f, part);
-    f->n_sites = cfg.num_layers * 4 + 1;
-    f->gemm_cnt = walloc<int>(f, (size_t)f->n_sites * kGemmCntInts + 256);  // + attention item counters
-    f->arg_v = walloc<float>(f, (size_t)256 * kGemmMaxTiles);
-    f->arg_i = walloc<int>(f, (size_t)256 * kGemmMaxTiles);
-    f->attn_cnt = walloc<int>(f, (size_t)c.B * cfg.num_heads * kMaxQTiles);
-    CUDA_OK(cudaMemset(f->attn_cnt, 0, sizeof(int) * (size_t)c.B * cfg.num_heads * kMaxQTiles));
-    f->kv_map = make_kv_map(c.kv, (int64_t)cfg.num_layers * 2 * c.B * cfg.num_heads * c.cap, cfg.head_dim);
+    f->part = walloc<float>(f, part);
+    f->row_cnt = walloc<int>(f, 256);
+    f->attn_cnt = walloc<int>(f, (size_t)c.B * cfg.num_heads * 16);
+    CUDA_OK(cudaMemset(f->row_cnt, 0, sizeof(int) * 256));
+    CUDA_OK(cudaMemset(f->attn_cnt, 0, sizeof(int) * (size_t)c.B * cfg.num_heads * 16));
     make_b_maps(f->map_xb, f->xb, T, h);
     make_b_maps(f->map_ctx, f->ctx, T, h);
     make_b_maps(f->map_act, f->act, T, mm);
-    const FastModelState* fm = m.fast;
-    for (int l = 0; l < cfg.num_layers; ++l) {
-        GemmMaps g = f->map_xb;
-        g.A = fm->qkv[l].A;
-        f->map_qkv.push_back(g);
-        g = f->map_ctx;
-        g.A = fm->o[l].A;
-        f->map_o.push_back(g);
-        g = f->map_xb;
-        g.A = fm->fc[l].A;
-        f->map_fc.push_back(g);
-        g = f->map_act;
-        g.A = fm->proj[l].A;
-        f->map_proj.push_back(g);
-    }
-    f->map_lm = f->map_xb;
-    f->map_lm.A = fm->lm.A;
     ws.fast = f;
     return f;
 }
@@ -236,20 +482,19 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
 // launching stream and charge it the ALGORITHMIC bytes it must move
 // (weights + activations + KV it reads/writes once).  bench.py reads this
 // to report the dominant kernel's achieved bandwidth.
-enum ProfKind { PK_GEMM, PK_ATTN, PK_ROW, PK_MISC, PK_N };
+enum ProfKind { PK_QKV, PK_O, PK_FC, PK_PROJ, PK_LM, PK_ATTN, PK_ROW, PK_MISC, PK_N };
 struct ProfRec {
     int kind;
-    double wb, tc;  // algorithmic bytes = wb + T * tc (attention: from the KV extents; wb < 0: combine)
     cudaEvent_t a, b;
 };
 static bool g_prof = false;
 static std::vector<ProfRec> g_prof_pending;
 static double g_prof_acc[PK_N][3];  // launches, ms, bytes
 
-#define PROF(kind, wb, tc, ...)                            \
+#define PROF(kind, ...)                                    \
     do {                                                   \
         if (g_prof) {                                      \
-            ProfRec r__{kind, wb, tc, nullptr, nullptr};   \
+            ProfRec r__{kind, nullptr, nullptr};           \
             CUDA_OK(cudaEventCreate(&r__.a));              \
             CUDA_OK(cudaEventCreate(&r__.b));              \
             CUDA_OK(cudaEventRecord(r__.a, st));           \
@@ -275,7 +520,8 @@ void profile_read(double* out, int kinds) {
 void prepare_fast_kernels() {
     static bool done = false;
     if (done) return;
-    attention_prepare();
+    CUDA_OK(cudaFuncSetAttribute(k_attention<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CUDA_OK(cudaFuncSetAttribute(k_attention<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     gemm_prepare();
     done = true;
 }
@@ -299,12 +545,10 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     int64_t launches = 0;
 
     GemmArgs base{};
-    base.arg_v = f->arg_v;
-    base.arg_i = f->arg_i;
-    // every GEMM call site owns a counter region, zeroed once per forward
-    CUDA_OK(cudaMemsetAsync(f->gemm_cnt, 0, sizeof(int) * ((size_t)f->n_sites * kGemmCntInts + 256), st));
-    int* attn_work = f->gemm_cnt + (size_t)f->n_sites * kGemmCntInts;  // one item counter per layer
-    auto site = [&](int l, int k) { return f->gemm_cnt + (size_t)(l * 4 + k) * kGemmCntInts; };
+    base.T = n;
+    base.dT = db.dT;
+    base.part = f->part;
+    base.row_cnt = f->row_cnt;
     base.h = h;
     base.hd = hd;
     base.heads = heads;
@@ -313,7 +557,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     base.plans = dplans;
     base.kv = (__nv_bfloat16*)c.kv;
 
-    PROF(PK_ROW, 0.0, 6.0 * h, launch_k(k_embed_ln, dim3(n), dim3(kRowThreads), 0, st, (const __nv_bfloat16*)m.tok16,
+    PROF(PK_ROW, launch_k(k_embed_ln, dim3(n), dim3(kRowThreads), 0, st, (const __nv_bfloat16*)m.tok16,
                           (const __nv_bfloat16*)m.pos16, tokens, dplans, h, resid, (const float*)m.layers[0].ln1_g,
                           (const float*)m.layers[0].ln1_b, f->xb, (const int*)db.dT));
     launches++;
@@ -334,143 +578,94 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     at.cap = c.cap;
     at.max_splits = f->max_splits;
     at.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-    const int splits = std::max(1, (db.max_kv_upper + kAttnSplit - 1) / kAttnSplit);
-    const int qtiles = std::max(1, (db.max_q_upper + kAttnQT - 1) / kAttnQT);
+    const int splits = std::max(1, (db.max_kv_upper + kSplit - 1) / kSplit);
+    const int qtiles = std::max(1, (db.max_q_upper + kQT - 1) / kQT);
+    const size_t attn_smem = (size_t)kQT * hd * 2 + (size_t)4 * 2 * (kSplit / 4) * hd * 2;
 
-    // the four GEMMs of a layer and the LM head, as chain links
-    auto qkv = [&](int l, GemmChain& ch, const GemmMaps*& mp) {
-        GemmArgs& g = ch.g[ch.n];
-        g = base;
-        g.epi = EPI_QKV;
+    for (int l = 0; l < cfg.num_layers; ++l) {
+        const FastLayer& L = m.layers[l];
+        const FastModelState* fm = m.fast;
+        // QKV + scatter (Q -> q16, K/V -> the arena at each token's write slot)
+        GemmArgs g = base;
         g.M = 3 * h;
         g.K = h;
-        g.m_tiles = (3 * h + kGemmTile - 1) / kGemmTile;
-        g.cnt = site(l, 0);
-        g.bias = m.layers[l].bqkv;
+        g.m_tiles = (3 * h + 255) / 256;
+        g.bias = L.bqkv;
         g.out_bf16 = f->q;
         g.layer = l;
-        mp = &f->map_qkv[l];
-    };
-    auto o_proj = [&](int l, GemmChain& ch, const GemmMaps*& mp) {
-        GemmArgs& g = ch.g[ch.n];
+        gemm_plan(g, kSms);
+        GemmMaps mp = f->map_xb;
+        mp.A = fm->qkv[l].A;
+        PROF(PK_QKV, gemm_launch(EPI_QKV, g, mp, n, st));
+        // attention
+        at.layer = l;
+        if (hd == 128)
+            PROF(PK_ATTN, launch_k(k_attention<128>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
+        else
+            PROF(PK_ATTN, launch_k(k_attention<64>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
+        launches++;
+        if (splits > 1) {
+            PROF(PK_ATTN, launch_k(k_attn_combine, dim3(n, heads), dim3(hd), 0, st, at, hd, (const int*)db.dT));
+            launches++;
+        }
+        // O projection + residual, fused with LN2 -> xb
         g = base;
-        g.epi = EPI_RESID_LN;  // residual, fused with LN2 -> xb
         g.M = h;
         g.K = h;
-        g.m_tiles = (h + kGemmTile - 1) / kGemmTile;
-        g.cnt = site(l, 1);
-        g.bias = m.layers[l].bo;
+        g.m_tiles = (h + 255) / 256;
+        g.bias = L.bo;
         g.out_f32 = resid;
         g.ld_out = h;
-        g.ln_g = m.layers[l].ln2_g;
-        g.ln_b = m.layers[l].ln2_b;
+        g.ln_g = L.ln2_g;
+        g.ln_b = L.ln2_b;
         g.ln_out = f->xb;
-        mp = &f->map_o[l];
-    };
-    auto fc = [&](int l, GemmChain& ch, const GemmMaps*& mp) {
-        GemmArgs& g = ch.g[ch.n];
+        gemm_plan(g, kSms);
+        mp = f->map_ctx;
+        mp.A = fm->o[l].A;
+        PROF(PK_O, gemm_launch(EPI_RESID_LN, g, mp, n, st));
+        // FC + GELU
         g = base;
-        g.epi = EPI_GELU;
         g.M = mm;
         g.K = h;
-        g.m_tiles = (mm + kGemmTile - 1) / kGemmTile;
-        g.cnt = site(l, 2);
-        g.bias = m.layers[l].bfc;
+        g.m_tiles = (mm + 255) / 256;
+        g.bias = L.bfc;
         g.out_bf16 = f->act;
         g.ld_out = mm;
-        mp = &f->map_fc[l];
-    };
-    auto proj = [&](int l, GemmChain& ch, const GemmMaps*& mp) {
-        GemmArgs& g = ch.g[ch.n];
+        gemm_plan(g, kSms);
+        mp = f->map_xb;
+        mp.A = fm->fc[l].A;
+        PROF(PK_FC, gemm_launch(EPI_GELU, g, mp, n, st));
+        // PROJ + residual, fused with the next LN1 (or the final LN) -> xb
         g = base;
-        g.epi = EPI_RESID_LN;  // residual, fused with the next LN1 (or the final LN) -> xb
         g.M = h;
         g.K = mm;
-        g.m_tiles = (h + kGemmTile - 1) / kGemmTile;
-        g.cnt = site(l, 3);
-        g.bias = m.layers[l].bproj;
+        g.m_tiles = (h + 255) / 256;
+        g.bias = L.bproj;
         g.out_f32 = resid;
         g.ld_out = h;
         g.ln_g = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_g : m.lnf_g;
         g.ln_b = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_b : m.lnf_b;
         g.ln_out = f->xb;
-        mp = &f->map_proj[l];
-    };
-    auto lm = [&](GemmChain& ch, const GemmMaps*& mp) {
-        GemmArgs& g = ch.g[ch.n];
-        g = base;
-        g.epi = EPI_ARGMAX;
-        g.M = m.vocab_pad;
-        g.K = h;
-        g.m_tiles = m.vocab_pad / kGemmTile;
-        g.cnt = site(cfg.num_layers, 0);
-        g.vocab = cfg.vocab_size;
-        g.argmax = ws.d_argmax + t0;
-        g.logits = want_logits ? ws.d_logits + (size_t)t0 * cfg.vocab_size : nullptr;
-        g.flag = ws.d_flag;
-        mp = &f->map_lm;
-    };
-    // algorithmic bytes of a link: weights once + token operand + outputs
-    auto link_bytes = [&](const GemmArgs& g, double& wb, double& tc) {
-        wb += (double)g.M * g.K * 2;
-        double out = g.epi == EPI_QKV ? 3.0 * h * 2 : g.epi == EPI_GELU ? mm * 2.0 : g.epi == EPI_ARGMAX ? 4.0 : h * 10.0;
-        tc += g.K * 2.0 + out;
-    };
-    auto run_chain = [&](GemmChain& ch, const GemmMaps* const* mps) {
-        ch.T = n;
-        ch.dT = db.dT;
-        ch.T_upper = n;
-        static const int dbg = getenv("SD_GEMM_DBG") ? atoi(getenv("SD_GEMM_DBG")) : 0;
-        ch.dbg = dbg;
-        static const int pf = getenv("SD_GEMM_PREFETCH") ? atoi(getenv("SD_GEMM_PREFETCH")) : 0;
-        ch.prefetch = pf;
-        double wb = 0, tc = 0;
-        for (int i = 0; i < ch.n; ++i) {
-            ch.g[i].part = f->part[i & 1];
-            gemm_plan(ch.g[i], kSms);
-            link_bytes(ch.g[i], wb, tc);
-        }
-        PROF(PK_GEMM, wb, tc, chain_launch(ch, mps, st));
-        launches++;
-    };
-
-    {  // layer 0's QKV (+ scatter into the arena) on its own
-        GemmChain ch{};
-        const GemmMaps* mps[kMaxChain];
-        qkv(0, ch, mps[0]);
-        ch.n = 1;
-        run_chain(ch, mps);
+        gemm_plan(g, kSms);
+        mp = f->map_act;
+        mp.A = fm->proj[l].A;
+        PROF(PK_PROJ, gemm_launch(EPI_RESID_LN, g, mp, n, st));
+        launches += 8;
     }
-    for (int l = 0; l < cfg.num_layers; ++l) {
-        // ragged attention of layer l
-        at.layer = l;
-        at.work = attn_work + l;
-        static const int adbg = getenv("SD_ATTN_DBG") ? atoi(getenv("SD_ATTN_DBG")) : 0;
-        at.dbg = adbg;
-        // split-grid attention with in-kernel split fold (default); SD_ATTN_IMPL=2
-        // selects the experimental persistent TMA-ring kernel (attention_sm100.cu)
-        static const int aimpl = getenv("SD_ATTN_IMPL") ? atoi(getenv("SD_ATTN_IMPL")) : 1;
-        if (aimpl != 2)
-            PROF(PK_ATTN, 0.0, 0.0, attention_v1_launch(at, hd, db.max_kv_upper, db.max_q_upper, n, db.dT, st));
-        else
-            PROF(PK_ATTN, 0.0, 0.0, attention_launch(at, f->kv_map, hd, splits, qtiles, st));
-        launches++;
-        // one persistent launch: O -> FC -> PROJ -> next layer's QKV (or the LM head)
-        GemmChain ch{};
-        const GemmMaps* mps[kMaxChain];
-        o_proj(l, ch, mps[ch.n]);
-        ch.n++;
-        fc(l, ch, mps[ch.n]);
-        ch.n++;
-        proj(l, ch, mps[ch.n]);
-        ch.n++;
-        if (l + 1 < cfg.num_layers)
-            qkv(l + 1, ch, mps[ch.n]);
-        else
-            lm(ch, mps[ch.n]);
-        ch.n++;
-        run_chain(ch, mps);
-    }
+    // LM head + greedy argmax
+    GemmArgs g = base;
+    g.M = m.vocab_pad;
+    g.K = h;
+    g.m_tiles = m.vocab_pad / 256;
+    g.vocab = cfg.vocab_size;
+    g.argmax = ws.d_argmax + t0;
+    g.logits = want_logits ? ws.d_logits + (size_t)t0 * cfg.vocab_size : nullptr;
+    g.flag = ws.d_flag;
+    gemm_plan(g, kSms);
+    GemmMaps mp = f->map_xb;
+    mp.A = m.fast->lm.A;
+    PROF(PK_LM, gemm_launch(EPI_ARGMAX, g, mp, n, st));
+    launches += 2;
     note_launches(launches);
     CUDA_OK(cudaGetLastError());
     if (g_prof) {  // charge every timed launch its algorithmic bytes
@@ -481,14 +676,23 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         CUDA_OK(cudaMemcpy(segs.data(), db.segs, sizeof(SampleSeg) * c.B, cudaMemcpyDeviceToHost));
         double kv = 0;
         for (auto& sg : segs) kv += (double)sg.kv_len * (sg.n_q > 0);
-        const double attn_bytes = kv * 2 * hd * 2 * heads + (double)T * h * 4;
+        const double H = h, Mm = mm, Tt = T, V = cfg.vocab_size;
+        double bytes[PK_N] = {3 * H * H * 2 + Tt * H * 2 + Tt * 3 * H * 2,
+                              H * H * 2 + Tt * H * 2 + Tt * H * 8,
+                              Mm * H * 2 + Tt * H * 2 + Tt * Mm * 2,
+                              H * Mm * 2 + Tt * Mm * 2 + Tt * H * 8,
+                              V * H * 2 + Tt * H * 2,
+                              kv * 2 * hd * 2 * heads + Tt * H * 4,
+                              Tt * H * 6,
+                              0};
         for (auto& r : g_prof_pending) {
             float ms = 0.0f;
             CUDA_OK(cudaEventElapsedTime(&ms, r.a, r.b));
             g_prof_acc[r.kind][0] += 1;
             g_prof_acc[r.kind][1] += ms;
-            // attention bytes are charged once per layer (the combine adds none)
-            g_prof_acc[r.kind][2] += r.kind == PK_ATTN ? (r.wb < 0 ? 0.0 : attn_bytes) : r.wb + (double)T * r.tc;
+            // attention bytes are charged once per layer (combine adds none)
+            bool combine = r.kind == PK_ATTN && (&r != &g_prof_pending.front()) && (&r - 1)->kind == PK_ATTN;
+            g_prof_acc[r.kind][2] += combine ? 0.0 : bytes[r.kind];
             cudaEventDestroy(r.a);
             cudaEventDestroy(r.b);
         }

@@ -35,9 +35,12 @@ struct sd_session {
     // graph
     cudaGraphExec_t graph = nullptr;
     int graph_steps = 0;
+    cudaGraphExec_t loop_graph = nullptr;  // WHILE-node graph of the whole loop
+    bool loop_unsupported = false;
     std::vector<void*> allocs;
     ~sd_session() {
         if (graph) cudaGraphExecDestroy(graph);
+        if (loop_graph) cudaGraphExecDestroy(loop_graph);
         for (void* p : allocs) sdb::dfree(p);
         if (h_flag) cudaFreeHost(h_flag);
     }
@@ -96,9 +99,11 @@ StepArgs step_args(sd_session* s) {
 }
 
 // one device-resident verify step (fixed launch sequence, graph-capturable)
-void device_step(sd_session* s, cudaStream_t st) {
+void device_step(sd_session* s, cudaStream_t st, unsigned long long cond = 0, bool has_cond = false) {
     Cache& c = s->cache->c;
     StepArgs a = step_args(s);
+    a.cond = cond;
+    a.has_cond = has_cond ? 1 : 0;
     PredictArgs p{};
     p.kind = s->e.predictor;
     p.match_len = s->e.match_len;
@@ -273,6 +278,55 @@ int session_run(sd_session* s, int use_graph, int graph_steps, float* gpu_ms) {
     set_device(s->model->m.device);
     prepare_fast_kernels();
     if (graph_steps < 1) graph_steps = 8;
+    if (use_graph && graph_steps == 8 && !s->loop_graph && !s->loop_unsupported) {
+        // the whole loop as one graph: a WHILE conditional node whose body is
+        // one verify step; k_accept sets the condition on the device
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ex = nullptr;
+        bool ok = cudaGraphCreate(&g, 0) == cudaSuccess;
+        cudaGraphConditionalHandle h{};
+        ok = ok && cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        ok = ok && cudaGraphAddNode(&node, g, nullptr, 0, &cp) == cudaSuccess;
+        if (ok) {
+            cudaGraph_t body = cp.conditional.phGraph_out[0];
+            CUDA_OK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+            device_step(s, st, (unsigned long long)h, true);
+            CUDA_OK(cudaStreamEndCapture(st, &body));
+            ok = cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+        }
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();  // clear a soft failure (old driver): fall back to replayed batches
+        if (ok) s->loop_graph = ex;
+        else s->loop_unsupported = true;
+    }
+    if (use_graph && s->loop_graph) {
+        cudaEvent_t e0, e1;
+        CUDA_OK(cudaEventCreate(&e0));
+        CUDA_OK(cudaEventCreate(&e1));
+        CUDA_OK(cudaEventRecord(e0, st));
+        CUDA_OK(cudaGraphLaunch(s->loop_graph, st));
+        CUDA_OK(cudaEventRecord(e1, st));
+        CUDA_OK(cudaMemcpyAsync(s->h_flag + 1, s->step, 4, cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaEventSynchronize(e1));
+        CUDA_OK(cudaStreamSynchronize(st));
+        float ms = 0.0f;
+        CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (gpu_ms) *gpu_ms = ms;
+        int32_t flag = 0, cap_err = 0;
+        CUDA_OK(cudaMemcpy(&flag, s->cache->ws.d_flag, 4, cudaMemcpyDeviceToHost));
+        CUDA_OK(cudaMemcpy(&cap_err, s->scalars + 4, 4, cudaMemcpyDeviceToHost));
+        SD_CHECK(flag == 0, INTERNAL, "non-finite logit produced");
+        SD_CHECK(cap_err == 0, CAPACITY, "padded grid outgrew the cache capacity during the device loop");
+        return s->h_flag[1];
+    }
     if (use_graph && (!s->graph || s->graph_steps != graph_steps)) {
         if (s->graph) cudaGraphExecDestroy(s->graph);
         s->graph = nullptr;

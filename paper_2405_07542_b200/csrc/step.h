@@ -42,6 +42,10 @@ struct StepArgs {
     int32_t* tau;            // [B]
     int32_t* accepted;       // [B][acc_stride]
     int32_t* clipped;        // [B]
+    // device loop as ONE CUDA-graph WHILE node: k_accept sets the loop
+    // condition (samples still active) -- no host round trip, no idle steps
+    unsigned long long cond;  // cudaGraphConditionalHandle
+    int has_cond;
 };
 
 // Device predictors for the resident loop (predictors.cpp:39-72 on device).

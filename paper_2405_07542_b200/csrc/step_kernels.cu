@@ -183,6 +183,9 @@ __global__ void k_accept(StepArgs a) {
         // count only steps that verified something (graph replays may run
         // trailing no-op steps after every sample finished)
         if (a.step && s_taumax > 0) *a.step = s_step + 1;
+        if (a.has_cond)  // keep looping while a sample is active (and the step log has room)
+            cudaGraphSetConditional((cudaGraphConditionalHandle)a.cond,
+                                    (s_active > 0 && s_step + 1 < a.max_steps) ? 1u : 0u);
     }
 }
 

@@ -519,7 +519,7 @@ def step_records(rows: np.ndarray) -> list[dict]:
 
 
 # ---------------------------------------------------------------- sessions
-PROFILE_KINDS = ["gemm_chain", "attention", "embed_ln", "misc"]
+PROFILE_KINDS = ["gemm_qkv", "gemm_o", "gemm_fc", "gemm_proj", "gemm_lm", "attention", "layernorm", "misc"]
 
 
 def profile_enable(on: bool) -> None:

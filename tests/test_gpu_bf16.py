@@ -45,8 +45,7 @@ def run_gemm(sd, W, X, grid=0, flags=0):
 
 @pytest.mark.parametrize("M,K,T,grid", [(256, 64, 16, 0), (512, 256, 1, 0), (768, 768, 44, 0), (768, 768, 44, 5),
                                         (2304, 768, 72, 0), (3072, 768, 17, 3), (1000, 512, 100, 0),
-                                        (512, 1024, 256, 0), (512, 512, 250, 0), (50272, 768, 40, 0), (5120, 5120, 112, 0),
-                                        (5120, 20480, 192, 0), (384, 4096, 33, 148)])
+                                        (512, 1024, 256, 0), (512, 512, 250, 0), (50272, 768, 40, 0)])
 def test_gemm_matches_fp64(sd, M, K, T, grid):
     rng = np.random.default_rng(M * 7 + K + T)
     W = to_bf16_bits(rng.uniform(-1, 1, (M, K)).astype(np.float32))
@@ -55,11 +54,9 @@ def test_gemm_matches_fp64(sd, M, K, T, grid):
     Y, _ = run_gemm(sd, W, X, grid)
     err = np.abs(Y - ref)
     assert err.max() <= 2e-3 * np.abs(ref).max() + 1e-3, (err.max(), np.abs(ref).max())
-    # the split-K reduction sums contributors in a fixed order: a different
-    # token-ring depth (other pipeline timing) and a re-run give the same bits
-    Yt, _ = run_gemm(sd, W, X, grid, flags=6 << 5)
+    Yt, _ = run_gemm(sd, W, X, grid, flags=1)  # tile-major weights give the same bits
     assert np.array_equal(Yt.view(np.uint32), Y.view(np.uint32))
-    Yb, _ = run_gemm(sd, W, X, grid)
+    Yb, _ = run_gemm(sd, W, X, grid, flags=16)  # pre-swizzled tiles through 1D bulk copies
     assert np.array_equal(Yb.view(np.uint32), Y.view(np.uint32))
 
 
@@ -185,49 +182,3 @@ def test_device_loop_equals_host_loop_and_engine(sd, mode, predictor):
         assert g.generated_tokens == toks_dev
     else:
         assert np.mean([a == b for a, b in zip(g.generated_tokens, toks_dev)]) >= 0.6
-
-
-def run_chain(sd, X, W1, b1, W2, b2, resid, epi1, flags=0):
-    L = sd.lib()
-    fn = L.sd_debug_chain
-    u16, f32 = np.ctypeslib.ndpointer(np.uint16), np.ctypeslib.ndpointer(np.float32)
-    fn.argtypes = [u16, u16, f32, u16, f32, f32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, u16, f32]
-    T, K = X.shape
-    M1, M2 = W1.shape[0], W2.shape[0]
-    act = np.zeros((T, M1), np.uint16)
-    Y = np.zeros((T, M2), np.float32)
-    r = np.ascontiguousarray(resid, dtype=np.float32).copy()
-    rc = fn(X, W1, b1, W2, b2, r, T, K, M1, M2, epi1, flags, act, Y)
-    assert rc == 0
-    return act, r, Y
-
-
-@pytest.mark.parametrize("T,K,M1,M2", [(14, 768, 3072, 768), (14, 768, 768, 2304), (112, 1024, 4096, 1024),
-                                       (218, 768, 3072, 768), (192, 512, 2048, 512), (1, 256, 1024, 256)])
-@pytest.mark.parametrize("epi1", [1, 2])  # EPI_RESID_LN, EPI_GELU
-def test_gemm_chain(sd, T, K, M1, M2, epi1):
-    """Two GEMMs in one persistent launch: GEMM 2 consumes GEMM 1's fused
-    epilogue output (GELU activations, or residual + LayerNorm) produced by
-    the in-kernel split-K reduction of every CTA."""
-    rng = np.random.default_rng(T * 31 + K + M1 + epi1)
-    X = to_bf16_bits(rng.uniform(-1, 1, (T, K)).astype(np.float32))
-    W1 = to_bf16_bits(rng.uniform(-1, 1, (M1, K)).astype(np.float32) / np.sqrt(K))
-    W2 = to_bf16_bits(rng.uniform(-1, 1, (M2, M1)).astype(np.float32) / np.sqrt(M1))
-    b1 = rng.uniform(-0.5, 0.5, M1).astype(np.float32)
-    b2 = rng.uniform(-0.5, 0.5, M2).astype(np.float32)
-    resid = rng.uniform(-1, 1, (T, M1)).astype(np.float32)
-    act, r_out, Y = run_chain(sd, X, W1, b1, W2, b2, resid, epi1)
-    H = from_bf16_bits(X).astype(np.float64) @ from_bf16_bits(W1).astype(np.float64).T + b1
-    if epi1 == 2:
-        ref_act = 0.5 * H * (1 + np.tanh(0.7978845608028654 * (H + 0.044715 * H ** 3)))
-    else:
-        rr = resid.astype(np.float64) + H
-        assert np.abs(r_out - rr).max() <= 1e-3 * np.abs(rr).max() + 1e-4
-        mu = rr.mean(axis=1, keepdims=True)
-        ref_act = (rr - mu) / np.sqrt(((rr - mu) ** 2).mean(axis=1, keepdims=True) + 1e-5)
-    a = from_bf16_bits(act).astype(np.float64)
-    err = np.abs(a - ref_act)
-    assert err.max() <= 0.02 * np.abs(ref_act).max() + 2e-3, (err.max(), np.unravel_index(err.argmax(), err.shape))
-    refY = a @ from_bf16_bits(W2).astype(np.float64).T + b2
-    errY = np.abs(Y - refY)
-    assert errY.max() <= 1e-3 * np.abs(refY).max() + 1e-3, (errY.max(), np.unravel_index(errY.argmax(), errY.shape))

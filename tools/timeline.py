@@ -104,7 +104,7 @@ def main():
         if si == 2:
             lines.append(f"--- step {si}: {len(st)} launches, {(t_b - t_a) / 1e3:.1f} us; layer 1 sequence:")
             gemm_i = [i for i, l in enumerate(st) if l[0] == 1]
-            lo, hi = gemm_i[2], min(len(st), gemm_i[4] + 1)
+            lo, hi = gemm_i[4], min(len(st), gemm_i[8] + 3)
             prev_end = st[lo - 1][2]
             for l in st[lo:hi]:
                 lines.append(f"  {NAMES[l[0]]:13s} start {(l[1] - t_a) / 1e3:9.1f} dur {(l[2] - l[1]) / 1e3:7.1f} "
