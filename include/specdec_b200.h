@@ -168,6 +168,13 @@ int sd_decode(const sd_engine_config* cfg, sd_model* target, sd_model* draft,
 typedef struct sd_session sd_session;
 const char* sd_session_last_error(void);
 int sd_session_create(sd_model* m, const sd_engine_config* cfg, int capacity, sd_session** out);
+/* draft-model speculative decoding (cfg->predictor 0, predictors.cpp:9-37) on
+ * the device: the draft model keeps a persistent per-sample KV cache (the
+ * reference re-prefills the whole context per call), feeds only the 1-2
+ * context tokens it has not seen, then rolls out cfg->k greedy drafts; rollback
+ * after verification is metadata.  Drafts are identical by prefix purity. */
+int sd_session_create_draft(sd_model* target, sd_model* draft, const sd_engine_config* cfg, int capacity,
+                            sd_session** out);
 /* prefill (engine.cpp:330-385) and snapshot the post-prefill state */
 int sd_session_prefill(sd_session* s, const int32_t* prompts, const int32_t* prompt_lens);
 /* traj[B][stride]: each sample's greedy continuation (synthetic predictor) */

@@ -18,6 +18,12 @@
 struct sd_session {
     sd_model* model = nullptr;
     std::unique_ptr<sd_cache> cache;
+    // draft predictor (engine predictor 0): the draft model and its own
+    // persistent per-sample cache, device draft commit lengths
+    sd_model* draft = nullptr;
+    std::unique_ptr<sd_cache> dcache;
+    int32_t *dcommit = nullptr, *lsnap = nullptr;
+    std::vector<int32_t> snap_dcommit;
     sd_engine_config e{};
     int B = 0, ctx_cap = 0, kcap = 0, max_steps = 0;
     // device state
@@ -98,12 +104,56 @@ StepArgs step_args(sd_session* s) {
     return a;
 }
 
+DraftArgs draft_args(sd_session* s) {
+    Workspace& dws = s->dcache->ws;
+    DraftArgs d{};
+    d.B = s->B;
+    d.k = s->e.k;
+    d.kcap = s->kcap;
+    d.cap = s->dcache->c.cap;
+    d.active = s->active;
+    d.ctx = s->ctx;
+    d.ctx_len = s->ctx_len;
+    d.ctx_cap = s->ctx_cap;
+    d.dcommit = s->dcommit;
+    d.lsnap = s->lsnap;
+    d.drafts = s->drafts;
+    d.counts = s->counts;
+    d.tau = s->tau;
+    d.tokens = dws.d_tokens;
+    d.plans = dws.d_plans;
+    d.segs = dws.d_segs;
+    d.qidx = dws.d_qidx;
+    d.dT = dws.d_T;
+    d.argmax = dws.d_argmax;
+    return d;
+}
+
 // one device-resident verify step (fixed launch sequence, graph-capturable)
 void device_step(sd_session* s, cudaStream_t st, unsigned long long cond = 0, bool has_cond = false) {
     Cache& c = s->cache->c;
     StepArgs a = step_args(s);
     a.cond = cond;
     a.has_cond = has_cond ? 1 : 0;
+    if (s->e.predictor == 0) {  // k draft-model steps over the persistent draft cache
+        DraftArgs d = draft_args(s);
+        Workspace& dws = s->dcache->ws;
+        DeviceBatch dbd{dws.d_segs, dws.d_qidx, dws.d_T, 2 * s->B, s->dcache->c.cap, 2};
+        for (int j = 0; j < s->e.k; ++j) {
+            launch_draft_pack(d, j, st);
+            forward_fast_dev(s->draft->m, s->dcache->c, dws, dbd, 0, false, st);
+            launch_draft_take(d, j, st);
+        }
+        note_launches(2 * s->e.k);
+        launch_pack(a, st);
+        DeviceBatch db{a.segs, a.qidx, a.scalars, s->B * (s->kcap + 1), c.cap, s->kcap + 1};
+        forward_fast_dev(s->model->m, c, s->cache->ws, db, 0, false, st);
+        launch_accept(a, st);
+        if (c.layout == PADDED) launch_pad_fill(a, c, st);
+        launch_draft_commit(d, st);
+        note_launches(c.layout == PADDED ? 4 : 3);
+        return;
+    }
     PredictArgs p{};
     p.kind = s->e.predictor;
     p.match_len = s->e.match_len;
@@ -129,10 +179,17 @@ void device_step(sd_session* s, cudaStream_t st, unsigned long long cond = 0, bo
 
 }  // namespace
 
-sd_session* session_create(sd_model* m, const sd_engine_config& e, int capacity) {
+sd_session* session_create(sd_model* m, const sd_engine_config& e, int capacity, sd_model* draft = nullptr) {
     SD_CHECK(m->m.precision == BF16, CONFIG, "sessions run the bf16 performance path");
     SD_CHECK(e.mode == 1 || e.mode == 2, CONFIG, "speculative decoding needs the vanilla or ems mode");
-    SD_CHECK(e.predictor == 1 || e.predictor == 2, CONFIG, "device loop supports the retrieval / synthetic predictors");
+    SD_CHECK(e.predictor >= 0 && e.predictor <= 2, CONFIG, "unknown predictor");
+    if (e.predictor == 0) {
+        SD_CHECK(draft != nullptr, CONFIG, "draft predictor needs a draft model");
+        SD_CHECK(draft->m.precision == BF16, CONFIG, "the device draft rollout runs the bf16 path");
+        SD_CHECK(draft->m.cfg.vocab_size == m->m.cfg.vocab_size, CONFIG, "draft and target vocabularies differ");
+        SD_CHECK(draft->m.device == m->m.device, CONFIG, "draft and target must live on the same device");
+        SD_CHECK(e.k >= 1, CONFIG, "draft length must be >= 1");
+    }
     SD_CHECK(e.batch_size >= 1 && e.max_new_tokens >= 1, CONFIG, "batch_size and max_new_tokens must be >= 1");
     auto* s = new sd_session();
     try {
@@ -140,6 +197,7 @@ sd_session* session_create(sd_model* m, const sd_engine_config& e, int capacity)
         s->e = e;
         s->B = e.batch_size;
         s->kcap = e.predictor == 1 ? e.copy_len : e.k;
+        s->draft = e.predictor == 0 ? draft : nullptr;
         SD_CHECK(s->B * (s->kcap + 1) <= 256, CONFIG, "batch x (drafts + 1) must be <= 256 tokens per step");
         s->ctx_cap = capacity + 16;
         s->max_steps = e.max_new_tokens + 2;
@@ -163,6 +221,12 @@ sd_session* session_create(sd_model* m, const sd_engine_config& e, int capacity)
         s->accepted = ialloc(s, (size_t)B * (s->kcap + 1));
         CUDA_OK(cudaMallocHost(&s->h_flag, 16));
         s->cache->ws.ensure(m->m, s->cache->c, 256);
+        if (s->draft) {
+            s->dcache.reset(create_cache(draft, B, capacity, UNPAD));
+            s->dcache->ws.ensure(draft->m, s->dcache->c, 256);
+            s->dcommit = ialloc(s, B);
+            s->lsnap = ialloc(s, B);
+        }
     } catch (...) {
         delete s;
         throw;
@@ -196,6 +260,8 @@ void session_reset(sd_session* s) {
     CUDA_OK(cudaMemsetAsync(s->scalars, 0, 32, st));
     CUDA_OK(cudaMemsetAsync(s->log_tau, 0, 4 * (size_t)s->max_steps * B, st));
     CUDA_OK(cudaMemsetAsync(s->log_k, 0xff, 4 * (size_t)s->max_steps * B, st));
+    if (s->draft)  // the draft cache keeps the prompt KV; later positions are rewritten
+        CUDA_OK(cudaMemcpyAsync(s->dcommit, s->snap_dcommit.data(), 4 * (size_t)B, cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaStreamSynchronize(st));
 }
 
@@ -253,6 +319,21 @@ void session_prefill(sd_session* s, const int32_t* prompts, const int32_t* lens)
         s->snap_active[b] = fin ? 0 : 1;
         CUDA_OK(cudaMemcpy(s->ctx + (size_t)b * s->ctx_cap, s->prompts[b].data(), 4 * (size_t)lens[b],
                            cudaMemcpyHostToDevice));
+    }
+    if (s->draft) {  // the draft model prefills the same prompts into its own cache
+        const Config& dcfg = s->draft->m.cfg;
+        std::vector<Plan> dplans;
+        for (int b = 0; b < B; ++b) {
+            SD_CHECK(lens[b] + s->e.max_new_tokens + s->e.k <= dcfg.max_positions, CAPACITY,
+                     "prompt plus generation budget exceeds the draft model's max_positions");
+            for (int i = 0; i < lens[b]; ++i) dplans.push_back(Plan{b, i, i, 1});
+        }
+        reset_cache(s->dcache.get());
+        std::vector<int32_t> dam(flat.size());
+        forward_planned_host(s->draft, s->dcache.get(), flat.data(), dplans.data(), (int)flat.size(), nullptr,
+                             dam.data());
+        for (int b = 0; b < B; ++b) commit_accepted_host(s->dcache.get(), b, lens[b]);
+        s->snap_dcommit.assign(lens, lens + B);
     }
     s->snap_committed = c.committed;
     s->snap_logical = c.logical;
@@ -375,6 +456,7 @@ int session_run(sd_session* s, int use_graph, int graph_steps, float* gpu_ms) {
 // predictor on the host, H2D drafts, D2H tau + accepted every step).
 int session_run_host(sd_session* s, float* gpu_ms, int64_t* h2d_bytes, int64_t* d2h_bytes) {
     SD_CHECK(s->prefilled, CONTRACT, "session has not been prefilled");
+    SD_CHECK(s->e.predictor != 0, CONFIG, "the host-driven loop runs the retrieval / synthetic predictors");
     cudaStream_t st = s->model->st;
     set_device(s->model->m.device);
     const int B = s->B;
@@ -490,6 +572,10 @@ const char* sd_session_last_error(void) { return g_serr.c_str(); }
 
 int sd_session_create(sd_model* m, const sd_engine_config* cfg, int capacity, sd_session** out) {
     return sguard([&] { *out = session_create(m, *cfg, capacity); });
+}
+int sd_session_create_draft(sd_model* target, sd_model* draft, const sd_engine_config* cfg, int capacity,
+                            sd_session** out) {
+    return sguard([&] { *out = session_create(target, *cfg, capacity, draft); });
 }
 int sd_session_prefill(sd_session* s, const int32_t* prompts, const int32_t* lens) {
     return sguard([&] { session_prefill(s, prompts, lens); });

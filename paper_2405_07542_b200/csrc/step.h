@@ -58,6 +58,34 @@ struct PredictArgs {
     int traj_stride;
 };
 
+// Device draft-model rollout (predictors.cpp:9-37) with a PERSISTENT per-sample
+// draft KV cache: the reference re-prefills the whole context on every call;
+// here only the 1-2 context tokens the draft cache has not seen are fed, then
+// k-1 single-token steps.  Drafts are identical by prefix purity
+// (model.hpp:54-57): a token's output depends only on its own prefix.
+struct DraftArgs {
+    int B, k, kcap, cap;        // draft length, drafts stride, draft-cache capacity
+    const int32_t* active;      // [B] target-loop active flags (start of the step)
+    const int32_t* ctx;         // [B][ctx_cap] accepted context
+    const int32_t* ctx_len;     // [B]
+    int ctx_cap;
+    int32_t* dcommit;           // [B] draft-cache positions holding context KV
+    int32_t* lsnap;             // [B] context length when this step's rollout began
+    int32_t* drafts;            // [B][kcap] -> the target verify step
+    int32_t* counts;            // [B]
+    const int32_t* tau;         // [B] target accept output (commit)
+    // the draft forward's ragged batch (the draft cache's workspace)
+    int32_t* tokens;
+    Plan* plans;
+    SampleSeg* segs;
+    int32_t* qidx;
+    int32_t* dT;
+    const int32_t* argmax;      // draft greedy_next per row
+};
+void launch_draft_pack(const DraftArgs& d, int j, cudaStream_t st);
+void launch_draft_take(const DraftArgs& d, int j, cudaStream_t st);
+void launch_draft_commit(const DraftArgs& d, cudaStream_t st);
+
 void launch_pack(const StepArgs& a, cudaStream_t st);
 void launch_accept(const StepArgs& a, cudaStream_t st);
 void launch_pad_fill(const StepArgs& a, const Cache& c, cudaStream_t st);

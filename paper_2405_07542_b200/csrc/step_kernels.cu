@@ -270,6 +270,81 @@ __global__ void k_predict(StepArgs a, PredictArgs p) {
     }
 }
 
+// Draft step j's ragged batch: j == 0 feeds the context tokens the draft
+// cache lacks (1 after a rejection, 2 when every draft was accepted plus the
+// bonus token), j > 0 feeds draft j-1.  One block.
+__global__ void k_draft_pack(DraftArgs d, int j) {
+    CtaTrace trace__(TK_PACK);
+    pdl_trigger();
+    pdl_wait();
+    __shared__ int s_row0[256 + 1];
+    const int B = d.B;
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int s = 0; s < B; ++s) {
+            s_row0[s] = t;
+            if (d.active[s]) t += j == 0 ? d.ctx_len[s] - d.dcommit[s] : 1;
+        }
+        s_row0[B] = t;
+        *d.dT = t;
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < B; s += blockDim.x) {
+        const int row0 = s_row0[s], n = s_row0[s + 1] - row0;
+        if (n == 0) {
+            d.segs[s] = SampleSeg{row0, 0, 0, 0};
+            continue;
+        }
+        if (j == 0) d.lsnap[s] = d.ctx_len[s];
+        const int pos0 = j == 0 ? d.dcommit[s] : d.ctx_len[s] + j - 1;
+        for (int o = 0; o < n; ++o) {
+            const int pos = pos0 + o;
+            d.tokens[row0 + o] = j == 0 ? d.ctx[(size_t)s * d.ctx_cap + pos] : d.drafts[(size_t)s * d.kcap + j - 1];
+            d.plans[row0 + o] = Plan{s, pos, pos, 1};
+            d.qidx[row0 + o] = row0 + o;
+        }
+        d.segs[s] = SampleSeg{row0, n, pos0 + n, 0};
+    }
+}
+
+// draft j = greedy_next of the sample's last row (model.cpp:34-41)
+__global__ void k_draft_take(DraftArgs d, int j) {
+    CtaTrace trace__(TK_PACK);
+    pdl_trigger();
+    pdl_wait();
+    for (int s = threadIdx.x; s < d.B; s += blockDim.x) {
+        if (!d.active[s]) {
+            d.counts[s] = 0;
+            continue;
+        }
+        const SampleSeg g = d.segs[s];
+        d.drafts[(size_t)s * d.kcap + j] = d.argmax[g.q_start + g.n_q - 1];
+        d.counts[s] = j + 1;
+        if (j == 0) d.dcommit[s] = d.lsnap[s];  // every context token is in the draft cache
+    }
+}
+
+// After verification: the draft KV of positions lsnap .. lsnap+tau-2 holds the
+// accepted x_0..x_{tau-2} (= the drafts), so it stays; the rest is forgotten
+// (rollback by metadata, as UnpadArena::commit_accepted, kv_cache.cpp:158).
+__global__ void k_draft_commit(DraftArgs d) {
+    CtaTrace trace__(TK_ACCEPT);
+    pdl_trigger();
+    pdl_wait();
+    for (int s = threadIdx.x; s < d.B; s += blockDim.x) {
+        const int tau = d.tau[s];
+        if (tau > 0) d.dcommit[s] = d.lsnap[s] + min(tau - 1, d.k - 1);
+    }
+}
+
+void launch_draft_pack(const DraftArgs& d, int j, cudaStream_t st) {
+    launch_k(k_draft_pack, dim3(1), dim3(256), 0, st, d, j);
+}
+void launch_draft_take(const DraftArgs& d, int j, cudaStream_t st) {
+    launch_k(k_draft_take, dim3(1), dim3(256), 0, st, d, j);
+}
+void launch_draft_commit(const DraftArgs& d, cudaStream_t st) { launch_k(k_draft_commit, dim3(1), dim3(256), 0, st, d); }
+
 void launch_pack(const StepArgs& a, cudaStream_t st) { launch_k(k_pack, dim3(1), dim3(256), 0, st, a); }
 void launch_accept(const StepArgs& a, cudaStream_t st) { launch_k(k_accept, dim3(1), dim3(256), 0, st, a); }
 void launch_pad_fill(const StepArgs& a, const Cache& c, cudaStream_t st) {

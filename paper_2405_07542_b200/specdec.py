@@ -110,6 +110,7 @@ def lib() -> C.CDLL:
         "sd_profile_read": ([np.ctypeslib.ndpointer(np.float64), C.c_int], C.c_int),
         "sd_session_last_error": ([], C.c_char_p),
         "sd_session_create": ([vp, C.POINTER(_EngineConfigT), C.c_int, pp], C.c_int),
+        "sd_session_create_draft": ([vp, vp, C.POINTER(_EngineConfigT), C.c_int, pp], C.c_int),
         "sd_session_prefill": ([vp, I32P, I32P], C.c_int),
         "sd_session_set_trajectory": ([vp, I32P, C.c_int], C.c_int),
         "sd_session_reset": ([vp], C.c_int),
@@ -541,11 +542,17 @@ def _scheck(rc: int) -> None:
 class Session:
     """A prefilled batch whose decode loop (engine.cpp:391-489) runs on the GPU."""
 
-    def __init__(self, model: Model, config: EngineConfig, capacity: int):
+    def __init__(self, model: Model, config: EngineConfig, capacity: int, draft: Model | None = None):
         h = C.c_void_p()
-        _scheck(lib().sd_session_create(model._h, C.byref(config._c()), capacity, C.byref(h)))
+        if config.predictor == "draft":
+            if draft is None:
+                raise ConfigError("draft predictor needs a draft model")
+            _scheck(lib().sd_session_create_draft(model._h, draft._h, C.byref(config._c()), capacity, C.byref(h)))
+        else:
+            _scheck(lib().sd_session_create(model._h, C.byref(config._c()), capacity, C.byref(h)))
         self._h = h.value
         self.model = model
+        self.draft = draft  # keeps the draft model alive with the session
         self.config = config
 
     def close(self):

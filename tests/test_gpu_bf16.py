@@ -182,3 +182,36 @@ def test_device_loop_equals_host_loop_and_engine(sd, mode, predictor):
         assert g.generated_tokens == toks_dev
     else:
         assert np.mean([a == b for a, b in zip(g.generated_tokens, toks_dev)]) >= 0.6
+
+
+@pytest.mark.parametrize("self_draft", [True, False])
+def test_device_draft_loop(sd, self_draft):
+    """Draft-model speculative decoding on the device with a persistent draft
+    KV cache (predictors.cpp:9-37 re-prefills instead): the token streams are
+    the target's greedy streams (losslessness), and the drafts -- hence every
+    step record -- equal the reference-shaped host engine's, which re-prefills
+    the draft on every call (prefix purity, model.hpp:54-57)."""
+    cfg = dict(num_layers=2, num_heads=4, head_dim=128, vocab_size=700, max_positions=512, init_seed=0xD7AF)
+    dcfg = dict(cfg) if self_draft else dict(cfg, num_layers=1, init_seed=0xD7B0)
+    rng = np.random.default_rng(5)
+    B, new, k = 5, 30, 4
+    prompts = [[0] + rng.integers(3, 700, size=int(rng.integers(20, 60))).tolist() for _ in range(B)]
+    m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.BF16)
+    d = sd.Model.init(sd.ModelConfig(**dcfg), precision=sd.BF16)
+    e = sd.EngineConfig(mode="ems", predictor="draft", k=k, batch_size=B, max_new_tokens=new, stop_on_eos=False)
+    s = sd.Session(m, e, 512, draft=d)
+    s.prefill(prompts)
+    steps, _ = s.run()
+    toks, lk, lt = s.outputs()
+    s.reset()
+    steps2, _ = s.run(use_graph=False)
+    assert s.outputs()[0] == toks
+    g = sd.decode(sd.EngineConfig(mode="greedy", batch_size=B, max_new_tokens=new, stop_on_eos=False), m, prompts)
+    assert g.generated_tokens == toks
+    r = sd.decode(e, m, prompts, draft=d)
+    assert r.generated_tokens == toks
+    taus = [x["tau"] for st in r.steps for x in st["samples"]]
+    act = lk[:steps] >= 0
+    assert taus == (lt[:steps][act] & 0xFFFF).tolist()
+    if self_draft:  # the draft is the target: every draft is accepted
+        assert steps == -(-(new - 1) // (k + 1))
