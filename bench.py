@@ -102,6 +102,30 @@ def measured_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
+def ncu_traffic(kernel_substr):
+    """DRAM bytes (read + write) per launch of a kernel from the committed ncu
+    launch list of tools/profile_step.py (profiles/*_step_launches.csv, newest
+    first): the traffic figure next to the algorithmic bytes."""
+    import csv
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_step_launches.csv")), reverse=True):
+        try:
+            rows = list(csv.reader(open(path)))
+            start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+            hdr = rows[start]
+            ki, mi, vi, ii = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
+            per = {}
+            for r in rows[start + 1:]:
+                if kernel_substr in r[ki] and r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    per[r[ii]] = per.get(r[ii], 0.0) + float(r[vi].replace(",", ""))
+            if per:
+                return sum(per.values()) / len(per), os.path.basename(path)
+        except (OSError, StopIteration, ValueError):
+            continue
+    return None, None
+
+
 def step_stats(log_k, log_tau):
     """make_step_record / compute_metrics (engine.cpp:78-126) from the device logs."""
     taus, rbar, useful, pad_kv, pad_in, steps = [], [], 0, 0, 0, 0
@@ -464,6 +488,12 @@ def main():
     gemm_ms = sum(kinds[k]["ms"] for k in kinds if k.startswith("gemm"))
     gemm_b = sum(kinds[k]["bytes"] for k in kinds if k.startswith("gemm"))
     step_b = sum(v["bytes"] for v in kinds.values())
+    tk = {"attention": "k_attention", "attn_combine": "k_attn_combine"}.get(dom, "k_gemm")
+    traffic, src_csv = ncu_traffic(tk)
+    if traffic is not None:
+        roof["traffic"] = round(traffic / 1e6, 2)
+        roof["traffic_unit"] = "MB per launch (ncu dram__bytes_read+write, %s)" % src_csv
+        roof["algorithmic_mb_per_launch"] = round(kinds[dom]["bytes"] / max(1, kinds[dom]["launches"]) / 1e6, 2)
     roof["all_gemms_gbs"] = round(gemm_b / (gemm_ms / 1000) / 1e9, 1) if gemm_ms else None
     roof["whole_step_gbs"] = round(step_b / (total_ms / 1000) / 1e9, 1) if total_ms else None
 

@@ -482,7 +482,7 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
 // launching stream and charge it the ALGORITHMIC bytes it must move
 // (weights + activations + KV it reads/writes once).  bench.py reads this
 // to report the dominant kernel's achieved bandwidth.
-enum ProfKind { PK_QKV, PK_O, PK_FC, PK_PROJ, PK_LM, PK_ATTN, PK_ROW, PK_MISC, PK_N };
+enum ProfKind { PK_QKV, PK_O, PK_FC, PK_PROJ, PK_LM, PK_ATTN, PK_ROW, PK_MISC, PK_COMBINE, PK_N };
 struct ProfRec {
     int kind;
     cudaEvent_t a, b;
@@ -605,7 +605,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
             PROF(PK_ATTN, launch_k(k_attention<64>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
         launches++;
         if (splits > 1) {
-            PROF(PK_ATTN, launch_k(k_attn_combine, dim3(n, heads), dim3(hd), 0, st, at, hd, (const int*)db.dT));
+            PROF(PK_COMBINE, launch_k(k_attn_combine, dim3(n, heads), dim3(hd), 0, st, at, hd, (const int*)db.dT));
             launches++;
         }
         // O projection + residual, fused with LN2 -> xb
@@ -684,15 +684,15 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
                               V * H * 2 + Tt * H * 2,
                               kv * 2 * hd * 2 * heads + Tt * H * 4,
                               Tt * H * 6,
-                              0};
+                              0,
+                              // split partials read (max_splits upper bound) + context written
+                              Tt * heads * f->max_splits * (hd + 2) * 4.0 + Tt * H * 2};
         for (auto& r : g_prof_pending) {
             float ms = 0.0f;
             CUDA_OK(cudaEventElapsedTime(&ms, r.a, r.b));
             g_prof_acc[r.kind][0] += 1;
             g_prof_acc[r.kind][1] += ms;
-            // attention bytes are charged once per layer (combine adds none)
-            bool combine = r.kind == PK_ATTN && (&r != &g_prof_pending.front()) && (&r - 1)->kind == PK_ATTN;
-            g_prof_acc[r.kind][2] += combine ? 0.0 : bytes[r.kind];
+            g_prof_acc[r.kind][2] += bytes[r.kind];
             cudaEventDestroy(r.a);
             cudaEventDestroy(r.b);
         }

@@ -280,10 +280,22 @@ __global__ void __launch_bounds__(256) k_reduce_tile(const GemmArgs a, const Red
     float v[RT];
 #pragma unroll
     for (int i = 0; i < RT; ++i) v[i] = 0.0f;
-    for (int c = 0; c < nc; ++c) {
+    // every load of CB contributors x RT tokens is issued before the first add:
+    // one L2 round trip per CB contributors instead of one per contributor
+    // (the sum itself still runs in contributor order: deterministic)
+    constexpr int CB = RT <= 4 ? 8 : 4;
+    for (int c0 = 0; c0 < nc; c0 += CB) {
+        float x[CB][RT];
 #pragma unroll
-        for (int i = 0; i < RT; ++i)
-            if (i < nt) v[i] += __ldcg(p + ((size_t)c * 256 + i) * 256);
+        for (int cc = 0; cc < CB; ++cc)
+#pragma unroll
+            for (int i = 0; i < RT; ++i)
+                x[cc][i] = (c0 + cc < nc && i < nt) ? __ldcg(p + ((size_t)(c0 + cc) * 256 + i) * 256) : 0.0f;
+#pragma unroll
+        for (int cc = 0; cc < CB; ++cc)
+#pragma unroll
+            for (int i = 0; i < RT; ++i)
+                if (c0 + cc < nc) v[i] += x[cc][i];
     }
     const float b = a.bias ? a.bias[m] : 0.0f;
     if constexpr (EPI == EPI_RESID_LN) {  // residual add; the LayerNorm runs in k_ln_rows

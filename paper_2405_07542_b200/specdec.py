@@ -520,7 +520,8 @@ def step_records(rows: np.ndarray) -> list[dict]:
 
 
 # ---------------------------------------------------------------- sessions
-PROFILE_KINDS = ["gemm_qkv", "gemm_o", "gemm_fc", "gemm_proj", "gemm_lm", "attention", "layernorm", "misc"]
+PROFILE_KINDS = ["gemm_qkv", "gemm_o", "gemm_fc", "gemm_proj", "gemm_lm", "attention", "layernorm", "misc",
+                 "attn_combine"]
 
 
 def profile_enable(on: bool) -> None:
