@@ -543,7 +543,11 @@ void make_b_maps(GemmMaps& maps, const void* x, int64_t rows, int64_t cols) {
 void gemm_plan(GemmArgs& a, int sms) {
     SD_CHECK(a.K % kBK == 0, CONFIG, "bf16 mode needs K % 64 == 0");
     long long U = (long long)a.m_tiles * (a.K / kBK);
-    a.grid = (int)std::min<long long>(U, sms);
+    // at least kMinUnits k-blocks (128 KB of weights) per CTA: a small GEMM
+    // (e.g. a 125M-parameter draft model) otherwise splits every tile over a
+    // dozen CTAs and pays more in partials and reduction than in streaming
+    constexpr long long kMinUnits = 4;
+    a.grid = (int)std::max<long long>(1, std::min<long long>((U + kMinUnits - 1) / kMinUnits, sms));
     a.max_contrib = max_contrib_for(a.m_tiles, a.K / kBK, a.grid);
 }
 

@@ -274,7 +274,7 @@ __global__ void k_predict(StepArgs a, PredictArgs p) {
 // cache lacks (1 after a rejection, 2 when every draft was accepted plus the
 // bonus token), j > 0 feeds draft j-1.  One block.
 __global__ void k_draft_pack(DraftArgs d, int j) {
-    CtaTrace trace__(TK_PACK);
+    CtaTrace trace__(TK_DRAFT_PACK);
     pdl_trigger();
     pdl_wait();
     __shared__ int s_row0[256 + 1];
@@ -309,7 +309,7 @@ __global__ void k_draft_pack(DraftArgs d, int j) {
 
 // draft j = greedy_next of the sample's last row (model.cpp:34-41)
 __global__ void k_draft_take(DraftArgs d, int j) {
-    CtaTrace trace__(TK_PACK);
+    CtaTrace trace__(TK_DRAFT_TAKE);
     pdl_trigger();
     pdl_wait();
     for (int s = threadIdx.x; s < d.B; s += blockDim.x) {
@@ -328,7 +328,7 @@ __global__ void k_draft_take(DraftArgs d, int j) {
 // accepted x_0..x_{tau-2} (= the drafts), so it stays; the rest is forgotten
 // (rollback by metadata, as UnpadArena::commit_accepted, kv_cache.cpp:158).
 __global__ void k_draft_commit(DraftArgs d) {
-    CtaTrace trace__(TK_ACCEPT);
+    CtaTrace trace__(TK_DRAFT_COMMIT);
     pdl_trigger();
     pdl_wait();
     for (int s = threadIdx.x; s < d.B; s += blockDim.x) {

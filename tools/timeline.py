@@ -22,7 +22,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 NAMES = {1: "gemm", 2: "red_store", 3: "red_gelu", 4: "red_qkv", 5: "red_resid", 6: "ln_rows", 7: "argmax",
-         8: "embed_ln", 9: "attention", 10: "attn_combine", 11: "predict", 12: "pack", 13: "accept", 14: "pad_fill"}
+         8: "embed_ln", 9: "attention", 10: "attn_combine", 11: "predict", 12: "pack", 13: "accept", 14: "pad_fill",
+         15: "draft_pack", 16: "draft_take", 17: "draft_commit"}
 REC = np.dtype([("kid", "<u4"), ("blk", "<u4"), ("smid", "<u4"), ("n", "<u4"), ("t0", "<u8"), ("t1", "<u8")])
 
 
@@ -48,6 +49,7 @@ def main():
     ap.add_argument("--batch", type=int, default=24)
     ap.add_argument("--cap", type=int, default=6_000_000)
     ap.add_argument("--mode", default="ems")
+    ap.add_argument("--draft", action="store_true", help="C4: OPT-125m-shaped draft model, k=4")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "timeline.txt"))
     a = ap.parse_args()
     import bench
@@ -60,9 +62,15 @@ def main():
     m = sd.Model.init(sd.ModelConfig(**cfg), device=0, precision=sd.BF16)
     prompts = bench.prompts_for(range(a.batch), cfg["vocab_size"], 600, 900)
     cap = max(len(p) for p in prompts) + 128 + 9 if a.mode == "ems" else cfg["max_positions"]
-    e = sd.EngineConfig(mode=a.mode, predictor="retrieval", k=7, match_len=2, copy_len=7, batch_size=a.batch,
-                        max_new_tokens=128, stop_on_eos=False, seed=1)
-    s = sd.Session(m, e, cap)
+    if a.draft:
+        d = sd.Model.init(sd.ModelConfig(**dict(bench.C2, init_seed=cfg["init_seed"] + 1)), device=0, precision=sd.BF16)
+        e = sd.EngineConfig(mode=a.mode, predictor="draft", k=4, batch_size=a.batch, max_new_tokens=128,
+                            stop_on_eos=False)
+        s = sd.Session(m, e, cap, draft=d)
+    else:
+        e = sd.EngineConfig(mode=a.mode, predictor="retrieval", k=7, match_len=2, copy_len=7, batch_size=a.batch,
+                            max_new_tokens=128, stop_on_eos=False, seed=1)
+        s = sd.Session(m, e, cap)
     s.prefill(prompts)
     for _ in range(2):
         s.reset()
@@ -78,7 +86,7 @@ def main():
     print(f"traced: {steps} steps {ms:.1f} ms, {n.value} records", flush=True)
     ls = launches(rec)
     # verify steps delimited by k_predict launches; drop the last (possibly truncated) one
-    starts = [l[1] for l in ls if l[0] == 11]
+    starts = [l[1] for l in ls if l[0] == (17 if a.draft else 11)]
     lines = []
     tot = defaultdict(float)
     gaps_tot, n_steps, step_tot = 0.0, 0, 0.0
@@ -104,7 +112,7 @@ def main():
         if si == 2:
             lines.append(f"--- step {si}: {len(st)} launches, {(t_b - t_a) / 1e3:.1f} us; layer 1 sequence:")
             gemm_i = [i for i, l in enumerate(st) if l[0] == 1]
-            lo, hi = gemm_i[4], min(len(st), gemm_i[8] + 3)
+            lo, hi = (0, min(len(st), 60)) if a.draft else (gemm_i[4], min(len(st), gemm_i[8] + 3))
             prev_end = st[lo - 1][2]
             for l in st[lo:hi]:
                 lines.append(f"  {NAMES[l[0]]:13s} start {(l[1] - t_a) / 1e3:9.1f} dur {(l[2] - l[1]) / 1e3:7.1f} "
