@@ -14,10 +14,12 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gemm.h"
 #include "handles.h"
 #include "pdl.cuh"
+#include "sm100_ptx.cuh"
 #include "trace.cuh"
 
 SD_TRACE_TU(fast)
@@ -43,6 +45,9 @@ struct FastWorkspace {
     int* row_cnt = nullptr;    // per-token LayerNorm arrival counters [256]
     int* attn_cnt = nullptr;   // split-KV arrival counters [B * heads * 16]
     GemmMaps map_xb, map_ctx, map_act;
+    CUtensorMap kv_map;        // TMA view of the KV arena [L*2*B*heads*cap][hd], box {64, 128}
+    CUtensorMap q_map;         // TMA view of the queries [256][h], one-row boxes {64, 1}
+    int* attn_work = nullptr;  // persistent attention item counters [num_layers], zeroed per forward
     std::vector<void*> allocs;
 };
 
@@ -207,6 +212,7 @@ struct AttnArgs {
     float* part_o;
     float* part_ml;
     int* cnt;                  // [B * heads * q_tiles] split arrival counters (self-resetting)
+    int* work;                 // persistent kernel: this launch's item counter (zeroed per forward)
     int h, heads, B, cap, layer, max_splits;
     float scale_log2;          // log2(e) / sqrt(hd)
 };
@@ -409,6 +415,486 @@ __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
     }
 }
 
+// Same work decomposition as k_attention, math on the 5th-generation tensor
+// cores (HD = 128).  K and V arrive by TMA (128-byte swizzle); one thread
+// issues tcgen05.mma with the accumulators in TMEM (32 columns per CTA):
+//   S^T = K Q^T   : M = 128 keys, N = 8 queries, K = 128 (A = K tile,
+//                   K-major; B = the Q rows, K-major)
+//   O^T = V^T P^T : M = 128 (hd), N = 8 queries, K = 128 keys (A = the SAME
+//                   V tile read MN-major: no transpose pass; B = P^T written
+//                   by the softmax threads in the swizzled K-major layout)
+// Thread = key for the softmax (one tcgen05.ld of its 8 scores), thread = hd
+// row for the output.  Split partials merge in k_attn_combine as before.
+constexpr int kTcKeys = 128;
+constexpr int kTcSmem = 1024 + 4 * kTcKeys * 128 + 2 * 8 * 128 * 2 + 8 * kTcKeys * 4;
+__global__ void __launch_bounds__(128) k_attention_tc(const __grid_constant__ CUtensorMap tm_kv, AttnArgs a) {
+    CtaTrace trace__(TK_ATTN);
+    constexpr int HD = 128;
+    pdl_trigger();
+    const int sh = blockIdx.x, split = blockIdx.y, qt = blockIdx.z;
+    const int s = sh / a.heads, head = sh % a.heads;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, tid = threadIdx.x;
+    extern __shared__ uint8_t smraw[];
+    uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+    uint8_t* sK = sm;                          // 2 boxes [128 keys][64 hd] SW128
+    uint8_t* sV = sK + 2 * kTcKeys * 128;      // same
+    uint8_t* sQ = sV + 2 * kTcKeys * 128;      // 2 atoms [8 q][64 hd] SW128 (K-major B)
+    uint8_t* sP = sQ + 2 * 8 * 128;            // 2 atoms [8 q][64 keys] SW128 (K-major B)
+    float* sS = (float*)(sP + 2 * 8 * 128);    // [8 q][128 keys]
+    __shared__ uint64_t bar_load, bar_mma;
+    __shared__ uint32_t tslot;
+    __shared__ float sM[kQT], sL[kQT];
+    __shared__ int sTok[kQT], sWs[kQT];
+
+    pdl_wait();
+    const SampleSeg seg = a.segs[s];
+    const int k_begin = split * kTcKeys;
+    if (seg.n_q == 0 || qt * kQT >= seg.n_q || k_begin >= seg.kv_len) return;
+    const int nq = min(kQT, seg.n_q - qt * kQT);
+    const int kv_end = min(seg.kv_len, k_begin + kTcKeys);
+    if (warp == 0) ptx::tmem_alloc32(&tslot);
+    if (tid == 0) {
+        ptx::mbar_init(&bar_load, 1);
+        ptx::mbar_init(&bar_mma, 1);
+        ptx::fence_barrier_init();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tslot;
+    const int row_k = (((a.layer * 2 + 0) * a.B + s) * a.heads + head) * a.cap + k_begin;
+    const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap + k_begin;
+    if (tid == 0) {  // K / V tiles: keys past the extent are masked below
+        const uint64_t pol = ptx::policy_evict_first();
+        ptx::mbar_arrive_expect_tx(&bar_load, 4 * kTcKeys * 128);
+        ptx::tma_load_2d(sK, &tm_kv, &bar_load, 0, row_k, pol);
+        ptx::tma_load_2d(sK + kTcKeys * 128, &tm_kv, &bar_load, 64, row_k, pol);
+        ptx::tma_load_2d(sV, &tm_kv, &bar_load, 0, row_v, pol);
+        ptx::tma_load_2d(sV + kTcKeys * 128, &tm_kv, &bar_load, 64, row_v, pol);
+    }
+    {  // Q rows -> swizzled K-major B tile (rows past nq repeat row 0: unused columns)
+        const int r = tid / 16, c8 = tid % 16;
+        const int tok = a.qidx[seg.q_start + qt * kQT + (r < nq ? r : 0)];
+        const uint4 v = *(const uint4*)(a.q + (size_t)tok * a.h + head * HD + c8 * 8);
+        *(uint4*)(sQ + (c8 / 8) * 1024 + r * 128 + (((c8 % 8) ^ (r & 7)) << 4)) = v;
+        if (tid < kQT) {
+            const int t2 = tid < nq ? a.qidx[seg.q_start + qt * kQT + tid] : -1;
+            sTok[tid] = t2;
+            sWs[tid] = t2 >= 0 ? a.plans[t2].write_slot : -1;
+        }
+    }
+    ptx::fence_proxy_async_smem();  // generic smem writes (Q) -> visible to the tensor core
+    __syncthreads();
+    if (tid == 0) {
+        ptx::mbar_wait(&bar_load, 0);
+        ptx::tc_fence_after();
+        const uint32_t idesc = ptx::umma_idesc_bf16(kTcKeys, kQT);
+        const uint32_t ka = ptx::smem_u32(sK), qa = ptx::smem_u32(sQ);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+            ptx::umma_bf16(tmem, ptx::umma_desc_kmajor_sw128(ka + (k / 4) * (kTcKeys * 128) + (k % 4) * 32),
+                           ptx::umma_desc_kmajor_sw128(qa + (k / 4) * 1024 + (k % 4) * 32), idesc, k > 0 ? 1u : 0u);
+        ptx::umma_commit(&bar_mma);
+    }
+    ptx::mbar_wait(&bar_mma, 0);
+    ptx::tc_fence_after();
+    // ---- softmax over this split's keys: thread = key
+    const int key = k_begin + tid;
+    float x[kQT];
+    ptx::tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16), x);
+    const bool in_ext = key < kv_end && !(a.pad && a.pad[(size_t)s * a.cap + key]);
+#pragma unroll
+    for (int q = 0; q < kQT; ++q) {
+        x[q] = (in_ext && key <= sWs[q]) ? x[q] * a.scale_log2 : -INFINITY;
+        sS[q * kTcKeys + tid] = x[q];
+    }
+    __syncthreads();
+    {  // per-query max: 16 threads per query, 8 keys each
+        const int q = tid / 16, part = tid % 16;
+        float m = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) m = fmaxf(m, sS[q * kTcKeys + part * 8 + i]);
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (part == 0) sM[q] = m;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kQT; ++q) {
+        const float p = (x[q] == -INFINITY) ? 0.0f : exp2f(x[q] - sM[q]);
+        sS[q * kTcKeys + tid] = p;
+        // P^T [q][key], K-major SW128: atom = key / 64, 16-byte chunk = (key % 64) / 8 ^ (q % 8)
+        *(__nv_bfloat16*)(sP + (tid / 64) * 1024 + q * 128 + ((((tid % 64) / 8) ^ (q & 7)) << 4) + (tid % 8) * 2) =
+            __float2bfloat16_rn(p);
+    }
+    ptx::fence_proxy_async_smem();
+    __syncthreads();
+    {  // per-query sum
+        const int q = tid / 16, part = tid % 16;
+        float l = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) l += sS[q * kTcKeys + part * 8 + i];
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+        if (part == 0) sL[q] = l;
+    }
+    if (tid == 0) {
+        ptx::tc_fence_after();
+        const uint32_t idesc = ptx::umma_idesc_bf16_amn(HD, kQT);
+        const uint32_t va = ptx::smem_u32(sV), pa = ptx::smem_u32(sP);
+#pragma unroll
+        for (int k = 0; k < kTcKeys / 16; ++k)  // 16 keys per step: V rows k*16.., P^T columns k*16..
+            ptx::umma_bf16(tmem + 16, ptx::umma_desc_mn_sw128(va + k * 16 * 128, kTcKeys * 128, 1024),
+                           ptx::umma_desc_kmajor_sw128(pa + (k / 4) * 1024 + (k % 4) * 32), idesc, k > 0 ? 1u : 0u);
+        ptx::umma_commit(&bar_mma);
+    }
+    ptx::mbar_wait(&bar_mma, 1);
+    ptx::tc_fence_after();
+    __syncthreads();  // sL complete
+    float o[kQT];  // thread = hd row d
+    ptx::tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + 16, o);
+    const int d = tid;
+    const int nsplit = (seg.kv_len + kTcKeys - 1) / kTcKeys;
+#pragma unroll
+    for (int q = 0; q < kQT; ++q) {
+        if (q >= nq) break;
+        const int tok = sTok[q];
+        if (nsplit == 1) {
+            a.ctx[(size_t)tok * a.h + head * HD + d] = __float2bfloat16_rn(o[q] / sL[q]);
+        } else {
+            const size_t base = ((size_t)tok * a.heads + head) * a.max_splits + split;
+            a.part_o[base * HD + d] = o[q];
+            if (d == 0) {
+                a.part_ml[base * 2] = sM[q];
+                a.part_ml[base * 2 + 1] = sL[q];
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc32(tmem);
+}
+
+// Persistent tcgen05 attention (HD = 128): one CTA per SM walks (sample,
+// head, 8-query tile) items from an atomic counter; each item streams the
+// sample's WHOLE visible KV extent in 128-key chunks, so there are no split
+// partials and no combine kernel.
+//   warp 4     TMA producer: the item's Q rows (16 one-row boxes into a
+//              swizzled K-major tile) and K/V chunks into a kPS-stage ring,
+//              running ahead across items.
+//   warp 5     MMA issuer: S^T(c+1) = K Q^T is issued before waiting for the
+//              softmax of chunk c (double-buffered S in TMEM), then
+//              O^T += V^T P^T (V read MN-major from the same tile).
+//   warps 0-3  softmax (thread = key): per-chunk max through smem, online
+//              softmax with a lazy reference max (rescale O^T in TMEM only
+//              when the max grows by more than 2^8), P^T to smem; at the
+//              item end O^T / l -> the context row (thread = hd).
+constexpr int kPS = 3, kPQ = 2, kPThreads = 192;
+constexpr int kPStage = 4 * kTcKeys * 128;  // K + V, 2 boxes each
+constexpr int kPSmem = 1024 + kPS * kPStage + kPQ * 2048 + 2 * 2048 + 8 * kTcKeys * 4;
+
+__global__ void __launch_bounds__(kPThreads, 1)
+    k_attention_tcp(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q, AttnArgs a,
+                    int qtiles) {
+    CtaTrace trace__(TK_ATTN);
+    constexpr int HD = 128;
+    extern __shared__ uint8_t smraw[];
+    uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+    uint8_t* ring = sm;                                  // [kPS][K 2 boxes | V 2 boxes]
+    uint8_t* qring = ring + kPS * kPStage;               // [kPQ][2 atoms of 8 x 128 B]
+    uint8_t* sP = qring + kPQ * 2048;                    // [2][2 atoms of 8 x 128 B]
+    float* sS = (float*)(sP + 2 * 2048);                 // [8][128]
+    __shared__ uint64_t full[kPS], empty[kPS], qfull[kPQ], qempty[kPQ], sfull[2], pfull[2], pvdone[2], ofree;
+    __shared__ int sq_item[kPQ];
+    __shared__ uint32_t tslot;
+    __shared__ float sMx[8], sL[8];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, tid = threadIdx.x;
+    const int n_items = a.B * a.heads * qtiles;
+    if (tid == 0) {
+        ptx::prefetch_tmap(&tm_kv);
+        ptx::prefetch_tmap(&tm_q);
+        for (int i = 0; i < kPS; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < kPQ; ++i) {
+            ptx::mbar_init(&qfull[i], 1);
+            ptx::mbar_init(&qempty[i], 5);  // the MMA (its S^T read Q) + the 4 softmax warps (read sq_item)
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&sfull[i], 1);
+            ptx::mbar_init(&pfull[i], 128);
+            ptx::mbar_init(&pvdone[i], 1);
+        }
+        ptx::mbar_init(&ofree, 128);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 5) ptx::tmem_alloc32(&tslot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tslot;  // S: cols [0,8) and [8,16); O^T: cols [16,24)
+    pdl_trigger();
+    pdl_wait();  // batch descriptors, Q and this layer's K/V come from earlier kernels
+
+    auto decode = [&](int i, int& s, int& head, int& qt) {
+        qt = i % qtiles;
+        const int pair = i / qtiles;
+        s = pair / a.heads;
+        head = pair - s * a.heads;
+    };
+
+    if (warp == 4) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            const uint64_t pol = ptx::policy_evict_first();
+            int st = 0, qs = 0;
+            uint32_t ph = 0, qph = 0;
+            int next = atomicAdd(a.work, 1);
+            for (;;) {
+                const int i = next;
+                if (i >= n_items) break;
+                next = atomicAdd(a.work, 1);  // in flight while this item is issued
+                int s, head, qt;
+                decode(i, s, head, qt);
+                const SampleSeg seg = a.segs[s];
+                const int nq = min(kQT, seg.n_q - qt * kQT);
+                if (nq <= 0 || seg.kv_len <= 0) continue;
+                int toks[kQT];
+#pragma unroll
+                for (int r = 0; r < kQT; ++r) toks[r] = a.qidx[seg.q_start + qt * kQT + (r < nq ? r : 0)];
+                ptx::mbar_wait(&qempty[qs], qph ^ 1);
+                sq_item[qs] = i;  // published by the arrive below
+                ptx::mbar_arrive_expect_tx(&qfull[qs], 2048);
+#pragma unroll
+                for (int r = 0; r < kQT; ++r)  // one-row boxes: the TMA swizzles by destination address
+#pragma unroll
+                    for (int hx = 0; hx < 2; ++hx)
+                        ptx::tma_load_2d(qring + qs * 2048 + hx * 1024 + r * 128, &tm_q, &qfull[qs],
+                                         head * HD + hx * 64, toks[r], pol);
+                if (++qs == kPQ) {
+                    qs = 0;
+                    qph ^= 1;
+                }
+                const int row_k = (((a.layer * 2 + 0) * a.B + s) * a.heads + head) * a.cap;
+                const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap;
+                for (int k0 = 0; k0 < seg.kv_len; k0 += kTcKeys) {
+                    ptx::mbar_wait(&empty[st], ph ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[st], kPStage);
+                    uint8_t* b = ring + st * kPStage;
+                    ptx::tma_load_2d(b, &tm_kv, &full[st], 0, row_k + k0, pol);
+                    ptx::tma_load_2d(b + kTcKeys * 128, &tm_kv, &full[st], 64, row_k + k0, pol);
+                    ptx::tma_load_2d(b + 2 * kTcKeys * 128, &tm_kv, &full[st], 0, row_v + k0, pol);
+                    ptx::tma_load_2d(b + 3 * kTcKeys * 128, &tm_kv, &full[st], 64, row_v + k0, pol);
+                    if (++st == kPS) {
+                        st = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+            ptx::mbar_wait(&qempty[qs], qph ^ 1);  // end of work
+            sq_item[qs] = -1;
+            ptx::mbar_arrive(&qfull[qs]);
+        }
+    } else if (warp == 5) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t id_s = ptx::umma_idesc_bf16(kTcKeys, kQT), id_o = ptx::umma_idesc_bf16_amn(HD, kQT);
+            int st = 0, qs = 0, items = 0;
+            uint32_t ph = 0, qph = 0;
+            uint32_t gc = 0;  // chunks processed (S / P buffers alternate)
+            for (;;) {
+                ptx::mbar_wait(&qfull[qs], qph);
+                const int i = sq_item[qs];
+                if (i < 0) break;
+                int s, head, qt;
+                decode(i, s, head, qt);
+                const int nch = (a.segs[s].kv_len + kTcKeys - 1) / kTcKeys;
+                const uint32_t qa = ptx::smem_u32(qring + qs * 2048);
+                // S^T(c) into TMEM buffer (gc + c) & 1
+                auto issue_s = [&](int c, int stc, uint32_t phc) {
+                    ptx::mbar_wait(&full[stc], phc);
+                    ptx::tc_fence_after();
+                    const uint32_t ka = ptx::smem_u32(ring + stc * kPStage);
+#pragma unroll
+                    for (int k = 0; k < HD / 16; ++k)
+                        ptx::umma_bf16(tmem + ((gc + c) & 1) * 8,
+                                       ptx::umma_desc_kmajor_sw128(ka + (k / 4) * (kTcKeys * 128) + (k % 4) * 32),
+                                       ptx::umma_desc_kmajor_sw128(qa + (k / 4) * 1024 + (k % 4) * 32), id_s,
+                                       k > 0 ? 1u : 0u);
+                    ptx::umma_commit(&sfull[(gc + c) & 1]);
+                };
+                int stn = st;  // ring position of the next S
+                uint32_t phn = ph;
+                issue_s(0, stn, phn);
+                if (++stn == kPS) {
+                    stn = 0;
+                    phn ^= 1;
+                }
+                if (items > 0) ptx::mbar_wait(&ofree, (items - 1) & 1);  // the previous item's O^T was read
+                for (int c = 0; c < nch; ++c) {
+                    if (c + 1 < nch) {
+                        issue_s(c + 1, stn, phn);
+                        if (++stn == kPS) {
+                            stn = 0;
+                            phn ^= 1;
+                        }
+                    } else {
+                        ptx::umma_commit(&qempty[qs]);  // every S of the item issued: the Q slot frees
+                    }
+                    const uint32_t g = gc + c;
+                    ptx::mbar_wait(&pfull[g & 1], (g >> 1) & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t va = ptx::smem_u32(ring + st * kPStage + 2 * kTcKeys * 128);
+                    const uint32_t pa = ptx::smem_u32(sP + (g & 1) * 2048);
+#pragma unroll
+                    for (int k = 0; k < kTcKeys / 16; ++k)
+                        ptx::umma_bf16(tmem + 16, ptx::umma_desc_mn_sw128(va + k * 16 * 128, kTcKeys * 128, 1024),
+                                       ptx::umma_desc_kmajor_sw128(pa + (k / 4) * 1024 + (k % 4) * 32), id_o,
+                                       (c > 0 || k > 0) ? 1u : 0u);
+                    ptx::umma_commit(&empty[st]);
+                    ptx::umma_commit(&pvdone[g & 1]);
+                    if (++st == kPS) {
+                        st = 0;
+                        ph ^= 1;
+                    }
+                }
+                gc += nch;
+                ++items;
+                if (++qs == kPQ) {
+                    qs = 0;
+                    qph ^= 1;
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ softmax warps
+        int qs = 0, items = 0;
+        uint32_t qph = 0, gc = 0;
+        const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+        for (;;) {
+            ptx::mbar_wait(&qfull[qs], qph);
+            const int i = sq_item[qs];
+            __syncwarp();
+            if (i >= 0 && lane == 0) ptx::mbar_arrive(&qempty[qs]);
+            if (++qs == kPQ) {
+                qs = 0;
+                qph ^= 1;
+            }
+            if (i < 0) break;
+            int s, head, qt;
+            decode(i, s, head, qt);
+            const SampleSeg seg = a.segs[s];
+            const int nq = min(kQT, seg.n_q - qt * kQT);
+            const int nch = (seg.kv_len + kTcKeys - 1) / kTcKeys;
+            int ws[kQT];
+#pragma unroll
+            for (int q = 0; q < kQT; ++q) {
+                const int tok = q < nq ? a.qidx[seg.q_start + qt * kQT + q] : -1;
+                ws[q] = tok >= 0 ? a.plans[tok].write_slot : -1;
+            }
+            float mref[kQT], lp[kQT];
+#pragma unroll
+            for (int q = 0; q < kQT; ++q) {
+                mref[q] = -INFINITY;
+                lp[q] = 0.0f;
+            }
+            for (int c = 0; c < nch; ++c) {
+                const uint32_t g = gc + c;
+                const int key = c * kTcKeys + tid;
+                ptx::mbar_wait(&sfull[g & 1], (g >> 1) & 1);
+                ptx::tc_fence_after();
+                float x[kQT];
+                ptx::tmem_ld8(trow + (g & 1) * 8, x);
+                const bool in_ext = key < seg.kv_len && !(a.pad && a.pad[(size_t)s * a.cap + key]);
+#pragma unroll
+                for (int q = 0; q < kQT; ++q) {
+                    x[q] = (in_ext && key <= ws[q]) ? x[q] * a.scale_log2 : -INFINITY;
+                    sS[q * kTcKeys + tid] = x[q];
+                }
+                ptx::named_bar_sync(1, 128);
+                {  // chunk max per query: 16 threads per query
+                    const int q = tid / 16, part = tid % 16;
+                    float m = -INFINITY;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) m = fmaxf(m, sS[q * kTcKeys + part * 8 + j]);
+#pragma unroll
+                    for (int o = 1; o < 16; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                    if (part == 0) sMx[q] = m;
+                }
+                ptx::named_bar_sync(1, 128);
+                float alpha[kQT];
+                bool rescale = false;
+#pragma unroll
+                for (int q = 0; q < kQT; ++q) {
+                    const float cm = sMx[q];
+                    alpha[q] = 1.0f;
+                    if (cm > mref[q] + 8.0f) {  // lazy: keep the reference unless the max grows by > 2^8
+                        if (mref[q] != -INFINITY) {
+                            alpha[q] = exp2f(mref[q] - cm);
+                            rescale = true;
+                        }
+                        mref[q] = cm;
+                    }
+                }
+                if (g >= 2) ptx::mbar_wait(&pvdone[g & 1], ((g - 2) >> 1) & 1);  // PV(g-2) done with sP[g&1]
+                uint8_t* pb = sP + (g & 1) * 2048;
+#pragma unroll
+                for (int q = 0; q < kQT; ++q) {
+                    const float p = x[q] == -INFINITY ? 0.0f : exp2f(x[q] - mref[q]);
+                    lp[q] = lp[q] * alpha[q] + p;
+                    *(__nv_bfloat16*)(pb + (tid / 64) * 1024 + q * 128 + ((((tid % 64) / 8) ^ (q & 7)) << 4) +
+                                      (tid % 8) * 2) = __float2bfloat16_rn(p);
+                }
+                if (rescale && c > 0) {  // O^T (thread = hd row) *= alpha once PV(g-1) has landed
+                    ptx::mbar_wait(&pvdone[(g - 1) & 1], ((g - 1) >> 1) & 1);
+                    ptx::tc_fence_after();
+                    float o[kQT];
+                    ptx::tmem_ld8(trow + 16, o);
+#pragma unroll
+                    for (int q = 0; q < kQT; ++q) o[q] *= alpha[q];
+                    ptx::tmem_st8(trow + 16, o);
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&pfull[g & 1]);
+            }
+            // ---- item end: l = sum over keys, O^T / l -> context rows (thread = hd)
+#pragma unroll
+            for (int q = 0; q < kQT; ++q) sS[q * kTcKeys + tid] = lp[q];
+            ptx::named_bar_sync(1, 128);
+            {
+                const int q = tid / 16, part = tid % 16;
+                float l = 0.0f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) l += sS[q * kTcKeys + part * 8 + j];
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+                if (part == 0) sL[q] = l;
+            }
+            const uint32_t gl = gc + nch - 1;
+            ptx::mbar_wait(&pvdone[gl & 1], (gl >> 1) & 1);
+            ptx::tc_fence_after();
+            ptx::named_bar_sync(1, 128);  // sL complete
+            float o[kQT];
+            ptx::tmem_ld8(trow + 16, o);
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&ofree);
+#pragma unroll
+            for (int q = 0; q < kQT; ++q) {
+                if (q >= nq) break;
+                const int tok = a.qidx[seg.q_start + qt * kQT + q];
+                a.ctx[(size_t)tok * a.h + head * HD + tid] = __float2bfloat16_rn(o[q] / sL[q]);
+            }
+            gc += nch;
+            ++items;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 5) ptx::tmem_dealloc32(tmem);
+}
+
 // merge split-KV partials: grid (T, heads), block HD
 __global__ void k_attn_combine(AttnArgs a, int hd, const int* __restrict__ dT) {
     CtaTrace trace__(TK_ATTN_COMBINE);
@@ -471,6 +957,9 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     make_b_maps(f->map_xb, f->xb, T, h);
     make_b_maps(f->map_ctx, f->ctx, T, h);
     make_b_maps(f->map_act, f->act, T, mm);
+    f->kv_map = make_tmap_2d(c.kv, (int64_t)cfg.num_layers * 2 * c.B * cfg.num_heads * c.cap, cfg.head_dim, 128);
+    f->q_map = make_tmap_2d(f->q, (int64_t)T, (int64_t)h, 1);
+    f->attn_work = walloc<int>(f, (size_t)cfg.num_layers);
     ws.fast = f;
     return f;
 }
@@ -522,6 +1011,8 @@ void prepare_fast_kernels() {
     if (done) return;
     CUDA_OK(cudaFuncSetAttribute(k_attention<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CUDA_OK(cudaFuncSetAttribute(k_attention<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CUDA_OK(cudaFuncSetAttribute(k_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+    CUDA_OK(cudaFuncSetAttribute(k_attention_tcp, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
     gemm_prepare();
     done = true;
 }
@@ -557,6 +1048,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     base.plans = dplans;
     base.kv = (__nv_bfloat16*)c.kv;
 
+    CUDA_OK(cudaMemsetAsync(f->attn_work, 0, sizeof(int) * (size_t)cfg.num_layers, st));
     PROF(PK_ROW, launch_k(k_embed_ln, dim3(n), dim3(kRowThreads), 0, st, (const __nv_bfloat16*)m.tok16,
                           (const __nv_bfloat16*)m.pos16, tokens, dplans, h, resid, (const float*)m.layers[0].ln1_g,
                           (const float*)m.layers[0].ln1_b, f->xb, (const int*)db.dT));
@@ -599,12 +1091,20 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         PROF(PK_QKV, gemm_launch(EPI_QKV, g, mp, n, st));
         // attention
         at.layer = l;
-        if (hd == 128)
+        static const int aimpl = getenv("SD_ATTN_IMPL") ? atoi(getenv("SD_ATTN_IMPL")) : 4;
+        at.work = f->attn_work + l;
+        if (hd == 128 && aimpl == 4)
+            PROF(PK_ATTN, launch_k(k_attention_tcp, dim3(std::min(c.B * heads * qtiles, kSms)), dim3(kPThreads), kPSmem,
+                                   st, f->kv_map, f->q_map, at, qtiles));
+        else if (hd == 128 && aimpl == 3)
+            PROF(PK_ATTN, launch_k(k_attention_tc, dim3(c.B * heads, splits, qtiles), dim3(128), kTcSmem, st, f->kv_map,
+                                   at));
+        else if (hd == 128)
             PROF(PK_ATTN, launch_k(k_attention<128>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
         else
             PROF(PK_ATTN, launch_k(k_attention<64>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
         launches++;
-        if (splits > 1) {
+        if (splits > 1 && !(hd == 128 && aimpl == 4)) {  // the persistent kernel writes final rows
             PROF(PK_COMBINE, launch_k(k_attn_combine, dim3(n, heads), dim3(hd), 0, st, at, hd, (const int*)db.dT));
             launches++;
         }
