@@ -1,0 +1,865 @@
+// C ABI (include/specdec_b200.h) and the host-side validation that mirrors the
+// reference's contracts before any device work is launched.
+#include <algorithm>
+#include <cstdlib>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "handles.h"
+
+namespace sdb {
+
+static std::atomic<int64_t> g_launches{0};
+void note_launches(int64_t n) { g_launches += n; }
+
+void set_device(int device) { CUDA_OK(cudaSetDevice(device)); }
+
+bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("SD_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on != 0;
+}
+
+// ---------------------------------------------------------------- workspace
+void Workspace::ensure(const Model& m, const Cache& c, int T) {
+    if (T <= cap_tokens) return;
+    int T2 = std::max(T, std::max(64, cap_tokens * 2));
+    this->~Workspace();
+    new (this) Workspace();
+    const Config& cfg = m.cfg;
+    size_t h = cfg.hidden(), mm = cfg.mlp(), V = cfg.vocab_size;
+    d_tokens = (int32_t*)dmalloc(sizeof(int32_t) * T2);
+    d_plans = (Plan*)dmalloc(sizeof(Plan) * T2);
+    d_resid = (float*)dmalloc(sizeof(float) * T2 * h);
+    d_tmp = (float*)dmalloc(sizeof(float) * T2 * 3 * h);
+    d_tmp2 = (float*)dmalloc(sizeof(float) * T2 * (3 * h + mm));
+    d_logits = (float*)dmalloc(sizeof(float) * T2 * V);
+    d_argmax = (int32_t*)dmalloc(sizeof(int32_t) * T2);
+    d_flag = (int32_t*)dmalloc(sizeof(int32_t) * 4);
+    CUDA_OK(cudaMemset(d_flag, 0, sizeof(int32_t) * 4));
+    if (m.precision == FP32_CHECK)
+        d_scores = (float*)dmalloc(sizeof(float) * 2 * (size_t)T2 * cfg.num_heads * c.cap);
+    d_segs = (SampleSeg*)dmalloc(sizeof(SampleSeg) * (size_t)c.B);
+    d_qidx = (int32_t*)dmalloc(sizeof(int32_t) * T2);
+    d_T = (int32_t*)dmalloc(sizeof(int32_t) * 4);
+    segs_cap = c.B;
+    cap_tokens = T2;
+}
+
+Workspace::~Workspace() {
+    dfree(d_tokens);
+    dfree(d_plans);
+    dfree(d_resid);
+    dfree(d_tmp);
+    dfree(d_tmp2);
+    dfree(d_logits);
+    dfree(d_argmax);
+    dfree(d_flag);
+    dfree(d_scores);
+    dfree(d_segs);
+    dfree(d_qidx);
+    dfree(d_T);
+    free_fast_workspace(fast);
+    fast = nullptr;
+    cap_tokens = 0;
+}
+
+// -------------------------------------------------------------- construction
+sd_model* create_model(const Config& cfg, int device, int precision, const float* host_weights) {
+    SD_CHECK(cfg.num_layers >= 1, CONFIG, "num_layers must be >= 1");
+    SD_CHECK(cfg.num_heads >= 1, CONFIG, "num_heads must be >= 1");
+    SD_CHECK(cfg.head_dim >= 1, CONFIG, "head_dim must be >= 1");
+    SD_CHECK(cfg.vocab_size >= 2, CONFIG, "vocab_size must be >= 2");
+    SD_CHECK(cfg.max_positions >= 1, CONFIG, "max_positions must be >= 1");
+    SD_CHECK(precision == FP32_CHECK || precision == BF16, CONFIG, "unknown precision");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw Error(INTERNAL, "no CUDA device: the B200 kernels have no CPU fallback");
+    SD_CHECK(device >= 0 && device < ndev, CONFIG, "device index out of range");
+    cudaDeviceProp prop;
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        throw Error(INTERNAL, "device is sm_" + std::to_string(prop.major * 10 + prop.minor) +
+                                  "; these kernels are built for sm_100a (B200) only");
+    set_device(device);
+    auto* h = new sd_model();
+    try {
+        Model& m = h->m;
+        m.cfg = cfg;
+        m.precision = precision;
+        m.device = device;
+        m.lay.build(cfg);
+        CUDA_OK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+        int64_t hh = cfg.hidden(), mm = cfg.mlp();
+        auto alloc = [&](size_t bytes) {
+            void* p = dmalloc(bytes);
+            m.allocations.push_back(p);
+            m.weight_bytes += (int64_t)bytes;
+            return p;
+        };
+        if (precision == FP32_CHECK) {
+            m.w32 = (float*)alloc(sizeof(float) * (size_t)m.lay.total);
+            if (host_weights) upload_weights_fp32(m, host_weights, h->st);
+            else init_weights_fp32(m, h->st);
+            note_launches(host_weights ? 0 : 2 + 17 * cfg.num_layers + 3);
+        } else {
+            m.vocab_pad = (cfg.vocab_size + 255) / 256 * 256;
+            m.tok16 = (uint16_t*)alloc(2 * (size_t)cfg.vocab_size * hh);
+            m.pos16 = (uint16_t*)alloc(2 * (size_t)cfg.max_positions * hh);
+            m.lm16 = (uint16_t*)alloc(2 * (size_t)m.vocab_pad * hh);
+            m.lnf_g = (float*)alloc(4 * hh);
+            m.lnf_b = (float*)alloc(4 * hh);
+            m.layers.resize(cfg.num_layers);
+            for (FastLayer& f : m.layers) {
+                f.wqkv = (uint16_t*)alloc(2 * (size_t)3 * hh * hh);
+                f.wo = (uint16_t*)alloc(2 * (size_t)hh * hh);
+                f.wfc = (uint16_t*)alloc(2 * (size_t)mm * hh);
+                f.wproj = (uint16_t*)alloc(2 * (size_t)hh * mm);
+                f.bqkv = (float*)alloc(4 * 3 * hh);
+                f.bo = (float*)alloc(4 * hh);
+                f.bfc = (float*)alloc(4 * mm);
+                f.bproj = (float*)alloc(4 * hh);
+                f.ln1_g = (float*)alloc(4 * hh);
+                f.ln1_b = (float*)alloc(4 * hh);
+                f.ln2_g = (float*)alloc(4 * hh);
+                f.ln2_b = (float*)alloc(4 * hh);
+            }
+            if (host_weights) upload_weights_bf16(m, host_weights, h->st);
+            else init_weights_bf16(m, h->st);
+            build_fast_model(m);
+            note_launches(host_weights ? 0 : 2 + 14 * cfg.num_layers + 3);
+        }
+        CUDA_OK(cudaStreamSynchronize(h->st));
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    return h;
+}
+
+sd_cache* create_cache(sd_model* mh, int batch, int capacity, int layout) {
+    const Model& m = mh->m;
+    SD_CHECK(batch >= 1 && capacity >= 1, CONFIG, "cache dimensions must be positive");
+    SD_CHECK(layout == UNPAD || layout == PADDED, CONFIG, "unknown cache layout");
+    set_device(m.device);
+    auto* h = new sd_cache();
+    try {
+        Cache& c = h->c;
+        c.layout = layout;
+        c.L = m.cfg.num_layers;
+        c.B = batch;
+        c.cap = capacity;
+        c.heads = m.cfg.num_heads;
+        c.hd = m.cfg.head_dim;
+        c.elem_bytes = m.precision == FP32_CHECK ? 4 : 2;
+        c.model = &m;
+        h->model = mh;
+        size_t bytes = (size_t)c.L * 2 * c.B * c.heads * (size_t)c.cap * c.hd * c.elem_bytes;
+        c.kv = dmalloc(bytes);
+        CUDA_OK(cudaMemset(c.kv, 0, bytes));
+        c.d_committed = (int32_t*)dmalloc(4 * (size_t)batch);
+        c.d_logical = (int32_t*)dmalloc(4 * (size_t)batch);
+        c.d_pad = (uint8_t*)dmalloc((size_t)batch * capacity);
+        CUDA_OK(cudaMemset(c.d_committed, 0, 4 * (size_t)batch));
+        CUDA_OK(cudaMemset(c.d_logical, 0, 4 * (size_t)batch));
+        CUDA_OK(cudaMemset(c.d_pad, 0, (size_t)batch * capacity));
+        c.committed.assign(batch, 0);
+        c.logical.assign(batch, 0);
+        c.staged.assign(batch, 0);
+        c.pad.assign((size_t)batch * capacity, 0);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    return h;
+}
+
+void reset_cache(sd_cache* h) {
+    Cache& c = h->c;
+    std::fill(c.committed.begin(), c.committed.end(), 0);
+    std::fill(c.logical.begin(), c.logical.end(), 0);
+    std::fill(c.staged.begin(), c.staged.end(), 0);
+    std::fill(c.pad.begin(), c.pad.end(), 0);
+    c.useful = c.padding = 0;
+    CUDA_OK(cudaMemsetAsync(c.d_committed, 0, 4 * (size_t)c.B, h->model->st));
+    CUDA_OK(cudaMemsetAsync(c.d_logical, 0, 4 * (size_t)c.B, h->model->st));
+    CUDA_OK(cudaMemsetAsync(c.d_pad, 0, (size_t)c.B * c.cap, h->model->st));
+}
+
+// ------------------------------------------------------------------ forward
+static void sync_descriptors_to_device(sd_cache* h) {
+    Cache& c = h->c;
+    cudaStream_t st = h->model->st;
+    CUDA_OK(cudaMemcpyAsync(c.d_committed, c.committed.data(), 4 * (size_t)c.B, cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(c.d_logical, c.logical.data(), 4 * (size_t)c.B, cudaMemcpyHostToDevice, st));
+    if (c.layout == PADDED)
+        CUDA_OK(cudaMemcpyAsync(c.d_pad, c.pad.data(), c.pad.size(), cudaMemcpyHostToDevice, st));
+}
+
+static void run_forward(sd_model* mh, sd_cache* h, int T, float* logits, int32_t* argmax) {
+    Model& m = mh->m;
+    cudaStream_t st = mh->st;
+    if (m.precision == FP32_CHECK) {
+        forward_check(m, h->c, h->ws, T, true, st);
+        note_launches(3 + 11 * (int64_t)m.cfg.num_layers + 3);
+    } else {
+        forward_fast(m, h->c, h->ws, T, logits != nullptr, st);
+    }
+    int32_t flag = 0;
+    CUDA_OK(cudaMemcpyAsync(&flag, h->ws.d_flag, 4, cudaMemcpyDeviceToHost, st));
+    if (argmax) CUDA_OK(cudaMemcpyAsync(argmax, h->ws.d_argmax, 4 * (size_t)T, cudaMemcpyDeviceToHost, st));
+    if (logits)
+        CUDA_OK(cudaMemcpyAsync(logits, h->ws.d_logits, 4 * (size_t)T * m.cfg.vocab_size,
+                                cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    if (flag != 0) {
+        CUDA_OK(cudaMemset(h->ws.d_flag, 0, 4));
+        if (flag == 3) throw Error(CONTRACT, prefixed(CONTRACT, "token with an empty visible set"));
+        throw Error(INTERNAL, "non-finite logit produced");
+    }
+}
+
+void forward_planned_host(sd_model* mh, sd_cache* h, const int32_t* tokens, const Plan* plans, int n,
+                          float* logits, int32_t* argmax) {
+    Model& m = mh->m;
+    Cache& c = h->c;
+    const Config& cfg = m.cfg;
+    set_device(m.device);
+    // model.cpp:266-285
+    SD_CHECK(n > 0, CONTRACT, "forward pass over zero tokens");
+    SD_CHECK(c.model == &m && c.heads * c.hd == cfg.hidden(), CONTRACT, "cache width does not match the model");
+    SD_CHECK(c.L == cfg.num_layers, CONTRACT, "cache depth does not match the model");
+    for (int t = 0; t < n; ++t) {
+        const Plan& p = plans[t];
+        SD_CHECK(tokens[t] >= 0 && tokens[t] < cfg.vocab_size, CONTRACT, "token id out of vocabulary");
+        SD_CHECK(p.sample >= 0 && p.sample < c.B, CONTRACT, "plan sample out of range");
+        SD_CHECK(p.logical_pos >= 0, CONTRACT, "negative position");
+        SD_CHECK(p.logical_pos < cfg.max_positions, CAPACITY,
+                 "position " + std::to_string(p.logical_pos) + " exceeds max_positions " +
+                     std::to_string(cfg.max_positions));
+        if (!p.store) {  // CacheArena::mark_hole
+            SD_CHECK(c.layout == PADDED, CONTRACT, "this cache layout has no masked holes");
+            SD_CHECK(p.write_slot >= 0, CONTRACT, "cache position negative");
+            SD_CHECK(p.write_slot < c.cap, CAPACITY,
+                     "cache position " + std::to_string(p.write_slot) + " exceeds capacity " +
+                         std::to_string(c.cap));
+            c.pad[(size_t)p.sample * c.cap + p.write_slot] = 1;
+            c.staged[p.sample] = std::max(c.staged[p.sample], p.write_slot + 1);
+        }
+    }
+    // phase-1 write_kv checks and bookkeeping (kv_cache.cpp:93-103, 128-138, 203-213)
+    for (int t = 0; t < n; ++t) {
+        const Plan& p = plans[t];
+        if (!p.store) continue;
+        SD_CHECK(p.write_slot >= 0, CONTRACT, "cache position negative");
+        SD_CHECK(p.write_slot < c.cap, CAPACITY,
+                 "cache position " + std::to_string(p.write_slot) + " exceeds capacity " +
+                     std::to_string(c.cap));
+    }
+    for (int t = 0; t < n; ++t) {
+        const Plan& p = plans[t];
+        if (!p.store) continue;
+        if (c.layout == PADDED) c.pad[(size_t)p.sample * c.cap + p.write_slot] = 0;
+        c.staged[p.sample] = std::max(c.staged[p.sample], p.write_slot + 1);
+        c.useful += 1;
+    }
+    // phase-2 gather checks (kv_cache.cpp:140-150): unpad reads stay below `written`
+    if (c.layout == UNPAD)
+        for (int t = 0; t < n; ++t)
+            SD_CHECK(plans[t].write_slot < c.staged[plans[t].sample], CONTRACT, "read past the written extent");
+
+    h->ws.ensure(m, c, n);
+    cudaStream_t st = mh->st;
+    sync_descriptors_to_device(h);
+    CUDA_OK(cudaMemcpyAsync(h->ws.d_tokens, tokens, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(h->ws.d_plans, plans, sizeof(Plan) * (size_t)n, cudaMemcpyHostToDevice, st));
+    run_forward(mh, h, n, logits, argmax);
+}
+
+void forward_ragged_host(sd_model* mh, sd_cache* h, const int32_t* tokens, const int32_t* counts, int batch,
+                         const int32_t* slot_sample, const int32_t* slot_pos, float* logits,
+                         int32_t* argmax) {
+    Cache& c = h->c;
+    SD_CHECK(batch >= 1, CONTRACT, "batch must have at least one sample");  // ragged.cpp:7
+    SD_CHECK(batch <= c.B, CONTRACT, "batch has more samples than the cache");
+    int n = 0;
+    for (int s = 0; s < batch; ++s) {
+        SD_CHECK(counts[s] >= 0, CONTRACT, "negative token count");
+        n += counts[s];
+    }
+    std::vector<Plan> plans(n);
+    int flat = 0;
+    for (int s = 0; s < batch; ++s) {
+        for (int o = 0; o < counts[s]; ++o, ++flat) {
+            // restore_indices (ragged.cpp:19-36) collapses to this walk
+            int expected = c.committed[s] + o;
+            SD_CHECK(slot_sample[flat] == s && slot_pos[flat] == expected, CONTRACT,
+                     "slot " + std::to_string(flat) + " does not continue its sample");
+            plans[flat] = Plan{s, expected, expected, 1};
+        }
+    }
+    forward_planned_host(mh, h, tokens, plans.data(), n, logits, argmax);
+}
+
+void commit_accepted_host(sd_cache* h, int s, int tau) {  // kv_cache.cpp:152-161
+    Cache& c = h->c;
+    SD_CHECK(c.layout == UNPAD, CONTRACT, "not an unpad arena");
+    SD_CHECK(s >= 0 && s < c.B, CONTRACT, "cache sample out of range");
+    SD_CHECK(tau >= 1, CONTRACT, "commit needs tau >= 1");
+    SD_CHECK(tau <= c.staged[s] - c.committed[s], CONTRACT, "commit exceeds the slots written this step");
+    c.committed[s] += tau;
+    c.logical[s] = c.committed[s];
+    c.staged[s] = c.committed[s];
+}
+
+// --------------------------------------------------------------- verify step
+int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32_t* counts,
+                     const int32_t* drafts, const int32_t* budget, const int32_t* active, int stop_on_eos,
+                     int32_t* tau, int32_t* accepted, int32_t* clipped, float* logits) {
+    Model& m = mh->m;
+    Cache& c = h->c;
+    const Config& cfg = m.cfg;
+    const int B = c.B;
+    set_device(m.device);
+    // host validation (engine.cpp:427-444 / 408-426 and the forward contracts)
+    int kmax = 0, nact = 0, ndraft = 0, base = -1;
+    for (int s = 0; s < B; ++s) {
+        SD_CHECK(counts[s] >= 0, CONTRACT, "negative draft count");
+        ndraft += counts[s];
+        if (!active[s]) {
+            SD_CHECK(counts[s] == 0, CONTRACT, "inactive sample with drafts");
+            continue;
+        }
+        nact++;
+        kmax = std::max(kmax, counts[s]);
+        SD_CHECK(budget[s] >= 1, CONTRACT, "active sample without generation budget");
+        SD_CHECK(last[s] >= 0 && last[s] < cfg.vocab_size, CONTRACT, "token id out of vocabulary");
+        if (c.layout == PADDED) {
+            if (base < 0) base = c.committed[s];
+            SD_CHECK(c.committed[s] == base, INTERNAL, "internal: aligned samples drifted apart");
+        }
+    }
+    for (int i = 0; i < ndraft; ++i)
+        SD_CHECK(drafts[i] >= 0 && drafts[i] < cfg.vocab_size, CONTRACT, "token id out of vocabulary");
+    SD_CHECK(nact > 0, CONTRACT, "forward pass over zero tokens");
+    int T = 0, max_kv = 0, max_q = 0;
+    for (int s = 0; s < B; ++s) {
+        if (!active[s]) continue;
+        int n = c.layout == PADDED ? 1 + kmax : 1 + counts[s];
+        int last_logical = (c.layout == PADDED ? c.logical[s] : c.committed[s]) + n - 1;
+        int last_slot = (c.layout == PADDED ? base : c.committed[s]) + n - 1;
+        SD_CHECK(last_logical < cfg.max_positions, CAPACITY,
+                 "position " + std::to_string(last_logical) + " exceeds max_positions " +
+                     std::to_string(cfg.max_positions));
+        SD_CHECK(last_slot < c.cap, CAPACITY,
+                 "cache position " + std::to_string(last_slot) + " exceeds capacity " + std::to_string(c.cap));
+        T += n;
+        max_kv = std::max(max_kv, last_slot + 1);
+        max_q = std::max(max_q, n);
+    }
+    // device buffers: inputs [5B + kcap*B], scratch, outputs
+    int kcap = std::max(kmax, 1);
+    if (kcap > h->kcap || h->d_step == nullptr) {
+        dfree(h->d_step);
+        if (h->h_step) cudaFreeHost(h->h_step);
+        h->kcap = std::max(kcap, 8);
+        h->step_words = (size_t)B * (16 + 3 * (h->kcap + 1)) + 64;
+        h->d_step = (int32_t*)dmalloc(4 * h->step_words);
+        CUDA_OK(cudaMallocHost(&h->h_step, 4 * h->step_words));
+    }
+    int K1 = h->kcap + 1;
+    int32_t* hs = h->h_step;
+    int32_t* ds = h->d_step;
+    // layout of the step block (words)
+    size_t o_last = 0, o_counts = B, o_budget = 2 * B, o_active = 3 * B, o_drafts = 4 * B;
+    size_t o_first = o_drafts + (size_t)B * h->kcap, o_doff = o_first + B, o_scal = o_doff + B;
+    size_t o_tau = o_scal + 8, o_clip = o_tau + B, o_acc = o_clip + B;
+    std::memcpy(hs + o_last, last, 4 * (size_t)B);
+    std::memcpy(hs + o_counts, counts, 4 * (size_t)B);
+    std::memcpy(hs + o_budget, budget, 4 * (size_t)B);
+    std::memcpy(hs + o_active, active, 4 * (size_t)B);
+    std::memcpy(hs + o_drafts, drafts, 4 * (size_t)ndraft);
+    h->ws.ensure(m, c, T);
+    cudaStream_t st = mh->st;
+    sync_descriptors_to_device(h);
+    CUDA_OK(cudaMemcpyAsync(ds, hs, 4 * (o_drafts + ndraft), cudaMemcpyHostToDevice, st));
+    StepArgs a{};
+    a.B = B;
+    a.cap = c.cap;
+    a.layout = c.layout;
+    a.stop_on_eos = stop_on_eos;
+    a.acc_stride = K1;
+    a.last = ds + o_last;
+    a.counts = ds + o_counts;
+    a.drafts = ds + o_drafts;
+    a.budget = ds + o_budget;
+    a.active = ds + o_active;
+    a.committed = c.d_committed;
+    a.logical = c.d_logical;
+    a.pad = c.layout == PADDED ? c.d_pad : nullptr;
+    a.tokens = h->ws.d_tokens;
+    a.plans = h->ws.d_plans;
+    a.segs = h->ws.d_segs;
+    a.qidx = h->ws.d_qidx;
+    a.first_row = ds + o_first;
+    a.draft_off = ds + o_doff;
+    a.scalars = ds + o_scal;
+    a.argmax = h->ws.d_argmax;
+    a.tau = ds + o_tau;
+    a.accepted = ds + o_acc;
+    a.clipped = ds + o_clip;
+    launch_pack(a, st);
+    note_launches(1);
+    // run the forward (argmax always; logits on request)
+    if (m.precision == FP32_CHECK) {
+        forward_check(m, c, h->ws, T, true, st);
+        note_launches(3 + 11 * (int64_t)cfg.num_layers + 3);
+    } else if (T <= 256) {
+        DeviceBatch db{h->ws.d_segs, h->ws.d_qidx, ds + o_scal, T, max_kv, max_q};
+        forward_fast_dev(m, c, h->ws, db, 0, logits != nullptr, st);
+    } else {
+        forward_fast(m, c, h->ws, T, logits != nullptr, st);
+    }
+    launch_accept(a, st);
+    note_launches(1);
+    if (c.layout == PADDED) {
+        launch_pad_fill(a, c, st);
+        note_launches(1);
+    }
+    int32_t flag = 0;
+    CUDA_OK(cudaMemcpyAsync(&flag, h->ws.d_flag, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(hs + o_tau, ds + o_tau, 4 * ((size_t)2 * B + (size_t)B * K1), cudaMemcpyDeviceToHost, st));
+    if (logits)
+        CUDA_OK(cudaMemcpyAsync(logits, h->ws.d_logits, 4 * (size_t)T * cfg.vocab_size, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    if (flag != 0) {
+        CUDA_OK(cudaMemset(h->ws.d_flag, 0, 4));
+        if (flag == 3) throw Error(CONTRACT, prefixed(CONTRACT, "token with an empty visible set"));
+        throw Error(INTERNAL, "non-finite logit produced");
+    }
+    // outputs + host mirrors of the device-side commit
+    int tmax = 0;
+    for (int s = 0; s < B; ++s) {
+        tau[s] = hs[o_tau + s];
+        clipped[s] = hs[o_clip + s];
+        int W = kmax + 1;
+        for (int j = 0; j < W; ++j) accepted[s * W + j] = active[s] && j < tau[s] ? hs[o_acc + (size_t)s * K1 + j] : -1;
+        tmax = std::max(tmax, tau[s]);
+    }
+    for (int s = 0; s < B; ++s) {
+        if (!active[s]) continue;
+        if (c.layout == UNPAD) {
+            c.useful += 1 + counts[s];
+            c.committed[s] += tau[s];
+            c.logical[s] = c.committed[s];
+            c.staged[s] = c.committed[s];
+        } else {
+            c.useful += 1 + counts[s];
+            for (int o = 0; o <= kmax; ++o) c.pad[(size_t)s * c.cap + base + o] = o <= counts[s] ? 0 : 1;
+            for (int r = base + tau[s]; r < base + tmax; ++r) c.pad[(size_t)s * c.cap + r] = 1;
+            c.padding += tmax - tau[s];
+            c.committed[s] = base + tmax;
+            c.logical[s] += tau[s];
+            c.staged[s] = c.committed[s];
+        }
+    }
+    return kmax;
+}
+
+void commit_prefill_host(sd_cache* h, const int32_t* samples, const int32_t* lens, int n) {  // kv_cache.cpp:237-267
+        Cache& c = h->c;
+        SD_CHECK(c.layout == PADDED, CONTRACT, "not a padded grid");
+        SD_CHECK(n >= 1, CONTRACT, "prefill commit needs matching sample and length lists");
+        int rows = -1;
+        for (int i = 0; i < n; ++i) {
+            int s = samples[i], len = lens[i];
+            SD_CHECK(s >= 0 && s < c.B, CONTRACT, "cache sample out of range");
+            SD_CHECK(len >= 1, CONTRACT, "prompt length must be >= 1");
+            SD_CHECK(c.committed[s] == 0, CONTRACT, "prefill commit on a non-empty sample");
+            if (rows < 0) rows = c.staged[s];
+            SD_CHECK(c.staged[s] == rows, CONTRACT, "prefill commit requires equally staged samples");
+            SD_CHECK(len <= rows, CONTRACT, "prompt length exceeds staged rows");
+            for (int r = 0; r < rows - len; ++r)
+                SD_CHECK(c.pad[(size_t)s * c.cap + r], CONTRACT, "prefill left-pad row was not marked as a hole");
+            for (int r = rows - len; r < rows; ++r)
+                SD_CHECK(!c.pad[(size_t)s * c.cap + r], CONTRACT, "prefill prompt row was never written");
+        }
+        for (int i = 0; i < n; ++i) {
+            c.committed[samples[i]] = rows;
+            c.logical[samples[i]] = lens[i];
+        }
+}
+
+void mark_hole_host(sd_cache* h, int s, int pos) {  // kv_cache.cpp:215-219
+        Cache& c = h->c;
+        SD_CHECK(c.layout == PADDED, CONTRACT, "this cache layout has no masked holes");
+        SD_CHECK(s >= 0 && s < c.B, CONTRACT, "cache sample out of range");
+        SD_CHECK(pos >= 0, CONTRACT, "cache position negative");
+        SD_CHECK(pos < c.cap, CAPACITY, "cache position " + std::to_string(pos) + " exceeds capacity " + std::to_string(c.cap));
+        c.pad[(size_t)s * c.cap + pos] = 1;
+        c.staged[s] = std::max(c.staged[s], pos + 1);
+}
+
+}  // namespace sdb
+
+sd_model::~sd_model() {
+    if (st) cudaStreamDestroy(st);
+}
+sd_cache::~sd_cache() {
+    sdb::dfree(d_step);
+    if (h_step) cudaFreeHost(h_step);
+}
+
+// ===================================================================== C ABI
+using namespace sdb;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return INTERNAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return INTERNAL;
+    }
+}
+
+Config to_cfg(const sd_model_config* c) {
+    return Config{c->num_layers, c->num_heads, c->head_dim, c->vocab_size, c->max_positions, c->init_seed};
+}
+
+// SDCK v1 (model.cpp:143-221)
+std::vector<float> read_sdck(const char* path, Config& cfg) {
+    std::ifstream in(path, std::ios::binary);
+    SD_CHECK(in.good(), IO, std::string("cannot open checkpoint: ") + path);
+    auto rd = [&](void* p, size_t n, const char* what) {
+        in.read((char*)p, (std::streamsize)n);
+        SD_CHECK((size_t)in.gcount() == n, IO, std::string("checkpoint truncated while reading ") + what);
+    };
+    char magic[4];
+    rd(magic, 4, "magic");
+    SD_CHECK(std::memcmp(magic, "SDCK", 4) == 0, IO, std::string("not a model checkpoint: ") + path);
+    uint32_t ver = 0;
+    rd(&ver, 4, "version");
+    SD_CHECK(ver == 1, IO, "unsupported checkpoint version " + std::to_string(ver));
+    int32_t dims[5];
+    rd(dims, sizeof dims, "dimensions");
+    cfg = Config{dims[0], dims[1], dims[2], dims[3], dims[4], 0};
+    rd(&cfg.init_seed, 8, "seed");
+    SD_CHECK(cfg.num_layers >= 1, CONFIG, "num_layers must be >= 1");
+    SD_CHECK(cfg.num_heads >= 1, CONFIG, "num_heads must be >= 1");
+    SD_CHECK(cfg.head_dim >= 1, CONFIG, "head_dim must be >= 1");
+    SD_CHECK(cfg.vocab_size >= 2, CONFIG, "vocab_size must be >= 2");
+    SD_CHECK(cfg.max_positions >= 1, CONFIG, "max_positions must be >= 1");
+    WeightLayout lay;
+    lay.build(cfg);
+    std::vector<float> w((size_t)lay.total);
+    rd(w.data(), sizeof(float) * w.size(), "weights");
+    char extra;
+    in.read(&extra, 1);
+    SD_CHECK(in.gcount() == 0, IO, std::string("checkpoint has trailing bytes: ") + path);
+    return w;
+}
+
+std::vector<float> download_fp32(const sd_model* m) {
+    SD_CHECK(m->m.precision == FP32_CHECK, CONTRACT, "fp32 weights exist only in the fp32 check mode");
+    std::vector<float> w((size_t)m->m.lay.total);
+    CUDA_OK(cudaSetDevice(m->m.device));
+    CUDA_OK(cudaMemcpy(w.data(), m->m.w32, sizeof(float) * w.size(), cudaMemcpyDeviceToHost));
+    return w;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sd_last_error(void) { return g_err.c_str(); }
+int64_t sd_kernel_launches(void) { return g_launches.load(); }
+
+int sd_profile_enable(int on) {
+    return guarded([&] { profile_enable(on != 0); });
+}
+int sd_profile_read(double* out, int kinds) {
+    return guarded([&] { profile_read(out, kinds); });
+}
+
+int sd_config_validate(const sd_model_config* cfg) {
+    return guarded([&] {
+        SD_CHECK(cfg->num_layers >= 1, CONFIG, "num_layers must be >= 1");
+        SD_CHECK(cfg->num_heads >= 1, CONFIG, "num_heads must be >= 1");
+        SD_CHECK(cfg->head_dim >= 1, CONFIG, "head_dim must be >= 1");
+        SD_CHECK(cfg->vocab_size >= 2, CONFIG, "vocab_size must be >= 2");
+        SD_CHECK(cfg->max_positions >= 1, CONFIG, "max_positions must be >= 1");
+    });
+}
+
+int sd_model_init(const sd_model_config* cfg, int device, int precision, sd_model** out) {
+    return guarded([&] { *out = create_model(to_cfg(cfg), device, precision, nullptr); });
+}
+
+int sd_model_load(const char* path, int device, int precision, sd_model** out) {
+    return guarded([&] {
+        Config cfg;
+        std::vector<float> w = read_sdck(path, cfg);
+        *out = create_model(cfg, device, precision, w.data());
+    });
+}
+
+int sd_model_save(const sd_model* m, const char* path) {
+    return guarded([&] {
+        std::vector<float> w = download_fp32(m);
+        std::ofstream out(path, std::ios::binary);
+        SD_CHECK(out.good(), IO, std::string("cannot open checkpoint for writing: ") + path);
+        const Config& c = m->m.cfg;
+        uint32_t ver = 1;
+        int32_t dims[5] = {c.num_layers, c.num_heads, c.head_dim, c.vocab_size, c.max_positions};
+        out.write("SDCK", 4);
+        out.write((const char*)&ver, 4);
+        out.write((const char*)dims, sizeof dims);
+        out.write((const char*)&c.init_seed, 8);
+        out.write((const char*)w.data(), (std::streamsize)(sizeof(float) * w.size()));
+        SD_CHECK(out.good(), IO, std::string("checkpoint write failed: ") + path);
+    });
+}
+
+int sd_model_checksum(const sd_model* m, uint64_t* out) {
+    return guarded([&] {
+        std::vector<float> w = download_fp32(m);
+        uint64_t hash = 14695981039346656037ULL;  // FNV-1a, model.cpp:223-233
+        const unsigned char* b = (const unsigned char*)w.data();
+        for (size_t i = 0; i < w.size() * sizeof(float); ++i) {
+            hash ^= b[i];
+            hash *= 1099511628211ULL;
+        }
+        *out = hash;
+    });
+}
+
+int sd_model_get_config(const sd_model* m, sd_model_config* out) {
+    return guarded([&] {
+        const Config& c = m->m.cfg;
+        *out = sd_model_config{c.num_layers, c.num_heads, c.head_dim, c.vocab_size, c.max_positions, c.init_seed};
+    });
+}
+
+int64_t sd_model_weight_bytes(const sd_model* m) { return m->m.weight_bytes; }
+
+void sd_model_destroy(sd_model* m) {
+    if (m) {
+        cudaSetDevice(m->m.device);
+        delete m;
+    }
+}
+
+int sd_cache_create(const sd_model* m, int batch, int capacity, int layout, sd_cache** out) {
+    return guarded([&] { *out = create_cache(const_cast<sd_model*>(m), batch, capacity, layout); });
+}
+
+int sd_cache_committed_len(const sd_cache* c, int s, int32_t* out) {
+    return guarded([&] {
+        SD_CHECK(s >= 0 && s < c->c.B, CONTRACT, "cache sample out of range");
+        *out = c->c.committed[s];
+    });
+}
+int sd_cache_logical_len(const sd_cache* c, int s, int32_t* out) {
+    return guarded([&] {
+        SD_CHECK(s >= 0 && s < c->c.B, CONTRACT, "cache sample out of range");
+        *out = c->c.layout == UNPAD ? c->c.committed[s] : c->c.logical[s];
+    });
+}
+int sd_cache_start_offset(const sd_cache* c, int s, int32_t* out) {  // kv_cache.cpp:116-120
+    return guarded([&] {
+        SD_CHECK(c->c.layout == UNPAD, CONTRACT, "not an unpad arena");
+        SD_CHECK(s >= 0 && s < c->c.B, CONTRACT, "cache sample out of range");
+        *out = s * c->c.cap;
+    });
+}
+int sd_cache_commit_accepted(sd_cache* c, int s, int tau) {
+    return guarded([&] { commit_accepted_host(c, s, tau); });
+}
+
+int sd_cache_commit_prefill(sd_cache* h, const int32_t* samples, const int32_t* lens, int n) {
+    return guarded([&] { commit_prefill_host(h, samples, lens, n); });
+}
+
+int sd_cache_commit_padded(sd_cache* h, const int32_t* samples, const int32_t* taus, int n) {
+    return guarded([&] {  // kv_cache.cpp:269-314
+        Cache& c = h->c;
+        SD_CHECK(c.layout == PADDED, CONTRACT, "not a padded grid");
+        SD_CHECK(n >= 1, CONTRACT, "padded commit needs matching sample and tau lists");
+        int tmax = 0;
+        for (int i = 0; i < n; ++i) {
+            SD_CHECK(taus[i] >= 1, CONTRACT, "commit needs tau >= 1");
+            tmax = std::max(tmax, taus[i]);
+        }
+        int base = -1;
+        for (int i = 0; i < n; ++i) {
+            int s = samples[i];
+            SD_CHECK(s >= 0 && s < c.B, CONTRACT, "cache sample out of range");
+            if (base < 0) base = c.committed[s];
+            SD_CHECK(c.committed[s] == base, CONTRACT, "padded commit requires aligned samples");
+            SD_CHECK(base + tmax <= c.cap, CAPACITY, "padded commit exceeds cache capacity");
+            SD_CHECK(taus[i] <= c.staged[s] - base, CONTRACT, "commit exceeds the slots written this step");
+            for (int r = base; r < base + taus[i]; ++r)
+                SD_CHECK(!c.pad[(size_t)s * c.cap + r], CONTRACT, "accepted row was never written");
+        }
+        set_device(h->model->m.device);
+        cudaStream_t st = h->model->st;
+        for (int i = 0; i < n; ++i) {
+            int s = samples[i];
+            for (int r = base + taus[i]; r < base + tmax; ++r) {
+                for (int l = 0; l < c.L; ++l)
+                    for (int w = 0; w < 2; ++w)
+                        for (int hd = 0; hd < c.heads; ++hd)
+                            CUDA_OK(cudaMemsetAsync((char*)c.kv + c.kv_offset(l, w, s, hd, r) * c.elem_bytes, 0,
+                                                    (size_t)c.hd * c.elem_bytes, st));
+                c.pad[(size_t)s * c.cap + r] = 1;
+                c.padding += 1;
+            }
+            c.committed[s] += tmax;
+            c.logical[s] += taus[i];
+            c.staged[s] = c.committed[s];
+        }
+        CUDA_OK(cudaStreamSynchronize(st));
+    });
+}
+
+int sd_cache_mark_hole(sd_cache* h, int s, int pos) {
+    return guarded([&] { mark_hole_host(h, s, pos); });
+}
+
+int sd_cache_is_pad(const sd_cache* h, int s, int row, int32_t* out) {
+    return guarded([&] {
+        const Cache& c = h->c;
+        SD_CHECK(c.layout == PADDED, CONTRACT, "not a padded grid");
+        SD_CHECK(s >= 0 && s < c.B, CONTRACT, "cache sample out of range");
+        SD_CHECK(row >= 0, CONTRACT, "cache position negative");
+        SD_CHECK(row < c.cap, CAPACITY, "cache position " + std::to_string(row) + " exceeds capacity " + std::to_string(c.cap));
+        *out = c.pad[(size_t)s * c.cap + row];
+    });
+}
+
+int sd_cache_ledger(const sd_cache* c, int64_t* useful, int64_t* padding) {
+    return guarded([&] {
+        *useful = c->c.useful;
+        *padding = c->c.padding;
+    });
+}
+
+int sd_cache_gather_visible(const sd_cache* h, int s, int upto, int layer, float* k_out, float* v_out,
+                            int32_t* count) {
+    return guarded([&] {
+        const Cache& c = h->c;
+        SD_CHECK(s >= 0 && s < c.B, CONTRACT, "cache sample out of range");
+        SD_CHECK(layer >= 0 && layer < c.L, CONTRACT, "cache layer out of range");
+        SD_CHECK(upto >= 0, CONTRACT, "cache position negative");
+        SD_CHECK(upto < c.cap, CAPACITY, "cache position " + std::to_string(upto) + " exceeds capacity " + std::to_string(c.cap));
+        if (c.layout == UNPAD) SD_CHECK(upto < c.staged[s], CONTRACT, "read past the written extent");
+        set_device(h->model->m.device);
+        int hidden = c.heads * c.hd, n = 0;
+        std::vector<float> kh((size_t)(upto + 1) * c.hd), vh(kh.size());
+        std::vector<uint16_t> kb(kh.size()), vb(kh.size());
+        std::vector<int> rows;
+        for (int r = 0; r <= upto; ++r)
+            if (c.layout == UNPAD || !c.pad[(size_t)s * c.cap + r]) rows.push_back(r);
+        for (int hd = 0; hd < c.heads; ++hd) {
+            for (int w = 0; w < 2; ++w) {
+                const char* src = (const char*)c.kv + c.kv_offset(layer, w, s, hd, 0) * c.elem_bytes;
+                float* dst = w == 0 ? kh.data() : vh.data();
+                if (c.elem_bytes == 4) {
+                    CUDA_OK(cudaMemcpy(dst, src, sizeof(float) * kh.size(), cudaMemcpyDeviceToHost));
+                } else {
+                    uint16_t* tmp = w == 0 ? kb.data() : vb.data();
+                    CUDA_OK(cudaMemcpy(tmp, src, 2 * kh.size(), cudaMemcpyDeviceToHost));
+                    for (size_t i = 0; i < kh.size(); ++i) {
+                        uint32_t u = (uint32_t)tmp[i] << 16;
+                        std::memcpy(&dst[i], &u, 4);
+                    }
+                }
+            }
+            for (size_t j = 0; j < rows.size(); ++j) {
+                std::memcpy(k_out + j * hidden + (size_t)hd * c.hd, kh.data() + (size_t)rows[j] * c.hd, 4 * (size_t)c.hd);
+                std::memcpy(v_out + j * hidden + (size_t)hd * c.hd, vh.data() + (size_t)rows[j] * c.hd, 4 * (size_t)c.hd);
+            }
+        }
+        n = (int)rows.size();
+        *count = n;
+    });
+}
+
+void sd_cache_destroy(sd_cache* c) {
+    if (c) {
+        cudaSetDevice(c->model->m.device);
+        delete c;
+    }
+}
+
+int sd_restore_indices(const int32_t* counts, int batch, int flat, int32_t* sample, int32_t* pos) {
+    return guarded([&] {  // ragged.cpp:19-36
+        SD_CHECK(flat >= 0, CONTRACT, "flat index must be nonnegative");
+        int s = 0, p = flat;
+        for (int i = 0; i < batch; ++i) {
+            if (p >= counts[i]) {
+                s += 1;
+                p -= counts[i];
+            } else {
+                break;
+            }
+        }
+        SD_CHECK(s < batch, CONTRACT, "flat index " + std::to_string(flat) + " outside batch");
+        *sample = s;
+        *pos = p;
+    });
+}
+
+int sd_forward(const sd_model* m, sd_cache* c, const int32_t* tokens, const int32_t* counts, int batch,
+               const int32_t* slot_sample, const int32_t* slot_pos, float* logits, int32_t* argmax) {
+    return guarded([&] {
+        forward_ragged_host(const_cast<sd_model*>(m), c, tokens, counts, batch, slot_sample, slot_pos, logits, argmax);
+    });
+}
+
+int sd_forward_planned(const sd_model* m, sd_cache* c, const int32_t* tokens, int n, const int32_t* sample,
+                       const int32_t* logical, const int32_t* slot, const int32_t* store, float* logits,
+                       int32_t* argmax) {
+    return guarded([&] {
+        std::vector<Plan> plans(n > 0 ? n : 0);
+        for (int i = 0; i < n; ++i) plans[i] = Plan{sample[i], logical[i], slot[i], store[i] != 0};
+        forward_planned_host(const_cast<sd_model*>(m), c, tokens, plans.data(), n, logits, argmax);
+    });
+}
+
+int sd_decode(const sd_engine_config* cfg, sd_model* target, sd_model* draft, const int32_t* prompts,
+              const int32_t* prompt_lens, int32_t* gen_tokens, int32_t* gen_counts, int32_t* rec, int64_t rec_cap,
+              int64_t* n_rec, int64_t* ledger, double* timing) {
+    return guarded([&] {
+        decode_impl(*cfg, target, draft, prompts, prompt_lens, gen_tokens, gen_counts, rec, rec_cap, n_rec, ledger,
+                    timing);
+    });
+}
+
+int sd_verify_step(sd_model* m, sd_cache* c, const int32_t* last, const int32_t* counts, const int32_t* drafts,
+                   const int32_t* budget, const int32_t* active, int stop_on_eos, int32_t* tau,
+                   int32_t* accepted, int32_t* clipped, float* logits) {
+    return guarded([&] {
+        verify_step_host(m, c, last, counts, drafts, budget, active, stop_on_eos, tau, accepted, clipped, logits);
+    });
+}
+
+}  // extern "C"

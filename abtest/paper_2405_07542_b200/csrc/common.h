@@ -1,0 +1,175 @@
+// Internal shared declarations for libspecdec_b200 (host C++ + CUDA).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace sdb {
+
+// Error taxonomy of the reference (common.hpp:13-34); the C-ABI maps each to
+// its status code (include/specdec_b200.h).
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+enum Status { OK = 0, CONFIG = 1, CAPACITY = 2, CONTRACT = 3, IO = 4, INTERNAL = 5 };
+
+inline std::string prefixed(int code, const std::string& m) {
+    static const char* p[] = {"", "config: ", "capacity: ", "contract: ", "io: ", ""};
+    return std::string(p[code]) + m;
+}
+#define SD_CHECK(cond, code, msg)                                              \
+    do {                                                                       \
+        if (!(cond)) throw ::sdb::Error((code), ::sdb::prefixed((code), (msg))); \
+    } while (0)
+#define CUDA_OK(expr)                                                          \
+    do {                                                                       \
+        cudaError_t e__ = (expr);                                              \
+        if (e__ != cudaSuccess)                                                \
+            throw ::sdb::Error(::sdb::INTERNAL, std::string("cuda: ") + #expr +  \
+                                                    ": " + cudaGetErrorString(e__)); \
+    } while (0)
+
+enum Precision { FP32_CHECK = 0, BF16 = 1 };
+enum Layout { UNPAD = 0, PADDED = 1 };
+
+struct Config {
+    int32_t num_layers, num_heads, head_dim, vocab_size, max_positions;
+    uint64_t init_seed;
+    int hidden() const { return num_heads * head_dim; }
+    int mlp() const { return 4 * hidden(); }
+};
+
+// Offsets (in elements) of every tensor in the reference declaration order
+// (model.cpp:166-175).  The fp32 check mode stores exactly this flat layout.
+struct LayerOff {
+    int64_t ln1_g, ln1_b, wq, bq, wk, bk, wv, bv, wo, bo, ln2_g, ln2_b, w_fc, b_fc, w_proj, b_proj;
+};
+struct WeightLayout {
+    int64_t tok, pos, lnf_g, lnf_b, lm, total;
+    std::vector<LayerOff> layer;
+    void build(const Config& c);
+};
+
+// Device-side bf16 weights for the performance mode: GEMM operands stay in
+// the reference's row-major [out, in] (= K-major) layout; Q/K/V are fused into
+// one [3h, h] operand; the LM head is zero-padded to a multiple of the GEMM
+// M tile.  Biases / LayerNorm parameters stay fp32.
+struct FastLayer {
+    uint16_t *wqkv, *wo, *wfc, *wproj;  // bf16 bits
+    float *bqkv, *bo, *bfc, *bproj, *ln1_g, *ln1_b, *ln2_g, *ln2_b;
+};
+
+struct Model {
+    Config cfg;
+    int precision = FP32_CHECK;
+    int device = 0;
+    WeightLayout lay;
+    float* w32 = nullptr;        // check mode: all tensors fp32, declaration order
+    // perf mode
+    uint16_t* tok16 = nullptr;   // [V, h] bf16
+    uint16_t* pos16 = nullptr;   // [P, h] bf16
+    uint16_t* lm16 = nullptr;    // [V_pad, h] bf16
+    float *lnf_g = nullptr, *lnf_b = nullptr;
+    int vocab_pad = 0;
+    std::vector<FastLayer> layers;
+    std::vector<void*> allocations;
+    int64_t weight_bytes = 0;
+    struct FastModelState* fast = nullptr;  // TMA descriptors of the bf16 weights
+    ~Model();
+};
+struct FastModelState;
+struct FastWorkspace;
+void free_fast_model(FastModelState* f);
+void free_fast_workspace(FastWorkspace* f);
+void build_fast_model(Model& m);
+
+// Per-sample KV arena.  K and V live in [L][2][B][heads][cap][head_dim]
+// (head-major per sample so the attention kernel streams one contiguous
+// extent per (sample, head)).  Slot coordinates follow the reference: sample s
+// owns slots [s*cap, (s+1)*cap) (kv_cache.cpp:116-120).
+struct Cache {
+    int layout = UNPAD;
+    int L = 0, B = 0, cap = 0, heads = 0, hd = 0;
+    int elem_bytes = 4;            // 4 (check) / 2 (bf16)
+    void* kv = nullptr;            // arena
+    int32_t* d_committed = nullptr;  // committed_len per sample (slot/grid-row coords)
+    int32_t* d_logical = nullptr;    // logical length (padded grid); == committed for unpad
+    uint8_t* d_pad = nullptr;        // [B*cap] pad flags (padded grid)
+    // host mirrors (the host validates every call exactly like the reference)
+    std::vector<int32_t> committed, logical, staged;
+    std::vector<uint8_t> pad;
+    int64_t useful = 0, padding = 0;
+    const Model* model = nullptr;
+    ~Cache();
+    size_t kv_offset(int layer, int which, int s, int head, int pos) const {
+        return ((((size_t)layer * 2 + which) * B + s) * heads + head) * (size_t)cap * hd +
+               (size_t)pos * hd;
+    }
+};
+
+// A token's route through the forward pass (model.hpp:41-46 TokenPlan).
+struct Plan {
+    int32_t sample, logical_pos, write_slot, store;
+};
+
+// Per-sample ragged descriptor consumed by the attention kernel: the sample's
+// query tokens are qidx[q_start .. q_start + n_q) of the packed stream and its
+// visible KV extent is slots [0, kv_len) (each query still sees only slots
+// <= its own write_slot).
+struct SampleSeg {
+    int q_start, n_q, kv_len, pad_;
+};
+
+// Where a device-described batch lives (written by k_pack or uploaded by the
+// host) and the host-side upper bounds the launch grids are sized for.
+struct DeviceBatch {
+    const SampleSeg* segs;
+    const int32_t* qidx;
+    const int32_t* dT;   // device token count
+    int T_upper;         // grid bound for token-parallel kernels (<= 256)
+    int max_kv_upper;    // bound on any sample's kv_len
+    int max_q_upper;     // bound on any sample's query count
+};
+
+// ---- device entry points (defined in the .cu files) -------------------------
+void init_weights_fp32(Model& m, cudaStream_t st);
+void init_weights_bf16(Model& m, cudaStream_t st);
+void upload_weights_fp32(Model& m, const float* host, cudaStream_t st);  // load path
+void upload_weights_bf16(Model& m, const float* host, cudaStream_t st);
+
+// Scratch for one forward pass, grown on demand.
+struct Workspace {
+    int cap_tokens = 0;
+    int device = 0;
+    int32_t* d_tokens = nullptr;
+    Plan* d_plans = nullptr;
+    float* d_resid = nullptr;     // [T, h] fp32 residual stream
+    float* d_tmp = nullptr;       // [T, max(3h, m)] fp32 (check mode activations)
+    float* d_tmp2 = nullptr;      // [T, max(3h, m)]
+    float* d_logits = nullptr;    // [T, V] fp32 (materialised when requested)
+    int32_t* d_argmax = nullptr;  // [T]
+    int32_t* d_flag = nullptr;    // non-finite logit flag
+    float* d_scores = nullptr;    // check-mode attention scratch [T, heads, cap]
+    FastWorkspace* fast = nullptr;  // bf16-mode buffers and TMA descriptors
+    SampleSeg* d_segs = nullptr;    // [batch] ragged descriptors
+    int32_t* d_qidx = nullptr;      // [T]
+    int32_t* d_T = nullptr;         // device token count
+    int segs_cap = 0;
+    void ensure(const Model& m, const Cache& c, int T);
+    ~Workspace();
+};
+
+// Run the whole-model forward over T planned tokens already on device.
+// Writes argmax (always) and fp32 logits when want_logits.
+void forward_check(const Model& m, Cache& c, Workspace& ws, int T, bool want_logits,
+                   cudaStream_t st);
+
+void* dmalloc(size_t bytes);
+void dfree(void* p);
+
+}  // namespace sdb

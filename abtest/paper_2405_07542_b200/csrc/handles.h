@@ -1,0 +1,73 @@
+// Opaque handle types behind the C ABI and the host-side operations shared by
+// capi.cpp (entry points) and engine.cpp (the decode-loop driver).
+#pragma once
+
+#include <memory>
+
+#include "../../include/specdec_b200.h"
+#include "common.h"
+#include "step.h"
+
+struct sd_model {
+    sdb::Model m;
+    cudaStream_t st = nullptr;
+    ~sd_model();
+};
+
+struct sd_cache {
+    sdb::Cache c;
+    sd_model* model = nullptr;
+    sdb::Workspace ws;
+    // verify-step device buffers
+    int kcap = 0;                 // drafts per sample the buffers hold
+    int32_t* d_step = nullptr;    // inputs + scratch + outputs, one allocation
+    int32_t* h_step = nullptr;    // pinned host mirror for the H2D / D2H copies
+    size_t step_words = 0;
+    ~sd_cache();
+};
+
+namespace sdb {
+
+void note_launches(int64_t n);
+void set_device(int device);
+
+// Host-validated forward over planned tokens (model.cpp:256-373 contract).
+// tokens / plans are host arrays of length n.  Mutates the cache exactly like
+// the reference (KV writes, ledger, written extent) and optionally returns
+// logits [n][V] and argmax [n].
+void forward_planned_host(sd_model* m, sd_cache* c, const int32_t* tokens, const Plan* plans, int n,
+                          float* logits, int32_t* argmax);
+
+// Ragged forward (model.cpp:235-254): validates slots against the cache.
+void forward_ragged_host(sd_model* m, sd_cache* c, const int32_t* tokens, const int32_t* counts,
+                         int batch, const int32_t* slot_sample, const int32_t* slot_pos,
+                         float* logits, int32_t* argmax);
+
+// One verify step (see sd_verify_step).  accepted has stride kmax+1 where
+// kmax = max active draft count; returns that kmax.
+int verify_step_host(sd_model* m, sd_cache* c, const int32_t* last, const int32_t* counts,
+                     const int32_t* drafts, const int32_t* budget, const int32_t* active,
+                     int stop_on_eos, int32_t* tau, int32_t* accepted, int32_t* clipped,
+                     float* logits);
+
+void commit_accepted_host(sd_cache* c, int sample, int tau);
+void commit_prefill_host(sd_cache* c, const int32_t* samples, const int32_t* lens, int n);
+void mark_hole_host(sd_cache* c, int sample, int pos);
+int decode_impl(const sd_engine_config& e, sd_model* target, sd_model* draft, const int32_t* prompts,
+                const int32_t* prompt_lens, int32_t* gen_tokens, int32_t* gen_counts, int32_t* rec,
+                int64_t rec_cap, int64_t* n_rec, int64_t* ledger, double* timing);
+void reset_cache(sd_cache* c);  // back to an empty arena (fresh-cache semantics)
+std::vector<int32_t> retrieval_predict(const std::vector<int32_t>& ctx, int match_len, int copy_len);
+
+sd_model* create_model(const Config& cfg, int device, int precision, const float* host_weights);
+sd_cache* create_cache(sd_model* m, int batch, int capacity, int layout);
+
+// forward for the bf16 performance mode (fast_kernels.cu)
+void forward_fast(const Model& m, Cache& c, Workspace& ws, int T, bool want_logits, cudaStream_t st);
+void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch& db, int t0, bool want_logits,
+                      cudaStream_t st);
+void prepare_fast_kernels();
+void profile_enable(bool on);
+void profile_read(double* out, int kinds);
+
+}  // namespace sdb

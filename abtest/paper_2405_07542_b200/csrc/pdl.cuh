@@ -1,0 +1,38 @@
+// Programmatic dependent launch (PDL) for the verify-step kernel chain.
+//
+// Every kernel of the step is launched with programmatic stream
+// serialization: it may be scheduled as soon as all CTAs of its predecessor
+// have started (they trigger at entry), so its launch, TMEM allocation,
+// barrier setup and descriptor prefetch overlap the predecessor's tail.
+// griddepcontrol.wait then blocks until the predecessor grid has COMPLETED and
+// its writes are visible, before any dependent read (or WAR-hazard write).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <utility>
+
+#include "common.h"
+
+namespace sdb {
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();  // SD_PDL=0 disables (A/B measurement)
+
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    CUDA_OK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
+}  // namespace sdb

@@ -1,0 +1,600 @@
+"""Python mirror of the reference `specdec` hot-path API over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference C++ library
+(/root/reference/proj/include/specdec/*.hpp) so tests read like its own
+tests.  Everything computes through libspecdec_b200.so (CUDA, sm_100a); there
+is no CPU fallback -- importing works anywhere, but creating a Model without a
+B200 raises SpecdecError (SD_INTERNAL).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libspecdec_b200.so")
+
+I32P = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+I64P = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+F32P = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+
+# tokenizer.hpp:16-28
+BOS, EOS, PAD, BYTE_OFFSET, VOCAB_SIZE = 0, 1, 2, 3, 259
+
+FP32_CHECK, BF16 = 0, 1
+UNPAD, PADDED = 0, 1
+
+
+# ---------------------------------------------------------------- errors
+class SpecdecError(RuntimeError):
+    """specdec::Error (common.hpp:13-15)."""
+
+    code = 5
+
+
+class ConfigError(SpecdecError):
+    code = 1
+
+
+class CapacityError(SpecdecError):
+    code = 2
+
+
+class ContractError(SpecdecError):
+    code = 3
+
+
+class IoError(SpecdecError):
+    code = 4
+
+
+_ERRORS = {1: ConfigError, 2: CapacityError, 3: ContractError, 4: IoError, 5: SpecdecError}
+
+
+class _ModelConfigT(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("num_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("vocab_size", C.c_int32), ("max_positions", C.c_int32), ("init_seed", C.c_uint64)]
+
+
+class _EngineConfigT(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("predictor", C.c_int32), ("k", C.c_int32), ("match_len", C.c_int32),
+                ("copy_len", C.c_int32), ("batch_size", C.c_int32), ("max_new_tokens", C.c_int32),
+                ("stop_on_eos", C.c_int32), ("seed", C.c_uint64), ("synthetic_accuracy", C.c_double)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libspecdec_b200.so (fails loudly when it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python __graft_entry__.py build` (no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, pp = C.c_void_p, C.POINTER(C.c_void_p)
+    sig = {
+        "sd_last_error": ([], C.c_char_p),
+        "sd_kernel_launches": ([], C.c_int64),
+        "sd_config_validate": ([C.POINTER(_ModelConfigT)], C.c_int),
+        "sd_model_init": ([C.POINTER(_ModelConfigT), C.c_int, C.c_int, pp], C.c_int),
+        "sd_model_load": ([C.c_char_p, C.c_int, C.c_int, pp], C.c_int),
+        "sd_model_save": ([vp, C.c_char_p], C.c_int),
+        "sd_model_checksum": ([vp, C.POINTER(C.c_uint64)], C.c_int),
+        "sd_model_get_config": ([vp, C.POINTER(_ModelConfigT)], C.c_int),
+        "sd_model_weight_bytes": ([vp], C.c_int64),
+        "sd_model_destroy": ([vp], None),
+        "sd_cache_create": ([vp, C.c_int, C.c_int, C.c_int, pp], C.c_int),
+        "sd_cache_committed_len": ([vp, C.c_int, C.POINTER(C.c_int32)], C.c_int),
+        "sd_cache_logical_len": ([vp, C.c_int, C.POINTER(C.c_int32)], C.c_int),
+        "sd_cache_start_offset": ([vp, C.c_int, C.POINTER(C.c_int32)], C.c_int),
+        "sd_cache_commit_accepted": ([vp, C.c_int, C.c_int], C.c_int),
+        "sd_cache_commit_padded": ([vp, I32P, I32P, C.c_int], C.c_int),
+        "sd_cache_commit_prefill": ([vp, I32P, I32P, C.c_int], C.c_int),
+        "sd_cache_mark_hole": ([vp, C.c_int, C.c_int], C.c_int),
+        "sd_cache_is_pad": ([vp, C.c_int, C.c_int, C.POINTER(C.c_int32)], C.c_int),
+        "sd_cache_ledger": ([vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
+        "sd_cache_gather_visible": ([vp, C.c_int, C.c_int, C.c_int, F32P, F32P, C.POINTER(C.c_int32)], C.c_int),
+        "sd_cache_destroy": ([vp], None),
+        "sd_restore_indices": ([I32P, C.c_int, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int),
+        "sd_forward": ([vp, vp, I32P, I32P, C.c_int, I32P, I32P, vp, vp], C.c_int),
+        "sd_forward_planned": ([vp, vp, I32P, C.c_int, I32P, I32P, I32P, I32P, vp, vp], C.c_int),
+        "sd_verify_step": ([vp, vp, I32P, I32P, I32P, I32P, I32P, C.c_int, I32P, I32P, I32P, vp], C.c_int),
+        "sd_decode": ([C.POINTER(_EngineConfigT), vp, vp, I32P, I32P, I32P, I32P, I32P, C.c_int64,
+                       C.POINTER(C.c_int64), I64P, np.ctypeslib.ndpointer(np.float64)], C.c_int),
+        "sd_profile_enable": ([C.c_int], C.c_int),
+        "sd_profile_read": ([np.ctypeslib.ndpointer(np.float64), C.c_int], C.c_int),
+        "sd_session_last_error": ([], C.c_char_p),
+        "sd_session_create": ([vp, C.POINTER(_EngineConfigT), C.c_int, pp], C.c_int),
+        "sd_session_create_draft": ([vp, vp, C.POINTER(_EngineConfigT), C.c_int, pp], C.c_int),
+        "sd_session_prefill": ([vp, I32P, I32P], C.c_int),
+        "sd_session_set_trajectory": ([vp, I32P, C.c_int], C.c_int),
+        "sd_session_reset": ([vp], C.c_int),
+        "sd_session_run": ([vp, C.c_int, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_float)], C.c_int),
+        "sd_session_run_host": ([vp, C.POINTER(C.c_int32), C.POINTER(C.c_float), C.POINTER(C.c_int64),
+                                 C.POINTER(C.c_int64)], C.c_int),
+        "sd_session_outputs": ([vp, I32P, I32P, vp, vp, C.c_int], C.c_int),
+        "sd_session_destroy": ([vp], None),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise _ERRORS.get(rc, SpecdecError)(lib().sd_last_error().decode())
+
+
+def kernel_launches() -> int:
+    return int(lib().sd_kernel_launches())
+
+
+def _i32(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.int32).reshape(-1))
+
+
+# ---------------------------------------------------------------- model
+@dataclass
+class ModelConfig:
+    """model.hpp:14-25"""
+
+    num_layers: int = 2
+    num_heads: int = 2
+    head_dim: int = 16
+    vocab_size: int = VOCAB_SIZE
+    max_positions: int = 512
+    init_seed: int = 0xD5EED
+
+    def hidden(self) -> int:
+        return self.num_heads * self.head_dim
+
+    def mlp_hidden(self) -> int:
+        return 4 * self.hidden()
+
+    def _c(self) -> _ModelConfigT:
+        return _ModelConfigT(self.num_layers, self.num_heads, self.head_dim, self.vocab_size, self.max_positions,
+                             self.init_seed)
+
+    def validate(self) -> None:
+        _check(lib().sd_config_validate(C.byref(self._c())))
+
+
+@dataclass
+class TokenSlot:
+    """ragged.hpp:23-28"""
+
+    original_batch_index: int = 0
+    original_sequence_position: int = 0
+
+
+@dataclass
+class TokenPlan:
+    """model.hpp:41-46"""
+
+    sample: int = 0
+    logical_pos: int = 0
+    write_slot: int = 0
+    store: bool = True
+
+
+@dataclass
+class RaggedBatch:
+    """ragged.hpp:13-19"""
+
+    concatenated_tokens: list = field(default_factory=list)
+    token_nums_per_sample: list = field(default_factory=list)
+    total_input_token_nums: int = 0
+
+    def batch_size(self) -> int:
+        return len(self.token_nums_per_sample)
+
+
+def concatenate_inputs(per_sample) -> RaggedBatch:
+    """Algorithm 1 (ragged.cpp:6-17)."""
+    if len(per_sample) == 0:
+        raise ContractError("contract: batch must have at least one sample")
+    out = RaggedBatch()
+    for seq in per_sample:
+        out.concatenated_tokens.extend(int(t) for t in seq)
+        out.token_nums_per_sample.append(len(seq))
+        out.total_input_token_nums += len(seq)
+    return out
+
+
+def restore_indices(counts, flat_index: int) -> TokenSlot:
+    """Algorithm 2 (ragged.cpp:19-36), through the C ABI."""
+    s, p = C.c_int32(), C.c_int32()
+    _check(lib().sd_restore_indices(_i32(counts), len(counts), int(flat_index), C.byref(s), C.byref(p)))
+    return TokenSlot(s.value, p.value)
+
+
+def attention_extent(slot: TokenSlot, cache_committed_len: int) -> int:
+    """ragged.hpp:41-43"""
+    return cache_committed_len + slot.original_sequence_position + 1
+
+
+def greedy_next(row) -> int:
+    """model.cpp:34-41: argmax, ties toward the lowest id (np.argmax keeps the first)."""
+    row = np.asarray(row)
+    if row.size == 0:
+        raise ContractError("contract: argmax over an empty row")
+    return int(np.argmax(row))
+
+
+@dataclass
+class VerifyResult:
+    accepted: list
+    tau: int
+
+
+def verify(rows, drafts) -> VerifyResult:
+    """engine.cpp:60-76 over host logits rows (the device path fuses this into k_accept)."""
+    if len(rows) != len(drafts) + 1:
+        raise ContractError("contract: verification needs one logits row per draft plus the bonus row")
+    acc = []
+    k = len(drafts)
+    for j in range(k + 1):
+        x = greedy_next(rows[j])
+        acc.append(x)
+        if j == k:
+            return VerifyResult(acc, k + 1)
+        if x != drafts[j]:
+            return VerifyResult(acc, j + 1)
+    raise AssertionError("unreachable")
+
+
+class Model:
+    """specdec::Model (model.hpp:54-103) resident on one B200."""
+
+    def __init__(self, handle: int, precision: int):
+        self._h = handle
+        self.precision = precision
+
+    @staticmethod
+    def init(config: ModelConfig, device: int = 0, precision: int = FP32_CHECK) -> "Model":
+        h = C.c_void_p()
+        _check(lib().sd_model_init(C.byref(config._c()), device, precision, C.byref(h)))
+        return Model(h.value, precision)
+
+    @staticmethod
+    def load(path: str, device: int = 0, precision: int = FP32_CHECK) -> "Model":
+        h = C.c_void_p()
+        _check(lib().sd_model_load(path.encode(), device, precision, C.byref(h)))
+        return Model(h.value, precision)
+
+    def save(self, path: str) -> None:
+        _check(lib().sd_model_save(self._h, path.encode()))
+
+    def close(self) -> None:
+        if self._h:
+            lib().sd_model_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def config(self) -> ModelConfig:
+        c = _ModelConfigT()
+        _check(lib().sd_model_get_config(self._h, C.byref(c)))
+        return ModelConfig(c.num_layers, c.num_heads, c.head_dim, c.vocab_size, c.max_positions, c.init_seed)
+
+    def weight_checksum(self) -> int:
+        v = C.c_uint64()
+        _check(lib().sd_model_checksum(self._h, C.byref(v)))
+        return int(v.value)
+
+    def weight_bytes(self) -> int:
+        return int(lib().sd_model_weight_bytes(self._h))
+
+    def forward(self, batch: RaggedBatch, cache: "CacheArena", slots, want_logits: bool = True):
+        """Model::forward (model.cpp:235-254). Returns (logits [T,V] or None, argmax [T])."""
+        T = batch.total_input_token_nums
+        V = self.config.vocab_size
+        logits = np.zeros((T, V), dtype=np.float32) if want_logits else None
+        am = np.zeros(max(T, 1), dtype=np.int32)
+        ss = _i32([s.original_batch_index for s in slots])
+        sp = _i32([s.original_sequence_position for s in slots])
+        if len(slots) != T:
+            raise ContractError("contract: slot list does not cover the batch")
+        _check(lib().sd_forward(self._h, cache._h, _i32(batch.concatenated_tokens),
+                                _i32(batch.token_nums_per_sample), batch.batch_size(), ss, sp,
+                                logits.ctypes.data if want_logits else None, am.ctypes.data))
+        return logits, am[:T]
+
+    def forward_planned(self, tokens, plans, cache: "CacheArena", want_logits: bool = True):
+        """Model::forward_planned (model.cpp:256-373)."""
+        n = len(tokens)
+        if len(plans) != n:
+            raise ContractError("contract: token and plan lists differ in length")
+        V = self.config.vocab_size
+        logits = np.zeros((n, V), dtype=np.float32) if want_logits else None
+        am = np.zeros(max(n, 1), dtype=np.int32)
+        _check(lib().sd_forward_planned(self._h, cache._h, _i32(tokens), n, _i32([p.sample for p in plans]),
+                                        _i32([p.logical_pos for p in plans]), _i32([p.write_slot for p in plans]),
+                                        _i32([1 if p.store else 0 for p in plans]),
+                                        logits.ctypes.data if want_logits else None, am.ctypes.data))
+        return logits, am[:n]
+
+
+# ---------------------------------------------------------------- caches
+class CacheArena:
+    """CacheArena read contract (kv_cache.hpp:65-100) over the device arena."""
+
+    layout = UNPAD
+
+    def __init__(self, model: Model, batch_size: int, capacity: int):
+        h = C.c_void_p()
+        _check(lib().sd_cache_create(model._h, batch_size, capacity, self.layout, C.byref(h)))
+        self._h = h.value
+        self.model = model
+        self._batch = batch_size
+        self._capacity = capacity
+
+    def batch_size(self) -> int:
+        return self._batch
+
+    def capacity(self) -> int:
+        return self._capacity
+
+    def close(self) -> None:
+        if self._h:
+            lib().sd_cache_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def committed_len(self, sample: int) -> int:
+        v = C.c_int32()
+        _check(lib().sd_cache_committed_len(self._h, sample, C.byref(v)))
+        return v.value
+
+    def logical_len(self, sample: int) -> int:
+        v = C.c_int32()
+        _check(lib().sd_cache_logical_len(self._h, sample, C.byref(v)))
+        return v.value
+
+    def mark_hole(self, sample: int, position: int) -> None:
+        _check(lib().sd_cache_mark_hole(self._h, sample, position))
+
+    def ledger(self) -> tuple[int, int]:
+        u, p = C.c_int64(), C.c_int64()
+        _check(lib().sd_cache_ledger(self._h, C.byref(u), C.byref(p)))
+        return u.value, p.value
+
+    def gather_visible(self, sample: int, upto: int, layer: int):
+        hidden = self.model.config.hidden()
+        k = np.zeros((upto + 1) * hidden, dtype=np.float32)
+        v = np.zeros_like(k)
+        n = C.c_int32()
+        _check(lib().sd_cache_gather_visible(self._h, sample, upto, layer, k, v, C.byref(n)))
+        return k.reshape(-1, hidden)[: n.value], v.reshape(-1, hidden)[: n.value]
+
+    def verify_step(self, last_tokens, draft_counts, drafts, budget_left, active, stop_on_eos: bool,
+                    want_logits: bool = False):
+        """One fused device verify step (sd_verify_step)."""
+        B = self._batch
+        counts = _i32(draft_counts)
+        kmax = int(max([c for c, a in zip(counts, active) if a] or [0]))
+        tau = np.zeros(B, dtype=np.int32)
+        clipped = np.zeros(B, dtype=np.int32)
+        acc = np.full(B * (kmax + 1), -1, dtype=np.int32)
+        T = sum((1 + (kmax if self.layout == PADDED else c)) for c, a in zip(counts, active) if a)
+        logits = np.zeros((max(T, 1), self.model.config.vocab_size), dtype=np.float32) if want_logits else None
+        _check(lib().sd_verify_step(self.model._h, self._h, _i32(last_tokens), counts,
+                                    _i32(drafts) if len(drafts) else np.zeros(1, np.int32), _i32(budget_left),
+                                    _i32(active), int(stop_on_eos), tau, acc, clipped,
+                                    logits.ctypes.data if want_logits else None))
+        return tau, acc.reshape(B, kmax + 1), clipped.astype(bool), (logits[:T] if want_logits else None)
+
+
+class UnpadArena(CacheArena):
+    """kv_cache.hpp:105-128"""
+
+    layout = UNPAD
+
+    def start_offset(self, sample: int) -> int:
+        v = C.c_int32()
+        _check(lib().sd_cache_start_offset(self._h, sample, C.byref(v)))
+        return v.value
+
+    def commit_accepted(self, sample: int, tau: int) -> None:
+        _check(lib().sd_cache_commit_accepted(self._h, sample, tau))
+
+
+class PaddedGrid(CacheArena):
+    """kv_cache.hpp:133-168"""
+
+    layout = PADDED
+
+    def is_pad(self, sample: int, row: int) -> bool:
+        v = C.c_int32()
+        _check(lib().sd_cache_is_pad(self._h, sample, row, C.byref(v)))
+        return bool(v.value)
+
+    def commit_prefill(self, samples, prompt_lens) -> None:
+        _check(lib().sd_cache_commit_prefill(self._h, _i32(samples), _i32(prompt_lens), len(samples)))
+
+    def commit_padded(self, samples, taus) -> None:
+        _check(lib().sd_cache_commit_padded(self._h, _i32(samples), _i32(taus), len(samples)))
+
+
+# ---------------------------------------------------------------- engine
+MODES = {"greedy": 0, "vanilla": 1, "ems": 2}
+PREDICTORS = {"draft": 0, "retrieval": 1, "synthetic": 2}
+
+
+@dataclass
+class EngineConfig:
+    """engine.hpp:21-34"""
+
+    mode: str = "ems"
+    predictor: str = "draft"
+    k: int = 4
+    match_len: int = 2
+    copy_len: int = 7
+    batch_size: int = 1
+    max_new_tokens: int = 64
+    stop_on_eos: bool = True
+    seed: int = 1
+    synthetic_accuracy: float = 0.8
+
+    def _c(self) -> _EngineConfigT:
+        if self.mode not in MODES:
+            raise ConfigError(f"config: unknown mode: {self.mode}")
+        if self.predictor not in PREDICTORS:
+            raise ConfigError(f"config: unknown predictor: {self.predictor}")
+        return _EngineConfigT(MODES[self.mode], PREDICTORS[self.predictor], self.k, self.match_len, self.copy_len,
+                              self.batch_size, self.max_new_tokens, int(self.stop_on_eos), self.seed,
+                              self.synthetic_accuracy)
+
+
+@dataclass
+class DecodeResult:
+    generated_tokens: list
+    steps: list
+    useful_kv_writes: int
+    padding_kv_writes: int
+    prefill_seconds: float
+    decode_seconds: float
+
+
+def tokenize_prompt(text: str) -> list[int]:
+    """engine.cpp:136-145: BOS + byte tokens."""
+    return [BOS] + [b + BYTE_OFFSET for b in text.encode()]
+
+
+def decode(config: EngineConfig, target: Model, prompts, draft: Model | None = None) -> DecodeResult:
+    """decode_greedy / decode_speculative (engine.cpp:206-489) through sd_decode.
+    prompts: list of token-id lists (BOS included) or of strings."""
+    toks = [tokenize_prompt(p) if isinstance(p, str) else list(p) for p in prompts]
+    if len(toks) != config.batch_size:
+        raise ContractError("contract: prompt count does not match batch_size")
+    b = config.batch_size
+    mx = max(config.max_new_tokens, 1)
+    gen = np.zeros(b * mx, dtype=np.int32)
+    cnt = np.zeros(b, dtype=np.int32)
+    cap = b * (config.max_new_tokens + 2) + 16
+    rec = np.zeros(cap * 6, dtype=np.int32)
+    nrec = C.c_int64()
+    ledger = np.zeros(2, dtype=np.int64)
+    timing = np.zeros(2, dtype=np.float64)
+    flat = _i32([t for p in toks for t in p])
+    lens = _i32([len(p) for p in toks])
+    _check(lib().sd_decode(C.byref(config._c()), target._h, draft._h if draft else None, flat, lens, gen, cnt, rec,
+                           cap, C.byref(nrec), ledger, timing))
+    tokens = [gen[s * mx: s * mx + cnt[s]].tolist() for s in range(b)]
+    rows = rec[: nrec.value * 6].reshape(-1, 6)
+    return DecodeResult(tokens, step_records(rows), int(ledger[0]), int(ledger[1]), float(timing[0]),
+                        float(timing[1]))
+
+
+def step_records(rows: np.ndarray) -> list[dict]:
+    """make_step_record (engine.cpp:78-105) from flat {step, sample, k, tau, clipped} rows."""
+    out = []
+    for step in sorted(set(rows[:, 0].tolist())):
+        r = rows[rows[:, 0] == step]
+        ks, taus = r[:, 2].tolist(), r[:, 3].tolist()
+        kmax, tmax = max(ks), max(taus)
+        out.append(dict(
+            samples=[dict(sample=int(x[1]), k=int(x[2]), input_padding=kmax - int(x[2]), tau=int(x[3]),
+                          kv_padding=tmax - int(x[3]), clipped=bool(x[4])) for x in r],
+            tau_max=tmax,
+        ))
+    return out
+
+
+# ---------------------------------------------------------------- sessions
+PROFILE_KINDS = ["gemm_qkv", "gemm_o", "gemm_fc", "gemm_proj", "gemm_lm", "attention", "layernorm", "misc",
+                 "attn_combine"]
+
+
+def profile_enable(on: bool) -> None:
+    _check(lib().sd_profile_enable(int(on)))
+
+
+def profile_read() -> dict:
+    out = np.zeros(len(PROFILE_KINDS) * 3, dtype=np.float64)
+    _check(lib().sd_profile_read(out, len(PROFILE_KINDS)))
+    out = out.reshape(-1, 3)
+    return {k: dict(launches=int(r[0]), ms=float(r[1]), bytes=float(r[2])) for k, r in zip(PROFILE_KINDS, out)}
+
+
+def _scheck(rc: int) -> None:
+    if rc != 0:
+        raise _ERRORS.get(rc, SpecdecError)(lib().sd_session_last_error().decode())
+
+
+class Session:
+    """A prefilled batch whose decode loop (engine.cpp:391-489) runs on the GPU."""
+
+    def __init__(self, model: Model, config: EngineConfig, capacity: int, draft: Model | None = None):
+        h = C.c_void_p()
+        if config.predictor == "draft":
+            if draft is None:
+                raise ConfigError("draft predictor needs a draft model")
+            _scheck(lib().sd_session_create_draft(model._h, draft._h, C.byref(config._c()), capacity, C.byref(h)))
+        else:
+            _scheck(lib().sd_session_create(model._h, C.byref(config._c()), capacity, C.byref(h)))
+        self._h = h.value
+        self.model = model
+        self.draft = draft  # keeps the draft model alive with the session
+        self.config = config
+
+    def close(self):
+        if self._h:
+            lib().sd_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def prefill(self, prompts) -> None:
+        flat = _i32([t for p in prompts for t in p])
+        _scheck(lib().sd_session_prefill(self._h, flat, _i32([len(p) for p in prompts])))
+
+    def set_trajectory(self, traj: np.ndarray) -> None:
+        traj = np.ascontiguousarray(traj, dtype=np.int32)
+        _scheck(lib().sd_session_set_trajectory(self._h, traj.reshape(-1), traj.shape[1]))
+
+    def reset(self) -> None:
+        _scheck(lib().sd_session_reset(self._h))
+
+    def run(self, use_graph: bool = True, graph_steps: int = 8):
+        steps, ms = C.c_int32(), C.c_float()
+        _scheck(lib().sd_session_run(self._h, int(use_graph), graph_steps, C.byref(steps), C.byref(ms)))
+        return steps.value, ms.value
+
+    def run_host(self):
+        steps, ms, h2d, d2h = C.c_int32(), C.c_float(), C.c_int64(), C.c_int64()
+        _scheck(lib().sd_session_run_host(self._h, C.byref(steps), C.byref(ms), C.byref(h2d), C.byref(d2h)))
+        return steps.value, ms.value, h2d.value, d2h.value
+
+    def outputs(self):
+        B, mx = self.config.batch_size, self.config.max_new_tokens
+        gen = np.zeros(B * mx, dtype=np.int32)
+        cnt = np.zeros(B, dtype=np.int32)
+        steps = mx + 2
+        lk = np.zeros(steps * B, dtype=np.int32)
+        lt = np.zeros(steps * B, dtype=np.int32)
+        _scheck(lib().sd_session_outputs(self._h, gen, cnt, lk.ctypes.data, lt.ctypes.data, steps))
+        tokens = [gen[s * mx: s * mx + min(cnt[s], mx)].tolist() for s in range(B)]
+        return tokens, lk.reshape(steps, B), lt.reshape(steps, B)

@@ -1,0 +1,27 @@
+"""Untraced ms per verify step of the C3 device loop (A/B helper: run under
+different SD_* environment settings in the same box)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from paper_2405_07542_b200 import specdec as sd  # noqa: E402
+import bench  # noqa: E402
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+cfg = bench.C3
+m = sd.Model.init(sd.ModelConfig(**cfg), device=0, precision=sd.BF16)
+prompts = bench.prompts_for(range(B), cfg["vocab_size"], 600, 900)
+cap = max(len(p) for p in prompts) + 128 + 9
+e = sd.EngineConfig(mode="ems", predictor="retrieval", k=7, match_len=2, copy_len=7, batch_size=B, max_new_tokens=128,
+                    stop_on_eos=False, seed=1)
+s = sd.Session(m, e, cap)
+s.prefill(prompts)
+best = 1e9
+for _ in range(4):
+    s.reset()
+    steps, ms = s.run()
+    best = min(best, ms / steps)
+env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("SD_"))
+print(f"[{env or 'default'}] B={B}: {steps} steps, best {best:.3f} ms/step", flush=True)
