@@ -635,7 +635,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem = tslot;  // S: cols [0,8) and [8,16); O^T: cols [16,24)
     pdl_trigger();
-    pdl_wait();  // batch descriptors, Q and this layer's K/V come from earlier kernels
+    // The producer waits below, after pre-issuing its first item's OLD chunks.
+    if (warp != 4) pdl_wait();  // Q and this step's K/V rows come from the QKV reduction
 
     auto decode = [&](int i, int& s, int& head, int& qt) {
         qt = i % qtiles;
@@ -651,6 +652,38 @@ __global__ void __launch_bounds__(kPThreads, 1)
             int st = 0, qs = 0;
             uint32_t ph = 0, qph = 0;
             int next = atomicAdd(a.work, 1);
+            // Before griddepcontrol.wait: K/V rows of positions committed in EARLIER
+            // steps cannot change, and this CTA only became resident once the QKV
+            // GEMM's CTA on this SM exited -- i.e. after every kernel up to the last
+            // LayerNorm (and k_pack, which wrote segs) completed.  So the first
+            // item's chunks below its new tokens stream during the QKV reduction.
+            int pre_item = -1, pre_chunks = 0;
+            const auto issue_chunk = [&](int row_k, int row_v, int k0) {
+                ptx::mbar_wait(&empty[st], ph ^ 1);
+                ptx::mbar_arrive_expect_tx(&full[st], kPStage);
+                uint8_t* b = ring + st * kPStage;
+                ptx::tma_load_2d(b, &tm_kv, &full[st], 0, row_k + k0, pol);
+                ptx::tma_load_2d(b + kTcKeys * 128, &tm_kv, &full[st], 64, row_k + k0, pol);
+                ptx::tma_load_2d(b + 2 * kTcKeys * 128, &tm_kv, &full[st], 0, row_v + k0, pol);
+                ptx::tma_load_2d(b + 3 * kTcKeys * 128, &tm_kv, &full[st], 64, row_v + k0, pol);
+                if (++st == kPS) {
+                    st = 0;
+                    ph ^= 1;
+                }
+            };
+            if (next < n_items) {
+                int s, head, qt;
+                decode(next, s, head, qt);
+                const SampleSeg seg = a.segs[s];
+                if (seg.n_q - qt * kQT > 0 && seg.kv_len > 0) {
+                    pre_item = next;
+                    pre_chunks = min(kPS, max(0, seg.kv_len - seg.n_q) / kTcKeys);
+                    const int row_k = (((a.layer * 2 + 0) * a.B + s) * a.heads + head) * a.cap;
+                    const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap;
+                    for (int c = 0; c < pre_chunks; ++c) issue_chunk(row_k, row_v, c * kTcKeys);
+                }
+            }
+            pdl_wait();
             for (;;) {
                 const int i = next;
                 if (i >= n_items) break;
@@ -678,19 +711,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 }
                 const int row_k = (((a.layer * 2 + 0) * a.B + s) * a.heads + head) * a.cap;
                 const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap;
-                for (int k0 = 0; k0 < seg.kv_len; k0 += kTcKeys) {
-                    ptx::mbar_wait(&empty[st], ph ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[st], kPStage);
-                    uint8_t* b = ring + st * kPStage;
-                    ptx::tma_load_2d(b, &tm_kv, &full[st], 0, row_k + k0, pol);
-                    ptx::tma_load_2d(b + kTcKeys * 128, &tm_kv, &full[st], 64, row_k + k0, pol);
-                    ptx::tma_load_2d(b + 2 * kTcKeys * 128, &tm_kv, &full[st], 0, row_v + k0, pol);
-                    ptx::tma_load_2d(b + 3 * kTcKeys * 128, &tm_kv, &full[st], 64, row_v + k0, pol);
-                    if (++st == kPS) {
-                        st = 0;
-                        ph ^= 1;
-                    }
-                }
+                const int c0 = i == pre_item ? pre_chunks : 0;  // already in the ring
+                for (int k0 = c0 * kTcKeys; k0 < seg.kv_len; k0 += kTcKeys) issue_chunk(row_k, row_v, k0);
             }
             ptx::mbar_wait(&qempty[qs], qph ^ 1);  // end of work
             sq_item[qs] = -1;
