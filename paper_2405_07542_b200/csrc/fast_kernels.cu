@@ -46,6 +46,7 @@ struct FastWorkspace {
     int* attn_cnt = nullptr;   // split-KV arrival counters [B * heads * 16]
     GemmMaps map_xb, map_ctx, map_act;
     CUtensorMap kv_map;        // TMA view of the KV arena [L*2*B*heads*cap][hd], box {64, 128}
+    CUtensorMap kv_map64;      // ... with box {64, 64} (attention tail chunks)
     CUtensorMap q_map;         // TMA view of the queries [256][h], one-row boxes {64, 1}
     int* attn_work = nullptr;  // persistent attention item counters [num_layers], zeroed per forward
     std::vector<void*> allocs;
@@ -594,8 +595,8 @@ constexpr int kPStage = 4 * kTcKeys * 128;  // K + V, 2 boxes each
 constexpr int kPSmem = 1024 + kPS * kPStage + kPQ * 2048 + 2 * 2048 + 8 * kTcKeys * 4;
 
 __global__ void __launch_bounds__(kPThreads, 1)
-    k_attention_tcp(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q, AttnArgs a,
-                    int qtiles) {
+    k_attention_tcp(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv64,
+                    const __grid_constant__ CUtensorMap tm_q, AttnArgs a, int qtiles) {
     CtaTrace trace__(TK_ATTN);
     constexpr int HD = 128;
     extern __shared__ uint8_t smraw[];
@@ -610,8 +611,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
     __shared__ float sMx[8], sL[8];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, tid = threadIdx.x;
     const int n_items = a.B * a.heads * qtiles;
+    // a tail chunk of <= 64 keys loads half a stage: keep the other half finite (zero) once
+    for (int i = tid; i < kPS * kPStage / 16; i += kPThreads) ((uint4*)ring)[i] = make_uint4(0u, 0u, 0u, 0u);
+    ptx::fence_proxy_async_smem();
     if (tid == 0) {
         ptx::prefetch_tmap(&tm_kv);
+        ptx::prefetch_tmap(&tm_kv64);
         ptx::prefetch_tmap(&tm_q);
         for (int i = 0; i < kPS; ++i) {
             ptx::mbar_init(&full[i], 1);
@@ -658,14 +663,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
             // LayerNorm (and k_pack, which wrote segs) completed.  So the first
             // item's chunks below its new tokens stream during the QKV reduction.
             int pre_item = -1, pre_chunks = 0;
-            const auto issue_chunk = [&](int row_k, int row_v, int k0) {
+            // rows: keys left in the extent; <= 64 -> the 64-row boxes (no over-read of
+            // a whole 128-key chunk past the extent; the stage's other half stays finite)
+            const auto issue_chunk = [&](int row_k, int row_v, int k0, int rows) {
                 ptx::mbar_wait(&empty[st], ph ^ 1);
-                ptx::mbar_arrive_expect_tx(&full[st], kPStage);
+                const bool half = rows <= 64;
+                const CUtensorMap* m = half ? &tm_kv64 : &tm_kv;
+                ptx::mbar_arrive_expect_tx(&full[st], half ? kPStage / 2 : kPStage);
                 uint8_t* b = ring + st * kPStage;
-                ptx::tma_load_2d(b, &tm_kv, &full[st], 0, row_k + k0, pol);
-                ptx::tma_load_2d(b + kTcKeys * 128, &tm_kv, &full[st], 64, row_k + k0, pol);
-                ptx::tma_load_2d(b + 2 * kTcKeys * 128, &tm_kv, &full[st], 0, row_v + k0, pol);
-                ptx::tma_load_2d(b + 3 * kTcKeys * 128, &tm_kv, &full[st], 64, row_v + k0, pol);
+                ptx::tma_load_2d(b, m, &full[st], 0, row_k + k0, pol);
+                ptx::tma_load_2d(b + kTcKeys * 128, m, &full[st], 64, row_k + k0, pol);
+                ptx::tma_load_2d(b + 2 * kTcKeys * 128, m, &full[st], 0, row_v + k0, pol);
+                ptx::tma_load_2d(b + 3 * kTcKeys * 128, m, &full[st], 64, row_v + k0, pol);
                 if (++st == kPS) {
                     st = 0;
                     ph ^= 1;
@@ -680,7 +689,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     pre_chunks = min(kPS, max(0, seg.kv_len - seg.n_q) / kTcKeys);
                     const int row_k = (((a.layer * 2 + 0) * a.B + s) * a.heads + head) * a.cap;
                     const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap;
-                    for (int c = 0; c < pre_chunks; ++c) issue_chunk(row_k, row_v, c * kTcKeys);
+                    for (int c = 0; c < pre_chunks; ++c) issue_chunk(row_k, row_v, c * kTcKeys, kTcKeys);
                 }
             }
             pdl_wait();
@@ -712,7 +721,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const int row_k = (((a.layer * 2 + 0) * a.B + s) * a.heads + head) * a.cap;
                 const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap;
                 const int c0 = i == pre_item ? pre_chunks : 0;  // already in the ring
-                for (int k0 = c0 * kTcKeys; k0 < seg.kv_len; k0 += kTcKeys) issue_chunk(row_k, row_v, k0);
+                for (int k0 = c0 * kTcKeys; k0 < seg.kv_len; k0 += kTcKeys) issue_chunk(row_k, row_v, k0, seg.kv_len - k0);
             }
             ptx::mbar_wait(&qempty[qs], qph ^ 1);  // end of work
             sq_item[qs] = -1;
@@ -980,6 +989,7 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     make_b_maps(f->map_ctx, f->ctx, T, h);
     make_b_maps(f->map_act, f->act, T, mm);
     f->kv_map = make_tmap_2d(c.kv, (int64_t)cfg.num_layers * 2 * c.B * cfg.num_heads * c.cap, cfg.head_dim, 128);
+    f->kv_map64 = make_tmap_2d(c.kv, (int64_t)cfg.num_layers * 2 * c.B * cfg.num_heads * c.cap, cfg.head_dim, 64);
     f->q_map = make_tmap_2d(f->q, (int64_t)T, (int64_t)h, 1);
     f->attn_work = walloc<int>(f, (size_t)cfg.num_layers);
     ws.fast = f;
@@ -1117,7 +1127,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         at.work = f->attn_work + l;
         if (hd == 128 && aimpl == 4)
             PROF(PK_ATTN, launch_k(k_attention_tcp, dim3(std::min(c.B * heads * qtiles, kSms)), dim3(kPThreads), kPSmem,
-                                   st, f->kv_map, f->q_map, at, qtiles));
+                                   st, f->kv_map, f->kv_map64, f->q_map, at, qtiles));
         else if (hd == 128 && aimpl == 3)
             PROF(PK_ATTN, launch_k(k_attention_tc, dim3(c.B * heads, splits, qtiles), dim3(128), kTcSmem, st, f->kv_map,
                                    at));
