@@ -1,15 +1,14 @@
 // bf16 PERFORMANCE mode forward of the verify step.
 //
 // Per layer (model.cpp:303-359, restructured for the GPU):
-//   LN1 (fp32 residual -> bf16)          k_layernorm
-//   QKV  tcgen05 GEMM + scatter epilogue  Q -> q16, K/V -> unpadded arena
-//   ragged multi-query attention          k_attention (+ k_attn_combine)
-//   O    tcgen05 GEMM + residual epilogue
-//   LN2                                   k_layernorm
-//   FC   tcgen05 GEMM + GELU epilogue
-//   PROJ tcgen05 GEMM + residual epilogue
-// then final LN, LM-head GEMM with the (max, lowest id) argmax epilogue, and
-// k_argmax_reduce over the vocab tiles.  Weights and KV are bf16; the
+//   QKV  tcgen05 GEMM (gemm_sm100.cu) + split-K reduction: Q -> q16, K/V ->
+//        the unpadded arena at each token's write slot
+//   ragged multi-query attention          k_attention_tcp (tcgen05, persistent)
+//   O    tcgen05 GEMM + residual reduction, then LN2 (k_ln_rows)
+//   FC   tcgen05 GEMM + GELU reduction
+//   PROJ tcgen05 GEMM + residual reduction, then the next LN1 (k_ln_rows)
+// then the LM-head GEMM with the (max, lowest id) argmax reduction.  Layer 0's
+// LN1 is fused with the embedding (k_embed_ln).  Weights and KV are bf16; the
 // residual stream, accumulators and softmax are fp32.
 #include <cuda_bf16.h>
 
@@ -115,15 +114,6 @@ __device__ __forceinline__ void ln_row(const float* x, const float* g, const flo
     for (int i = threadIdx.x; i < h; i += kRowThreads, ++n) y[i] = __float2bfloat16_rn((v[n] - mean) * inv * g[i] + b[i]);
 }
 
-__global__ void __launch_bounds__(kRowThreads) k_layernorm(const float* __restrict__ x, const float* __restrict__ g,
-                                                           const float* __restrict__ b, int h,
-                                                           __nv_bfloat16* __restrict__ y, const int* __restrict__ dT) {
-    __shared__ float scratch[32];
-    int t = blockIdx.x;
-    if (t >= *dT) return;
-    ln_row(x + (size_t)t * h, g, b, h, y + (size_t)t * h, scratch);
-}
-
 // embedding (model.cpp:287-294) fused with layer 0's LN1
 __global__ void __launch_bounds__(kRowThreads) k_embed_ln(const __nv_bfloat16* __restrict__ tok,
                                                           const __nv_bfloat16* __restrict__ pos,
@@ -144,24 +134,6 @@ __global__ void __launch_bounds__(kRowThreads) k_embed_ln(const __nv_bfloat16* _
     for (int i = threadIdx.x; i < h; i += kRowThreads) r[i] = __bfloat162float(e[i]) + __bfloat162float(p[i]);
     __syncthreads();
     ln_row(r, g, b, h, y + (size_t)t * h, scratch);
-}
-
-// per-token argmax over the LM-head tile partials (lowest id on ties)
-__global__ void k_argmax_reduce(const float* __restrict__ pv, const int* __restrict__ pi, int m_tiles, int ld,
-                                int32_t* __restrict__ out, const int* __restrict__ dT) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= *dT) return;
-    float bv = pv[t];
-    int bi = pi[t];
-    for (int k = 1; k < m_tiles; ++k) {
-        float v = pv[(size_t)k * ld + t];
-        int i = pi[(size_t)k * ld + t];
-        if (v > bv || (v == bv && i < bi)) {
-            bv = v;
-            bi = i;
-        }
-    }
-    out[t] = bi;
 }
 
 // ------------------------------------------------------------- attention
@@ -434,7 +406,7 @@ __global__ void __launch_bounds__(128) k_attention_tc(const __grid_constant__ CU
     pdl_trigger();
     const int sh = blockIdx.x, split = blockIdx.y, qt = blockIdx.z;
     const int s = sh / a.heads, head = sh % a.heads;
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, tid = threadIdx.x;
+    const int warp = threadIdx.x / 32, tid = threadIdx.x;
     extern __shared__ uint8_t smraw[];
     uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
     uint8_t* sK = sm;                          // 2 boxes [128 keys][64 hd] SW128
