@@ -23,6 +23,7 @@
 // allocator, w4-7 epilogue (TMEM lanes 0-127).
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -263,7 +264,10 @@ __device__ __forceinline__ void tile_contrib(const RedInfo& r, int tile, int& n)
 // grid (m_tiles, ceil(T_upper / RT)), block 256: thread = one output feature
 // (tile row) for RT consecutive tokens, read as float4; contributors summed in
 // order (deterministic).
-constexpr int kRT = 16;
+// tokens per reduction thread: 8 (2 for the residual GEMMs, whose ~8
+// contributors per tile make every token a long sum) -- same-box A/B:
+// (16, 4) 8.29 ms -> (8, 2) 8.19 ms per C3 step
+constexpr int kRT = 8;
 template <int EPI, int RT = kRT>
 __global__ void __launch_bounds__(256) k_reduce_tile(const GemmArgs a, const RedInfo r) {
     CtaTrace trace__(EPI == EPI_STORE ? TK_RED_STORE : EPI == EPI_GELU ? TK_RED_GELU : EPI == EPI_QKV ? TK_RED_QKV : TK_RED_RESID);
@@ -583,7 +587,7 @@ void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, 
         case EPI_QKV: launch_k(k_reduce_tile<EPI_QKV>, tg, dim3(256), 0, st, ab, r); break;
         case EPI_RESID_LN:  // tile-parallel split-K sum + residual, then the row LayerNorm
             SD_CHECK(a.M % 4 == 0 && a.M <= 8192, CONFIG, "bf16 mode needs hidden % 4 == 0 and <= 8192");
-            launch_k(k_reduce_tile<EPI_RESID_LN, 4>, dim3(a.m_tiles, (T_upper + 3) / 4), dim3(256), 0, st, ab, r);
+            launch_k(k_reduce_tile<EPI_RESID_LN, 2>, dim3(a.m_tiles, (T_upper + 1) / 2), dim3(256), 0, st, ab, r);
             launch_k(k_ln_rows, dim3(T_upper), dim3(256), 0, st, ab);
             break;
         case EPI_ARGMAX: {
