@@ -126,6 +126,71 @@ def ncu_traffic(kernel_substr):
     return None, None
 
 
+TRACE_REC = np.dtype([("kid", "<u4"), ("blk", "<u4"), ("smid", "<u4"), ("n", "<u4"), ("t0", "<u8"), ("t1", "<u8")])
+
+
+def trace_launches(rec):
+    """Launches from in-graph CTA records (one per CTA, kid < 100): records of
+    one kernel id sorted by entry time, chunked by grid size.  Returns
+    (kid, t0, t1, ctas, sms) sorted by start."""
+    out = []
+    for kid in np.unique(rec["kid"][rec["kid"] < 100]):
+        r = rec[rec["kid"] == kid]
+        r = r[np.argsort(r["t0"], kind="stable")]
+        i = 0
+        while i < len(r):
+            n = int(r["n"][i])
+            chunk = r[i:i + n]
+            out.append((int(kid), int(chunk["t0"].min()), int(chunk["t1"].max()), len(chunk),
+                        len(np.unique(chunk["smid"]))))
+            i += n
+    out.sort(key=lambda x: x[1])
+    return out
+
+
+def in_graph_attention(session, hbm, cap=4_000_000):
+    """Attention roofline inside the replayed CUDA graph (PDL chain intact):
+    %globaltimer records of every CTA (sd_debug_trace_*) give each launch's
+    span; its exposed time is from the moment its last predecessor finished
+    (the QKV reduction) to its last CTA's exit, and its algorithmic K/V bytes
+    are the sum of the per-CTA TK_ATTN_BYTES trace points.  Only the first
+    ~80% of the trace window is used (the ring may cut the tail)."""
+    import ctypes as C
+    from paper_2405_07542_b200 import specdec as sd
+    L = sd.lib()
+    L.sd_debug_trace_begin.argtypes = [C.c_int]
+    L.sd_debug_trace_end.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int)]
+    session.reset()
+    if L.sd_debug_trace_begin(cap) != 0:
+        return None
+    session.run()
+    buf = np.zeros(cap, TRACE_REC)
+    n = C.c_int()
+    if L.sd_debug_trace_end(buf.ctypes.data, cap, C.byref(n)) != 0:
+        return None
+    rec = buf[:n.value]
+    ls = trace_launches(rec)
+    if not ls:
+        return None
+    t_lo, t_hi = ls[0][1], ls[0][1] + 0.8 * (max(l[2] for l in ls) - ls[0][1])
+    pts = rec[rec["kid"] == 110]
+    ready, tot_ns, tot_b, nl = 0, 0, 0, 0
+    for kid, t0, t1, ctas, sms in ls:
+        if kid == 9 and t1 < t_hi and t0 > t_lo:
+            sel = pts[(pts["t0"] >= t0) & (pts["t0"] <= t1)]
+            tot_b += int(sel["blk"].astype(np.int64).sum()) * 1024
+            tot_ns += t1 - max(t0, ready)
+            nl += 1
+        ready = max(ready, t1)
+    if not nl or not tot_ns:
+        return None
+    gbs = tot_b / tot_ns
+    return {"achieved": round(gbs, 1), "frac": round(gbs / hbm, 4), "launches": nl,
+            "us_per_launch": round(tot_ns / nl / 1e3, 2), "mb_per_launch": round(tot_b / nl / 1e6, 2),
+            "method": "graph replay with per-CTA %globaltimer records; exposed time = last CTA exit - "
+                      "max(first CTA entry, predecessor exit); bytes = per-CTA algorithmic K/V bytes"}
+
+
 def step_stats(log_k, log_tau):
     """make_step_record / compute_metrics (engine.cpp:78-126) from the device logs."""
     taus, rbar, useful, pad_kv, pad_in, steps = [], [], 0, 0, 0, 0
@@ -494,6 +559,11 @@ def main():
         roof["traffic"] = round(traffic / 1e6, 2)
         roof["traffic_unit"] = "MB per launch (ncu dram__bytes_read+write, %s)" % src_csv
         roof["algorithmic_mb_per_launch"] = round(kinds[dom]["bytes"] / max(1, kinds[dom]["launches"]) / 1e6, 2)
+    if dom == "attention":
+        try:
+            roof["in_graph"] = in_graph_attention(ems, hbm)
+        except Exception as e:  # diagnostics only
+            roof["in_graph"] = {"error": str(e)[:200]}
     roof["all_gemms_gbs"] = round(gemm_b / (gemm_ms / 1000) / 1e9, 1) if gemm_ms else None
     roof["whole_step_gbs"] = round(step_b / (total_ms / 1000) / 1e9, 1) if total_ms else None
 

@@ -41,11 +41,11 @@ struct FastWorkspace {
     float* part_o = nullptr;   // [T][heads][max_splits][hd]
     float* part_ml = nullptr;  // [T][heads][max_splits][2]
     float* part = nullptr;     // stream-K partial sums (largest GEMM of the model)
-    int* row_cnt = nullptr;    // per-token LayerNorm arrival counters [256]
     int* attn_cnt = nullptr;   // split-KV arrival counters [B * heads * 16]
     GemmMaps map_xb, map_ctx, map_act;
     CUtensorMap kv_map;        // TMA view of the KV arena [L*2*B*heads*cap][hd], box {64, 128}
     CUtensorMap kv_map64;      // ... with box {64, 64} (attention tail chunks)
+    CUtensorMap kv_map32;      // ... with box {64, 32}
     CUtensorMap q_map;         // TMA view of the queries [256][h], one-row boxes {64, 1}
     int* attn_work = nullptr;  // persistent attention item counters [num_layers], zeroed per forward
     std::vector<void*> allocs;
@@ -568,7 +568,7 @@ constexpr int kPSmem = 1024 + kPS * kPStage + kPQ * 2048 + 2 * 2048 + 8 * kTcKey
 
 __global__ void __launch_bounds__(kPThreads, 1)
     k_attention_tcp(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv64,
-                    const __grid_constant__ CUtensorMap tm_q, AttnArgs a, int qtiles) {
+                    const __grid_constant__ CUtensorMap tm_kv32, const __grid_constant__ CUtensorMap tm_q, AttnArgs a, int qtiles) {
     CtaTrace trace__(TK_ATTN);
     constexpr int HD = 128;
     extern __shared__ uint8_t smraw[];
@@ -589,6 +589,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     if (tid == 0) {
         ptx::prefetch_tmap(&tm_kv);
         ptx::prefetch_tmap(&tm_kv64);
+        ptx::prefetch_tmap(&tm_kv32);
         ptx::prefetch_tmap(&tm_q);
         for (int i = 0; i < kPS; ++i) {
             ptx::mbar_init(&full[i], 1);
@@ -629,19 +630,21 @@ __global__ void __launch_bounds__(kPThreads, 1)
             int st = 0, qs = 0;
             uint32_t ph = 0, qph = 0;
             int next = atomicAdd(a.work, 1);
+            unsigned long long algo = 0;
             // Before griddepcontrol.wait: K/V rows of positions committed in EARLIER
             // steps cannot change, and this CTA only became resident once the QKV
             // GEMM's CTA on this SM exited -- i.e. after every kernel up to the last
             // LayerNorm (and k_pack, which wrote segs) completed.  So the first
             // item's chunks below its new tokens stream during the QKV reduction.
             int pre_item = -1, pre_chunks = 0;
-            // rows: keys left in the extent; <= 64 -> the 64-row boxes (no over-read of
-            // a whole 128-key chunk past the extent; the stage's other half stays finite)
+            // rows: keys left in the extent; <= 32 / <= 64 -> the 32- / 64-row boxes (no
+            // over-read of a whole 128-key chunk past the extent; the rest of the stage
+            // holds finite data: zeros or an earlier chunk, masked by the softmax)
             const auto issue_chunk = [&](int row_k, int row_v, int k0, int rows) {
                 ptx::mbar_wait(&empty[st], ph ^ 1);
-                const bool half = rows <= 64;
-                const CUtensorMap* m = half ? &tm_kv64 : &tm_kv;
-                ptx::mbar_arrive_expect_tx(&full[st], half ? kPStage / 2 : kPStage);
+                const int box = rows <= 32 ? 32 : rows <= 64 ? 64 : kTcKeys;
+                const CUtensorMap* m = box == 32 ? &tm_kv32 : box == 64 ? &tm_kv64 : &tm_kv;
+                ptx::mbar_arrive_expect_tx(&full[st], kPStage / kTcKeys * box);
                 uint8_t* b = ring + st * kPStage;
                 ptx::tma_load_2d(b, m, &full[st], 0, row_k + k0, pol);
                 ptx::tma_load_2d(b + kTcKeys * 128, m, &full[st], 64, row_k + k0, pol);
@@ -694,7 +697,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap;
                 const int c0 = i == pre_item ? pre_chunks : 0;  // already in the ring
                 for (int k0 = c0 * kTcKeys; k0 < seg.kv_len; k0 += kTcKeys) issue_chunk(row_k, row_v, k0, seg.kv_len - k0);
+                algo += (unsigned long long)seg.kv_len * (2 * HD * 2);
             }
+            // in-graph roofline: this CTA's algorithmic K/V bytes (KiB) next to its timeline record
+            trace_point(TK_ATTN_BYTES, (uint32_t)(algo >> 10));
             ptx::mbar_wait(&qempty[qs], qph ^ 1);  // end of work
             sq_item[qs] = -1;
             ptx::mbar_arrive(&qfull[qs]);
@@ -953,15 +959,14 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
                     std::make_pair(m.vocab_pad, (int)h)})
         part = std::max(part, gemm_part_floats(mk.first, mk.second, kSms));
     f->part = walloc<float>(f, part);
-    f->row_cnt = walloc<int>(f, 256);
     f->attn_cnt = walloc<int>(f, (size_t)c.B * cfg.num_heads * 16);
-    CUDA_OK(cudaMemset(f->row_cnt, 0, sizeof(int) * 256));
     CUDA_OK(cudaMemset(f->attn_cnt, 0, sizeof(int) * (size_t)c.B * cfg.num_heads * 16));
     make_b_maps(f->map_xb, f->xb, T, h);
     make_b_maps(f->map_ctx, f->ctx, T, h);
     make_b_maps(f->map_act, f->act, T, mm);
     f->kv_map = make_tmap_2d(c.kv, (int64_t)cfg.num_layers * 2 * c.B * cfg.num_heads * c.cap, cfg.head_dim, 128);
     f->kv_map64 = make_tmap_2d(c.kv, (int64_t)cfg.num_layers * 2 * c.B * cfg.num_heads * c.cap, cfg.head_dim, 64);
+    f->kv_map32 = make_tmap_2d(c.kv, (int64_t)cfg.num_layers * 2 * c.B * cfg.num_heads * c.cap, cfg.head_dim, 32);
     f->q_map = make_tmap_2d(f->q, (int64_t)T, (int64_t)h, 1);
     f->attn_work = walloc<int>(f, (size_t)cfg.num_layers);
     ws.fast = f;
@@ -1043,7 +1048,6 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     base.T = n;
     base.dT = db.dT;
     base.part = f->part;
-    base.row_cnt = f->row_cnt;
     base.h = h;
     base.hd = hd;
     base.heads = heads;
@@ -1099,7 +1103,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         at.work = f->attn_work + l;
         if (hd == 128 && aimpl == 4)
             PROF(PK_ATTN, launch_k(k_attention_tcp, dim3(std::min(c.B * heads * qtiles, kSms)), dim3(kPThreads), kPSmem,
-                                   st, f->kv_map, f->kv_map64, f->q_map, at, qtiles));
+                                   st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
         else if (hd == 128 && aimpl == 3)
             PROF(PK_ATTN, launch_k(k_attention_tc, dim3(c.B * heads, splits, qtiles), dim3(128), kTcSmem, st, f->kv_map,
                                    at));

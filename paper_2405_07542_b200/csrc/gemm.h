@@ -32,7 +32,6 @@ struct GemmArgs {
     int ld_out;
     const float *ln_g, *ln_b; // EPI_RESID_LN
     __nv_bfloat16* ln_out;
-    int* row_cnt;             // EPI_RESID_LN: per-token tile arrival counters (zeroed, self-resetting)
     // EPI_QKV scatter into the KV arena [L][2][B][heads][cap][hd]
     __nv_bfloat16* kv;
     const Plan* plans;

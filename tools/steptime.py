@@ -1,14 +1,22 @@
 """Untraced ms per verify step of the C3 device loop (A/B helper: run under
-different SD_* environment settings in the same box)."""
+different SD_* environment settings in the same box).
+
+  python tools/steptime.py [B] [--lib path/to/other/libspecdec_b200.so]
+"""
 import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-import bench  # noqa: E402
 from paper_2405_07542_b200 import specdec as sd  # noqa: E402
+import bench  # noqa: E402
 
-B = int(sys.argv[1]) if len(sys.argv) > 1 else 24
+args = sys.argv[1:]
+if "--lib" in args:  # A/B against another build of the library
+    i = args.index("--lib")
+    sd.LIB_PATH = os.path.abspath(args[i + 1])
+    del args[i:i + 2]
+B = int(args[0]) if args else 24
 cfg = bench.C3
 m = sd.Model.init(sd.ModelConfig(**cfg), device=0, precision=sd.BF16)
 prompts = bench.prompts_for(range(B), cfg["vocab_size"], 600, 900)
@@ -22,5 +30,6 @@ for _ in range(4):
     s.reset()
     steps, ms = s.run()
     best = min(best, ms / steps)
-env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("SD_"))
+env = " ".join([f"{k}={v}" for k, v in os.environ.items() if k.startswith("SD_")] +
+               ([os.path.relpath(sd.LIB_PATH, ROOT)] if "--lib" in sys.argv else []))
 print(f"[{env or 'default'}] B={B}: {steps} steps, best {best:.3f} ms/step", flush=True)

@@ -24,24 +24,7 @@ sys.path.insert(0, ROOT)
 NAMES = {1: "gemm", 2: "red_store", 3: "red_gelu", 4: "red_qkv", 5: "red_resid", 6: "ln_rows", 7: "argmax",
          8: "embed_ln", 9: "attention", 10: "attn_combine", 11: "predict", 12: "pack", 13: "accept", 14: "pad_fill",
          15: "draft_pack", 16: "draft_take", 17: "draft_commit"}
-REC = np.dtype([("kid", "<u4"), ("blk", "<u4"), ("smid", "<u4"), ("n", "<u4"), ("t0", "<u8"), ("t1", "<u8")])
-
-
-def launches(rec):
-    out = []
-    for kid in np.unique(rec["kid"][rec["kid"] < 100]):
-        r = rec[rec["kid"] == kid]
-        r = r[np.argsort(r["t0"], kind="stable")]
-        i = 0
-        while i < len(r):
-            n = int(r["n"][i])
-            # kernels may exit early for unused blocks; still every block records once
-            chunk = r[i:i + n]
-            out.append((int(kid), int(chunk["t0"].min()), int(chunk["t1"].max()), len(chunk),
-                        len(np.unique(chunk["smid"]))))
-            i += n
-    out.sort(key=lambda x: x[1])
-    return out
+from bench import TRACE_REC as REC, trace_launches as launches  # noqa: E402
 
 
 def main():
