@@ -281,6 +281,14 @@ __global__ void __launch_bounds__(256) k_reduce_tile(const GemmArgs a, const Red
     tile_contrib(r, tile, nc);
     const float* __restrict__ p = a.part + ((size_t)tile * a.max_contrib * 256 + t0) * 256 + row;
     const int nt = min(RT, T - t0);
+    // independent of the partials: issued before them, so the residual
+    // read-modify-write and the bias cost no extra L2 round trip
+    const float b = a.bias ? a.bias[m] : 0.0f;
+    float old[RT];
+    if constexpr (EPI == EPI_RESID_LN) {
+#pragma unroll
+        for (int i = 0; i < RT; ++i) old[i] = i < nt ? a.out_f32[(size_t)(t0 + i) * a.ld_out + m] : 0.0f;
+    }
     float v[RT];
 #pragma unroll
     for (int i = 0; i < RT; ++i) v[i] = 0.0f;
@@ -301,11 +309,10 @@ __global__ void __launch_bounds__(256) k_reduce_tile(const GemmArgs a, const Red
             for (int i = 0; i < RT; ++i)
                 if (c0 + cc < nc) v[i] += x[cc][i];
     }
-    const float b = a.bias ? a.bias[m] : 0.0f;
     if constexpr (EPI == EPI_RESID_LN) {  // residual add; the LayerNorm runs in k_ln_rows
 #pragma unroll
         for (int i = 0; i < RT; ++i)
-            if (i < nt) a.out_f32[(size_t)(t0 + i) * a.ld_out + m] += v[i] + b;
+            if (i < nt) a.out_f32[(size_t)(t0 + i) * a.ld_out + m] = old[i] + (v[i] + b);
     } else if constexpr (EPI == EPI_QKV) {
         const int which = m / a.h, hm = m - which * a.h;
         const int head = hm / a.hd, d = hm - head * a.hd;
@@ -362,15 +369,20 @@ __global__ void __launch_bounds__(256) k_ln_rows(const GemmArgs a) {
     if (t >= T) return;
     const float4* __restrict__ row = (const float4*)(a.out_f32 + (size_t)t * a.ld_out);
     constexpr int kPer = 8;  // float4 per thread
-    float4 x[kPer];
+    float4 x[kPer], g[kPer], bb[kPer];
     float s = 0.0f;
     const int n4 = a.M / 4;
+    const float4* g4 = (const float4*)a.ln_g;
+    const float4* b4 = (const float4*)a.ln_b;
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
+    for (int k = 0; k < kPer; ++k) {  // gamma / beta in flight with the row: one L2 round trip
         const int i = threadIdx.x + k * 256;
         x[k] = i < n4 ? row[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-        s += x[k].x + x[k].y + x[k].z + x[k].w;
+        g[k] = i < n4 ? g4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        bb[k] = i < n4 ? b4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) s += x[k].x + x[k].y + x[k].z + x[k].w;
     const float mean = block_sum<256>(s, scratch) / a.M;
     float q = 0.0f;
 #pragma unroll
@@ -383,16 +395,14 @@ __global__ void __launch_bounds__(256) k_ln_rows(const GemmArgs a) {
     }
     const float inv = rsqrtf(block_sum<256>(q, scratch) / a.M + 1e-5f);
     __nv_bfloat162* y = (__nv_bfloat162*)(a.ln_out + (size_t)t * a.M);
-    const float4* g4 = (const float4*)a.ln_g;
-    const float4* b4 = (const float4*)a.ln_b;
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
         const int i = threadIdx.x + k * 256;
         if (i < n4) {
-            float4 g = g4[i], b = b4[i];
-            y[2 * i] = __floats2bfloat162_rn((x[k].x - mean) * inv * g.x + b.x, (x[k].y - mean) * inv * g.y + b.y);
-            y[2 * i + 1] =
-                __floats2bfloat162_rn((x[k].z - mean) * inv * g.z + b.z, (x[k].w - mean) * inv * g.w + b.w);
+            y[2 * i] = __floats2bfloat162_rn((x[k].x - mean) * inv * g[k].x + bb[k].x,
+                                             (x[k].y - mean) * inv * g[k].y + bb[k].y);
+            y[2 * i + 1] = __floats2bfloat162_rn((x[k].z - mean) * inv * g[k].z + bb[k].z,
+                                                 (x[k].w - mean) * inv * g[k].w + bb[k].w);
         }
     }
 }
