@@ -566,11 +566,16 @@ constexpr int kPS = 3, kPQ = 2, kPThreads = 192;
 constexpr int kPStage = 4 * kTcKeys * 128;  // K + V, 2 boxes each
 constexpr int kPSmem = 1024 + kPS * kPStage + kPQ * 2048 + 2 * 2048 + 8 * kTcKeys * 4;
 
+// HD = 64 (OPT-125m-shaped draft models): one 64-column box per K / V chunk
+// and per Q row; the O^T MMA keeps M = 128 (rows 64-127 read the unused,
+// zeroed second box and are never stored).
+template <int HD>
 __global__ void __launch_bounds__(kPThreads, 1)
     k_attention_tcp(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv64,
                     const __grid_constant__ CUtensorMap tm_kv32, const __grid_constant__ CUtensorMap tm_q, AttnArgs a, int qtiles) {
     CtaTrace trace__(TK_ATTN);
-    constexpr int HD = 128;
+    static_assert(HD == 64 || HD == 128, "persistent attention: head_dim 64 or 128");
+    constexpr int kBoxes = HD / 64;  // 64-column boxes per K / V chunk and per Q row
     extern __shared__ uint8_t smraw[];
     uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
     uint8_t* ring = sm;                                  // [kPS][K 2 boxes | V 2 boxes]
@@ -644,12 +649,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 ptx::mbar_wait(&empty[st], ph ^ 1);
                 const int box = rows <= 32 ? 32 : rows <= 64 ? 64 : kTcKeys;
                 const CUtensorMap* m = box == 32 ? &tm_kv32 : box == 64 ? &tm_kv64 : &tm_kv;
-                ptx::mbar_arrive_expect_tx(&full[st], kPStage / kTcKeys * box);
+                ptx::mbar_arrive_expect_tx(&full[st], 2 * kBoxes * 128 * box);
                 uint8_t* b = ring + st * kPStage;
-                ptx::tma_load_2d(b, m, &full[st], 0, row_k + k0, pol);
-                ptx::tma_load_2d(b + kTcKeys * 128, m, &full[st], 64, row_k + k0, pol);
-                ptx::tma_load_2d(b + 2 * kTcKeys * 128, m, &full[st], 0, row_v + k0, pol);
-                ptx::tma_load_2d(b + 3 * kTcKeys * 128, m, &full[st], 64, row_v + k0, pol);
+#pragma unroll
+                for (int bx = 0; bx < kBoxes; ++bx) {
+                    ptx::tma_load_2d(b + bx * kTcKeys * 128, m, &full[st], bx * 64, row_k + k0, pol);
+                    ptx::tma_load_2d(b + (2 + bx) * kTcKeys * 128, m, &full[st], bx * 64, row_v + k0, pol);
+                }
                 if (++st == kPS) {
                     st = 0;
                     ph ^= 1;
@@ -682,11 +688,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 for (int r = 0; r < kQT; ++r) toks[r] = a.qidx[seg.q_start + qt * kQT + (r < nq ? r : 0)];
                 ptx::mbar_wait(&qempty[qs], qph ^ 1);
                 sq_item[qs] = i;  // published by the arrive below
-                ptx::mbar_arrive_expect_tx(&qfull[qs], 2048);
+                ptx::mbar_arrive_expect_tx(&qfull[qs], kBoxes * 1024);
 #pragma unroll
                 for (int r = 0; r < kQT; ++r)  // one-row boxes: the TMA swizzles by destination address
 #pragma unroll
-                    for (int hx = 0; hx < 2; ++hx)
+                    for (int hx = 0; hx < kBoxes; ++hx)
                         ptx::tma_load_2d(qring + qs * 2048 + hx * 1024 + r * 128, &tm_q, &qfull[qs],
                                          head * HD + hx * 64, toks[r], pol);
                 if (++qs == kPQ) {
@@ -708,7 +714,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     } else if (warp == 5) {
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
-            const uint32_t id_s = ptx::umma_idesc_bf16(kTcKeys, kQT), id_o = ptx::umma_idesc_bf16_amn(HD, kQT);
+            const uint32_t id_s = ptx::umma_idesc_bf16(kTcKeys, kQT), id_o = ptx::umma_idesc_bf16_amn(128, kQT);
             int st = 0, qs = 0, items = 0;
             uint32_t ph = 0, qph = 0;
             uint32_t gc = 0;  // chunks processed (S / P buffers alternate)
@@ -893,7 +899,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             for (int q = 0; q < kQT; ++q) {
                 if (q >= nq) break;
                 const int tok = a.qidx[seg.q_start + qt * kQT + q];
-                a.ctx[(size_t)tok * a.h + head * HD + tid] = __float2bfloat16_rn(o[q] / sL[q]);
+                if (tid < HD) a.ctx[(size_t)tok * a.h + head * HD + tid] = __float2bfloat16_rn(o[q] / sL[q]);
             }
             gc += nch;
             ++items;
@@ -1021,7 +1027,8 @@ void prepare_fast_kernels() {
     CUDA_OK(cudaFuncSetAttribute(k_attention<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CUDA_OK(cudaFuncSetAttribute(k_attention<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CUDA_OK(cudaFuncSetAttribute(k_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
-    CUDA_OK(cudaFuncSetAttribute(k_attention_tcp, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
+    CUDA_OK(cudaFuncSetAttribute(k_attention_tcp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
+    CUDA_OK(cudaFuncSetAttribute(k_attention_tcp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
     gemm_prepare();
     done = true;
 }
@@ -1101,9 +1108,13 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         at.layer = l;
         static const int aimpl = getenv("SD_ATTN_IMPL") ? atoi(getenv("SD_ATTN_IMPL")) : 4;
         at.work = f->attn_work + l;
-        if (hd == 128 && aimpl == 4)
-            PROF(PK_ATTN, launch_k(k_attention_tcp, dim3(std::min(c.B * heads * qtiles, kSms)), dim3(kPThreads), kPSmem,
-                                   st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
+        const bool tcp = (hd == 128 || hd == 64) && aimpl == 4;
+        if (tcp && hd == 128)
+            PROF(PK_ATTN, launch_k(k_attention_tcp<128>, dim3(std::min(c.B * heads * qtiles, kSms)), dim3(kPThreads),
+                                   kPSmem, st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
+        else if (tcp)
+            PROF(PK_ATTN, launch_k(k_attention_tcp<64>, dim3(std::min(c.B * heads * qtiles, kSms)), dim3(kPThreads),
+                                   kPSmem, st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
         else if (hd == 128 && aimpl == 3)
             PROF(PK_ATTN, launch_k(k_attention_tc, dim3(c.B * heads, splits, qtiles), dim3(128), kTcSmem, st, f->kv_map,
                                    at));
@@ -1112,7 +1123,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         else
             PROF(PK_ATTN, launch_k(k_attention<64>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
         launches++;
-        if (splits > 1 && !(hd == 128 && aimpl == 4)) {  // the persistent kernel writes final rows
+        if (splits > 1 && !tcp) {  // the persistent kernel writes final rows
             PROF(PK_COMBINE, launch_k(k_attn_combine, dim3(n, heads), dim3(hd), 0, st, at, hd, (const int*)db.dT));
             launches++;
         }
