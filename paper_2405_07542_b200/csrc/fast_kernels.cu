@@ -186,6 +186,7 @@ struct AttnArgs {
     float* part_ml;
     int* cnt;                  // [B * heads * q_tiles] split arrival counters (self-resetting)
     int* work;                 // persistent kernel: this launch's item counter (zeroed per forward)
+    int pre_ok;                // persistent kernel: may read segs before griddepcontrol.wait (see producer)
     int h, heads, B, cap, layer, max_splits;
     float scale_log2;          // log2(e) / sqrt(hd)
 };
@@ -637,10 +638,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
             int next = atomicAdd(a.work, 1);
             unsigned long long algo = 0;
             // Before griddepcontrol.wait: K/V rows of positions committed in EARLIER
-            // steps cannot change, and this CTA only became resident once the QKV
-            // GEMM's CTA on this SM exited -- i.e. after every kernel up to the last
+            // steps cannot change, and -- when the QKV GEMM ran one CTA on EVERY SM
+            // (a.pre_ok, set by the host) -- this CTA only became resident once the
+            // GEMM's CTA on this SM exited, i.e. after every kernel up to the last
             // LayerNorm (and k_pack, which wrote segs) completed.  So the first
             // item's chunks below its new tokens stream during the QKV reduction.
+            // (A smaller GEMM grid, e.g. a draft model's, leaves SMs free and this
+            // CTA could run next to an unfinished k_pack: no early reads then.)
             int pre_item = -1, pre_chunks = 0;
             // rows: keys left in the extent; <= 32 / <= 64 -> the 32- / 64-row boxes (no
             // over-read of a whole 128-key chunk past the extent; the rest of the stage
@@ -661,7 +665,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     ph ^= 1;
                 }
             };
-            if (next < n_items) {
+            if (next < n_items && a.pre_ok) {
                 int s, head, qt;
                 decode(next, s, head, qt);
                 const SampleSeg seg = a.segs[s];
@@ -1021,6 +1025,16 @@ void profile_read(double* out, int kinds) {
 }
 
 // One-time kernel attributes (must run before any CUDA-graph capture).
+static int device_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        CUDA_OK(cudaGetDevice(&dev));
+        CUDA_OK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return n;
+}
+
 void prepare_fast_kernels() {
     static bool done = false;
     if (done) return;
@@ -1109,6 +1123,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         static const int aimpl = getenv("SD_ATTN_IMPL") ? atoi(getenv("SD_ATTN_IMPL")) : 4;
         at.work = f->attn_work + l;
         const bool tcp = (hd == 128 || hd == 64) && aimpl == 4;
+        at.pre_ok = g.grid == device_sms() ? 1 : 0;  // the QKV GEMM above held every SM
         if (tcp && hd == 128)
             PROF(PK_ATTN, launch_k(k_attention_tcp<128>, dim3(std::min(c.B * heads * qtiles, kSms)), dim3(kPThreads),
                                    kPSmem, st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
