@@ -564,19 +564,29 @@ __global__ void __launch_bounds__(128) k_attention_tc(const __grid_constant__ CU
 //              when the max grows by more than 2^8), P^T to smem; at the
 //              item end O^T / l -> the context row (thread = hd).
 constexpr int kPS = 3, kPQ = 2, kPThreads = 192;
-constexpr int kPStage = 4 * kTcKeys * 128;  // K + V, 2 boxes each
-constexpr int kPSmem = 1024 + kPS * kPStage + kPQ * 2048 + 2 * 2048 + 8 * kTcKeys * 4;
+// stage = K boxes then V boxes (one 64-column box per 64 of head_dim)
+template <int HD>
+constexpr int kPStageB = 2 * (HD / 64) * kTcKeys * 128;
+template <int HD>
+constexpr int kPSmemB = 1024 + kPS * kPStageB<HD> + kPQ * 2048 + 2 * 2048 + 8 * kTcKeys * 4;
+constexpr int kPSmem = kPSmemB<128>;  // 205 KB: one CTA per SM; HD = 64 fits two
 
 // HD = 64 (OPT-125m-shaped draft models): one 64-column box per K / V chunk
 // and per Q row; the O^T MMA keeps M = 128 (rows 64-127 read the unused,
 // zeroed second box and are never stored).
 template <int HD>
-__global__ void __launch_bounds__(kPThreads, 1)
+__global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
     k_attention_tcp(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv64,
                     const __grid_constant__ CUtensorMap tm_kv32, const __grid_constant__ CUtensorMap tm_q, AttnArgs a, int qtiles) {
     CtaTrace trace__(TK_ATTN);
     static_assert(HD == 64 || HD == 128, "persistent attention: head_dim 64 or 128");
     constexpr int kBoxes = HD / 64;  // 64-column boxes per K / V chunk and per Q row
+    constexpr int kPStage = kPStageB<HD>;
+    constexpr int kVOff = kBoxes * kTcKeys * 128;  // V boxes within a stage
+    // O^T = V^T P^T is M = 128 (hd) x N = 8: the second 64-row M chunk of V^T sits
+    // LBO bytes after the first; with HD = 64 it aliases the first (LBO = 0), so
+    // O^T rows 64-127 duplicate rows 0-63 and are never stored
+    constexpr uint32_t kVLbo = HD == 128 ? kTcKeys * 128 : 0;
     extern __shared__ uint8_t smraw[];
     uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
     uint8_t* ring = sm;                                  // [kPS][K 2 boxes | V 2 boxes]
@@ -658,7 +668,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
                 for (int bx = 0; bx < kBoxes; ++bx) {
                     ptx::tma_load_2d(b + bx * kTcKeys * 128, m, &full[st], bx * 64, row_k + k0, pol);
-                    ptx::tma_load_2d(b + (2 + bx) * kTcKeys * 128, m, &full[st], bx * 64, row_v + k0, pol);
+                    ptx::tma_load_2d(b + kVOff + bx * kTcKeys * 128, m, &full[st], bx * 64, row_v + k0, pol);
                 }
                 if (++st == kPS) {
                     st = 0;
@@ -764,11 +774,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
                     const uint32_t g = gc + c;
                     ptx::mbar_wait(&pfull[g & 1], (g >> 1) & 1);
                     ptx::tc_fence_after();
-                    const uint32_t va = ptx::smem_u32(ring + st * kPStage + 2 * kTcKeys * 128);
+                    const uint32_t va = ptx::smem_u32(ring + st * kPStage + kVOff);
                     const uint32_t pa = ptx::smem_u32(sP + (g & 1) * 2048);
 #pragma unroll
                     for (int k = 0; k < kTcKeys / 16; ++k)
-                        ptx::umma_bf16(tmem + 16, ptx::umma_desc_mn_sw128(va + k * 16 * 128, kTcKeys * 128, 1024),
+                        ptx::umma_bf16(tmem + 16, ptx::umma_desc_mn_sw128(va + k * 16 * 128, kVLbo, 1024),
                                        ptx::umma_desc_kmajor_sw128(pa + (k / 4) * 1024 + (k % 4) * 32), id_o,
                                        (c > 0 || k > 0) ? 1u : 0u);
                     ptx::umma_commit(&empty[st]);
@@ -1042,7 +1052,7 @@ void prepare_fast_kernels() {
     CUDA_OK(cudaFuncSetAttribute(k_attention<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CUDA_OK(cudaFuncSetAttribute(k_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
     CUDA_OK(cudaFuncSetAttribute(k_attention_tcp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
-    CUDA_OK(cudaFuncSetAttribute(k_attention_tcp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
+    CUDA_OK(cudaFuncSetAttribute(k_attention_tcp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmemB<64>));
     gemm_prepare();
     done = true;
 }
@@ -1128,8 +1138,8 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
             PROF(PK_ATTN, launch_k(k_attention_tcp<128>, dim3(std::min(c.B * heads * qtiles, kSms)), dim3(kPThreads),
                                    kPSmem, st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
         else if (tcp)
-            PROF(PK_ATTN, launch_k(k_attention_tcp<64>, dim3(std::min(c.B * heads * qtiles, kSms)), dim3(kPThreads),
-                                   kPSmem, st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
+            PROF(PK_ATTN, launch_k(k_attention_tcp<64>, dim3(std::min(c.B * heads * qtiles, 2 * kSms)),
+                                   dim3(kPThreads), kPSmemB<64>, st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
         else if (hd == 128 && aimpl == 3)
             PROF(PK_ATTN, launch_k(k_attention_tc, dim3(c.B * heads, splits, qtiles), dim3(128), kTcSmem, st, f->kv_map,
                                    at));
