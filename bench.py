@@ -457,6 +457,18 @@ def main():
         s.prefill(prompts)
         return s, prompts
 
+    def roof_frac(sess, ms_per_gen):
+        """% HBM roof of a generation: its algorithmic bytes (weights + K/V
+        streamed by every launch, from one eager profiled generation -- the
+        same deterministic trajectory) / the graph-timed time / measured peak."""
+        sess.reset()
+        sd.profile_enable(True)
+        sess.run(use_graph=False, graph_steps=1)
+        prof = sd.profile_read()
+        sd.profile_enable(False)
+        gen_bytes = sum(v["bytes"] for v in prof.values())
+        return gen_bytes / (ms_per_gen / 1000.0) / (measured_peaks()[0] * 1e9)
+
     def timed(sess, K, W):
         for _ in range(W):
             sess.reset()
@@ -566,6 +578,8 @@ def main():
             roof["in_graph"] = {"error": str(e)[:200]}
     roof["all_gemms_gbs"] = round(gemm_b / (gemm_ms / 1000) / 1e9, 1) if gemm_ms else None
     roof["whole_step_gbs"] = round(step_b / (total_ms / 1000) / 1e9, 1) if total_ms else None
+    # the generation's algorithmic bytes over the GRAPH-timed generation (the value's clock)
+    roof["generation_hbm_roof_frac"] = round(step_b / (ems_ms / a.steps / 1000.0) / (hbm * 1e9), 4)
 
     # optional batch sweep (EMS vs padded at 8..20 per GPU)
     sweep = None
@@ -581,7 +595,9 @@ def main():
             r_e = timed(se, 2, 1)
             r_p = timed(sp, 2, 1)
             sweep[b] = {"ems": r_e[1] / (r_e[0] / 1000), "padded": r_p[1] / (r_p[0] / 1000),
-                        "ems_avg_tau": r_e[3]["avg_tau"], "padded_ratio": r_p[3]["avg_padding_ratio"]}
+                        "ems_avg_tau": r_e[3]["avg_tau"], "padded_ratio": r_p[3]["avg_padding_ratio"],
+                        "ems_ms_per_verify_step": r_e[0] / r_e[2],
+                        "ems_hbm_roof_frac": round(roof_frac(se, r_e[0] / 2), 4)}
             se.close()
             sp.close()
 
