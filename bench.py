@@ -314,6 +314,25 @@ def run_reference_arm(a, cfg, rank):
 C5 = dict(num_layers=32, num_heads=32, head_dim=128, vocab_size=50272, max_positions=4480, init_seed=0xD5EED)
 
 
+def dist_setup(world, local):
+    """One process per GPU over NCCL.  SD_BENCH_SHARED_GPU=1 is a smoke test of
+    the multi-rank code path on a single-GPU box: every rank shares device
+    0 and the collectives run over gloo on host tensors (numbers from such a
+    run are not measurements).  Returns (device index, collective device)."""
+    import torch
+    import torch.distributed as dist
+
+    shared = os.environ.get("SD_BENCH_SHARED_GPU") == "1"
+    dev = local % torch.cuda.device_count() if shared else local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    return dev, ("cpu" if shared else "cuda")
+
+
 def run_extra(a, rank, world, local):
     """C4: OPT-13B target + OPT-125m-shaped draft (seed + 1, as make-model,
     specdec_main.cpp:63-65), k = 4, global batch 24 sharded over the GPUs; the
@@ -326,9 +345,7 @@ def run_extra(a, rank, world, local):
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local, cdev = dist_setup(world, local)
     from paper_2405_07542_b200 import sharding
     from paper_2405_07542_b200 import specdec as sd
 
@@ -383,9 +400,9 @@ def run_extra(a, rank, world, local):
             acc += st["accepted"]
             steps_tot += steps
         if world > 1:
-            t = torch.tensor([ms_tot], device="cuda")
+            t = torch.tensor([ms_tot], device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            c = torch.tensor([float(acc)], device="cuda", dtype=torch.float64)
+            c = torch.tensor([float(acc)], device=cdev, dtype=torch.float64)
             dist.all_reduce(c)
             ms_tot, acc = t.item(), c.item()
         res[mode] = dict(value=acc / (ms_tot / 1000.0), ms_per_step=ms_tot / a.steps,
@@ -438,9 +455,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local, cdev = dist_setup(world, local)
     from paper_2405_07542_b200 import sharding
     from paper_2405_07542_b200 import specdec as sd
 
@@ -508,14 +523,14 @@ def main():
     pad_ms, pad_acc, pad_steps, pad_stats = timed(pad, a.steps, max(1, a.warmup // 2))
     torch.cuda.synchronize()
     if world > 1:
-        t = torch.tensor([ems_ms, pad_ms], device="cuda")
+        t = torch.tensor([ems_ms, pad_ms], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ems_ms_max, pad_ms_max = t.tolist()
-        c = torch.tensor([ems_acc, pad_acc], device="cuda", dtype=torch.float64)
+        c = torch.tensor([ems_acc, pad_acc], device=cdev, dtype=torch.float64)
         dist.all_reduce(c)
         ems_acc_all, pad_acc_all = c.tolist()
         # gather per-sample outputs (the run's only collective, NCCL over NVLink)
-        sharding.gather_outputs(ems.outputs()[0], a.max_new, dist, device="cuda")
+        sharding.gather_outputs(ems.outputs()[0], a.max_new, dist, device=cdev)
     else:
         ems_ms_max, pad_ms_max, ems_acc_all, pad_acc_all = ems_ms, pad_ms, ems_acc, pad_acc
     value = ems_acc_all / (ems_ms_max / 1000.0)
@@ -537,9 +552,9 @@ def main():
             e_d2h += d2h
             e_steps += steps
         if world > 1:
-            t = torch.tensor([e_ms], device="cuda")
+            t = torch.tensor([e_ms], device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            c = torch.tensor([float(e_acc)], device="cuda", dtype=torch.float64)
+            c = torch.tensor([float(e_acc)], device=cdev, dtype=torch.float64)
             dist.all_reduce(c)
             e_ms, e_acc = t.item(), c.item()
         e2e = {"value": e_acc / (e_ms / 1000.0), "unit": "tokens/s", "h2d_bytes_per_step": e_h2d / a.steps,
