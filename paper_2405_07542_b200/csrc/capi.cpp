@@ -28,6 +28,11 @@ bool pdl_enabled() {
     return on != 0;
 }
 
+static int getenv_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 // ---------------------------------------------------------------- workspace
 void Workspace::ensure(const Model& m, const Cache& c, int T) {
     if (T <= cap_tokens) return;
@@ -387,7 +392,9 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
     std::memcpy(hs + o_budget, budget, 4 * (size_t)B);
     std::memcpy(hs + o_active, active, 4 * (size_t)B);
     std::memcpy(hs + o_drafts, drafts, 4 * (size_t)ndraft);
-    h->ws.ensure(m, c, T);
+    // the graph path below sizes its grids for B x (kcap + 1): allocate for that
+    // bound up front (a reallocation would move buffers the StepArgs point at)
+    h->ws.ensure(m, c, m.precision != FP32_CHECK && !logits && B * K1 <= 256 ? std::max(T, B * K1) : T);
     cudaStream_t st = mh->st;
     sync_descriptors_to_device(h);
     CUDA_OK(cudaMemcpyAsync(ds, hs, 4 * (o_drafts + ndraft), cudaMemcpyHostToDevice, st));
@@ -416,10 +423,43 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
     a.tau = ds + o_tau;
     a.accepted = ds + o_acc;
     a.clipped = ds + o_clip;
-    launch_pack(a, st);
-    note_launches(1);
+    // bf16, no logits: replay one CUDA graph of pack -> forward -> accept [->
+    // pad_fill] whose grids are sized for the bound B x (kcap + 1) and read
+    // the true token count on the device (like the session loop); the first
+    // call runs eagerly so every lazily allocated buffer exists before capture
+    const int T_up = B * K1;
+    const bool graphable = m.precision != FP32_CHECK && !logits && T_up <= 256 && !profile_on() &&
+                           getenv_int("SD_VERIFY_GRAPH", 1) != 0;
+    const void* key[4] = {ds, h->ws.d_tokens, h->ws.fast, (const void*)(intptr_t)T_up};
+    const int flags = (stop_on_eos ? 1 : 0) | (c.layout == PADDED ? 2 : 0);
+    bool replay = false;
+    if (graphable && h->vg_calls++ > 0) {
+        if (!h->vgraph || h->vg_flags != flags || std::memcmp(h->vg_key, key, sizeof(key)) != 0) {
+            if (h->vgraph) cudaGraphExecDestroy(h->vgraph);
+            h->vgraph = nullptr;
+            cudaGraph_t g;
+            CUDA_OK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            launch_pack(a, st);
+            DeviceBatch dbu{h->ws.d_segs, h->ws.d_qidx, ds + o_scal, T_up, c.cap, K1};
+            forward_fast_dev(m, c, h->ws, dbu, 0, false, st);
+            launch_accept(a, st);
+            if (c.layout == PADDED) launch_pad_fill(a, c, st);
+            CUDA_OK(cudaStreamEndCapture(st, &g));
+            CUDA_OK(cudaGraphInstantiate(&h->vgraph, g, 0));
+            CUDA_OK(cudaGraphDestroy(g));
+            std::memcpy(h->vg_key, key, sizeof(key));
+            h->vg_flags = flags;
+        }
+        CUDA_OK(cudaGraphLaunch(h->vgraph, st));
+        replay = true;
+    }
+    if (!replay) {
+        launch_pack(a, st);
+        note_launches(1);
+    }
     // run the forward (argmax always; logits on request)
-    if (m.precision == FP32_CHECK) {
+    if (replay) {
+    } else if (m.precision == FP32_CHECK) {
         forward_check(m, c, h->ws, T, true, st);
         note_launches(3 + 11 * (int64_t)cfg.num_layers + 3);
     } else if (T <= 256) {
@@ -428,11 +468,13 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
     } else {
         forward_fast(m, c, h->ws, T, logits != nullptr, st);
     }
-    launch_accept(a, st);
-    note_launches(1);
-    if (c.layout == PADDED) {
-        launch_pad_fill(a, c, st);
+    if (!replay) {
+        launch_accept(a, st);
         note_launches(1);
+        if (c.layout == PADDED) {
+            launch_pad_fill(a, c, st);
+            note_launches(1);
+        }
     }
     int32_t flag = 0;
     CUDA_OK(cudaMemcpyAsync(&flag, h->ws.d_flag, 4, cudaMemcpyDeviceToHost, st));
@@ -514,6 +556,7 @@ sd_model::~sd_model() {
     if (st) cudaStreamDestroy(st);
 }
 sd_cache::~sd_cache() {
+    if (vgraph) cudaGraphExecDestroy(vgraph);
     sdb::dfree(d_step);
     if (h_step) cudaFreeHost(h_step);
 }

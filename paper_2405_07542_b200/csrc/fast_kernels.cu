@@ -1024,6 +1024,7 @@ static double g_prof_acc[PK_N][3];  // launches, ms, bytes
         }                                                  \
     } while (0)
 
+bool profile_on() { return g_prof; }
 void profile_enable(bool on) {
     g_prof = on;
     if (on)

@@ -23,6 +23,12 @@ struct sd_cache {
     int32_t* d_step = nullptr;    // inputs + scratch + outputs, one allocation
     int32_t* h_step = nullptr;    // pinned host mirror for the H2D / D2H copies
     size_t step_words = 0;
+    // sd_verify_step's CUDA graph (pack -> forward -> accept with device-side
+    // token counts), rebuilt when any buffer it bakes in changes
+    cudaGraphExec_t vgraph = nullptr;
+    const void* vg_key[4] = {nullptr, nullptr, nullptr, nullptr};
+    int vg_flags = -1;
+    int vg_calls = 0;
     ~sd_cache();
 };
 
@@ -68,6 +74,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
                       cudaStream_t st);
 void prepare_fast_kernels();
 void profile_enable(bool on);
+bool profile_on();
 void profile_read(double* out, int kinds);
 
 }  // namespace sdb
