@@ -624,19 +624,37 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
         ptx::fence_barrier_init();
     }
     if (warp == 5) ptx::tmem_alloc32(&tslot);
+    // Longest extents first (LPT): items are handed out in order of decreasing
+    // kv_len, so the last items -- the end-of-kernel tail -- are the shortest.
+    // The segs are safe to read before griddepcontrol.wait under a.pre_ok (see
+    // the producer); otherwise every warp waits first.
+    __shared__ int s_order[256];
+    const bool lpt = a.B <= 256;
+    if (!a.pre_ok) pdl_wait();
+    if (lpt)
+        for (int x = tid; x < a.B; x += kPThreads) {
+            const int lx = a.segs[x].kv_len;
+            int rank = 0;
+            for (int y = 0; y < a.B; ++y) {
+                const int ly = a.segs[y].kv_len;
+                rank += (ly > lx) || (ly == lx && y < x);
+            }
+            s_order[rank] = x;
+        }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = tslot;  // S: cols [0,8) and [8,16); O^T: cols [16,24)
     pdl_trigger();
     // The producer waits below, after pre-issuing its first item's OLD chunks.
-    if (warp != 4) pdl_wait();  // Q and this step's K/V rows come from the QKV reduction
+    if (warp != 4 && a.pre_ok) pdl_wait();  // Q and this step's K/V rows come from the QKV reduction
 
     auto decode = [&](int i, int& s, int& head, int& qt) {
         qt = i % qtiles;
         const int pair = i / qtiles;
         s = pair / a.heads;
         head = pair - s * a.heads;
+        if (lpt) s = s_order[s];
     };
 
     if (warp == 4) {
