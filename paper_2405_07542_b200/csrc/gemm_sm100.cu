@@ -23,6 +23,7 @@
 // allocator, w4-7 epilogue (TMEM lanes 0-127).
 #include <cuda_bf16.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -586,6 +587,9 @@ void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, 
     }
     SD_CHECK(T_upper <= 256, INTERNAL, "GEMM token tile is at most 256");
     GemmArgs ab = a;
+    // tools/energy_probe.py: SD_GEMM_DBG bit0 skips the MMAs, bit1 the partial stores (garbage results)
+    static const int dbg_env = getenv("SD_GEMM_DBG") ? atoi(getenv("SD_GEMM_DBG")) : 0;
+    ab.dbg |= dbg_env;
     ab.box = T_upper <= 32 ? 32 : T_upper <= 64 ? 64 : T_upper <= 128 ? 128 : 256;
     launch_k(k_gemm, dim3(a.grid), dim3(kThreads), kSmemBytes, st, maps.A, maps.B[0], maps.B[1], maps.B[2],
              maps.B[3], ab);
