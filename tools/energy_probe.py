@@ -13,11 +13,12 @@ from paper_2405_07542_b200 import specdec as sd  # noqa: E402
 import bench  # noqa: E402
 
 B = 24
+K = int(os.environ.get("PROBE_K", 7))  # drafts per sample: T = B * (K + 1) every step
 cfg = bench.C3
 m = sd.Model.init(sd.ModelConfig(**cfg), device=0, precision=sd.BF16)
 prompts = bench.prompts_for(range(B), cfg["vocab_size"], 600, 900)
 cap = max(len(p) for p in prompts) + 128 + 9
-e = sd.EngineConfig(mode="ems", predictor="synthetic", k=7, batch_size=B, max_new_tokens=64, stop_on_eos=False,
+e = sd.EngineConfig(mode="ems", predictor="synthetic", k=K, batch_size=B, max_new_tokens=64, stop_on_eos=False,
                     seed=1, synthetic_accuracy=0.0)
 s = sd.Session(m, e, cap)
 s.prefill(prompts)
@@ -28,5 +29,5 @@ for _ in range(3):
     s.reset()
     steps, ms = s.run()
     best = min(best, ms / steps)
-print(f"[SD_GEMM_DBG={os.environ.get('SD_GEMM_DBG', '0')}] T=192 fixed: {steps} steps, best {best:.3f} ms/step",
+print(f"[SD_GEMM_DBG={os.environ.get('SD_GEMM_DBG', '0')}] T={B * (K + 1)} fixed: {steps} steps, best {best:.3f} ms/step",
       flush=True)
