@@ -1,0 +1,103 @@
+// Exercises include/specdec_b200.hpp (the reference-shaped C++ layer) on the
+// GPU: C1 config, fp32 check mode, a ragged prefill and two EMS verify steps
+// driven exactly like engine.cpp:427-485 (concatenate_inputs ->
+// restore_indices -> forward -> verify -> commit_accepted).  Prints one line
+// per fact; tests/test_gpu_cpp_layer.py replays the same calls on the CPU
+// oracle and compares (fp32 check mode is bit-exact).
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "specdec_b200.hpp"
+
+using namespace specdec;
+
+static uint64_t fnv1a(const std::vector<float>& row) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(row.data());
+    for (size_t i = 0; i < row.size() * sizeof(float); ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
+// One forward of per-sample inputs placed right after each sample's committed extent.
+static std::vector<LogitsRow> step_forward(const Model& m, UnpadArena& arena, const std::vector<TokenSequence>& in,
+                                           int tag) {
+    RaggedBatch batch = ragged::concatenate_inputs(in);
+    std::vector<TokenSlot> slots;
+    for (int i = 0; i < batch.total_input_token_nums; ++i) {
+        TokenSlot s = ragged::restore_indices(batch.token_nums_per_sample, i);
+        s.original_sequence_position += arena.committed_len(s.original_batch_index);  // absolute position
+        slots.push_back(s);
+    }
+    std::vector<LogitsRow> rows = m.forward(batch, arena, slots);
+    for (size_t i = 0; i < rows.size(); ++i)
+        std::printf("fwd %d %zu %llu %d\n", tag, i, (unsigned long long)fnv1a(rows[i]), greedy_next(rows[i]));
+    return rows;
+}
+
+int main() {
+    const ModelConfig cfg{};  // C1: the reference's default ModelConfig
+    Model m = Model::init(cfg);
+    std::printf("checksum %llu\n", (unsigned long long)m.weight_checksum());
+    const int B = 3, cap = 64;
+    UnpadArena arena(cfg.num_layers, B, cap, cfg.hidden());
+    std::vector<TokenSequence> prompts = {{0, 72, 101, 108, 108, 111}, {0, 87, 111}, {0, 33, 34, 35, 36}};
+
+    // prefill: the whole prompts, then commit them; the last row gives the first token
+    std::vector<LogitsRow> rows = step_forward(m, arena, prompts, 0);
+    std::vector<TokenId> last(B);
+    size_t off = 0;
+    for (int s = 0; s < B; ++s) {
+        off += prompts[s].size();
+        last[s] = greedy_next(rows[off - 1]);
+        arena.commit_accepted(s, (int)prompts[s].size());
+    }
+    // two verify steps with fixed ragged drafts (sample 1 drafts nothing in step 1)
+    const std::vector<std::vector<TokenSequence>> drafts = {{{5, 6}, {}, {7}}, {{9}, {10, 11, 12}, {13, 14}}};
+    for (int step = 0; step < 2; ++step) {
+        std::vector<TokenSequence> in(B);
+        for (int s = 0; s < B; ++s) {
+            in[s] = {last[s]};
+            in[s].insert(in[s].end(), drafts[step][s].begin(), drafts[step][s].end());
+        }
+        rows = step_forward(m, arena, in, step + 1);
+        off = 0;
+        for (int s = 0; s < B; ++s) {
+            std::vector<LogitsRow> mine(rows.begin() + off, rows.begin() + off + in[s].size());
+            off += in[s].size();
+            VerifyResult v = verify(mine, drafts[step][s]);
+            arena.commit_accepted(s, v.tau);
+            last[s] = v.accepted.back();
+            std::printf("tau %d %d %d %d\n", step + 1, s, v.tau, arena.committed_len(s));
+        }
+    }
+    std::printf("ledger %lld %lld\n", (long long)arena.useful_writes(), (long long)arena.padding_writes());
+    std::printf("start_offset %d\n", arena.start_offset(2));
+
+    // error taxonomy: the reference's exception types come back
+    try {
+        ragged::restore_indices({1, 2}, 3);
+        std::printf("restore_indices did not throw\n");
+    } catch (const ContractError& e) {
+        std::printf("contract_error_ok %s\n", std::strncmp(e.what(), "contract: ", 10) == 0 ? "prefixed" : e.what());
+    }
+    try {
+        ModelConfig bad = cfg;
+        bad.num_heads = 0;
+        Model::init(bad);
+        std::printf("bad config did not throw\n");
+    } catch (const ConfigError&) {
+        std::printf("config_error_ok\n");
+    }
+    try {
+        arena.commit_accepted(0, cap);  // past the capacity
+        std::printf("over-commit did not throw\n");
+    } catch (const Error&) {
+        std::printf("commit_error_ok\n");
+    }
+    return 0;
+}
