@@ -97,6 +97,12 @@ int sd_cache_logical_len(const sd_cache* c, int sample, int32_t* out);
 int sd_cache_start_offset(const sd_cache* c, int sample, int32_t* out);
 /* UnpadArena::commit_accepted (kv_cache.cpp:152-161): metadata only */
 int sd_cache_commit_accepted(sd_cache* c, int sample, int tau);
+/* committed_len (and, for the unpad arena, start_offset) of all B samples at
+ * once (kv_cache.hpp:109-110); start_offset may be NULL. */
+int sd_cache_get_lengths(const sd_cache* c, int32_t* committed, int32_t* start_offset);
+/* UnpadArena::commit_accepted for every sample (taus[B]; 0 = not committed),
+ * all validated before any state changes. */
+int sd_commit_accepted(sd_cache* c, const int32_t* taus);
 /* PaddedGrid::commit_padded (kv_cache.cpp:269-314): zero-filler rows on device */
 int sd_cache_commit_padded(sd_cache* c, const int32_t* samples, const int32_t* taus, int n);
 /* PaddedGrid::commit_prefill (kv_cache.cpp:237-267) */

@@ -737,6 +737,30 @@ int sd_cache_commit_accepted(sd_cache* c, int s, int tau) {
     return guarded([&] { commit_accepted_host(c, s, tau); });
 }
 
+int sd_cache_get_lengths(const sd_cache* h, int32_t* committed, int32_t* start_offset) {
+    return guarded([&] {  // kv_cache.hpp:109-110 for every sample at once
+        const Cache& c = h->c;
+        SD_CHECK(committed || start_offset, CONTRACT, "no output buffer");
+        SD_CHECK(!start_offset || c.layout == UNPAD, CONTRACT, "start offsets exist for the unpad arena only");
+        for (int s = 0; s < c.B; ++s) {
+            if (committed) committed[s] = c.committed[s];
+            if (start_offset) start_offset[s] = s * c.cap;
+        }
+    });
+}
+
+int sd_commit_accepted(sd_cache* h, const int32_t* taus) {
+    return guarded([&] {  // UnpadArena::commit_accepted for every sample with tau > 0
+        const Cache& c = h->c;
+        SD_CHECK(c.layout == UNPAD, CONTRACT, "not an unpad arena");
+        for (int s = 0; s < c.B; ++s)  // validate everything before any state changes (kv_cache.cpp:152-161)
+            SD_CHECK(taus[s] >= 0 && taus[s] <= c.staged[s] - c.committed[s], CONTRACT,
+                     "commit exceeds the slots written this step");
+        for (int s = 0; s < c.B; ++s)
+            if (taus[s] > 0) commit_accepted_host(h, s, taus[s]);
+    });
+}
+
 int sd_cache_commit_prefill(sd_cache* h, const int32_t* samples, const int32_t* lens, int n) {
     return guarded([&] { commit_prefill_host(h, samples, lens, n); });
 }

@@ -2,7 +2,7 @@
 // GPU: C1 config, fp32 check mode, a ragged prefill and two EMS verify steps
 // driven exactly like engine.cpp:427-485 (concatenate_inputs ->
 // restore_indices -> forward -> verify -> commit_accepted).  Prints one line
-// per fact; tests/test_gpu_cpp_layer.py replays the same calls on the CPU
+// per fact; tests/test_cpp_layer.py replays the same calls on the CPU
 // oracle and compares (fp32 check mode is bit-exact).
 #include <cstdint>
 #include <cstdio>
@@ -76,6 +76,14 @@ int main() {
         }
     }
     std::printf("ledger %lld %lld\n", (long long)arena.useful_writes(), (long long)arena.padding_writes());
+    // the array forms of the C ABI: all lengths at once, batched commit
+    int32_t com[3], so[3];
+    b200::check(sd_cache_get_lengths(arena.handle(), com, so));
+    std::printf("lengths %d %d %d %d %d %d\n", com[0], com[1], com[2], so[0], so[1], so[2]);
+    const int32_t too_many[3] = {0, 5, 0};  // nothing was staged since the last commit
+    const int rc = sd_commit_accepted(arena.handle(), too_many);
+    b200::check(sd_cache_get_lengths(arena.handle(), com, nullptr));
+    std::printf("batched_commit_rejected %d %d %d %d\n", rc, com[0], com[1], com[2]);
     std::printf("start_offset %d\n", arena.start_offset(2));
 
     // error taxonomy: the reference's exception types come back

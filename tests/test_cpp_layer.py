@@ -88,4 +88,7 @@ def test_cpp_layer_matches_oracle(tmp_path, oracle):
     assert tail["ledger"] == [str(useful), "0"]  # every written slot counted once, no padding
     assert tail["start_offset"] == [str(2 * cap)]  # kv_cache.cpp:116-120
     assert tail["contract_error_ok"] == ["prefixed"]
+    committed = [e[4] for e in expect if e[0] == "tau" and e[1] == "2"]
+    assert tail["lengths"] == committed + [str(s * cap) for s in range(B)]
+    assert tail["batched_commit_rejected"] == ["3"] + committed  # SD_CONTRACT, nothing mutated
     assert "config_error_ok" in tail and "commit_error_ok" in tail
