@@ -439,6 +439,8 @@ def main():
     ap.add_argument("--max-new", type=int, default=128)
     ap.add_argument("--predictor", default="retrieval", choices=["retrieval", "synthetic"])
     ap.add_argument("--sweep", action="store_true", help="also run batch 8/12/16/20 (EMS and padded)")
+    ap.add_argument("--ablation", action="store_true",
+                    help="also run the paper's 2x2 ablation: unpadded input only / unpadded KV only")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-ctx", type=int, default=256)
@@ -465,7 +467,8 @@ def main():
 
     def make_session(mode, B, gids):
         prompts = prompts_for(gids, V, 600, 900)
-        cap = max(len(p) for p in prompts) + a.max_new + kcap + 2 if mode == "ems" else cfg["max_positions"]
+        cap = (max(len(p) for p in prompts) + a.max_new + kcap + 2 if mode in ("ems", "unpad_kv")
+               else cfg["max_positions"])  # unpadded arena vs the padded grid
         e = sd.EngineConfig(mode=mode, predictor=a.predictor, k=kcap, match_len=2, copy_len=kcap, batch_size=B,
                             max_new_tokens=a.max_new, stop_on_eos=False, seed=1, synthetic_accuracy=0.7)
         s = sd.Session(m, e, cap)
@@ -616,6 +619,18 @@ def main():
             se.close()
             sp.close()
 
+    # the paper's 2x2 ablation on the same generations
+    ablation = None
+    if a.ablation:
+        ablation = {"ems (unpad input + unpad KV)": round(value / world, 2),
+                    "vanilla (padded input + padded KV)": round(padded_value / world, 2)}
+        for mode, label in (("unpad_input", "unpad input + padded KV"), ("unpad_kv", "padded input + unpad KV")):
+            sa, _ = make_session(mode, B, gids)
+            r_a = timed(sa, a.steps, max(1, a.warmup // 2))
+            ablation[label] = round(r_a[1] / (r_a[0] / 1000), 2)
+            ablation[label + " ms_per_verify_step"] = round(r_a[0] / r_a[2], 3)
+            sa.close()
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -660,6 +675,8 @@ def main():
     }
     if sweep:
         line["sweep_per_gpu"] = sweep
+    if ablation:
+        line["ablation_per_gpu"] = ablation
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

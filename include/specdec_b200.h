@@ -52,7 +52,9 @@ typedef struct {
     uint64_t init_seed;
 } sd_model_config;
 
-/* specdec::EngineConfig (engine.hpp:21-34); mode 0 greedy, 1 vanilla, 2 ems;
+/* specdec::EngineConfig (engine.hpp:21-34); mode 0 greedy, 1 vanilla, 2 ems,
+ * and for sd_session_* only the paper's ablation: 3 unpadded
+ * input over the padded KV grid, 4 padded input over the unpadded KV arena;
  * predictor 0 draft, 1 retrieval, 2 synthetic. */
 typedef struct {
     int32_t mode, predictor, k, match_len, copy_len, batch_size, max_new_tokens, stop_on_eos;

@@ -69,6 +69,7 @@ StepArgs step_args(sd_session* s) {
     a.B = s->B;
     a.cap = c.cap;
     a.layout = c.layout;
+    a.ablation = s->e.mode == 3 ? 1 : s->e.mode == 4 ? 2 : 0;
     a.stop_on_eos = s->e.stop_on_eos;
     a.acc_stride = s->kcap + 1;
     a.last = nullptr;
@@ -181,7 +182,8 @@ void device_step(sd_session* s, cudaStream_t st, unsigned long long cond = 0, bo
 
 sd_session* session_create(sd_model* m, const sd_engine_config& e, int capacity, sd_model* draft = nullptr) {
     SD_CHECK(m->m.precision == BF16, CONFIG, "sessions run the bf16 performance path");
-    SD_CHECK(e.mode == 1 || e.mode == 2, CONFIG, "speculative decoding needs the vanilla or ems mode");
+    SD_CHECK(e.mode >= 1 && e.mode <= 4, CONFIG,
+             "speculative decoding needs the vanilla, ems or an ablation mode (unpad_input, unpad_kv)");
     SD_CHECK(e.predictor >= 0 && e.predictor <= 2, CONFIG, "unknown predictor");
     if (e.predictor == 0) {
         SD_CHECK(draft != nullptr, CONFIG, "draft predictor needs a draft model");
@@ -201,7 +203,7 @@ sd_session* session_create(sd_model* m, const sd_engine_config& e, int capacity,
         SD_CHECK(s->B * (s->kcap + 1) <= 256, CONFIG, "batch x (drafts + 1) must be <= 256 tokens per step");
         s->ctx_cap = capacity + 16;
         s->max_steps = e.max_new_tokens + 2;
-        s->cache.reset(create_cache(m, s->B, capacity, e.mode == 1 ? PADDED : UNPAD));
+        s->cache.reset(create_cache(m, s->B, capacity, e.mode == 1 || e.mode == 3 ? PADDED : UNPAD));
         int B = s->B;
         s->ctx = ialloc(s, (size_t)B * s->ctx_cap);
         s->ctx_len = ialloc(s, B);
@@ -457,6 +459,7 @@ int session_run(sd_session* s, int use_graph, int graph_steps, float* gpu_ms) {
 int session_run_host(sd_session* s, float* gpu_ms, int64_t* h2d_bytes, int64_t* d2h_bytes) {
     SD_CHECK(s->prefilled, CONTRACT, "session has not been prefilled");
     SD_CHECK(s->e.predictor != 0, CONFIG, "the host-driven loop runs the retrieval / synthetic predictors");
+    SD_CHECK(s->e.mode <= 2, CONFIG, "the ablation modes run in the device-resident loop only");
     cudaStream_t st = s->model->st;
     set_device(s->model->m.device);
     const int B = s->B;

@@ -6,6 +6,11 @@ namespace sdb {
 
 struct StepArgs {
     int B, cap, layout, stop_on_eos, acc_stride;
+    // the paper's 2x2 ablation: 0 = as the layout says
+    // (unpad: unpadded input + KV; padded: padded input + KV); 1 = unpadded
+    // input over the padded KV grid; 2 = padded input (PAD spectators) over
+    // the unpadded KV arena
+    int ablation;
     // inputs (host-driven step) ----------------------------------------------
     const int32_t* last;     // [B] tokens.back(); null in device mode (read from ctx)
     int32_t* counts;         // [B] draft counts k_s (written by the device predictor)

@@ -34,6 +34,9 @@ __global__ void k_pack(StepArgs a) {
     pdl_trigger();
     pdl_wait();
     const int B = a.B;
+    // padded input rows (1 + k_max per sample)?  The layout's own choice unless
+    // an ablation mode decouples input padding from KV padding.
+    const bool pad_in = a.layout == PADDED ? a.ablation != 1 : a.ablation == 2;
     if (threadIdx.x == 0) {
         int t = 0, d = 0, kmax = 0;
         for (int s = 0; s < B; ++s)
@@ -44,19 +47,15 @@ __global__ void k_pack(StepArgs a) {
             d += a.active[s] ? a.counts[s] : 0;
             a.first_row[s] = t;
             if (!a.active[s]) continue;
-            if (a.layout == PADDED) {
-                if (base < 0) base = a.committed[s];
-                t += 1 + kmax;
-            } else {
-                t += 1 + a.counts[s];
-            }
+            if (a.layout == PADDED && base < 0) base = a.committed[s];
+            t += 1 + (pad_in ? kmax : a.counts[s]);
         }
         // Capacity guard for the device-resident loop (the host-driven step
         // checks on the host first): never write past a sample's extent.
         bool over = false;
         for (int s = 0; s < B; ++s) {
             if (!a.active[s]) continue;
-            int last = a.layout == PADDED ? base + kmax : a.committed[s] + a.counts[s];
+            int last = a.layout == PADDED ? base + kmax : a.committed[s] + (pad_in ? kmax : a.counts[s]);
             if (last >= a.cap) over = true;
         }
         if (over) {
@@ -77,8 +76,10 @@ __global__ void k_pack(StepArgs a) {
             continue;
         }
         int ks = a.counts[s], d0 = a.draft_off[s];
-        int n = a.layout == PADDED ? 1 + kmax : 1 + ks;
+        int n = pad_in ? 1 + kmax : 1 + ks;
         int kv_len = 0;
+        if (a.layout == PADDED && !pad_in)  // unpadded input over the grid: the alignment rows are holes
+            for (int o = 1 + ks; o <= kmax; ++o) a.pad[(size_t)s * a.cap + base + o] = 1;
         for (int o = 0; o < n; ++o) {
             bool real = o <= ks;
             int tok = o == 0 ? last_token(a, s) : (real ? draft_at(a, s, d0, o - 1) : 2 /* tok::kPad */);
@@ -92,7 +93,7 @@ __global__ void k_pack(StepArgs a) {
             } else {
                 p.logical_pos = a.committed[s] + o;
                 p.write_slot = p.logical_pos;
-                p.store = 1;
+                p.store = real ? 1 : 0;  // PAD spectators (ablation 2) store nothing
             }
             a.tokens[row0 + o] = tok;
             a.plans[row0 + o] = p;

@@ -435,7 +435,10 @@ class PaddedGrid(CacheArena):
 
 
 # ---------------------------------------------------------------- engine
-MODES = {"greedy": 0, "vanilla": 1, "ems": 2}
+# modes 3 / 4: the paper's 2x2 ablation, device-resident
+# sessions only -- "unpad_input": unpadded input tokens over the padded KV
+# grid; "unpad_kv": padded input (PAD spectators) over the unpadded KV arena
+MODES = {"greedy": 0, "vanilla": 1, "ems": 2, "unpad_input": 3, "unpad_kv": 4}
 PREDICTORS = {"draft": 0, "retrieval": 1, "synthetic": 2}
 
 

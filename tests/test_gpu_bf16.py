@@ -215,3 +215,35 @@ def test_device_draft_loop(sd, self_draft):
     assert taus == (lt[:steps][act] & 0xFFFF).tolist()
     if self_draft:  # the draft is the target: every draft is accepted
         assert steps == -(-(new - 1) // (k + 1))
+
+
+@pytest.mark.gpu
+def test_ablation_modes_match_their_parents(sd):
+    """The paper's 2x2 ablation in the device loop:
+    "unpad_kv" (PAD-spectator input over the unpadded arena) emits the EMS
+    streams and step records -- spectators neither store KV nor change any
+    real token's computation; "unpad_input" (no PAD input rows over the padded
+    grid) emits the vanilla streams and records -- the alignment rows it no
+    longer computes were holes there anyway."""
+    cfg = dict(num_layers=2, num_heads=4, head_dim=128, vocab_size=700, max_positions=512, init_seed=0xAB1A)
+    rng = np.random.default_rng(21)
+    B, new = 5, 36
+    base = rng.integers(3, 700, size=10).tolist()
+    prompts = [[0] + (base * 8)[: int(rng.integers(30, 70))] for _ in range(B)]
+    m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.BF16)
+    out = {}
+    for mode in ("ems", "unpad_kv", "vanilla", "unpad_input"):
+        e = sd.EngineConfig(mode=mode, predictor="retrieval", k=5, copy_len=5, batch_size=B, max_new_tokens=new,
+                            stop_on_eos=False, seed=3)
+        s = sd.Session(m, e, 512)
+        s.prefill(prompts)
+        steps, _ = s.run()
+        toks, lk, lt = s.outputs()
+        out[mode] = (toks, lk[:steps].copy(), lt[:steps].copy())
+        s.close()
+    for child, parent in (("unpad_kv", "ems"), ("unpad_input", "vanilla")):
+        assert out[child][0] == out[parent][0], child
+        assert (out[child][1] == out[parent][1]).all() and (out[child][2] == out[parent][2]).all(), child
+    assert max(int(x) for x in (out["ems"][2] & 0xFFFF).ravel()) > 1  # drafts were accepted
+    g = sd.decode(sd.EngineConfig(mode="greedy", batch_size=B, max_new_tokens=new, stop_on_eos=False), m, prompts)
+    assert g.generated_tokens == out["unpad_kv"][0]  # lossless
