@@ -475,6 +475,7 @@ class DecodeResult:
     padding_kv_writes: int
     prefill_seconds: float
     decode_seconds: float
+    prompt_lens: list = None
 
 
 def tokenize_prompt(text: str) -> list[int]:
@@ -504,7 +505,7 @@ def decode(config: EngineConfig, target: Model, prompts, draft: Model | None = N
     tokens = [gen[s * mx: s * mx + cnt[s]].tolist() for s in range(b)]
     rows = rec[: nrec.value * 6].reshape(-1, 6)
     return DecodeResult(tokens, step_records(rows), int(ledger[0]), int(ledger[1]), float(timing[0]),
-                        float(timing[1]))
+                        float(timing[1]), [len(p) for p in toks])
 
 
 def step_records(rows: np.ndarray) -> list[dict]:
@@ -514,12 +515,81 @@ def step_records(rows: np.ndarray) -> list[dict]:
         r = rows[rows[:, 0] == step]
         ks, taus = r[:, 2].tolist(), r[:, 3].tolist()
         kmax, tmax = max(ks), max(taus)
+        delta_bar = tmax - sum(taus) / len(taus)
         out.append(dict(
             samples=[dict(sample=int(x[1]), k=int(x[2]), input_padding=kmax - int(x[2]), tau=int(x[3]),
                           kv_padding=tmax - int(x[3]), clipped=bool(x[4])) for x in r],
             tau_max=tmax,
+            delta_bar=delta_bar,
+            r_bar=delta_bar / tmax,
         ))
     return out
+
+
+def detokenize_text(tokens) -> str:
+    """text_without_specials + tok::detokenize (engine.cpp:148-155): byte
+    tokens to bytes, specials dropped; ids outside the byte vocabulary (large
+    synthetic vocabularies) and invalid UTF-8 become U+FFFD, as the
+    reference's JSON dump does with error_handler_t::replace."""
+    out = bytearray()
+    for t in tokens:
+        if t in (BOS, EOS, PAD):
+            continue
+        out += bytes([t - BYTE_OFFSET]) if BYTE_OFFSET <= t < VOCAB_SIZE else "\ufffd".encode()
+    return out.decode("utf-8", errors="replace")
+
+
+def results_json(config: EngineConfig, result: DecodeResult) -> str:
+    """The reference's report (results_json, engine.cpp:531-587): config,
+    outputs (tokens + text), RunMetrics (engine.cpp:107-126, 255-287,
+    486-527), per-step records and the per-step write ledger
+    (WriteLedger::dump_json, kv_cache.cpp:53-62), same keys and meaning."""
+    import json
+
+    b = config.batch_size
+    gen = [len(t) for t in result.generated_tokens]
+    plens = result.prompt_lens or [0] * b
+    steps = result.steps
+    total_gen = sum(gen)
+    if config.mode == "greedy":
+        decode_steps = max(gen) - 1 if gen else 0
+        avg_tau, avg_r, in_pad, kv_pad = 1.0, 0.0, 0, 0
+        real = sum(p + g - 1 for p, g in zip(plens, gen))
+        pad_proc = 0
+        ledger = []
+    else:
+        decode_steps = len(steps)
+        taus = [x["tau"] for st in steps for x in st["samples"]]
+        avg_tau = sum(taus) / len(taus) if taus else 0.0
+        avg_r = sum(st["r_bar"] for st in steps) / len(steps) if steps else 0.0
+        in_pad = sum(x["input_padding"] for st in steps for x in st["samples"])
+        kv_pad = sum(x["kv_padding"] for st in steps for x in st["samples"])
+        real = sum(plens) + sum(1 + x["k"] for st in steps for x in st["samples"])
+        pad_proc = in_pad + kv_pad if config.mode == "vanilla" else 0
+        ledger = [dict(tau_list=[x["tau"] for x in st["samples"]], tau_max=st["tau_max"],
+                       pad_writes=sum(x["kv_padding"] for x in st["samples"]) if config.mode == "vanilla" else 0,
+                       useful_writes=sum(1 + x["k"] for x in st["samples"])) for st in steps]
+    wall = result.prefill_seconds + result.decode_seconds
+    out = {
+        "config": {"mode": config.mode, "predictor": config.predictor, "k": config.k, "match_len": config.match_len,
+                   "copy_len": config.copy_len, "batch_size": b, "max_new_tokens": config.max_new_tokens,
+                   "stop_on_eos": bool(config.stop_on_eos), "seed": config.seed,
+                   "synthetic_accuracy": config.synthetic_accuracy},
+        "outputs": [{"tokens": list(map(int, t)), "text": detokenize_text(t)} for t in result.generated_tokens],
+        "metrics": {"decode_steps": decode_steps, "tokens_generated": gen, "total_tokens_generated": total_gen,
+                    "avg_acceptance_length": avg_tau, "avg_padding_ratio": avg_r,
+                    "total_input_padding": in_pad, "total_kv_padding": kv_pad,
+                    "useful_kv_writes": result.useful_kv_writes, "padding_kv_writes": result.padding_kv_writes,
+                    "real_tokens_processed": real, "pad_tokens_processed": pad_proc,
+                    "total_tokens_processed": real + pad_proc,
+                    "prefill_seconds": result.prefill_seconds, "decode_seconds": result.decode_seconds,
+                    "tokens_per_second_decode": total_gen / result.decode_seconds if result.decode_seconds > 0 else 0.0,
+                    "tokens_per_second_total": total_gen / wall if wall > 0 else 0.0},
+        "steps": [{"samples": st["samples"], "tau_max": st["tau_max"], "delta_bar": st["delta_bar"],
+                   "r_bar": st["r_bar"]} for st in steps],
+        "ledger": ledger,
+    }
+    return json.dumps(out, indent=2, ensure_ascii=False)
 
 
 # ---------------------------------------------------------------- sessions

@@ -321,3 +321,25 @@ def test_gpu_random_verify_steps_match_oracle(sd, oracle, layout):
     assert np.array_equal(np.array(flat, np.int32).reshape(-1, 5), rec_o[:, :5])
     assert [r.useful_kv_writes, r.padding_kv_writes] == led_o.tolist()
     oracle.model_free(mo)
+
+
+@pytest.mark.parametrize("mode", ["greedy", "vanilla", "ems"])
+def test_gpu_results_json_matches_reference(sd, mode):
+    """specdec.results_json of a GPU decode (fp32 check mode) equals the
+    REFERENCE's own report (results_json, engine.cpp:531-587, fixture made by
+    tests/golden/make_results_json.py from oracle/_ref) key for key, minus the
+    wall-clock fields: outputs and texts, RunMetrics, step records and the
+    per-step write ledger."""
+    import json
+
+    fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", f"results_json_retrieval_{mode}.json")))
+    e = fx["engine"]
+    m = sd.Model.init(sd.ModelConfig(**fx["model"]))
+    cfg = sd.EngineConfig(mode=mode, predictor="retrieval", k=e["k"], match_len=e["match_len"],
+                          copy_len=e["copy_len"], batch_size=e["batch_size"], max_new_tokens=e["max_new_tokens"],
+                          stop_on_eos=bool(e["stop_on_eos"]), seed=e["seed"],
+                          synthetic_accuracy=e["synthetic_accuracy"])
+    got = json.loads(sd.results_json(cfg, sd.decode(cfg, m, fx["prompts"])))
+    for k in ("prefill_seconds", "decode_seconds", "tokens_per_second_decode", "tokens_per_second_total"):
+        got["metrics"].pop(k)
+    assert got == fx["results"]
