@@ -24,6 +24,27 @@ def split_ids(global_batch: int, world: int, rank: int) -> list[int]:
     return list(range(start, start + base + (1 if rank < extra else 0)))
 
 
+def split_ids_by_length(prompt_lens: list[int], world: int, rank: int) -> list[int]:
+    """Strong scaling balanced by prompt length: contiguous
+    blocks (rank order stays global sample order, so the end-of-run gather
+    needs no permutation) whose prompt-token totals are as even as the
+    boundaries allow -- rank r's block ends where the prefix sum first reaches
+    (r + 1) / world of the total, and every rank keeps at least one sample
+    while there are enough."""
+    n = len(prompt_lens)
+    cum = np.cumsum(np.asarray(prompt_lens, dtype=np.int64))
+    total = int(cum[-1]) if n else 0
+    bounds = [0]
+    for r in range(1, world):
+        target = total * r / world
+        b = int(np.searchsorted(cum, target, side="left")) + 1  # first prefix reaching the target
+        b = max(b, bounds[-1] + (1 if n - bounds[-1] > world - r else 0))
+        b = min(b, n - (world - r) if n >= world else n)
+        bounds.append(max(b, bounds[-1]))
+    bounds.append(n)
+    return list(range(bounds[rank], bounds[rank + 1]))
+
+
 def pad_tokens(seqs: list[list[int]], width: int) -> np.ndarray:
     out = np.full((len(seqs), width), -1, dtype=np.int32)
     for i, s in enumerate(seqs):

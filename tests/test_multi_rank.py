@@ -6,6 +6,7 @@ oracle; on GPUs the same sharding drives libspecdec_b200 over NCCL."""
 import os
 import socket
 
+import numpy as np
 import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -69,3 +70,20 @@ def test_sharded_decode_equals_single_process(strong):
     e = P.engine_config(mode=2, predictor=1, copy_len=4, batch_size=6, max_new_tokens=20, stop_on_eos=0)
     toks, _, _ = o.decode(e, m, prompts)
     assert gathered == toks
+
+
+def test_split_by_prompt_length_is_contiguous_and_balanced():
+    """contiguous blocks in global order, prompt-token totals
+    within one prompt of the ideal share."""
+    from paper_2405_07542_b200.sharding import split_ids_by_length
+
+    rng = np.random.default_rng(5)
+    for n, world in ((64, 8), (24, 4), (10, 3), (3, 4)):
+        lens = rng.integers(3968, 4225, size=n).tolist() if n > 10 else rng.integers(1, 100, size=n).tolist()
+        parts = [split_ids_by_length(lens, world, r) for r in range(world)]
+        assert sum(parts, []) == list(range(n))  # a partition, in global order
+        tot = sum(lens)
+        for p in parts:
+            if n >= world:
+                assert p, "every rank gets a sample"
+            assert abs(sum(lens[i] for i in p) - tot / world) <= max(lens) + 1
