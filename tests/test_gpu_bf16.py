@@ -247,3 +247,27 @@ def test_ablation_modes_match_their_parents(sd):
     assert max(int(x) for x in (out["ems"][2] & 0xFFFF).ravel()) > 1  # drafts were accepted
     g = sd.decode(sd.EngineConfig(mode="greedy", batch_size=B, max_new_tokens=new, stop_on_eos=False), m, prompts)
     assert g.generated_tokens == out["unpad_kv"][0]  # lossless
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["bf16", "check"])
+def test_batch_composition_invariance(sd, precision):
+    """test_engine.cpp:307-320 on the GPU path: a sample's EMS stream does not
+    depend on which other samples share its batch (the property that lets
+    samples shard across GPUs with no collective)."""
+    cfg = dict(num_layers=2, num_heads=4, head_dim=64 if precision == "check" else 128, vocab_size=600,
+               max_positions=512, init_seed=0xBA7C)
+    rng = np.random.default_rng(8)
+    base = rng.integers(3, 600, size=9).tolist()
+    prompts = [[0] + (base * 9)[: int(rng.integers(20, 60))] for _ in range(6)]
+    m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.BF16 if precision == "bf16" else sd.FP32_CHECK)
+
+    def run(ps):
+        e = sd.EngineConfig(mode="ems", predictor="retrieval", k=5, copy_len=5, batch_size=len(ps),
+                            max_new_tokens=30, stop_on_eos=False)
+        return sd.decode(e, m, ps).generated_tokens
+
+    whole = run(prompts)
+    parts = run(prompts[:2]) + run(prompts[2:3]) + run(prompts[3:])
+    assert parts == whole
+    assert run(prompts[::-1]) == whole[::-1]
