@@ -108,3 +108,15 @@ def test_no_cpu_fallback_without_gpu(sd):
     with pytest.raises(sd.SpecdecError) as e:
         sd.Model.init(sd.ModelConfig())
     assert "no CUDA device" in str(e.value) or "sm_100a" in str(e.value)
+
+
+def test_table1_scripted_trace_step_records(sd):
+    """acceptance.cpp:110-188 (the paper's Table 1): predictions (5,2) with
+    acceptances (4,1), then (2,5) with (2,6) -> input pads (0,3),(3,0) and KV
+    pads (0,3),(4,0) in the step records."""
+    rows = np.array([[0, 0, 5, 4, 0, 0], [0, 1, 2, 1, 0, 0], [1, 0, 2, 2, 0, 0], [1, 1, 5, 6, 0, 0]])
+    st = sd.step_records(rows)
+    assert [x["input_padding"] for x in st[0]["samples"]] == [0, 3]
+    assert [x["input_padding"] for x in st[1]["samples"]] == [3, 0]
+    assert [x["kv_padding"] for x in st[0]["samples"]] == [0, 3]
+    assert [x["kv_padding"] for x in st[1]["samples"]] == [4, 0]

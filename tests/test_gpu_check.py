@@ -343,3 +343,46 @@ def test_gpu_results_json_matches_reference(sd, mode):
     for k in ("prefill_seconds", "decode_seconds", "tokens_per_second_decode", "tokens_per_second_total"):
         got["metrics"].pop(k)
     assert got == fx["results"]
+
+
+def test_gpu_table1_scripted_trace_ledgers(sd):
+    """The same script driven through the device arenas (KV rows written by
+    forward_planned, commits through the C ABI): the aligned grid writes 3 + 4
+    PAD filler rows, the unpadded arena none (acceptance.cpp:125-176)."""
+    m = sd.Model.init(sd.ModelConfig())
+
+    def stage(cache, sample, start, count, logical0=None):
+        lp0 = start if logical0 is None else logical0
+        plans = [sd.TokenPlan(sample=sample, logical_pos=lp0 + i, write_slot=start + i, store=True)
+                 for i in range(count)]
+        m.forward_planned([5] * count, plans, cache, want_logits=False)
+
+    grid = sd.PaddedGrid(m, 2, 32)
+    stage(grid, 0, 0, 1)
+    stage(grid, 1, 0, 1)
+    grid.commit_prefill([0, 1], [1, 1])
+    stage(grid, 0, 1, 6)
+    stage(grid, 1, 1, 3)
+    grid.commit_padded([0, 1], [4, 1])
+    assert grid.ledger()[1] == 3
+    stage(grid, 0, 5, 3, logical0=5)
+    stage(grid, 1, 5, 6, logical0=2)
+    grid.commit_padded([0, 1], [2, 6])
+    assert grid.ledger()[1] == 3 + 4
+    assert [grid.committed_len(s) for s in (0, 1)] == [11, 11]
+
+    arena = sd.UnpadArena(m, 2, 32)
+    stage(arena, 0, 0, 1)
+    stage(arena, 1, 0, 1)
+    arena.commit_accepted(0, 1)
+    arena.commit_accepted(1, 1)
+    stage(arena, 0, 1, 6)
+    stage(arena, 1, 1, 3)
+    arena.commit_accepted(0, 4)
+    arena.commit_accepted(1, 1)
+    stage(arena, 0, 5, 3)
+    stage(arena, 1, 2, 6)
+    arena.commit_accepted(0, 2)
+    arena.commit_accepted(1, 6)
+    assert arena.ledger()[1] == 0
+    assert [arena.committed_len(s) for s in (0, 1)] == [7, 8]
