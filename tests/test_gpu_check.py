@@ -386,3 +386,21 @@ def test_gpu_table1_scripted_trace_ledgers(sd):
     arena.commit_accepted(1, 6)
     assert arena.ledger()[1] == 0
     assert [arena.committed_len(s) for s in (0, 1)] == [7, 8]
+
+
+def test_gpu_write_gap_is_the_padding_shortfall(sd):
+    """test_engine.cpp:216-239 on the GPU engine: the vanilla run writes exactly
+    the EMS run's useful KV rows plus one filler row per unit of tau_max - tau."""
+    m = sd.Model.init(sd.ModelConfig(num_layers=2, num_heads=2, head_dim=8, vocab_size=259, max_positions=160,
+                                     init_seed=0xACC7))
+    prompts = ["The quick brown fox", "jumps over", "the lazy dog.", "Again!"]
+    cfg = dict(predictor="synthetic", k=4, batch_size=4, max_new_tokens=31, seed=40, synthetic_accuracy=0.6,
+               stop_on_eos=False)
+    van = sd.decode(sd.EngineConfig(mode="vanilla", **cfg), m, prompts)
+    ems = sd.decode(sd.EngineConfig(mode="ems", **cfg), m, prompts)
+    shortfall = sum(st["tau_max"] - x["tau"] for st in van.steps for x in st["samples"])
+    assert shortfall > 0
+    assert van.generated_tokens == ems.generated_tokens
+    assert van.useful_kv_writes == ems.useful_kv_writes
+    assert ems.padding_kv_writes == 0 and van.padding_kv_writes == shortfall
+    assert sum(x["kv_padding"] for st in van.steps for x in st["samples"]) == shortfall
