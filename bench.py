@@ -550,8 +550,15 @@ def main():
         ems_acc_all, pad_acc_all = c.tolist()
         # gather per-sample outputs (the run's only collective, NCCL over NVLink)
         sharding.gather_outputs(ems.outputs()[0], a.max_new, dist, device=cdev)
+        # the padded grid aligns per shard (tau_max over the LOCAL batch): per-GPU stats
+        ps = torch.tensor([pad_stats["avg_padding_ratio"], float(pad_stats["padding_kv_writes"])], device=cdev,
+                          dtype=torch.float64)
+        parts = [torch.zeros_like(ps) for _ in range(world)]
+        dist.all_gather(parts, ps)
+        pad_per_gpu = [[round(float(x[0]), 4), int(x[1])] for x in parts]
     else:
         ems_ms_max, pad_ms_max, ems_acc_all, pad_acc_all = ems_ms, pad_ms, ems_acc, pad_acc
+        pad_per_gpu = [[round(float(pad_stats["avg_padding_ratio"]), 4), int(pad_stats["padding_kv_writes"])]]
     value = ems_acc_all / (ems_ms_max / 1000.0)
     padded_value = pad_acc_all / (pad_ms_max / 1000.0)
 
@@ -677,7 +684,8 @@ def main():
                    "l2": f"inputs exceed L2 ({m.weight_bytes() / 1e9:.2f} GB weights + KV streamed every step)"},
         "padded": {"value": round(padded_value, 2), "ms_per_step": round(pad_ms_max / a.steps, 3),
                    "avg_padding_ratio": pad_stats["avg_padding_ratio"],
-                   "padding_kv_writes": pad_stats["padding_kv_writes"], "verify_steps": pad_steps / a.steps},
+                   "padding_kv_writes": pad_stats["padding_kv_writes"], "verify_steps": pad_steps / a.steps,
+                   "per_gpu_padding_ratio_and_writes": pad_per_gpu},
         "ems_vs_padded": round(value / padded_value, 4),
         "ems": {"avg_acceptance_length": ems_stats["avg_tau"], "verify_steps": ems_steps / a.steps,
                 "ms_per_verify_step": round(ems_ms_max / max(1, ems_steps), 3),
