@@ -86,6 +86,30 @@ int main() {
     std::printf("batched_commit_rejected %d %d %d %d\n", rc, com[0], com[1], com[2]);
     std::printf("start_offset %d\n", arena.start_offset(2));
 
+    // the aligned layout through the same header: acceptance.cpp:125-147's
+    // scripted trace (PAD filler rows 3 + 4)
+    {
+        PaddedGrid grid(cfg.num_layers, 2, 32, cfg.hidden());
+        auto stage = [&](int sample, int row, int count, int logical) {
+            std::vector<TokenId> toks(count, 5);
+            std::vector<TokenPlan> plans;
+            for (int i = 0; i < count; ++i) plans.push_back(TokenPlan{sample, logical + i, row + i, true});
+            m.forward_planned(toks, plans, grid);
+        };
+        stage(0, 0, 1, 0);
+        stage(1, 0, 1, 0);
+        grid.commit_prefill({0, 1}, {1, 1});
+        stage(0, 1, 6, 1);
+        stage(1, 1, 3, 1);
+        grid.commit_padded({0, 1}, {4, 1});
+        const long long after1 = grid.padding_writes();
+        stage(0, 5, 3, 5);
+        stage(1, 5, 6, 2);
+        grid.commit_padded({0, 1}, {2, 6});
+        std::printf("grid_padding %lld %lld %d %d %d\n", after1, (long long)grid.padding_writes(),
+                    grid.committed_len(0), grid.logical_len(1), grid.is_pad(1, 2) ? 1 : 0);
+    }
+
     // error taxonomy: the reference's exception types come back
     try {
         ragged::restore_indices({1, 2}, 3);

@@ -92,3 +92,6 @@ def test_cpp_layer_matches_oracle(tmp_path, oracle):
     assert tail["lengths"] == committed + [str(s * cap) for s in range(B)]
     assert tail["batched_commit_rejected"] == ["3"] + committed  # SD_CONTRACT, nothing mutated
     assert "config_error_ok" in tail and "commit_error_ok" in tail
+    # PaddedGrid through the header: filler rows 3 then 3 + 4, rows advance by tau_max, sample 1's
+    # logical length by its own taus, and its first-step shortfall rows are pad rows
+    assert tail["grid_padding"] == ["3", "7", "11", str(1 + 1 + 6), "1"]
