@@ -26,13 +26,13 @@ def build_cpp(tmp_path):
     return exe
 
 
-def test_cpp_layer_compiles_and_links(tmp_path):
+def test_cpp_layer_compiles_and_links(sd, tmp_path):  # sd: the library is built and loads
     exe = build_cpp(tmp_path)
     assert os.path.getsize(exe) > 0
 
 
 @pytest.mark.gpu
-def test_cpp_layer_matches_oracle(tmp_path, oracle):
+def test_cpp_layer_matches_oracle(sd, tmp_path, oracle):
     exe = build_cpp(tmp_path)
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
