@@ -16,6 +16,9 @@ if "--lib" in args:  # A/B against another build of the library
     i = args.index("--lib")
     sd.LIB_PATH = os.path.abspath(args[i + 1])
     del args[i:i + 2]
+eager = "--eager" in args  # launch-by-launch instead of the CUDA-graph replay
+if eager:
+    args.remove("--eager")
 B = int(args[0]) if args else 24
 cfg = bench.C3
 m = sd.Model.init(sd.ModelConfig(**cfg), device=0, precision=sd.BF16)
@@ -28,8 +31,8 @@ s.prefill(prompts)
 best = 1e9
 for _ in range(4):
     s.reset()
-    steps, ms = s.run()
+    steps, ms = s.run(use_graph=not eager)
     best = min(best, ms / steps)
 env = " ".join([f"{k}={v}" for k, v in os.environ.items() if k.startswith("SD_")] +
-               ([os.path.relpath(sd.LIB_PATH, ROOT)] if "--lib" in sys.argv else []))
+               ([os.path.relpath(sd.LIB_PATH, ROOT)] if "--lib" in sys.argv else []) + (["eager"] if eager else []))
 print(f"[{env or 'default'}] B={B}: {steps} steps, best {best:.3f} ms/step", flush=True)
