@@ -60,6 +60,11 @@ typedef struct {
     int32_t mode, predictor, k, match_len, copy_len, batch_size, max_new_tokens, stop_on_eos;
     uint64_t seed;
     double synthetic_accuracy;
+    /* global id of local sample 0: a rank holding samples [base, base + B) of
+     * a sharded batch seeds the synthetic predictor with the GLOBAL sample id,
+     * mix_seed(seed, step, base + s) (engine.cpp:182-185), so its drafts and
+     * step records equal the single-process run's */
+    int32_t sample_id_base;
 } sd_engine_config;
 
 typedef struct sd_model sd_model;

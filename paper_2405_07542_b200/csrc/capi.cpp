@@ -19,6 +19,29 @@ void note_launches(int64_t n) { g_launches += n; }
 
 void set_device(int device) { CUDA_OK(cudaSetDevice(device)); }
 
+int device_sm_count() {
+    static std::mutex mu;
+    static std::vector<int> sms;
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    if ((int)sms.size() <= dev) sms.resize(dev + 1, 0);
+    if (!sms[dev]) CUDA_OK(cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev));
+    return sms[dev];
+}
+
+bool first_use_on_device(int key) {
+    static std::mutex mu;
+    static std::vector<std::pair<int, int>> seen;
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& p : seen)
+        if (p.first == dev && p.second == key) return false;
+    seen.emplace_back(dev, key);
+    return true;
+}
+
 bool pdl_enabled() {
     static int on = -1;
     if (on < 0) {
@@ -334,6 +357,9 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
     const Config& cfg = m.cfg;
     const int B = c.B;
     set_device(m.device);
+    // the cache must have been created for this model (model.cpp:273-276)
+    SD_CHECK(c.model == &m && c.heads * c.hd == cfg.hidden(), CONTRACT, "cache width does not match the model");
+    SD_CHECK(c.L == cfg.num_layers, CONTRACT, "cache depth does not match the model");
     // host validation (engine.cpp:427-444 / 408-426 and the forward contracts)
     int kmax = 0, nact = 0, ndraft = 0, base = -1;
     for (int s = 0; s < B; ++s) {
@@ -430,7 +456,7 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
     const int T_up = B * K1;
     const bool graphable = m.precision != FP32_CHECK && !logits && T_up <= 256 && !profile_on() &&
                            getenv_int("SD_VERIFY_GRAPH", 1) != 0;
-    const void* key[4] = {ds, h->ws.d_tokens, h->ws.fast, (const void*)(intptr_t)T_up};
+    const void* key[5] = {ds, h->ws.d_tokens, h->ws.fast, (const void*)(intptr_t)T_up, (const void*)&m};
     const int flags = (stop_on_eos ? 1 : 0) | (c.layout == PADDED ? 2 : 0);
     bool replay = false;
     if (graphable && h->vg_calls++ > 0) {
@@ -788,14 +814,26 @@ int sd_cache_commit_padded(sd_cache* h, const int32_t* samples, const int32_t* t
         }
         set_device(h->model->m.device);
         cudaStream_t st = h->model->st;
+        // the filler rows of every sample and layer in ONE launch (kv_cache.cpp:295-307)
+        std::vector<int32_t> rows(2 * (size_t)n);
+        for (int i = 0; i < n; ++i) {
+            rows[i] = samples[i];
+            rows[n + i] = base + taus[i];
+        }
+        int32_t* d = (int32_t*)dmalloc(sizeof(int32_t) * rows.size());
+        try {
+            CUDA_OK(cudaMemcpyAsync(d, rows.data(), sizeof(int32_t) * rows.size(), cudaMemcpyHostToDevice, st));
+            launch_zero_rows(c, d, d + n, n, base + tmax, st);
+            note_launches(1);
+            CUDA_OK(cudaStreamSynchronize(st));
+        } catch (...) {
+            dfree(d);
+            throw;
+        }
+        dfree(d);
         for (int i = 0; i < n; ++i) {
             int s = samples[i];
             for (int r = base + taus[i]; r < base + tmax; ++r) {
-                for (int l = 0; l < c.L; ++l)
-                    for (int w = 0; w < 2; ++w)
-                        for (int hd = 0; hd < c.heads; ++hd)
-                            CUDA_OK(cudaMemsetAsync((char*)c.kv + c.kv_offset(l, w, s, hd, r) * c.elem_bytes, 0,
-                                                    (size_t)c.hd * c.elem_bytes, st));
                 c.pad[(size_t)s * c.cap + r] = 1;
                 c.padding += 1;
             }
@@ -803,7 +841,6 @@ int sd_cache_commit_padded(sd_cache* h, const int32_t* samples, const int32_t* t
             c.logical[s] += taus[i];
             c.staged[s] = c.committed[s];
         }
-        CUDA_OK(cudaStreamSynchronize(st));
     });
 }
 

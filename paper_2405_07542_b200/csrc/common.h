@@ -172,4 +172,11 @@ void forward_check(const Model& m, Cache& c, Workspace& ws, int T, bool want_log
 void* dmalloc(size_t bytes);
 void dfree(void* p);
 
+// Per-device facts and one-time setup.  Kernel attributes
+// (cudaFuncSetAttribute) and the SM count belong to a device, so they are
+// keyed on the CURRENT device, never cached process-wide.
+int device_sm_count();
+// true exactly once per (current device, key): the caller then runs the setup
+bool first_use_on_device(int key);
+
 }  // namespace sdb

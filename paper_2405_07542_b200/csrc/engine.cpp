@@ -94,7 +94,7 @@ struct Decoder {
         SD_CHECK(e.synthetic_accuracy >= 0.0 && e.synthetic_accuracy < 1.0, CONFIG,
                  "predictor accuracy must lie in [0, 1)");
         std::vector<int32_t> d = draft_predict(target, target_scratch, st.tokens, e.k);  // predictors.cpp:61-72
-        uint64_t rs = mix_seed(e.seed, (uint64_t)step, (uint64_t)s);
+        uint64_t rs = mix_seed(e.seed, (uint64_t)step, (uint64_t)(e.sample_id_base + s));
         int V = target->m.cfg.vocab_size;
         for (int32_t& t : d) {
             double u = (double)(splitmix_next(rs) >> 11) * 0x1.0p-53;

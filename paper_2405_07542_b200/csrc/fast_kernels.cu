@@ -26,9 +26,7 @@ SD_TRACE_TU(fast)
 namespace sdb {
 
 constexpr int kChunkTokens = 256;  // tokens per forward chunk (GEMM N <= 256)
-constexpr int kSplit = 128;        // attention keys per CTA (4 warps x 32)
-constexpr int kQT = 8;             // queries per attention CTA (the mma N side)
-constexpr int kSms = 148;          // B200 SM count (stream-K GEMM grid)
+constexpr int kQT = 8;             // queries per attention item (the S^T MMA's N)
 
 struct FastModelState {
     std::vector<GemmMaps> qkv, o, fc, proj;  // per layer (A map only used)
@@ -36,12 +34,10 @@ struct FastModelState {
 };
 
 struct FastWorkspace {
-    int cap_tokens = 0, B = 0, cap = 0, max_splits = 0;
+    int cap_tokens = 0, B = 0, cap = 0;
     __nv_bfloat16 *xb = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr;
-    float* part_o = nullptr;   // [T][heads][max_splits][hd]
-    float* part_ml = nullptr;  // [T][heads][max_splits][2]
     float* part = nullptr;     // stream-K partial sums (largest GEMM of the model)
-    int* attn_cnt = nullptr;   // split-KV arrival counters [B * heads * 16]
+    ArgmaxScratch am;          // LM-head (max, id) partials per token + arrival counters
     GemmMaps map_xb, map_ctx, map_act;
     CUtensorMap kv_map;        // TMA view of the KV arena [L*2*B*heads*cap][hd], box {64, 128}
     CUtensorMap kv_map64;      // ... with box {64, 64} (attention tail chunks)
@@ -137,43 +133,6 @@ __global__ void __launch_bounds__(kRowThreads) k_embed_ln(const __nv_bfloat16* _
 }
 
 // ------------------------------------------------------------- attention
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-                 "l"(src), "r"(valid ? 16 : 0));
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                 : "r"(addr));
-}
-__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-    return *reinterpret_cast<uint32_t*>(&v);
-}
-
-// smem tile [rows][HD] bf16 with the 16-byte chunk index XOR-swizzled by row%8
-template <int HD>
-__device__ __forceinline__ uint32_t swz(int row, int col) {  // byte offset of element (row, col)
-    constexpr int kChunks = HD / 8;
-    int chunk = (col >> 3) ^ (row & 7);
-    return (uint32_t)(row * kChunks + chunk) * 16 + (col & 7) * 2;
-}
-
 struct AttnArgs {
     const __nv_bfloat16* q;    // [T][h]
     const __nv_bfloat16* kv;   // arena
@@ -182,372 +141,13 @@ struct AttnArgs {
     const int32_t* qidx;
     const uint8_t* pad;        // padded grid flags or null
     __nv_bfloat16* ctx;        // [T][h]
-    float* part_o;
-    float* part_ml;
-    int* cnt;                  // [B * heads * q_tiles] split arrival counters (self-resetting)
-    int* work;                 // persistent kernel: this launch's item counter (zeroed per forward)
-    int pre_ok;                // persistent kernel: may read segs before griddepcontrol.wait (see producer)
-    int h, heads, B, cap, layer, max_splits;
+    int* work;                 // this launch's item counter (zeroed per forward)
+    int pre_ok;                // may read segs before griddepcontrol.wait (see producer)
+    int h, heads, B, cap, layer;
     float scale_log2;          // log2(e) / sqrt(hd)
 };
 
-// Ragged multi-query attention, "keys as M" formulation.
-//
-// One CTA = (sample, head) x 128-key split x 8-query tile; 4 warps each own 32
-// keys.  With only n_s <= 8 draft queries per sample, the tensor-core tile is
-// transposed so the KEYS are the 16-row M side and the queries the 8-wide N
-// side of mma.sync m16n8k16:  S^T = K Q^T  and  O^T += V^T P^T.  P^T is
-// re-laid from the S^T accumulator fragments with movmatrix (no smem trip),
-// the softmax reduces over keys with 3 shuffles, and the O^T accumulators are
-// 32 registers per thread.  This halves the MMA count of a 16-query tile and
-// keeps register pressure low enough for several CTAs per SM.  The 4 warps'
-// (max, sum, O) states merge through smem; splits merge in k_attn_combine.
-// A sample's K/V extent is read once per split, not once per query token (the
-// paper's per-token grid, re-reads it n_s times).
-__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
-    uint32_t y;
-    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
-    return y;
-}
-
-template <int HD>
-__global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
-    CtaTrace trace__(TK_ATTN);
-    pdl_trigger();
-    pdl_wait();
-    constexpr int kKeys = kSplit / 4;  // keys per warp (32)
-    const int sh = blockIdx.x, split = blockIdx.y, qt = blockIdx.z;
-    const int s = sh / a.heads, head = sh % a.heads;
-    const SampleSeg seg = a.segs[s];
-    const int k_begin = split * kSplit;
-    if (seg.n_q == 0 || qt * kQT >= seg.n_q || k_begin >= seg.kv_len) return;
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int nq = min(kQT, seg.n_q - qt * kQT);
-
-    extern __shared__ __align__(128) uint8_t sm[];
-    uint8_t* sQ = sm;                                    // [8][HD]
-    uint8_t* sK = sm + kQT * HD * 2 + warp * 2 * kKeys * HD * 2;
-    uint8_t* sV = sK + kKeys * HD * 2;
-    float* sMerge = (float*)(sm + kQT * HD * 2);         // reused: [4][8][HD] + [4][8][2]
-    __shared__ int sWslot[kQT];
-    __shared__ int sTok[kQT];
-
-    const int kw0 = k_begin + warp * kKeys;
-    const size_t kbase = ((((size_t)a.layer * 2 + 0) * a.B + s) * a.heads + head) * (size_t)a.cap * HD;
-    const size_t vbase = ((((size_t)a.layer * 2 + 1) * a.B + s) * a.heads + head) * (size_t)a.cap * HD;
-    const int kv_end = min(seg.kv_len, k_begin + kSplit);
-    for (int i = lane; i < kKeys * HD / 8; i += 32) {  // this warp's K / V rows (zero past the extent)
-        const int r = i / (HD / 8), c8 = i % (HD / 8);
-        const int key = kw0 + r;
-        const bool ok = key < kv_end;
-        const size_t off = (size_t)(ok ? key : 0) * HD + c8 * 8;
-        cp_async16(sK + swz<HD>(r, c8 * 8), a.kv + kbase + off, ok);
-        cp_async16(sV + swz<HD>(r, c8 * 8), a.kv + vbase + off, ok);
-    }
-    for (int i = threadIdx.x; i < kQT * HD / 8; i += 128) {  // Q tile (rows >= nq zero)
-        const int r = i / (HD / 8), c8 = i % (HD / 8);
-        const int tok = r < nq ? a.qidx[seg.q_start + qt * kQT + r] : 0;
-        cp_async16(sQ + swz<HD>(r, c8 * 8), a.q + (size_t)tok * a.h + head * HD + c8 * 8, r < nq);
-    }
-    if (threadIdx.x < kQT) {
-        const int r = threadIdx.x;
-        const int tok = r < nq ? a.qidx[seg.q_start + qt * kQT + r] : -1;
-        sTok[r] = tok;
-        sWslot[r] = tok >= 0 ? a.plans[tok].write_slot : -1;
-    }
-    cp_async_wait_all();
-    __syncthreads();
-
-    const int g = lane / 4, c = lane % 4;
-    // running softmax state for this thread's two query columns q = 2c, 2c+1
-    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
-    float o[HD / 16][4];  // O^T fragments: (hd d0+g / d0+g+8) x (q 2c, 2c+1)
-#pragma unroll
-    for (int n = 0; n < HD / 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.0f;
-
-    if (kw0 < kv_end) {
-        const uint32_t qa = (uint32_t)__cvta_generic_to_shared(sQ);
-        const uint32_t ka = (uint32_t)__cvta_generic_to_shared(sK);
-        const uint32_t va = (uint32_t)__cvta_generic_to_shared(sV);
-        // S^T = K Q^T : (kKeys keys) x (8 queries), as kKeys/16 m-tiles
-        float st[kKeys / 16][4];
-#pragma unroll
-        for (int t = 0; t < kKeys / 16; ++t) st[t][0] = st[t][1] = st[t][2] = st[t][3] = 0.0f;
-#pragma unroll
-        for (int kk = 0; kk < HD; kk += 32) {
-            // B = Q^T for two k-steps: matrices (q 0-7, hd kk), (kk+8), (kk+16), (kk+24)
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4(qa + swz<HD>(lane % 8, kk + (lane / 8) * 8), b0, b1, b2, b3);
-#pragma unroll
-            for (int t = 0; t < kKeys / 16; ++t) {
-                uint32_t a0, a1, a2, a3, e0, e1, e2, e3;
-                // A = K rows t*16.. : (keys 0-7, kk), (keys 8-15, kk), (keys 0-7, kk+8), (keys 8-15, kk+8)
-                ldsm_x4(ka + swz<HD>(t * 16 + (lane % 16), kk + (lane / 16) * 8), a0, a1, a2, a3);
-                ldsm_x4(ka + swz<HD>(t * 16 + (lane % 16), kk + 16 + (lane / 16) * 8), e0, e1, e2, e3);
-                mma_bf16(st[t], a0, a1, a2, a3, b0, b1);
-                mma_bf16(st[t], e0, e1, e2, e3, b2, b3);
-            }
-        }
-        // mask + max over this warp's keys for each query column
-        const int ws[2] = {sWslot[2 * c], sWslot[2 * c + 1]};
-        float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-        for (int t = 0; t < kKeys / 16; ++t) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int key = kw0 + t * 16 + g + (e >= 2 ? 8 : 0);
-                const int qi = e & 1;
-                const bool vis = key < kv_end && key <= ws[qi] && !(a.pad && a.pad[(size_t)s * a.cap + key]);
-                const float x = vis ? st[t][e] * a.scale_log2 : -INFINITY;
-                st[t][e] = x;
-                mx[qi] = fmaxf(mx[qi], x);
-            }
-        }
-#pragma unroll
-        for (int qi = 0; qi < 2; ++qi) {
-            mx[qi] = fmaxf(mx[qi], __shfl_xor_sync(0xffffffffu, mx[qi], 4));
-            mx[qi] = fmaxf(mx[qi], __shfl_xor_sync(0xffffffffu, mx[qi], 8));
-            mx[qi] = fmaxf(mx[qi], __shfl_xor_sync(0xffffffffu, mx[qi], 16));
-            m_run[qi] = mx[qi];
-        }
-        float sum[2] = {0.0f, 0.0f};
-        uint32_t pb[kKeys / 16][2];  // P^T as mma B fragments (keys 2c.. / 2c+8.., q g)
-#pragma unroll
-        for (int t = 0; t < kKeys / 16; ++t) {
-            const float p0 = m_run[0] == -INFINITY ? 0.0f : exp2f(st[t][0] - m_run[0]);
-            const float p1 = m_run[1] == -INFINITY ? 0.0f : exp2f(st[t][1] - m_run[1]);
-            const float p2 = m_run[0] == -INFINITY ? 0.0f : exp2f(st[t][2] - m_run[0]);
-            const float p3 = m_run[1] == -INFINITY ? 0.0f : exp2f(st[t][3] - m_run[1]);
-            sum[0] += p0 + p2;
-            sum[1] += p1 + p3;
-            pb[t][0] = movmatrix_t(pack_bf16(p0, p1));  // rows = keys 0-7 of the tile
-            pb[t][1] = movmatrix_t(pack_bf16(p2, p3));  // rows = keys 8-15
-        }
-#pragma unroll
-        for (int qi = 0; qi < 2; ++qi) {
-            sum[qi] += __shfl_xor_sync(0xffffffffu, sum[qi], 4);
-            sum[qi] += __shfl_xor_sync(0xffffffffu, sum[qi], 8);
-            sum[qi] += __shfl_xor_sync(0xffffffffu, sum[qi], 16);
-            l_run[qi] = sum[qi];
-        }
-        // O^T += V^T P^T : per 16 keys (k-step) and 16 hd rows (m-tile)
-#pragma unroll
-        for (int t = 0; t < kKeys / 16; ++t) {
-#pragma unroll
-            for (int n = 0; n < HD / 16; ++n) {
-                uint32_t a0, a1, a2, a3;
-                // A = V^T (hd x keys): trans of V blocks (keys t*16+[0,8)/[8,16), hd n*16+[0,8)/[8,16))
-                const int key = t * 16 + (lane % 8) + ((lane / 16) * 8);
-                const int col = n * 16 + ((lane / 8) % 2) * 8;
-                ldsm_x4_t(va + swz<HD>(key, col), a0, a1, a2, a3);
-                mma_bf16(o[n], a0, a1, a2, a3, pb[t][0], pb[t][1]);
-            }
-        }
-    }
-    __syncthreads();  // every warp is done with K / V: reuse the area for the merge
-    float* mO = sMerge + (size_t)warp * kQT * HD;   // [q][hd]
-    float* mML = sMerge + 4 * kQT * HD + warp * 2 * kQT;
-#pragma unroll
-    for (int n = 0; n < HD / 16; ++n) {
-        mO[(2 * c) * HD + n * 16 + g] = o[n][0];
-        mO[(2 * c + 1) * HD + n * 16 + g] = o[n][1];
-        mO[(2 * c) * HD + n * 16 + g + 8] = o[n][2];
-        mO[(2 * c + 1) * HD + n * 16 + g + 8] = o[n][3];
-    }
-    if (g == 0) {
-        mML[(2 * c) * 2] = m_run[0];
-        mML[(2 * c) * 2 + 1] = l_run[0];
-        mML[(2 * c + 1) * 2] = m_run[1];
-        mML[(2 * c + 1) * 2 + 1] = l_run[1];
-    }
-    __syncthreads();
-    const int nsplit = (seg.kv_len + kSplit - 1) / kSplit;
-    for (int i = threadIdx.x; i < kQT * HD; i += 128) {
-        const int r = i / HD, d = i % HD;
-        if (r >= nq) continue;
-        float M = -INFINITY;
-        for (int w = 0; w < 4; ++w) M = fmaxf(M, sMerge[4 * kQT * HD + w * 2 * kQT + r * 2]);
-        float L = 0.0f, O = 0.0f;
-        for (int w = 0; w < 4; ++w) {
-            const float mw = sMerge[4 * kQT * HD + w * 2 * kQT + r * 2];
-            if (mw == -INFINITY) continue;
-            const float f = exp2f(mw - M);
-            L += sMerge[4 * kQT * HD + w * 2 * kQT + r * 2 + 1] * f;
-            O += sMerge[(size_t)w * kQT * HD + r * HD + d] * f;
-        }
-        const int tok = sTok[r];
-        if (nsplit == 1) {
-            a.ctx[(size_t)tok * a.h + head * HD + d] = __float2bfloat16_rn(O / L);
-        } else {
-            const size_t base = ((size_t)tok * a.heads + head) * a.max_splits + split;
-            a.part_o[base * HD + d] = O;
-            if (d == 0) {
-                a.part_ml[base * 2] = M;
-                a.part_ml[base * 2 + 1] = L;
-            }
-        }
-    }
-}
-
-// Same work decomposition as k_attention, math on the 5th-generation tensor
-// cores (HD = 128).  K and V arrive by TMA (128-byte swizzle); one thread
-// issues tcgen05.mma with the accumulators in TMEM (32 columns per CTA):
-//   S^T = K Q^T   : M = 128 keys, N = 8 queries, K = 128 (A = K tile,
-//                   K-major; B = the Q rows, K-major)
-//   O^T = V^T P^T : M = 128 (hd), N = 8 queries, K = 128 keys (A = the SAME
-//                   V tile read MN-major: no transpose pass; B = P^T written
-//                   by the softmax threads in the swizzled K-major layout)
-// Thread = key for the softmax (one tcgen05.ld of its 8 scores), thread = hd
-// row for the output.  Split partials merge in k_attn_combine as before.
-constexpr int kTcKeys = 128;
-constexpr int kTcSmem = 1024 + 4 * kTcKeys * 128 + 2 * 8 * 128 * 2 + 8 * kTcKeys * 4;
-__global__ void __launch_bounds__(128) k_attention_tc(const __grid_constant__ CUtensorMap tm_kv, AttnArgs a) {
-    CtaTrace trace__(TK_ATTN);
-    constexpr int HD = 128;
-    pdl_trigger();
-    const int sh = blockIdx.x, split = blockIdx.y, qt = blockIdx.z;
-    const int s = sh / a.heads, head = sh % a.heads;
-    const int warp = threadIdx.x / 32, tid = threadIdx.x;
-    extern __shared__ uint8_t smraw[];
-    uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
-    uint8_t* sK = sm;                          // 2 boxes [128 keys][64 hd] SW128
-    uint8_t* sV = sK + 2 * kTcKeys * 128;      // same
-    uint8_t* sQ = sV + 2 * kTcKeys * 128;      // 2 atoms [8 q][64 hd] SW128 (K-major B)
-    uint8_t* sP = sQ + 2 * 8 * 128;            // 2 atoms [8 q][64 keys] SW128 (K-major B)
-    float* sS = (float*)(sP + 2 * 8 * 128);    // [8 q][128 keys]
-    __shared__ uint64_t bar_load, bar_mma;
-    __shared__ uint32_t tslot;
-    __shared__ float sM[kQT], sL[kQT];
-    __shared__ int sTok[kQT], sWs[kQT];
-
-    pdl_wait();
-    const SampleSeg seg = a.segs[s];
-    const int k_begin = split * kTcKeys;
-    if (seg.n_q == 0 || qt * kQT >= seg.n_q || k_begin >= seg.kv_len) return;
-    const int nq = min(kQT, seg.n_q - qt * kQT);
-    const int kv_end = min(seg.kv_len, k_begin + kTcKeys);
-    if (warp == 0) ptx::tmem_alloc32(&tslot);
-    if (tid == 0) {
-        ptx::mbar_init(&bar_load, 1);
-        ptx::mbar_init(&bar_mma, 1);
-        ptx::fence_barrier_init();
-    }
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem = tslot;
-    const int row_k = (((a.layer * 2 + 0) * a.B + s) * a.heads + head) * a.cap + k_begin;
-    const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap + k_begin;
-    if (tid == 0) {  // K / V tiles: keys past the extent are masked below
-        const uint64_t pol = ptx::policy_evict_first();
-        ptx::mbar_arrive_expect_tx(&bar_load, 4 * kTcKeys * 128);
-        ptx::tma_load_2d(sK, &tm_kv, &bar_load, 0, row_k, pol);
-        ptx::tma_load_2d(sK + kTcKeys * 128, &tm_kv, &bar_load, 64, row_k, pol);
-        ptx::tma_load_2d(sV, &tm_kv, &bar_load, 0, row_v, pol);
-        ptx::tma_load_2d(sV + kTcKeys * 128, &tm_kv, &bar_load, 64, row_v, pol);
-    }
-    {  // Q rows -> swizzled K-major B tile (rows past nq repeat row 0: unused columns)
-        const int r = tid / 16, c8 = tid % 16;
-        const int tok = a.qidx[seg.q_start + qt * kQT + (r < nq ? r : 0)];
-        const uint4 v = *(const uint4*)(a.q + (size_t)tok * a.h + head * HD + c8 * 8);
-        *(uint4*)(sQ + (c8 / 8) * 1024 + r * 128 + (((c8 % 8) ^ (r & 7)) << 4)) = v;
-        if (tid < kQT) {
-            const int t2 = tid < nq ? a.qidx[seg.q_start + qt * kQT + tid] : -1;
-            sTok[tid] = t2;
-            sWs[tid] = t2 >= 0 ? a.plans[t2].write_slot : -1;
-        }
-    }
-    ptx::fence_proxy_async_smem();  // generic smem writes (Q) -> visible to the tensor core
-    __syncthreads();
-    if (tid == 0) {
-        ptx::mbar_wait(&bar_load, 0);
-        ptx::tc_fence_after();
-        const uint32_t idesc = ptx::umma_idesc_bf16(kTcKeys, kQT);
-        const uint32_t ka = ptx::smem_u32(sK), qa = ptx::smem_u32(sQ);
-#pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-            ptx::umma_bf16(tmem, ptx::umma_desc_kmajor_sw128(ka + (k / 4) * (kTcKeys * 128) + (k % 4) * 32),
-                           ptx::umma_desc_kmajor_sw128(qa + (k / 4) * 1024 + (k % 4) * 32), idesc, k > 0 ? 1u : 0u);
-        ptx::umma_commit(&bar_mma);
-    }
-    ptx::mbar_wait(&bar_mma, 0);
-    ptx::tc_fence_after();
-    // ---- softmax over this split's keys: thread = key
-    const int key = k_begin + tid;
-    float x[kQT];
-    ptx::tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16), x);
-    const bool in_ext = key < kv_end && !(a.pad && a.pad[(size_t)s * a.cap + key]);
-#pragma unroll
-    for (int q = 0; q < kQT; ++q) {
-        x[q] = (in_ext && key <= sWs[q]) ? x[q] * a.scale_log2 : -INFINITY;
-        sS[q * kTcKeys + tid] = x[q];
-    }
-    __syncthreads();
-    {  // per-query max: 16 threads per query, 8 keys each
-        const int q = tid / 16, part = tid % 16;
-        float m = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) m = fmaxf(m, sS[q * kTcKeys + part * 8 + i]);
-#pragma unroll
-        for (int o = 1; o < 16; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (part == 0) sM[q] = m;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kQT; ++q) {
-        const float p = (x[q] == -INFINITY) ? 0.0f : exp2f(x[q] - sM[q]);
-        sS[q * kTcKeys + tid] = p;
-        // P^T [q][key], K-major SW128: atom = key / 64, 16-byte chunk = (key % 64) / 8 ^ (q % 8)
-        *(__nv_bfloat16*)(sP + (tid / 64) * 1024 + q * 128 + ((((tid % 64) / 8) ^ (q & 7)) << 4) + (tid % 8) * 2) =
-            __float2bfloat16_rn(p);
-    }
-    ptx::fence_proxy_async_smem();
-    __syncthreads();
-    {  // per-query sum
-        const int q = tid / 16, part = tid % 16;
-        float l = 0.0f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) l += sS[q * kTcKeys + part * 8 + i];
-#pragma unroll
-        for (int o = 1; o < 16; o <<= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-        if (part == 0) sL[q] = l;
-    }
-    if (tid == 0) {
-        ptx::tc_fence_after();
-        const uint32_t idesc = ptx::umma_idesc_bf16_amn(HD, kQT);
-        const uint32_t va = ptx::smem_u32(sV), pa = ptx::smem_u32(sP);
-#pragma unroll
-        for (int k = 0; k < kTcKeys / 16; ++k)  // 16 keys per step: V rows k*16.., P^T columns k*16..
-            ptx::umma_bf16(tmem + 16, ptx::umma_desc_mn_sw128(va + k * 16 * 128, kTcKeys * 128, 1024),
-                           ptx::umma_desc_kmajor_sw128(pa + (k / 4) * 1024 + (k % 4) * 32), idesc, k > 0 ? 1u : 0u);
-        ptx::umma_commit(&bar_mma);
-    }
-    ptx::mbar_wait(&bar_mma, 1);
-    ptx::tc_fence_after();
-    __syncthreads();  // sL complete
-    float o[kQT];  // thread = hd row d
-    ptx::tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + 16, o);
-    const int d = tid;
-    const int nsplit = (seg.kv_len + kTcKeys - 1) / kTcKeys;
-#pragma unroll
-    for (int q = 0; q < kQT; ++q) {
-        if (q >= nq) break;
-        const int tok = sTok[q];
-        if (nsplit == 1) {
-            a.ctx[(size_t)tok * a.h + head * HD + d] = __float2bfloat16_rn(o[q] / sL[q]);
-        } else {
-            const size_t base = ((size_t)tok * a.heads + head) * a.max_splits + split;
-            a.part_o[base * HD + d] = o[q];
-            if (d == 0) {
-                a.part_ml[base * 2] = sM[q];
-                a.part_ml[base * 2 + 1] = sL[q];
-            }
-        }
-    }
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == 0) ptx::tmem_dealloc32(tmem);
-}
+constexpr int kTcKeys = 128;  // keys per K/V chunk (the S^T MMA's M)
 
 // Persistent tcgen05 attention (HD = 128): one CTA per SM walks (sample,
 // head, 8-query tile) items from an atomic counter; each item streams the
@@ -942,30 +542,6 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
     if (warp == 5) ptx::tmem_dealloc32(tmem);
 }
 
-// merge split-KV partials: grid (T, heads), block HD
-__global__ void k_attn_combine(AttnArgs a, int hd, const int* __restrict__ dT) {
-    CtaTrace trace__(TK_ATTN_COMBINE);
-    pdl_trigger();
-    pdl_wait();
-    int t = blockIdx.x, head = blockIdx.y, d = threadIdx.x;
-    if (t >= *dT) return;
-    int s = a.plans[t].sample;
-    int nsplit = (a.segs[s].kv_len + kSplit - 1) / kSplit;
-    if (nsplit <= 1) return;
-    size_t base = ((size_t)t * a.heads + head) * a.max_splits;
-    float M = -INFINITY;
-    for (int k = 0; k < nsplit; ++k) M = fmaxf(M, a.part_ml[(base + k) * 2]);
-    float L = 0.0f, O = 0.0f;
-    for (int k = 0; k < nsplit; ++k) {
-        float mk = a.part_ml[(base + k) * 2];
-        if (mk == -INFINITY) continue;
-        float f = exp2f(mk - M);
-        L += a.part_ml[(base + k) * 2 + 1] * f;
-        O += a.part_o[(base + k) * hd + d] * f;
-    }
-    a.ctx[(size_t)t * a.h + head * hd + d] = __float2bfloat16_rn(O / L);
-}
-
 template <typename T>
 T* walloc(FastWorkspace* f, size_t n) {
     T* p = (T*)dmalloc(sizeof(T) * (n ? n : 1));
@@ -975,8 +551,7 @@ T* walloc(FastWorkspace* f, size_t n) {
 
 FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     FastWorkspace* f = ws.fast;
-    int max_splits = (c.cap + kSplit - 1) / kSplit;
-    if (f && f->B >= c.B && f->cap >= c.cap && f->max_splits >= max_splits) return f;
+    if (f && f->B >= c.B && f->cap >= c.cap) return f;
     free_fast_workspace(f);
     f = new FastWorkspace();
     const Config& cfg = m.cfg;
@@ -984,21 +559,20 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     f->cap_tokens = (int)T;
     f->B = c.B;
     f->cap = c.cap;
-    f->max_splits = max_splits;
     f->xb = walloc<__nv_bfloat16>(f, T * h);
     f->q = walloc<__nv_bfloat16>(f, T * h);
     f->ctx = walloc<__nv_bfloat16>(f, T * h);
     f->act = walloc<__nv_bfloat16>(f, T * mm);
-    f->part_o = walloc<float>(f, T * cfg.num_heads * max_splits * cfg.head_dim);
-    f->part_ml = walloc<float>(f, T * cfg.num_heads * max_splits * 2);
     size_t part = 0;
     for (auto mk : {std::make_pair((int)(3 * h), (int)h), std::make_pair((int)h, (int)h),
                     std::make_pair((int)mm, (int)h), std::make_pair((int)h, (int)mm),
                     std::make_pair(m.vocab_pad, (int)h)})
-        part = std::max(part, gemm_part_floats(mk.first, mk.second, kSms));
+        part = std::max(part, gemm_part_floats(mk.first, mk.second, device_sm_count()));
     f->part = walloc<float>(f, part);
-    f->attn_cnt = walloc<int>(f, (size_t)c.B * cfg.num_heads * 16);
-    CUDA_OK(cudaMemset(f->attn_cnt, 0, sizeof(int) * (size_t)c.B * cfg.num_heads * 16));
+    f->am.val = walloc<float>(f, (size_t)T * kArgmaxGroups);
+    f->am.idx = walloc<int>(f, (size_t)T * kArgmaxGroups);
+    f->am.cnt = walloc<int>(f, T);
+    CUDA_OK(cudaMemset(f->am.cnt, 0, sizeof(int) * T));  // self-resetting afterwards
     make_b_maps(f->map_xb, f->xb, T, h);
     make_b_maps(f->map_ctx, f->ctx, T, h);
     make_b_maps(f->map_act, f->act, T, mm);
@@ -1018,7 +592,7 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
 // launching stream and charge it the ALGORITHMIC bytes it must move
 // (weights + activations + KV it reads/writes once).  bench.py reads this
 // to report the dominant kernel's achieved bandwidth.
-enum ProfKind { PK_QKV, PK_O, PK_FC, PK_PROJ, PK_LM, PK_ATTN, PK_ROW, PK_MISC, PK_COMBINE, PK_N };
+enum ProfKind { PK_QKV, PK_O, PK_FC, PK_PROJ, PK_LM, PK_ATTN, PK_ROW, PK_MISC, PK_N };
 struct ProfRec {
     int kind;
     cudaEvent_t a, b;
@@ -1053,27 +627,13 @@ void profile_read(double* out, int kinds) {
         for (int j = 0; j < 3; ++j) out[k * 3 + j] = g_prof_acc[k][j];
 }
 
-// One-time kernel attributes (must run before any CUDA-graph capture).
-static int device_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        CUDA_OK(cudaGetDevice(&dev));
-        CUDA_OK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-    }
-    return n;
-}
-
+// Kernel attributes are per device: set once on each device, before any
+// CUDA-graph capture on it.
 void prepare_fast_kernels() {
-    static bool done = false;
-    if (done) return;
-    CUDA_OK(cudaFuncSetAttribute(k_attention<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CUDA_OK(cudaFuncSetAttribute(k_attention<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CUDA_OK(cudaFuncSetAttribute(k_attention_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+    if (!first_use_on_device(1)) return;
     CUDA_OK(cudaFuncSetAttribute(k_attention_tcp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
     CUDA_OK(cudaFuncSetAttribute(k_attention_tcp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmemB<64>));
     gemm_prepare();
-    done = true;
 }
 
 // Forward over a device-described batch of <= 256 tokens: tokens / plans in
@@ -1119,18 +679,13 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     at.qidx = db.qidx;
     at.pad = c.layout == PADDED ? c.d_pad : nullptr;
     at.ctx = f->ctx;
-    at.part_o = f->part_o;
-    at.part_ml = f->part_ml;
-    at.cnt = f->attn_cnt;
     at.h = h;
     at.heads = heads;
     at.B = c.B;
     at.cap = c.cap;
-    at.max_splits = f->max_splits;
     at.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-    const int splits = std::max(1, (db.max_kv_upper + kSplit - 1) / kSplit);
     const int qtiles = std::max(1, (db.max_q_upper + kQT - 1) / kQT);
-    const size_t attn_smem = (size_t)kQT * hd * 2 + (size_t)4 * 2 * (kSplit / 4) * hd * 2;
+    const int sms = device_sm_count();
 
     for (int l = 0; l < cfg.num_layers; ++l) {
         const FastLayer& L = m.layers[l];
@@ -1143,34 +698,21 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         g.bias = L.bqkv;
         g.out_bf16 = f->q;
         g.layer = l;
-        gemm_plan(g, kSms);
+        gemm_plan(g, sms);
         GemmMaps mp = f->map_xb;
         mp.A = fm->qkv[l].A;
         PROF(PK_QKV, gemm_launch(EPI_QKV, g, mp, n, st));
         // attention
         at.layer = l;
-        static const int aimpl = getenv("SD_ATTN_IMPL") ? atoi(getenv("SD_ATTN_IMPL")) : 4;
         at.work = f->attn_work + l;
-        const bool tcp = (hd == 128 || hd == 64) && aimpl == 4;
-        at.pre_ok = g.grid == device_sms() ? 1 : 0;  // the QKV GEMM above held every SM
-        if (tcp && hd == 128)
-            PROF(PK_ATTN, launch_k(k_attention_tcp<128>, dim3(std::min(c.B * heads * qtiles, kSms)), dim3(kPThreads),
+        at.pre_ok = g.grid == sms ? 1 : 0;  // the QKV GEMM above held every SM
+        if (hd == 128)
+            PROF(PK_ATTN, launch_k(k_attention_tcp<128>, dim3(std::min(c.B * heads * qtiles, sms)), dim3(kPThreads),
                                    kPSmem, st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
-        else if (tcp)
-            PROF(PK_ATTN, launch_k(k_attention_tcp<64>, dim3(std::min(c.B * heads * qtiles, 2 * kSms)),
-                                   dim3(kPThreads), kPSmemB<64>, st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
-        else if (hd == 128 && aimpl == 3)
-            PROF(PK_ATTN, launch_k(k_attention_tc, dim3(c.B * heads, splits, qtiles), dim3(128), kTcSmem, st, f->kv_map,
-                                   at));
-        else if (hd == 128)
-            PROF(PK_ATTN, launch_k(k_attention<128>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
         else
-            PROF(PK_ATTN, launch_k(k_attention<64>, dim3(c.B * heads, splits, qtiles), dim3(128), attn_smem, st, at));
+            PROF(PK_ATTN, launch_k(k_attention_tcp<64>, dim3(std::min(c.B * heads * qtiles, 2 * sms)),
+                                   dim3(kPThreads), kPSmemB<64>, st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
         launches++;
-        if (splits > 1 && !tcp) {  // the persistent kernel writes final rows
-            PROF(PK_COMBINE, launch_k(k_attn_combine, dim3(n, heads), dim3(hd), 0, st, at, hd, (const int*)db.dT));
-            launches++;
-        }
         // O projection + residual, fused with LN2 -> xb
         g = base;
         g.M = h;
@@ -1182,7 +724,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         g.ln_g = L.ln2_g;
         g.ln_b = L.ln2_b;
         g.ln_out = f->xb;
-        gemm_plan(g, kSms);
+        gemm_plan(g, sms);
         mp = f->map_ctx;
         mp.A = fm->o[l].A;
         PROF(PK_O, gemm_launch(EPI_RESID_LN, g, mp, n, st));
@@ -1194,7 +736,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         g.bias = L.bfc;
         g.out_bf16 = f->act;
         g.ld_out = mm;
-        gemm_plan(g, kSms);
+        gemm_plan(g, sms);
         mp = f->map_xb;
         mp.A = fm->fc[l].A;
         PROF(PK_FC, gemm_launch(EPI_GELU, g, mp, n, st));
@@ -1209,7 +751,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         g.ln_g = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_g : m.lnf_g;
         g.ln_b = l + 1 < cfg.num_layers ? m.layers[l + 1].ln1_b : m.lnf_b;
         g.ln_out = f->xb;
-        gemm_plan(g, kSms);
+        gemm_plan(g, sms);
         mp = f->map_act;
         mp.A = fm->proj[l].A;
         PROF(PK_PROJ, gemm_launch(EPI_RESID_LN, g, mp, n, st));
@@ -1224,7 +766,8 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     g.argmax = ws.d_argmax + t0;
     g.logits = want_logits ? ws.d_logits + (size_t)t0 * cfg.vocab_size : nullptr;
     g.flag = ws.d_flag;
-    gemm_plan(g, kSms);
+    g.am = f->am;
+    gemm_plan(g, sms);
     GemmMaps mp = f->map_xb;
     mp.A = m.fast->lm.A;
     PROF(PK_LM, gemm_launch(EPI_ARGMAX, g, mp, n, st));
@@ -1247,9 +790,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
                               V * H * 2 + Tt * H * 2,
                               kv * 2 * hd * 2 * heads + Tt * H * 4,
                               Tt * H * 6,
-                              0,
-                              // split partials read (max_splits upper bound) + context written
-                              Tt * heads * f->max_splits * (hd + 2) * 4.0 + Tt * H * 2};
+                              0};
         for (auto& r : g_prof_pending) {
             float ms = 0.0f;
             CUDA_OK(cudaEventElapsedTime(&ms, r.a, r.b));

@@ -16,15 +16,22 @@ enum Epilogue {
     EPI_ARGMAX = 4,   // argmax over the vocab (lowest id on ties) -> argmax[t]
 };
 
+// LM-head argmax scratch: per (token, vocab group) (max, lowest id) partials
+// and a self-resetting arrival counter per token.  Owned by the forward's
+// workspace (one per cache), never shared between streams or devices.
+constexpr int kArgmaxGroups = 64;
+struct ArgmaxScratch {
+    float* val = nullptr;  // [256][kArgmaxGroups]
+    int* idx = nullptr;    // [256][kArgmaxGroups]
+    int* cnt = nullptr;    // [256]
+};
+
 struct GemmArgs {
     int M, K, m_tiles;        // W is [m_tiles * 256][K] bf16 (zero-padded rows)
     int T;                    // token count when dT == nullptr (must be <= 256)
     const int* dT;            // device token count (graph-capturable), or nullptr
     int grid, max_contrib;    // stream-K schedule (set by gemm_plan)
     int box;                  // token-tile rows staged per k-block (set by gemm_launch)
-    int dbg;                  // probe only: bit0 skip MMAs, bit1 skip partial stores
-    int a_tiled;              // 1: W tile-major [m_tile][K/64][256][64] (TMA); 2: same, pre-swizzled (bulk copy)
-    const void* a_ptr;        // a_tiled == 2: base of the pre-swizzled tiles
     float* part;              // fp32 partial sums [m_tiles * max_contrib][256 tok][256 rows]
     const float* bias;        // [M] or nullptr
     float* out_f32;           // EPI_STORE output / EPI_RESID_LN residual stream
@@ -41,6 +48,7 @@ struct GemmArgs {
     int32_t* argmax;
     float* logits;            // optional [T][vocab]
     int* flag;                // non-finite flag
+    ArgmaxScratch am;
 };
 
 struct GemmMaps {

@@ -128,12 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(&emptyA[stage], phase ^ 1);
                 uint8_t* sa = a_base + stage * kABytes;
                 ptx::mbar_arrive_expect_tx(&fullA[stage], kABytes);
-                if (a.a_tiled == 2)  // pre-swizzled contiguous 32 KB tile: one bulk copy
-                    ptx::bulk_load(sa, (const uint8_t*)a.a_ptr + (size_t)u * kABytes, kABytes, &fullA[stage], pol_w);
-                else if (a.a_tiled)
-                    ptx::tma_load_2d(sa, &tmA, &fullA[stage], 0, (int)(u * kBM), pol_w);
-                else
-                    ptx::tma_load_2d(sa, &tmA, &fullA[stage], (int)(u % KB) * kBK, (int)(u / KB) * kBM, pol_w);
+                ptx::tma_load_2d(sa, &tmA, &fullA[stage], (int)(u % KB) * kBK, (int)(u / KB) * kBM, pol_w);
                 if (++stage == SA) {
                     stage = 0;
                     phase ^= 1;
@@ -187,16 +182,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ptx::tc_fence_after();
                             uint32_t sa = ptx::smem_u32(a_base + sa_i * kABytes);
                             uint32_t sb = ptx::smem_u32(b_base + sb_i * b_bytes);
-                            if (!(a.dbg & 1)) {
 #pragma unroll
-                                for (int k = 0; k < kBK / 16; ++k) {
-                                    uint64_t bdesc = ptx::umma_desc_kmajor_sw128(sb + k * 32);
+                            for (int k = 0; k < kBK / 16; ++k) {
+                                uint64_t bdesc = ptx::umma_desc_kmajor_sw128(sb + k * 32);
 #pragma unroll
-                                    for (int acc = 0; acc < 2; ++acc) {
-                                        uint64_t adesc = ptx::umma_desc_kmajor_sw128(sa + acc * (128 * 128) + k * 32);
-                                        ptx::umma_bf16(d0 + acc * (nbuf == 2 ? 128 : 256), adesc, bdesc, idesc,
-                                                       (kb > kb0 || k > 0) ? 1u : 0u);
-                                    }
+                                for (int acc = 0; acc < 2; ++acc) {
+                                    uint64_t adesc = ptx::umma_desc_kmajor_sw128(sa + acc * (128 * 128) + k * 32);
+                                    ptx::umma_bf16(d0 + acc * (nbuf == 2 ? 128 : 256), adesc, bdesc, idesc,
+                                                   (kb > kb0 || k > 0) ? 1u : 0u);
                                 }
                             }
                             ptx::umma_commit(&emptyB[sb_i]);
@@ -235,10 +228,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j0 = 0; j0 < BN; j0 += 16) {
                         float v[16];
                         ptx::tmem_ld16(trow + acc * (nbuf == 2 ? 128 : 256) + j0, v);
-                        if (!(a.dbg & 2)) {
 #pragma unroll
-                            for (int i = 0; i < 16; ++i) ptx::st_f32_hint(dcol + (size_t)(j0 + i) * 256, v[i], pol_keep);
-                        }
+                        for (int i = 0; i < 16; ++i) ptx::st_f32_hint(dcol + (size_t)(j0 + i) * 256, v[i], pol_keep);
                     }
                 }
                 ptx::tc_fence_before();
@@ -576,20 +567,14 @@ size_t gemm_part_floats(int M, int K, int sms) {
 }
 
 void gemm_prepare() {
-    CUDA_OK(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    if (first_use_on_device(2))
+        CUDA_OK(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
 }
 
 void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, cudaStream_t st) {
-    static bool prepared = false;
-    if (!prepared) {
-        gemm_prepare();
-        prepared = true;
-    }
+    gemm_prepare();
     SD_CHECK(T_upper <= 256, INTERNAL, "GEMM token tile is at most 256");
     GemmArgs ab = a;
-    // tools/energy_probe.py: SD_GEMM_DBG bit0 skips the MMAs, bit1 the partial stores (garbage results)
-    static const int dbg_env = getenv("SD_GEMM_DBG") ? atoi(getenv("SD_GEMM_DBG")) : 0;
-    ab.dbg |= dbg_env;
     ab.box = T_upper <= 32 ? 32 : T_upper <= 64 ? 64 : T_upper <= 128 ? 128 : 256;
     launch_k(k_gemm, dim3(a.grid), dim3(kThreads), kSmemBytes, st, maps.A, maps.B[0], maps.B[1], maps.B[2],
              maps.B[3], ab);
@@ -605,17 +590,11 @@ void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, 
             launch_k(k_ln_rows, dim3(T_upper), dim3(256), 0, st, ab);
             break;
         case EPI_ARGMAX: {
-            static float* pv = nullptr;
-            static int *pi = nullptr, *cnt = nullptr;
-            if (!pv) {  // per-process scratch for the vocab-group partials (<= 256 tokens)
-                pv = (float*)dmalloc(sizeof(float) * 256 * 64);
-                pi = (int*)dmalloc(sizeof(int) * 256 * 64);
-                cnt = (int*)dmalloc(sizeof(int) * 256);
-                CUDA_OK(cudaMemset(cnt, 0, sizeof(int) * 256));
-            }
             const int groups = (a.m_tiles + kArgTiles - 1) / kArgTiles;
-            SD_CHECK(groups <= 64, INTERNAL, "vocab too large for the argmax scratch");
-            launch_k(k_reduce_argmax, dim3((T_upper + 3) / 4, groups), dim3(256), 0, st, ab, r, pv, pi, cnt);
+            SD_CHECK(groups <= kArgmaxGroups, CONFIG, "vocab too large for the argmax scratch");
+            SD_CHECK(a.am.val && a.am.idx && a.am.cnt, INTERNAL, "argmax scratch missing");
+            launch_k(k_reduce_argmax, dim3((T_upper + 3) / 4, groups), dim3(256), 0, st, ab, r, a.am.val, a.am.idx,
+                     a.am.cnt);
             break;
         }
         case -1: break;  // probe: streaming kernel only
@@ -632,6 +611,7 @@ thread_local std::string g_dbg_err;
 }
 extern "C" int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K, int T, int grid, int flags,
                              float* Y, float* usec) {
+    // flags bit3: time the streaming kernel alone (no reduction; Y is not written)
     using namespace sdb;
     try {
         int m_tiles = (M + 255) / 256;
@@ -642,45 +622,18 @@ extern "C" int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K,
         a.K = K;
         a.m_tiles = m_tiles;
         a.T = T;
-        gemm_plan(a, grid > 0 ? grid : 148);
+        gemm_plan(a, grid > 0 ? grid : device_sm_count());
         void* dpart = dmalloc(sizeof(float) * (size_t)m_tiles * a.max_contrib * 256 * 256);
         CUDA_OK(cudaMemset(dW, 0, wbytes));
-        GemmMaps maps;
-        a.a_tiled = flags & 1;
-        a.dbg = (flags >> 1) & 3;                  // bit1 skip MMAs, bit2 skip partial stores
-        const int epi = (flags & 8) ? -1 : EPI_STORE;  // bit3: time the streaming kernel alone
-        if (flags & 16) {  // tile-major AND pre-swizzled (SW128 K-major smem image): bulk copies
-            a.a_tiled = 2;
-            int KB = K / 64;
-            std::vector<uint16_t> wt((size_t)m_tiles * 256 * K, 0);
-            for (int t = 0; t < m_tiles; ++t)
-                for (int kb = 0; kb < KB; ++kb)
-                    for (int r = 0; r < 256 && t * 256 + r < M; ++r)
-                        for (int j = 0; j < 8; ++j)
-                            std::memcpy(&wt[(((size_t)t * KB + kb) * 256 + r) * 64 + ((j ^ (r & 7)) * 8)],
-                                        &W[(size_t)(t * 256 + r) * K + kb * 64 + j * 8], 16);
-            CUDA_OK(cudaMemcpy(dW, wt.data(), wbytes, cudaMemcpyHostToDevice));
-            a.a_ptr = dW;
-            maps.A = make_tmap_2d(dW, (int64_t)m_tiles * KB * 256, 64, 256);  // unused
-        } else if (a.a_tiled) {  // tile-major weights: [m_tile][K/64][256][64]
-            int KB = K / 64;
-            std::vector<uint16_t> wt((size_t)m_tiles * 256 * K, 0);
-            for (int t = 0; t < m_tiles; ++t)
-                for (int kb = 0; kb < KB; ++kb)
-                    for (int r = 0; r < 256 && t * 256 + r < M; ++r)
-                        std::memcpy(&wt[(((size_t)t * KB + kb) * 256 + r) * 64], &W[(size_t)(t * 256 + r) * K + kb * 64],
-                                    128);
-            CUDA_OK(cudaMemcpy(dW, wt.data(), wbytes, cudaMemcpyHostToDevice));
-            maps.A = make_tmap_2d(dW, (int64_t)m_tiles * KB * 256, 64, 256);
-        } else {
-            CUDA_OK(cudaMemcpy(dW, W, (size_t)M * K * 2, cudaMemcpyHostToDevice));
-            maps.A = make_tmap_2d(dW, (int64_t)m_tiles * 256, K, 256);
-        }
+        CUDA_OK(cudaMemcpy(dW, W, (size_t)M * K * 2, cudaMemcpyHostToDevice));
         CUDA_OK(cudaMemcpy(dX, X, xbytes, cudaMemcpyHostToDevice));
+        GemmMaps maps;
+        maps.A = make_tmap_2d(dW, (int64_t)m_tiles * 256, K, 256);
         make_b_maps(maps, dX, T, K);
         a.part = (float*)dpart;
         a.out_f32 = (float*)dY;
         a.ld_out = M;
+        const int epi = (flags & 8) ? -1 : EPI_STORE;
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
@@ -692,8 +645,10 @@ extern "C" int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K,
         CUDA_OK(cudaDeviceSynchronize());
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
         if (usec) *usec = ms * 1000.0f;
-        CUDA_OK(cudaMemcpy(Y, dY, (size_t)T * M * 4, cudaMemcpyDeviceToHost));
+        if (epi == EPI_STORE) CUDA_OK(cudaMemcpy(Y, dY, (size_t)T * M * 4, cudaMemcpyDeviceToHost));
         dfree(dW);
         dfree(dX);
         dfree(dY);

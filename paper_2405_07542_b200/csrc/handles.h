@@ -26,7 +26,7 @@ struct sd_cache {
     // sd_verify_step's CUDA graph (pack -> forward -> accept with device-side
     // token counts), rebuilt when any buffer it bakes in changes
     cudaGraphExec_t vgraph = nullptr;
-    const void* vg_key[4] = {nullptr, nullptr, nullptr, nullptr};
+    const void* vg_key[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     int vg_flags = -1;
     int vg_calls = 0;
     ~sd_cache();

@@ -162,6 +162,7 @@ void device_step(sd_session* s, cudaStream_t st, unsigned long long cond = 0, bo
     p.k = s->e.k;
     p.vocab = s->model->m.cfg.vocab_size;
     p.seed = s->e.seed;
+    p.id_base = s->e.sample_id_base;
     p.accuracy = s->e.synthetic_accuracy;
     p.traj = s->traj;
     p.traj_stride = s->traj_stride;
@@ -192,7 +193,8 @@ sd_session* session_create(sd_model* m, const sd_engine_config& e, int capacity,
         SD_CHECK(draft->m.device == m->m.device, CONFIG, "draft and target must live on the same device");
         SD_CHECK(e.k >= 1, CONFIG, "draft length must be >= 1");
     }
-    SD_CHECK(e.batch_size >= 1 && e.max_new_tokens >= 1, CONFIG, "batch_size and max_new_tokens must be >= 1");
+    SD_CHECK(e.batch_size >= 1, CONFIG, "batch_size must be >= 1");  // engine.cpp:51-56
+    SD_CHECK(e.max_new_tokens >= 0, CONFIG, "max_new_tokens must be >= 0");
     auto* s = new sd_session();
     try {
         s->model = m;
@@ -249,11 +251,15 @@ void session_reset(sd_session* s) {
     CUDA_OK(cudaMemcpyAsync(c.d_logical, c.logical.data(), 4 * (size_t)B, cudaMemcpyHostToDevice, st));
     if (c.layout == PADDED)
         CUDA_OK(cudaMemcpyAsync(c.d_pad, c.pad.data(), c.pad.size(), cudaMemcpyHostToDevice, st));
-    std::vector<int32_t> len(B), gen(B, 1);
+    // after prefill the context holds prompt + the first generated token; a zero
+    // budget returns before prefill (engine.cpp:314-317): prompt only, no steps
+    const int first = s->e.max_new_tokens > 0 ? 1 : 0;
+    std::vector<int32_t> len(B), gen(B, first);
     for (int b = 0; b < B; ++b) {
-        len[b] = s->prompt_lens[b] + 1;
-        CUDA_OK(cudaMemcpyAsync(s->ctx + (size_t)b * s->ctx_cap + s->prompt_lens[b], &s->first_tok[b], 4,
-                                cudaMemcpyHostToDevice, st));
+        len[b] = s->prompt_lens[b] + first;
+        if (first)
+            CUDA_OK(cudaMemcpyAsync(s->ctx + (size_t)b * s->ctx_cap + s->prompt_lens[b], &s->first_tok[b], 4,
+                                    cudaMemcpyHostToDevice, st));
     }
     CUDA_OK(cudaMemcpyAsync(s->ctx_len, len.data(), 4 * (size_t)B, cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(s->gen, gen.data(), 4 * (size_t)B, cudaMemcpyHostToDevice, st));
@@ -290,7 +296,33 @@ void session_prefill(sd_session* s, const int32_t* prompts, const int32_t* lens)
                  "prompt plus generation budget exceeds the cache capacity");
         SD_CHECK(lens[b] + s->e.max_new_tokens + reach + 1 <= s->ctx_cap, CAPACITY, "context buffer too small");
     }
+    // the prefill may grow the workspaces (Workspace::ensure reallocates the
+    // token / plan / partial buffers), and the captured graphs bake in their
+    // pointers: drop them so the next run recaptures against the live buffers
+    if (s->graph) CUDA_OK(cudaGraphExecDestroy(s->graph));
+    if (s->loop_graph) CUDA_OK(cudaGraphExecDestroy(s->loop_graph));
+    s->graph = nullptr;
+    s->loop_graph = nullptr;
+    s->graph_steps = 0;
+    s->loop_unsupported = false;
     reset_cache(s->cache.get());
+    if (s->e.max_new_tokens == 0) {  // engine.cpp:314-317: nothing to prefill or decode
+        for (int b = 0; b < B; ++b)
+            CUDA_OK(cudaMemcpy(s->ctx + (size_t)b * s->ctx_cap, s->prompts[b].data(), 4 * (size_t)lens[b],
+                               cudaMemcpyHostToDevice));
+        s->first_tok.assign(B, 0);
+        s->snap_active.assign(B, 0);
+        if (s->draft) {
+            reset_cache(s->dcache.get());
+            s->snap_dcommit.assign(B, 0);
+        }
+        s->snap_committed = c.committed;
+        s->snap_logical = c.logical;
+        s->snap_pad = c.pad;
+        s->prefilled = true;
+        session_reset(s);
+        return;
+    }
     std::vector<int32_t> flat, am;
     std::vector<Plan> plans;
     std::vector<int> last_row(B);
@@ -470,11 +502,11 @@ int session_run_host(sd_session* s, float* gpu_ms, int64_t* h2d_bytes, int64_t* 
         traj.resize((size_t)B * s->traj_stride);
         CUDA_OK(cudaMemcpy(traj.data(), s->traj, 4 * traj.size(), cudaMemcpyDeviceToHost));
     }
-    std::vector<int32_t> gen(B, 1), active = s->snap_active, last(B), counts(B), budget(B), tau(B), clipped(B), acc,
+    std::vector<int32_t> gen(B, s->e.max_new_tokens > 0 ? 1 : 0), active = s->snap_active, last(B), counts(B), budget(B), tau(B), clipped(B), acc,
         drafts;
     for (int b = 0; b < B; ++b) {
         ctx[b] = s->prompts[b];
-        ctx[b].push_back(s->first_tok[b]);
+        if (s->e.max_new_tokens > 0) ctx[b].push_back(s->first_tok[b]);
     }
     int64_t h2d = 0, d2h = 0;
     cudaEvent_t e0, e1;
@@ -496,7 +528,7 @@ int session_run_host(sd_session* s, float* gpu_ms, int64_t* h2d_bytes, int64_t* 
                 d = retrieval_predict(ctx[b], s->e.match_len, s->e.copy_len);
             } else {  // predictors.cpp:61-72 over the greedy continuation
                 uint64_t rs = s->e.seed ^ ((uint64_t)steps * 0xD1B54A32D192ED03ULL) ^
-                              ((uint64_t)b * 0x8CB92BA72F3D8DD7ULL);
+                              ((uint64_t)(s->e.sample_id_base + b) * 0x8CB92BA72F3D8DD7ULL);  // global id
                 auto nx = [&]() {
                     uint64_t z = (rs += 0x9E3779B97F4A7C15ULL);
                     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;

@@ -58,6 +58,7 @@ struct PredictArgs {
     int kind;                // 1 retrieval (LLMA prompt lookup), 2 synthetic trajectory
     int match_len, copy_len, k, vocab;
     uint64_t seed;
+    int id_base;             // global id of local sample 0 (mix_seed uses global ids)
     double accuracy;
     const int32_t* traj;     // [B][traj_stride] greedy continuation (synthetic)
     int traj_stride;
@@ -94,6 +95,9 @@ void launch_draft_commit(const DraftArgs& d, cudaStream_t st);
 void launch_pack(const StepArgs& a, cudaStream_t st);
 void launch_accept(const StepArgs& a, cudaStream_t st);
 void launch_pad_fill(const StepArgs& a, const Cache& c, cudaStream_t st);
+// PaddedGrid::commit_padded's filler rows from the host API: zero K/V rows
+// [r0[i], r1) of sample samples[i] (device arrays, n entries) in every layer
+void launch_zero_rows(const Cache& c, const int32_t* samples, const int32_t* r0, int n, int r1, cudaStream_t st);
 void launch_predict(const StepArgs& a, const PredictArgs& p, cudaStream_t st);
 
 }  // namespace sdb

@@ -211,6 +211,22 @@ __global__ void k_pad_fill(StepArgs a, T* kv, int heads, int hd) {
     }
 }
 
+// grid = (L * 2, n), block 256: zero rows [r0[i], r1) of sample samples[i]
+template <typename T>
+__global__ void k_zero_rows(T* kv, const int32_t* samples, const int32_t* r0, int r1, int B, int heads, int cap,
+                            int hd) {
+    CtaTrace trace__(TK_PAD_FILL);
+    pdl_trigger();
+    pdl_wait();
+    const int lw = blockIdx.x, s = samples[blockIdx.y], a = r0[blockIdx.y];
+    const int rows = r1 - a;
+    if (rows <= 0) return;
+    for (int head = 0; head < heads; ++head) {
+        T* p = kv + (((size_t)lw * B + s) * heads + head) * (size_t)cap * hd + (size_t)a * hd;
+        for (int i = threadIdx.x; i < rows * hd; i += blockDim.x) p[i] = T(0.0f);
+    }
+}
+
 __device__ __forceinline__ uint64_t splitmix_next(uint64_t& st) {  // rng.hpp:15-20
     uint64_t z = (st += 0x9E3779B97F4A7C15ULL);
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -258,7 +274,7 @@ __global__ void k_predict(StepArgs a, PredictArgs p) {
         if (threadIdx.x == 0) {
             int g = a.gen[s];
             uint64_t st = p.seed ^ ((uint64_t)(*a.step) * 0xD1B54A32D192ED03ULL) ^
-                          ((uint64_t)s * 0x8CB92BA72F3D8DD7ULL);  // mix_seed (rng.hpp:43-46)
+                          ((uint64_t)(p.id_base + s) * 0x8CB92BA72F3D8DD7ULL);  // mix_seed (rng.hpp:43-46), global id
             st = splitmix_next(st);
             for (int i = 0; i < p.k; ++i) {
                 int t = p.traj[(size_t)s * p.traj_stride + g + i];
@@ -354,6 +370,14 @@ void launch_pad_fill(const StepArgs& a, const Cache& c, cudaStream_t st) {
         launch_k(k_pad_fill<float>, grid, dim3(256), 0, st, a, (float*)c.kv, c.heads, c.hd);
     else
         launch_k(k_pad_fill<__nv_bfloat16>, grid, dim3(256), 0, st, a, (__nv_bfloat16*)c.kv, c.heads, c.hd);
+}
+void launch_zero_rows(const Cache& c, const int32_t* samples, const int32_t* r0, int n, int r1, cudaStream_t st) {
+    dim3 grid(c.L * 2, n);
+    if (c.elem_bytes == 4)
+        launch_k(k_zero_rows<float>, grid, dim3(256), 0, st, (float*)c.kv, samples, r0, r1, c.B, c.heads, c.cap, c.hd);
+    else
+        launch_k(k_zero_rows<__nv_bfloat16>, grid, dim3(256), 0, st, (__nv_bfloat16*)c.kv, samples, r0, r1, c.B,
+                 c.heads, c.cap, c.hd);
 }
 void launch_predict(const StepArgs& a, const PredictArgs& p, cudaStream_t st) {
     launch_k(k_predict, dim3(a.B), dim3(128), 0, st, a, p);

@@ -62,7 +62,8 @@ class _ModelConfigT(C.Structure):
 class _EngineConfigT(C.Structure):
     _fields_ = [("mode", C.c_int32), ("predictor", C.c_int32), ("k", C.c_int32), ("match_len", C.c_int32),
                 ("copy_len", C.c_int32), ("batch_size", C.c_int32), ("max_new_tokens", C.c_int32),
-                ("stop_on_eos", C.c_int32), ("seed", C.c_uint64), ("synthetic_accuracy", C.c_double)]
+                ("stop_on_eos", C.c_int32), ("seed", C.c_uint64), ("synthetic_accuracy", C.c_double),
+                ("sample_id_base", C.c_int32)]
 
 
 _lib = None
@@ -456,6 +457,7 @@ class EngineConfig:
     stop_on_eos: bool = True
     seed: int = 1
     synthetic_accuracy: float = 0.8
+    sample_id_base: int = 0  # global id of local sample 0 (sharded runs, engine.cpp:182-185)
 
     def _c(self) -> _EngineConfigT:
         if self.mode not in MODES:
@@ -464,7 +466,7 @@ class EngineConfig:
             raise ConfigError(f"config: unknown predictor: {self.predictor}")
         return _EngineConfigT(MODES[self.mode], PREDICTORS[self.predictor], self.k, self.match_len, self.copy_len,
                               self.batch_size, self.max_new_tokens, int(self.stop_on_eos), self.seed,
-                              self.synthetic_accuracy)
+                              self.synthetic_accuracy, self.sample_id_base)
 
 
 @dataclass
@@ -551,7 +553,10 @@ def results_json(config: EngineConfig, result: DecodeResult) -> str:
     plens = result.prompt_lens or [0] * b
     steps = result.steps
     total_gen = sum(gen)
-    if config.mode == "greedy":
+    if config.max_new_tokens == 0:  # engine.cpp:223-226, 314-317: default RunMetrics, no prefill
+        decode_steps, avg_tau, avg_r, in_pad, kv_pad, real, pad_proc, ledger = 0, 0.0, 0.0, 0, 0, 0, 0, []
+        steps = []
+    elif config.mode == "greedy":
         decode_steps = max(gen) - 1 if gen else 0
         avg_tau, avg_r, in_pad, kv_pad = 1.0, 0.0, 0, 0
         real = sum(p + g - 1 for p, g in zip(plens, gen))
@@ -593,8 +598,7 @@ def results_json(config: EngineConfig, result: DecodeResult) -> str:
 
 
 # ---------------------------------------------------------------- sessions
-PROFILE_KINDS = ["gemm_qkv", "gemm_o", "gemm_fc", "gemm_proj", "gemm_lm", "attention", "layernorm", "misc",
-                 "attn_combine"]
+PROFILE_KINDS = ["gemm_qkv", "gemm_o", "gemm_fc", "gemm_proj", "gemm_lm", "attention", "layernorm", "misc"]
 
 
 def profile_enable(on: bool) -> None:

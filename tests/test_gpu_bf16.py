@@ -54,10 +54,8 @@ def test_gemm_matches_fp64(sd, M, K, T, grid):
     Y, _ = run_gemm(sd, W, X, grid)
     err = np.abs(Y - ref)
     assert err.max() <= 2e-3 * np.abs(ref).max() + 1e-3, (err.max(), np.abs(ref).max())
-    Yt, _ = run_gemm(sd, W, X, grid, flags=1)  # tile-major weights give the same bits
-    assert np.array_equal(Yt.view(np.uint32), Y.view(np.uint32))
-    Yb, _ = run_gemm(sd, W, X, grid, flags=16)  # pre-swizzled tiles through 1D bulk copies
-    assert np.array_equal(Yb.view(np.uint32), Y.view(np.uint32))
+    Y2, _ = run_gemm(sd, W, X, grid)  # deterministic split-K: the same bits every launch
+    assert np.array_equal(Y2.view(np.uint32), Y.view(np.uint32))
 
 
 def bf16_vs_oracle(sd, oracle, cfg, B, prompt_len, seed):
