@@ -94,6 +94,17 @@ int sd_model_save(const sd_model* m, const char* path);
 int sd_model_checksum(const sd_model* m, uint64_t* out);
 int sd_model_get_config(const sd_model* m, sd_model_config* out);
 int64_t sd_model_weight_bytes(const sd_model* m);
+/* Weight access for independent reimplementations in tests (model.hpp:81-87:
+ * token_embedding, position_embedding, layer(i), final_ln_gain/bias, lm_head).
+ * layer -1 selects the model-level tensors: 0 token_embedding [V][h],
+ * 1 position_embedding [P][h], 2 final_ln_gain [h], 3 final_ln_bias [h],
+ * 4 lm_head [V][h]; layer i >= 0 selects LayerWeights (model.hpp:27-32) in
+ * declaration order: 0 ln1_gain, 1 ln1_bias, 2 wq, 3 bq, 4 wk, 5 bk, 6 wv,
+ * 7 bv, 8 wo, 9 bo, 10 ln2_gain, 11 ln2_bias, 12 w_fc, 13 b_fc, 14 w_proj,
+ * 15 b_proj (matrices row-major [out][in]).  out receives `count` fp32 values
+ * (count must equal the tensor size); a bf16 model returns its stored bf16
+ * values widened to fp32. */
+int sd_model_get_tensor(const sd_model* m, int layer, int tensor, float* out, int64_t count);
 void sd_model_destroy(sd_model* m);
 
 /* ---- KV cache (CacheArena, kv_cache.hpp:65-168) -------------------------- */

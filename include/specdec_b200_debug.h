@@ -9,14 +9,22 @@ extern "C" {
 /* Y[T][M] = X[T][K] . W[M][K]^T with bf16 inputs (raw bits) and fp32 output,
  * through the stream-K tcgen05 kernel on `grid` CTAs (0 = one per SM).
  * Returns the kernel time in microseconds in *usec (CUDA events). */
-/* flags bit 0: store W tile-major ([m_tile][K/64][256][64], one contiguous 32 KB
- * TMA box per k-block) instead of row-major */
+/* flags bit 3: time the streaming kernel alone (no split-K reduction; Y untouched) */
 int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K, int T, int grid, int flags, float* Y,
                   float* usec);
 /* In-graph kernel timeline (tools/timeline.py): while on, every CTA of every
  * verify-step kernel appends {kernel id, block, SM, grid size, t_entry, t_exit}
  * (globaltimer ns, 32 bytes) to a device buffer of `cap` records. */
 int sd_debug_trace_begin(int cap);
+/* The production persistent tcgen05 attention (split-KV items, last-arriver
+ * combine) on caller-provided bf16 tensors of one layer:
+ *   q [T][heads*hd]; kv [2][B][heads][cap][hd] (K then V); queries packed
+ *   sample by sample, n_q[B] of them per sample, kv_len[B] visible extent,
+ *   write_slot[T] per query (it sees keys <= its slot), pad [B][cap] flags or
+ *   NULL -> ctx [T][heads*hd] bf16.  T <= 256.  *usec: one launch. */
+int sd_debug_attention(const uint16_t* q, const uint16_t* kv, int B, int heads, int hd, int cap, const int32_t* n_q,
+                       const int32_t* kv_len, const int32_t* write_slot, const uint8_t* pad, uint16_t* ctx,
+                       float* usec);
 int sd_debug_trace_end(void* out, int cap, int* n);
 #ifdef __cplusplus
 }

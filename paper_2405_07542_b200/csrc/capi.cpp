@@ -729,6 +729,61 @@ int sd_model_get_config(const sd_model* m, sd_model_config* out) {
 
 int64_t sd_model_weight_bytes(const sd_model* m) { return m->m.weight_bytes; }
 
+int sd_model_get_tensor(const sd_model* mh, int layer, int tensor, float* out, int64_t count) {
+    return guarded([&] {  // model.hpp:81-87
+        const Model& m = mh->m;
+        const Config& c = m.cfg;
+        const int64_t h = c.hidden(), mm = c.mlp();
+        SD_CHECK(layer >= -1 && layer < c.num_layers, CONTRACT, "layer out of range");
+        int64_t off32 = -1, n = 0;  // fp32 check mode: offset into the declaration-order blob
+        const void* src = nullptr;  // bf16 mode: the stored tensor
+        bool bf16 = true;
+        if (layer < 0) {
+            SD_CHECK(tensor >= 0 && tensor <= 4, CONTRACT, "unknown model tensor");
+            const int64_t sizes[5] = {(int64_t)c.vocab_size * h, (int64_t)c.max_positions * h, h, h,
+                                      (int64_t)c.vocab_size * h};
+            const int64_t offs[5] = {m.lay.tok, m.lay.pos, m.lay.lnf_g, m.lay.lnf_b, m.lay.lm};
+            n = sizes[tensor];
+            off32 = offs[tensor];
+            if (m.precision == BF16) {
+                const void* p[5] = {m.tok16, m.pos16, m.lnf_g, m.lnf_b, m.lm16};
+                src = p[tensor];
+                bf16 = tensor == 0 || tensor == 1 || tensor == 4;
+            }
+        } else {
+            SD_CHECK(tensor >= 0 && tensor <= 15, CONTRACT, "unknown layer tensor");
+            const LayerOff& o = m.lay.layer[layer];
+            const int64_t offs[16] = {o.ln1_g, o.ln1_b, o.wq, o.bq, o.wk, o.bk, o.wv, o.bv,
+                                      o.wo, o.bo, o.ln2_g, o.ln2_b, o.w_fc, o.b_fc, o.w_proj, o.b_proj};
+            const int64_t sizes[16] = {h, h, h * h, h, h * h, h, h * h, h, h * h, h, h, h, mm * h, mm, h * mm, h};
+            n = sizes[tensor];
+            off32 = offs[tensor];
+            if (m.precision == BF16) {
+                const FastLayer& f = m.layers[layer];
+                const void* p[16] = {f.ln1_g, f.ln1_b, f.wqkv, f.bqkv, f.wqkv + h * h, f.bqkv + h,
+                                     f.wqkv + 2 * h * h, f.bqkv + 2 * h, f.wo, f.bo, f.ln2_g, f.ln2_b,
+                                     f.wfc, f.bfc, f.wproj, f.bproj};
+                src = p[tensor];
+                bf16 = tensor == 2 || tensor == 4 || tensor == 6 || tensor == 8 || tensor == 12 || tensor == 14;
+            }
+        }
+        SD_CHECK(count == n, CONTRACT, "tensor size mismatch: expected " + std::to_string(n));
+        CUDA_OK(cudaSetDevice(m.device));
+        if (m.precision == FP32_CHECK) {
+            CUDA_OK(cudaMemcpy(out, m.w32 + off32, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost));
+        } else if (!bf16) {
+            CUDA_OK(cudaMemcpy(out, src, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost));
+        } else {
+            std::vector<uint16_t> b((size_t)n);
+            CUDA_OK(cudaMemcpy(b.data(), src, 2 * (size_t)n, cudaMemcpyDeviceToHost));
+            for (int64_t i = 0; i < n; ++i) {
+                uint32_t u = (uint32_t)b[i] << 16;
+                std::memcpy(out + i, &u, 4);
+            }
+        }
+    });
+}
+
 void sd_model_destroy(sd_model* m) {
     if (m) {
         cudaSetDevice(m->m.device);

@@ -37,6 +37,9 @@ struct FastWorkspace {
     int cap_tokens = 0, B = 0, cap = 0;
     __nv_bfloat16 *xb = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr;
     float* part = nullptr;     // stream-K partial sums (largest GEMM of the model)
+    int max_splits = 0;        // attention KV splits of the longest extent the cache holds
+    float *part_o = nullptr, *part_ml = nullptr;  // attention split partials
+    int* attn_cnt = nullptr;   // split arrival counters [256][heads]
     ArgmaxScratch am;          // LM-head (max, id) partials per token + arrival counters
     GemmMaps map_xb, map_ctx, map_act;
     CUtensorMap kv_map;        // TMA view of the KV arena [L*2*B*heads*cap][hd], box {64, 128}
@@ -143,27 +146,39 @@ struct AttnArgs {
     __nv_bfloat16* ctx;        // [T][h]
     int* work;                 // this launch's item counter (zeroed per forward)
     int pre_ok;                // may read segs before griddepcontrol.wait (see producer)
+    float* part_o;             // split partials [256 tiles][heads][max_splits][8 q][hd] (unnormalised O)
+    float* part_ml;            // [256][heads][max_splits][8 q][2] (reference max, sum)
+    int* cnt;                  // [256][heads] split arrival counters (self-resetting)
+    int max_splits;
     int h, heads, B, cap, layer;
     float scale_log2;          // log2(e) / sqrt(hd)
 };
 
 constexpr int kTcKeys = 128;  // keys per K/V chunk (the S^T MMA's M)
 
-// Persistent tcgen05 attention (HD = 128): one CTA per SM walks (sample,
-// head, 8-query tile) items from an atomic counter; each item streams the
-// sample's WHOLE visible KV extent in 128-key chunks, so there are no split
-// partials and no combine kernel.
-//   warp 4     TMA producer: the item's Q rows (16 one-row boxes into a
-//              swizzled K-major tile) and K/V chunks into a kPS-stage ring,
-//              running ahead across items.
+// Persistent tcgen05 attention: one CTA per SM (two for HD = 64) walks work
+// items from an atomic counter.  An item is (sample, head, 8-query tile,
+// KV split): the keys a tile can see, [0, last query's slot], are cut at FIXED
+// multiples of kSplitKeys from slot 0, so how a query's keys are grouped --
+// and therefore its rounding -- depends only on its own visible extent, never
+// on the batch around it (batch-composition invariance, test_engine.cpp:
+// 307-320).  A tile whose extent fits one split writes its context rows
+// directly; otherwise every split stores (max, sum, unnormalised O) partials
+// and the last split to finish folds them in split order (deterministic).
+//   warp 4     TMA producer: the item's Q rows (one-row boxes into a swizzled
+//              K-major tile) and its 128-key K/V chunks into a kPS-stage
+//              ring, running ahead across items; it also publishes each
+//              item's key range so the other roles agree on it.
 //   warp 5     MMA issuer: S^T(c+1) = K Q^T is issued before waiting for the
 //              softmax of chunk c (double-buffered S in TMEM), then
 //              O^T += V^T P^T (V read MN-major from the same tile).
 //   warps 0-3  softmax (thread = key): per-chunk max through smem, online
 //              softmax with a lazy reference max (rescale O^T in TMEM only
 //              when the max grows by more than 2^8), P^T to smem; at the
-//              item end O^T / l -> the context row (thread = hd).
+//              item end O^T / l -> the context row (thread = hd), or the
+//              split partial + combine.
 constexpr int kPS = 3, kPQ = 2, kPThreads = 192;
+constexpr int kSplitKeys = 1024;  // keys per KV split (8 chunks)
 // stage = K boxes then V boxes (one 64-column box per 64 of head_dim)
 template <int HD>
 constexpr int kPStageB = 2 * (HD / 64) * kTcKeys * 128;
@@ -194,11 +209,12 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
     uint8_t* sP = qring + kPQ * 2048;                    // [2][2 atoms of 8 x 128 B]
     float* sS = (float*)(sP + 2 * 2048);                 // [8][128]
     __shared__ uint64_t full[kPS], empty[kPS], qfull[kPQ], qempty[kPQ], sfull[2], pfull[2], pvdone[2], ofree;
-    __shared__ int sq_item[kPQ];
+    // published by the producer with each item: {item, first key, chunks, splits of the tile}
+    __shared__ int4 sq_item[kPQ];
     __shared__ uint32_t tslot;
     __shared__ float sMx[8], sL[8];
+    __shared__ int s_last;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, tid = threadIdx.x;
-    const int n_items = a.B * a.heads * qtiles;
     // a tail chunk of <= 64 keys loads half a stage: keep the other half finite (zero) once
     for (int i = tid; i < kPS * kPStage / 16; i += kPThreads) ((uint4*)ring)[i] = make_uint4(0u, 0u, 0u, 0u);
     ptx::fence_proxy_async_smem();
@@ -224,37 +240,57 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
         ptx::fence_barrier_init();
     }
     if (warp == 5) ptx::tmem_alloc32(&tslot);
-    // Longest extents first (LPT): items are handed out in order of decreasing
-    // kv_len, so the last items -- the end-of-kernel tail -- are the shortest.
-    // The segs are safe to read before griddepcontrol.wait under a.pre_ok (see
-    // the producer); otherwise every warp waits first.
-    __shared__ int s_order[256];
-    const bool lpt = a.B <= 256;
+    // Work list.  Samples in order of decreasing kv_len (LPT: the last items --
+    // the end-of-kernel tail -- are the shortest); a sample owns
+    // heads x qtiles x splits(kv_len) consecutive items, the splits of one
+    // (head, tile) adjacent so they finish together.  The segs are safe to
+    // read before griddepcontrol.wait under a.pre_ok (see the producer).
+    __shared__ int s_order[256], s_item0[257];
     if (!a.pre_ok) pdl_wait();
-    if (lpt)
-        for (int x = tid; x < a.B; x += kPThreads) {
-            const int lx = a.segs[x].kv_len;
-            int rank = 0;
-            for (int y = 0; y < a.B; ++y) {
-                const int ly = a.segs[y].kv_len;
-                rank += (ly > lx) || (ly == lx && y < x);
-            }
-            s_order[rank] = x;
+    for (int x = tid; x < a.B; x += kPThreads) {
+        const int lx = a.segs[x].kv_len;
+        int rank = 0;
+        for (int y = 0; y < a.B; ++y) {
+            const int ly = a.segs[y].kv_len;
+            rank += (ly > lx) || (ly == lx && y < x);
         }
+        s_order[rank] = x;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int at = 0;
+        for (int r = 0; r < a.B; ++r) {
+            s_item0[r] = at;
+            const SampleSeg g = a.segs[s_order[r]];
+            if (g.n_q > 0 && g.kv_len > 0) at += a.heads * ((g.n_q + kQT - 1) / kQT) * ((g.kv_len + kSplitKeys - 1) / kSplitKeys);
+        }
+        s_item0[a.B] = at;
+    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = tslot;  // S: cols [0,8) and [8,16); O^T: cols [16,24)
+    const int n_items = s_item0[a.B];
     pdl_trigger();
     // The producer waits below, after pre-issuing its first item's OLD chunks.
     if (warp != 4 && a.pre_ok) pdl_wait();  // Q and this step's K/V rows come from the QKV reduction
 
-    auto decode = [&](int i, int& s, int& head, int& qt) {
-        qt = i % qtiles;
-        const int pair = i / qtiles;
-        s = pair / a.heads;
-        head = pair - s * a.heads;
-        if (lpt) s = s_order[s];
+    // item -> (sample, head, q tile, split)
+    auto decode = [&](int i, int& s, int& head, int& qt, int& split) {
+        int lo = 0, hi = a.B - 1;  // last rank with s_item0 <= i
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_item0[mid] <= i) lo = mid;
+            else hi = mid - 1;
+        }
+        s = s_order[lo];
+        const SampleSeg g = a.segs[s];
+        const int ns = (g.kv_len + kSplitKeys - 1) / kSplitKeys;
+        int rest = i - s_item0[lo];
+        split = rest % ns;
+        rest /= ns;
+        qt = rest % ((g.n_q + kQT - 1) / kQT);
+        head = rest / ((g.n_q + kQT - 1) / kQT);
     };
 
     if (warp == 4) {
@@ -265,15 +301,6 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
             uint32_t ph = 0, qph = 0;
             int next = atomicAdd(a.work, 1);
             unsigned long long algo = 0;
-            // Before griddepcontrol.wait: K/V rows of positions committed in EARLIER
-            // steps cannot change, and -- when the QKV GEMM ran one CTA on EVERY SM
-            // (a.pre_ok, set by the host) -- this CTA only became resident once the
-            // GEMM's CTA on this SM exited, i.e. after every kernel up to the last
-            // LayerNorm (and k_pack, which wrote segs) completed.  So the first
-            // item's chunks below its new tokens stream during the QKV reduction.
-            // (A smaller GEMM grid, e.g. a draft model's, leaves SMs free and this
-            // CTA could run next to an unfinished k_pack: no early reads then.)
-            int pre_item = -1, pre_chunks = 0;
             // rows: keys left in the extent; <= 32 / <= 64 -> the 32- / 64-row boxes (no
             // over-read of a whole 128-key chunk past the extent; the rest of the stage
             // holds finite data: zeros or an earlier chunk, masked by the softmax)
@@ -293,16 +320,37 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                     ph ^= 1;
                 }
             };
+            // the keys a tile can see end at its LAST query's write slot (queries
+            // of a sample are in slot order); its splits are cut at multiples of
+            // kSplitKeys of that extent
+            const auto tile_extent = [&](const SampleSeg& g, int qt, int& nq) {
+                nq = min(kQT, g.n_q - qt * kQT);
+                const int tok = a.qidx[g.q_start + qt * kQT + nq - 1];
+                return min(g.kv_len, a.plans[tok].write_slot + 1);
+            };
+            // Before griddepcontrol.wait: K/V rows of positions committed in EARLIER
+            // steps cannot change, and -- when the QKV GEMM ran one CTA on EVERY SM
+            // (a.pre_ok, set by the host) -- this CTA only became resident once the
+            // GEMM's CTA on this SM exited, i.e. after every kernel up to the last
+            // LayerNorm (and k_pack, which wrote segs / plans) completed.  So the
+            // first item's chunks below its new tokens stream during the QKV
+            // reduction.  (A smaller GEMM grid, e.g. a draft model's, leaves SMs
+            // free and this CTA could run next to an unfinished k_pack: no early
+            // reads then.)
+            int pre_item = -1, pre_chunks = 0;
             if (next < n_items && a.pre_ok) {
-                int s, head, qt;
-                decode(next, s, head, qt);
-                const SampleSeg seg = a.segs[s];
-                if (seg.n_q - qt * kQT > 0 && seg.kv_len > 0) {
+                int s, head, qt, split, nq;
+                decode(next, s, head, qt, split);
+                const SampleSeg g = a.segs[s];
+                const int ext = tile_extent(g, qt, nq);
+                const int k_lo = split * kSplitKeys, k_hi = min(ext, k_lo + kSplitKeys);
+                const int old_hi = min(k_hi, g.kv_len - g.n_q);  // rows no kernel of this step writes
+                if (k_lo < k_hi && old_hi > k_lo) {
                     pre_item = next;
-                    pre_chunks = min(kPS, max(0, seg.kv_len - seg.n_q) / kTcKeys);
+                    pre_chunks = min(kPS, (old_hi - k_lo) / kTcKeys);
                     const int row_k = (((a.layer * 2 + 0) * a.B + s) * a.heads + head) * a.cap;
                     const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap;
-                    for (int c = 0; c < pre_chunks; ++c) issue_chunk(row_k, row_v, c * kTcKeys, kTcKeys);
+                    for (int c = 0; c < pre_chunks; ++c) issue_chunk(row_k, row_v, k_lo + c * kTcKeys, kTcKeys);
                 }
             }
             pdl_wait();
@@ -310,16 +358,19 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                 const int i = next;
                 if (i >= n_items) break;
                 next = atomicAdd(a.work, 1);  // in flight while this item is issued
-                int s, head, qt;
-                decode(i, s, head, qt);
-                const SampleSeg seg = a.segs[s];
-                const int nq = min(kQT, seg.n_q - qt * kQT);
-                if (nq <= 0 || seg.kv_len <= 0) continue;
+                int s, head, qt, split, nq;
+                decode(i, s, head, qt, split);
+                const SampleSeg g = a.segs[s];
+                const int ext = tile_extent(g, qt, nq);
+                const int k_lo = split * kSplitKeys, k_hi = min(ext, k_lo + kSplitKeys);
+                if (k_lo >= k_hi) continue;  // beyond this tile's last query: nothing to see
+                const int nch = (k_hi - k_lo + kTcKeys - 1) / kTcKeys;
+                const int ns = (ext + kSplitKeys - 1) / kSplitKeys;
                 int toks[kQT];
 #pragma unroll
-                for (int r = 0; r < kQT; ++r) toks[r] = a.qidx[seg.q_start + qt * kQT + (r < nq ? r : 0)];
+                for (int r = 0; r < kQT; ++r) toks[r] = a.qidx[g.q_start + qt * kQT + (r < nq ? r : 0)];
                 ptx::mbar_wait(&qempty[qs], qph ^ 1);
-                sq_item[qs] = i;  // published by the arrive below
+                sq_item[qs] = make_int4(i, k_lo, nch, ns);  // published by the arrive below
                 ptx::mbar_arrive_expect_tx(&qfull[qs], kBoxes * 1024);
 #pragma unroll
                 for (int r = 0; r < kQT; ++r)  // one-row boxes: the TMA swizzles by destination address
@@ -334,13 +385,13 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                 const int row_k = (((a.layer * 2 + 0) * a.B + s) * a.heads + head) * a.cap;
                 const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap;
                 const int c0 = i == pre_item ? pre_chunks : 0;  // already in the ring
-                for (int k0 = c0 * kTcKeys; k0 < seg.kv_len; k0 += kTcKeys) issue_chunk(row_k, row_v, k0, seg.kv_len - k0);
-                algo += (unsigned long long)seg.kv_len * (2 * HD * 2);
+                for (int k0 = k_lo + c0 * kTcKeys; k0 < k_hi; k0 += kTcKeys) issue_chunk(row_k, row_v, k0, k_hi - k0);
+                algo += (unsigned long long)(k_hi - k_lo) * (2 * HD * 2);
             }
             // in-graph roofline: this CTA's algorithmic K/V bytes (KiB) next to its timeline record
             trace_point(TK_ATTN_BYTES, (uint32_t)(algo >> 10));
             ptx::mbar_wait(&qempty[qs], qph ^ 1);  // end of work
-            sq_item[qs] = -1;
+            sq_item[qs] = make_int4(-1, 0, 0, 0);
             ptx::mbar_arrive(&qfull[qs]);
         }
     } else if (warp == 5) {
@@ -352,11 +403,9 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
             uint32_t gc = 0;  // chunks processed (S / P buffers alternate)
             for (;;) {
                 ptx::mbar_wait(&qfull[qs], qph);
-                const int i = sq_item[qs];
-                if (i < 0) break;
-                int s, head, qt;
-                decode(i, s, head, qt);
-                const int nch = (a.segs[s].kv_len + kTcKeys - 1) / kTcKeys;
+                const int4 it = sq_item[qs];
+                if (it.x < 0) break;
+                const int nch = it.z;
                 const uint32_t qa = ptx::smem_u32(qring + qs * 2048);
                 // S^T(c) into TMEM buffer (gc + c) & 1
                 auto issue_s = [&](int c, int stc, uint32_t phc) {
@@ -416,24 +465,24 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
         }
     } else {
         // ------------------------------------------------------------ softmax warps
-        int qs = 0, items = 0;
+        int qs = 0;
         uint32_t qph = 0, gc = 0;
         const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
         for (;;) {
             ptx::mbar_wait(&qfull[qs], qph);
-            const int i = sq_item[qs];
+            const int4 it = sq_item[qs];
             __syncwarp();
-            if (i >= 0 && lane == 0) ptx::mbar_arrive(&qempty[qs]);
+            if (it.x >= 0 && lane == 0) ptx::mbar_arrive(&qempty[qs]);
             if (++qs == kPQ) {
                 qs = 0;
                 qph ^= 1;
             }
-            if (i < 0) break;
-            int s, head, qt;
-            decode(i, s, head, qt);
+            if (it.x < 0) break;
+            int s, head, qt, split;
+            decode(it.x, s, head, qt, split);
+            const int k_lo = it.y, nch = it.z, ns = it.w;
             const SampleSeg seg = a.segs[s];
             const int nq = min(kQT, seg.n_q - qt * kQT);
-            const int nch = (seg.kv_len + kTcKeys - 1) / kTcKeys;
             int ws[kQT];
 #pragma unroll
             for (int q = 0; q < kQT; ++q) {
@@ -448,7 +497,7 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
             }
             for (int c = 0; c < nch; ++c) {
                 const uint32_t g = gc + c;
-                const int key = c * kTcKeys + tid;
+                const int key = k_lo + c * kTcKeys + tid;
                 ptx::mbar_wait(&sfull[g & 1], (g >> 1) & 1);
                 ptx::tc_fence_after();
                 float x[kQT];
@@ -527,14 +576,50 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
             ptx::tmem_ld8(trow + 16, o);
             ptx::tc_fence_before();
             ptx::mbar_arrive(&ofree);
+            const int tile_tok = seg.q_start + qt * kQT;  // the tile's first packed row: its combine slot
+            if (ns == 1) {
 #pragma unroll
-            for (int q = 0; q < kQT; ++q) {
-                if (q >= nq) break;
-                const int tok = a.qidx[seg.q_start + qt * kQT + q];
-                if (tid < HD) a.ctx[(size_t)tok * a.h + head * HD + tid] = __float2bfloat16_rn(o[q] / sL[q]);
+                for (int q = 0; q < kQT; ++q) {
+                    if (q >= nq) break;
+                    const int tok = a.qidx[tile_tok + q];
+                    if (tid < HD) a.ctx[(size_t)tok * a.h + head * HD + tid] = __float2bfloat16_rn(o[q] / sL[q]);
+                }
+            } else {
+                // split partial: (reference max, sum, unnormalised O) per query
+                const size_t pbase = ((size_t)tile_tok * a.heads + head) * a.max_splits;
+#pragma unroll
+                for (int q = 0; q < kQT; ++q) {
+                    if (q >= nq) break;
+                    if (tid < HD) a.part_o[((pbase + split) * kQT + q) * HD + tid] = o[q];
+                    if (tid == q) {
+                        a.part_ml[((pbase + split) * kQT + q) * 2] = mref[q];
+                        a.part_ml[((pbase + split) * kQT + q) * 2 + 1] = sL[q];
+                    }
+                }
+                __threadfence();
+                ptx::named_bar_sync(1, 128);
+                if (tid == 0) s_last = atomicAdd(&a.cnt[(size_t)tile_tok * a.heads + head], 1) == ns - 1;
+                ptx::named_bar_sync(1, 128);
+                if (s_last) {  // every split landed: fold them in split order
+                    __threadfence();
+                    for (int q = 0; q < nq; ++q) {
+                        float M = -INFINITY;
+                        for (int k = 0; k < ns; ++k) M = fmaxf(M, __ldcg(&a.part_ml[((pbase + k) * kQT + q) * 2]));
+                        float L = 0.0f, O = 0.0f;
+                        for (int k = 0; k < ns; ++k) {
+                            const float mk = __ldcg(&a.part_ml[((pbase + k) * kQT + q) * 2]);
+                            if (mk == -INFINITY) continue;
+                            const float f = exp2f(mk - M);
+                            L += __ldcg(&a.part_ml[((pbase + k) * kQT + q) * 2 + 1]) * f;
+                            if (tid < HD) O += __ldcg(&a.part_o[((pbase + k) * kQT + q) * HD + tid]) * f;
+                        }
+                        const int tok = a.qidx[tile_tok + q];
+                        if (tid < HD) a.ctx[(size_t)tok * a.h + head * HD + tid] = __float2bfloat16_rn(O / L);
+                    }
+                    if (tid == 0) a.cnt[(size_t)tile_tok * a.heads + head] = 0;  // self-resetting
+                }
             }
             gc += nch;
-            ++items;
         }
     }
     ptx::tc_fence_before();
@@ -581,11 +666,33 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     f->kv_map32 = make_tmap_2d(c.kv, (int64_t)cfg.num_layers * 2 * c.B * cfg.num_heads * c.cap, cfg.head_dim, 32);
     f->q_map = make_tmap_2d(f->q, (int64_t)T, (int64_t)h, 1);
     f->attn_work = walloc<int>(f, (size_t)cfg.num_layers);
+    f->max_splits = (c.cap + kSplitKeys - 1) / kSplitKeys;
+    f->part_o = walloc<float>(f, T * cfg.num_heads * f->max_splits * kQT * cfg.head_dim);
+    f->part_ml = walloc<float>(f, T * cfg.num_heads * f->max_splits * kQT * 2);
+    f->attn_cnt = walloc<int>(f, T * cfg.num_heads);
+    CUDA_OK(cudaMemset(f->attn_cnt, 0, sizeof(int) * T * cfg.num_heads));  // self-resetting afterwards
     ws.fast = f;
     return f;
 }
 
+// Grid of the persistent attention: one CTA per SM (two for HD = 64), never
+// more CTAs than the host-side bound on work items.
+void launch_attention(const AttnArgs& at, const CUtensorMap& kv, const CUtensorMap& kv64, const CUtensorMap& kv32,
+                      const CUtensorMap& qm, int hd, int qtiles, int max_kv_upper, cudaStream_t st) {
+    const int sms = device_sm_count();
+    const long long items =
+        (long long)at.B * at.heads * qtiles * std::max(1, (max_kv_upper + kSplitKeys - 1) / kSplitKeys);
+    if (hd == 128)
+        launch_k(k_attention_tcp<128>, dim3((unsigned)std::min<long long>(items, sms)), dim3(kPThreads), kPSmem, st,
+                 kv, kv64, kv32, qm, at, qtiles);
+    else
+        launch_k(k_attention_tcp<64>, dim3((unsigned)std::min<long long>(items, 2LL * sms)), dim3(kPThreads),
+                 kPSmemB<64>, st, kv, kv64, kv32, qm, at, qtiles);
+}
+
 }  // namespace
+
+void ensure_fast_workspace(const Model& m, Cache& c, Workspace& ws) { ensure_fast(m, c, ws); }
 
 // ------------------------------------------------------------- profiling
 // Eager (non-graph) runs can time every launch with CUDA events on the
@@ -679,6 +786,10 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     at.qidx = db.qidx;
     at.pad = c.layout == PADDED ? c.d_pad : nullptr;
     at.ctx = f->ctx;
+    at.part_o = f->part_o;
+    at.part_ml = f->part_ml;
+    at.cnt = f->attn_cnt;
+    at.max_splits = f->max_splits;
     at.h = h;
     at.heads = heads;
     at.B = c.B;
@@ -706,12 +817,8 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         at.layer = l;
         at.work = f->attn_work + l;
         at.pre_ok = g.grid == sms ? 1 : 0;  // the QKV GEMM above held every SM
-        if (hd == 128)
-            PROF(PK_ATTN, launch_k(k_attention_tcp<128>, dim3(std::min(c.B * heads * qtiles, sms)), dim3(kPThreads),
-                                   kPSmem, st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
-        else
-            PROF(PK_ATTN, launch_k(k_attention_tcp<64>, dim3(std::min(c.B * heads * qtiles, 2 * sms)),
-                                   dim3(kPThreads), kPSmemB<64>, st, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, at, qtiles));
+        PROF(PK_ATTN, launch_attention(at, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, hd, qtiles, db.max_kv_upper,
+                                       st));
         launches++;
         // O projection + residual, fused with LN2 -> xb
         g = base;
@@ -839,3 +946,104 @@ void forward_fast(const Model& m, Cache& c, Workspace& ws, int T, bool want_logi
 }
 
 }  // namespace sdb
+
+// --------------------------------------------------------------- test hook
+// The production attention launch on caller-provided bf16 tensors (one layer):
+//   q [T][heads*hd], kv [2][B][heads][cap][hd] (K then V), per-sample n_q / kv_len
+//   (queries packed sample by sample), write_slot [T], pad [B][cap] or NULL
+// -> ctx [T][heads*hd] bf16.  *usec = one timed launch (CUDA events).
+extern "C" int sd_debug_attention(const uint16_t* q, const uint16_t* kv, int B, int heads, int hd, int cap,
+                                  const int32_t* n_q, const int32_t* kv_len, const int32_t* write_slot,
+                                  const uint8_t* pad, uint16_t* ctx, float* usec) {
+    using namespace sdb;
+    std::vector<void*> mem;
+    auto dm = [&](size_t n) {
+        void* p = dmalloc(n ? n : 1);
+        mem.push_back(p);
+        return p;
+    };
+    try {
+        SD_CHECK(hd == 64 || hd == 128, CONFIG, "head_dim 64 or 128");
+        int T = 0, max_kv = 0, max_q = 0;
+        std::vector<SampleSeg> segs(B);
+        std::vector<int32_t> qidx;
+        std::vector<Plan> plans;
+        for (int s = 0; s < B; ++s) {
+            segs[s] = SampleSeg{T, n_q[s], kv_len[s], 0};
+            for (int i = 0; i < n_q[s]; ++i, ++T) {
+                qidx.push_back(T);
+                plans.push_back(Plan{s, write_slot[T], write_slot[T], 1});
+            }
+            max_kv = std::max(max_kv, kv_len[s]);
+            max_q = std::max(max_q, n_q[s]);
+        }
+        SD_CHECK(T >= 1 && T <= 256, CONFIG, "1..256 query rows");
+        const int h = heads * hd, max_splits = (cap + kSplitKeys - 1) / kSplitKeys;
+        prepare_fast_kernels();
+        auto* dq = (__nv_bfloat16*)dm(2 * (size_t)T * h);
+        auto* dkv = (__nv_bfloat16*)dm(2 * (size_t)2 * B * heads * cap * hd);
+        auto* dctx = (__nv_bfloat16*)dm(2 * (size_t)T * h);
+        auto* dsegs = (SampleSeg*)dm(sizeof(SampleSeg) * B);
+        auto* dq_idx = (int32_t*)dm(4 * (size_t)T);
+        auto* dplans = (Plan*)dm(sizeof(Plan) * T);
+        uint8_t* dpad = pad ? (uint8_t*)dm((size_t)B * cap) : nullptr;
+        auto* po = (float*)dm(sizeof(float) * 256 * heads * max_splits * kQT * hd);
+        auto* pml = (float*)dm(sizeof(float) * 256 * heads * max_splits * kQT * 2);
+        auto* cnt = (int*)dm(sizeof(int) * 256 * heads);
+        auto* work = (int*)dm(sizeof(int) * 2);
+        CUDA_OK(cudaMemcpy(dq, q, 2 * (size_t)T * h, cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMemcpy(dkv, kv, 2 * (size_t)2 * B * heads * cap * hd, cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMemcpy(dsegs, segs.data(), sizeof(SampleSeg) * B, cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMemcpy(dq_idx, qidx.data(), 4 * (size_t)T, cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMemcpy(dplans, plans.data(), sizeof(Plan) * T, cudaMemcpyHostToDevice));
+        if (pad) CUDA_OK(cudaMemcpy(dpad, pad, (size_t)B * cap, cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMemset(cnt, 0, sizeof(int) * 256 * heads));
+        CUDA_OK(cudaMemset(dctx, 0xff, 2 * (size_t)T * h));  // NaN: every row must be written
+        const int64_t rows = (int64_t)2 * B * heads * cap;
+        CUtensorMap m128 = make_tmap_2d(dkv, rows, hd, 128), m64 = make_tmap_2d(dkv, rows, hd, 64),
+                    m32 = make_tmap_2d(dkv, rows, hd, 32), mq = make_tmap_2d(dq, T, h, 1);
+        AttnArgs at{};
+        at.q = dq;
+        at.kv = dkv;
+        at.plans = dplans;
+        at.segs = dsegs;
+        at.qidx = dq_idx;
+        at.pad = dpad;
+        at.ctx = dctx;
+        at.part_o = po;
+        at.part_ml = pml;
+        at.cnt = cnt;
+        at.max_splits = max_splits;
+        at.h = h;
+        at.heads = heads;
+        at.B = B;
+        at.cap = cap;
+        at.layer = 0;
+        at.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+        const int qtiles = (max_q + kQT - 1) / kQT;
+        cudaEvent_t e0, e1;
+        CUDA_OK(cudaEventCreate(&e0));
+        CUDA_OK(cudaEventCreate(&e1));
+        for (int rep = 0; rep < 2; ++rep) {  // the second launch is timed (and must give the same bits)
+            CUDA_OK(cudaMemset(work, 0, sizeof(int) * 2));
+            at.work = work;
+            CUDA_OK(cudaEventRecord(e0));
+            launch_attention(at, m128, m64, m32, mq, hd, qtiles, max_kv, 0);
+            CUDA_OK(cudaEventRecord(e1));
+            CUDA_OK(cudaDeviceSynchronize());
+        }
+        float ms = 0.0f;
+        CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (usec) *usec = ms * 1000.0f;
+        CUDA_OK(cudaMemcpy(ctx, dctx, 2 * (size_t)T * h, cudaMemcpyDeviceToHost));
+        for (void* p : mem) dfree(p);
+        return 0;
+    } catch (const Error& e) {
+        for (void* p : mem) dfree(p);
+        fprintf(stderr, "sd_debug_attention: %s\n", e.what());
+        return e.code;
+    }
+}
+

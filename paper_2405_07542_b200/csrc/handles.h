@@ -73,6 +73,8 @@ void forward_fast(const Model& m, Cache& c, Workspace& ws, int T, bool want_logi
 void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch& db, int t0, bool want_logits,
                       cudaStream_t st);
 void prepare_fast_kernels();
+// allocate the bf16 forward's buffers now (not lazily inside a graph capture)
+void ensure_fast_workspace(const Model& m, Cache& c, Workspace& ws);
 void profile_enable(bool on);
 bool profile_on();
 void profile_read(double* out, int kinds);

@@ -225,9 +225,11 @@ sd_session* session_create(sd_model* m, const sd_engine_config& e, int capacity,
         s->accepted = ialloc(s, (size_t)B * (s->kcap + 1));
         CUDA_OK(cudaMallocHost(&s->h_flag, 16));
         s->cache->ws.ensure(m->m, s->cache->c, 256);
+        ensure_fast_workspace(m->m, s->cache->c, s->cache->ws);
         if (s->draft) {
             s->dcache.reset(create_cache(draft, B, capacity, UNPAD));
             s->dcache->ws.ensure(draft->m, s->dcache->c, 256);
+            ensure_fast_workspace(draft->m, s->dcache->c, s->dcache->ws);
             s->dcommit = ialloc(s, B);
             s->lsnap = ialloc(s, B);
         }

@@ -88,6 +88,7 @@ def lib() -> C.CDLL:
         "sd_model_checksum": ([vp, C.POINTER(C.c_uint64)], C.c_int),
         "sd_model_get_config": ([vp, C.POINTER(_ModelConfigT)], C.c_int),
         "sd_model_weight_bytes": ([vp], C.c_int64),
+        "sd_model_get_tensor": ([vp, C.c_int, C.c_int, np.ctypeslib.ndpointer(np.float32), C.c_int64], C.c_int),
         "sd_model_destroy": ([vp], None),
         "sd_cache_create": ([vp, C.c_int, C.c_int, C.c_int, pp], C.c_int),
         "sd_cache_committed_len": ([vp, C.c_int, C.POINTER(C.c_int32)], C.c_int),
@@ -298,6 +299,30 @@ class Model:
 
     def weight_bytes(self) -> int:
         return int(lib().sd_model_weight_bytes(self._h))
+
+    # weight access for independent reimplementations (model.hpp:81-87)
+    MODEL_TENSORS = ["token_embedding", "position_embedding", "final_ln_gain", "final_ln_bias", "lm_head"]
+    LAYER_TENSORS = ["ln1_gain", "ln1_bias", "wq", "bq", "wk", "bk", "wv", "bv", "wo", "bo", "ln2_gain", "ln2_bias",
+                     "w_fc", "b_fc", "w_proj", "b_proj"]
+
+    def tensor(self, name: str, layer: int = -1) -> np.ndarray:
+        c = self.config
+        h, m, V, P = c.hidden(), c.mlp_hidden(), c.vocab_size, c.max_positions
+        if layer < 0:
+            idx = self.MODEL_TENSORS.index(name)
+            shape = [(V, h), (P, h), (h,), (h,), (V, h)][idx]
+        else:
+            idx = self.LAYER_TENSORS.index(name)
+            shape = {"w_fc": (m, h), "b_fc": (m,), "w_proj": (h, m)}.get(name, (h, h) if name[0] == "w" else (h,))
+        out = np.empty(int(np.prod(shape)), np.float32)
+        _check(lib().sd_model_get_tensor(self._h, layer, idx, out, out.size))
+        return out.reshape(shape)
+
+    def tensors(self) -> dict:
+        """Every weight as fp32: {"token_embedding": ..., "layers": [{...}, ...], ...}."""
+        d = {n: self.tensor(n) for n in self.MODEL_TENSORS}
+        d["layers"] = [{n: self.tensor(n, l) for n in self.LAYER_TENSORS} for l in range(self.config.num_layers)]
+        return d
 
     def forward(self, batch: RaggedBatch, cache: "CacheArena", slots, want_logits: bool = True):
         """Model::forward (model.cpp:235-254). Returns (logits [T,V] or None, argmax [T])."""
