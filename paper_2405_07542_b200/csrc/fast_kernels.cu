@@ -165,6 +165,7 @@ constexpr int kTcKeys = 128;  // keys per K/V chunk (the S^T MMA's M)
 // 307-320).  A tile whose extent fits one split writes its context rows
 // directly; otherwise every split stores (max, sum, unnormalised O) partials
 // and the last split to finish folds them in split order (deterministic).
+// The fold runs on a dedicated warp, off the softmax warps' critical path.
 //   warp 4     TMA producer: the item's Q rows (one-row boxes into a swizzled
 //              K-major tile) and its 128-key K/V chunks into a kPS-stage
 //              ring, running ahead across items; it also publishes each
@@ -176,9 +177,13 @@ constexpr int kTcKeys = 128;  // keys per K/V chunk (the S^T MMA's M)
 //              softmax with a lazy reference max (rescale O^T in TMEM only
 //              when the max grows by more than 2^8), P^T to smem; at the
 //              item end O^T / l -> the context row (thread = hd), or the
-//              split partial + combine.
-constexpr int kPS = 3, kPQ = 2, kPThreads = 192;
+//              split partial, handed to
+//   warp 6     combiner: counts the tile's arrived splits; the CTA holding
+//              the last one folds all partials in split order (loads of a
+//              whole split in flight at once) into the context rows.
+constexpr int kPS = 3, kPQ = 2, kPThreads = 224, kCQ = 4;
 constexpr int kSplitKeys = 1024;  // keys per KV split (8 chunks)
+constexpr int kMaxSplits = 8;     // splits per tile the combiner folds (cap <= 8192 keys)
 // stage = K boxes then V boxes (one 64-column box per 64 of head_dim)
 template <int HD>
 constexpr int kPStageB = 2 * (HD / 64) * kTcKeys * 128;
@@ -213,7 +218,10 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
     __shared__ int4 sq_item[kPQ];
     __shared__ uint32_t tslot;
     __shared__ float sMx[8], sL[8];
-    __shared__ int s_last;
+    // softmax -> combiner queue: {tile's first packed row, head, splits, queries}
+    __shared__ int4 cq[kCQ];
+    __shared__ uint64_t cfull[kCQ], cempty[kCQ];
+    __shared__ float c_ml[kMaxSplits * kQT][2], c_f[kMaxSplits][kQT], c_l[kQT];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, tid = threadIdx.x;
     // a tail chunk of <= 64 keys loads half a stage: keep the other half finite (zero) once
     for (int i = tid; i < kPS * kPStage / 16; i += kPThreads) ((uint4*)ring)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -237,6 +245,10 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
             ptx::mbar_init(&pvdone[i], 1);
         }
         ptx::mbar_init(&ofree, 128);
+        for (int i = 0; i < kCQ; ++i) {
+            ptx::mbar_init(&cfull[i], 1);
+            ptx::mbar_init(&cempty[i], 1);
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 5) ptx::tmem_alloc32(&tslot);
@@ -245,7 +257,8 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
     // heads x qtiles x splits(kv_len) consecutive items, the splits of one
     // (head, tile) adjacent so they finish together.  The segs are safe to
     // read before griddepcontrol.wait under a.pre_ok (see the producer).
-    __shared__ int s_order[256], s_item0[257];
+    __shared__ uint8_t s_order[256];  // B <= 256 (two HD = 64 CTAs must fit one SM)
+    __shared__ int s_item0[257];
     if (!a.pre_ok) pdl_wait();
     for (int x = tid; x < a.B; x += kPThreads) {
         const int lx = a.segs[x].kv_len;
@@ -463,10 +476,83 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                 }
             }
         }
+    } else if (warp == 6) {
+        // ------------------------------------------------------------ combiner
+        int cqs = 0;
+        uint32_t cph = 0;
+        constexpr int kPer = HD / 32;  // context columns per lane
+        for (;;) {
+            ptx::mbar_wait(&cfull[cqs], cph);
+            const int4 e = cq[cqs];
+            if (e.x < 0) break;
+            const int tile_tok = e.x, head = e.y, ns = e.z, nq = e.w;
+            int last = 0;
+            if (lane == 0) last = atomicAdd(&a.cnt[(size_t)tile_tok * a.heads + head], 1) == ns - 1;
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {  // every split of the tile has landed: fold them in split order
+                __threadfence();
+                const size_t pbase = ((size_t)tile_tok * a.heads + head) * a.max_splits;
+                for (int j = lane; j < ns * kQT; j += 32) {  // (max, sum) of every split and query
+                    const int k = j / kQT, q = j % kQT;
+                    if (q < nq) {
+                        c_ml[j][0] = __ldcg(&a.part_ml[((pbase + k) * kQT + q) * 2]);
+                        c_ml[j][1] = __ldcg(&a.part_ml[((pbase + k) * kQT + q) * 2 + 1]);
+                    }
+                }
+                __syncwarp();
+                if (lane < nq) {
+                    const int q = lane;
+                    float M = -INFINITY;
+                    for (int k = 0; k < ns; ++k) M = fmaxf(M, c_ml[k * kQT + q][0]);
+                    float L = 0.0f;
+                    for (int k = 0; k < ns; ++k) {
+                        const float mk = c_ml[k * kQT + q][0];
+                        const float f = mk == -INFINITY ? 0.0f : exp2f(mk - M);
+                        c_f[k][q] = f;
+                        L += c_ml[k * kQT + q][1] * f;
+                    }
+                    c_l[q] = L;
+                }
+                __syncwarp();
+                float acc[kQT][kPer];
+#pragma unroll
+                for (int q = 0; q < kQT; ++q)
+#pragma unroll
+                    for (int j = 0; j < kPer; ++j) acc[q][j] = 0.0f;
+                for (int k = 0; k < ns; ++k) {  // one split's rows in flight at once
+                    float v[kQT][kPer];
+#pragma unroll
+                    for (int q = 0; q < kQT; ++q)
+#pragma unroll
+                        for (int j = 0; j < kPer; ++j)
+                            v[q][j] = q < nq ? __ldcg(&a.part_o[((pbase + k) * kQT + q) * HD + lane * kPer + j]) : 0.0f;
+#pragma unroll
+                    for (int q = 0; q < kQT; ++q)
+#pragma unroll
+                        for (int j = 0; j < kPer; ++j)
+                            if (q < nq && c_f[k][q] != 0.0f) acc[q][j] += v[q][j] * c_f[k][q];
+                }
+#pragma unroll
+                for (int q = 0; q < kQT; ++q) {
+                    if (q >= nq) break;
+                    const int tok = a.qidx[tile_tok + q];
+#pragma unroll
+                    for (int j = 0; j < kPer; ++j)
+                        a.ctx[(size_t)tok * a.h + head * HD + lane * kPer + j] = __float2bfloat16_rn(acc[q][j] / c_l[q]);
+                }
+                if (lane == 0) a.cnt[(size_t)tile_tok * a.heads + head] = 0;  // self-resetting
+                __syncwarp();
+            }
+            if (lane == 0) ptx::mbar_arrive(&cempty[cqs]);
+            if (++cqs == kCQ) {
+                cqs = 0;
+                cph ^= 1;
+            }
+        }
     } else {
         // ------------------------------------------------------------ softmax warps
-        int qs = 0;
-        uint32_t qph = 0, gc = 0;
+        int qs = 0, cqs = 0;
+        uint32_t qph = 0, gc = 0, cph = 0;
         const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
         for (;;) {
             ptx::mbar_wait(&qfull[qs], qph);
@@ -477,7 +563,14 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                 qs = 0;
                 qph ^= 1;
             }
-            if (it.x < 0) break;
+            if (it.x < 0) {  // end of work: release the combiner
+                if (tid == 0) {
+                    ptx::mbar_wait(&cempty[cqs], cph ^ 1);
+                    cq[cqs] = make_int4(-1, 0, 0, 0);
+                    ptx::mbar_arrive(&cfull[cqs]);
+                }
+                break;
+            }
             int s, head, qt, split;
             decode(it.x, s, head, qt, split);
             const int k_lo = it.y, nch = it.z, ns = it.w;
@@ -596,27 +689,16 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                         a.part_ml[((pbase + split) * kQT + q) * 2 + 1] = sL[q];
                     }
                 }
-                __threadfence();
+                __threadfence();  // this split's partial is visible before it is counted
                 ptx::named_bar_sync(1, 128);
-                if (tid == 0) s_last = atomicAdd(&a.cnt[(size_t)tile_tok * a.heads + head], 1) == ns - 1;
-                ptx::named_bar_sync(1, 128);
-                if (s_last) {  // every split landed: fold them in split order
-                    __threadfence();
-                    for (int q = 0; q < nq; ++q) {
-                        float M = -INFINITY;
-                        for (int k = 0; k < ns; ++k) M = fmaxf(M, __ldcg(&a.part_ml[((pbase + k) * kQT + q) * 2]));
-                        float L = 0.0f, O = 0.0f;
-                        for (int k = 0; k < ns; ++k) {
-                            const float mk = __ldcg(&a.part_ml[((pbase + k) * kQT + q) * 2]);
-                            if (mk == -INFINITY) continue;
-                            const float f = exp2f(mk - M);
-                            L += __ldcg(&a.part_ml[((pbase + k) * kQT + q) * 2 + 1]) * f;
-                            if (tid < HD) O += __ldcg(&a.part_o[((pbase + k) * kQT + q) * HD + tid]) * f;
-                        }
-                        const int tok = a.qidx[tile_tok + q];
-                        if (tid < HD) a.ctx[(size_t)tok * a.h + head * HD + tid] = __float2bfloat16_rn(O / L);
-                    }
-                    if (tid == 0) a.cnt[(size_t)tile_tok * a.heads + head] = 0;  // self-resetting
+                if (tid == 0) {  // hand the tile to the combiner warp
+                    ptx::mbar_wait(&cempty[cqs], cph ^ 1);
+                    cq[cqs] = make_int4(tile_tok, head, ns, nq);
+                    ptx::mbar_arrive(&cfull[cqs]);
+                }
+                if (++cqs == kCQ) {
+                    cqs = 0;
+                    cph ^= 1;
                 }
             }
             gc += nch;
@@ -637,6 +719,7 @@ T* walloc(FastWorkspace* f, size_t n) {
 FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     FastWorkspace* f = ws.fast;
     if (f && f->B >= c.B && f->cap >= c.cap) return f;
+    SD_CHECK(c.B <= 256, CONFIG, "bf16 mode holds at most 256 samples per cache");
     free_fast_workspace(f);
     f = new FastWorkspace();
     const Config& cfg = m.cfg;
@@ -667,6 +750,8 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     f->q_map = make_tmap_2d(f->q, (int64_t)T, (int64_t)h, 1);
     f->attn_work = walloc<int>(f, (size_t)cfg.num_layers);
     f->max_splits = (c.cap + kSplitKeys - 1) / kSplitKeys;
+    SD_CHECK(f->max_splits <= kMaxSplits, CONFIG,
+             "cache capacity above " + std::to_string(kMaxSplits * kSplitKeys) + " positions per sample");
     f->part_o = walloc<float>(f, T * cfg.num_heads * f->max_splits * kQT * cfg.head_dim);
     f->part_ml = walloc<float>(f, T * cfg.num_heads * f->max_splits * kQT * 2);
     f->attn_cnt = walloc<int>(f, T * cfg.num_heads);
@@ -979,6 +1064,7 @@ extern "C" int sd_debug_attention(const uint16_t* q, const uint16_t* kv, int B, 
         }
         SD_CHECK(T >= 1 && T <= 256, CONFIG, "1..256 query rows");
         const int h = heads * hd, max_splits = (cap + kSplitKeys - 1) / kSplitKeys;
+        SD_CHECK(max_splits <= kMaxSplits, CONFIG, "capacity above the combiner's split bound");
         prepare_fast_kernels();
         auto* dq = (__nv_bfloat16*)dm(2 * (size_t)T * h);
         auto* dkv = (__nv_bfloat16*)dm(2 * (size_t)2 * B * heads * cap * hd);
