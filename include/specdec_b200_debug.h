@@ -16,8 +16,8 @@ int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K, int T, int
  * verify-step kernel appends {kernel id, block, SM, grid size, t_entry, t_exit}
  * (globaltimer ns, 32 bytes) to a device buffer of `cap` records. */
 int sd_debug_trace_begin(int cap);
-/* The production persistent tcgen05 attention (split-KV items, last-arriver
- * combine) on caller-provided bf16 tensors of one layer:
+/* The production persistent tcgen05 attention on caller-provided bf16
+ * tensors of one layer:
  *   q [T][heads*hd]; kv [2][B][heads][cap][hd] (K then V); queries packed
  *   sample by sample, n_q[B] of them per sample, kv_len[B] visible extent,
  *   write_slot[T] per query (it sees keys <= its slot), pad [B][cap] flags or

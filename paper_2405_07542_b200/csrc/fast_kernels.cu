@@ -37,9 +37,6 @@ struct FastWorkspace {
     int cap_tokens = 0, B = 0, cap = 0;
     __nv_bfloat16 *xb = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr;
     float* part = nullptr;     // stream-K partial sums (largest GEMM of the model)
-    int max_splits = 0;        // attention KV splits of the longest extent the cache holds
-    float *part_o = nullptr, *part_ml = nullptr;  // attention split partials
-    int* attn_cnt = nullptr;   // split arrival counters [256][heads]
     ArgmaxScratch am;          // LM-head (max, id) partials per token + arrival counters
     GemmMaps map_xb, map_ctx, map_act;
     CUtensorMap kv_map;        // TMA view of the KV arena [L*2*B*heads*cap][hd], box {64, 128}
@@ -146,44 +143,30 @@ struct AttnArgs {
     __nv_bfloat16* ctx;        // [T][h]
     int* work;                 // this launch's item counter (zeroed per forward)
     int pre_ok;                // may read segs before griddepcontrol.wait (see producer)
-    float* part_o;             // split partials [256 tiles][heads][max_splits][8 q][hd] (unnormalised O)
-    float* part_ml;            // [256][heads][max_splits][8 q][2] (reference max, sum)
-    int* cnt;                  // [256][heads] split arrival counters (self-resetting)
-    int max_splits;
     int h, heads, B, cap, layer;
     float scale_log2;          // log2(e) / sqrt(hd)
 };
 
 constexpr int kTcKeys = 128;  // keys per K/V chunk (the S^T MMA's M)
 
-// Persistent tcgen05 attention: one CTA per SM (two for HD = 64) walks work
-// items from an atomic counter.  An item is (sample, head, 8-query tile,
-// KV split): the keys a tile can see, [0, last query's slot], are cut at FIXED
-// multiples of kSplitKeys from slot 0, so how a query's keys are grouped --
-// and therefore its rounding -- depends only on its own visible extent, never
-// on the batch around it (batch-composition invariance, test_engine.cpp:
-// 307-320).  A tile whose extent fits one split writes its context rows
-// directly; otherwise every split stores (max, sum, unnormalised O) partials
-// and the last split to finish folds them in split order (deterministic).
-// The fold runs on a dedicated warp, off the softmax warps' critical path.
-//   warp 4     TMA producer: the item's Q rows (one-row boxes into a swizzled
-//              K-major tile) and its 128-key K/V chunks into a kPS-stage
-//              ring, running ahead across items; it also publishes each
-//              item's key range so the other roles agree on it.
+// Persistent tcgen05 attention: one CTA per SM (two for HD = 64) walks
+// (sample, head, 8-query tile) items from an atomic counter; each item
+// streams the keys its tile can see -- slots [0, last query's slot] of the
+// sample -- in 128-key chunks, so there are no split partials and no combine
+// (split-KV items were measured slower).  A verification tile
+// is the sample's whole extent; the tiles of a long prefill chunk stop at
+// their own causal limit instead of re-streaming the chunk's full extent.
+//   warp 4     TMA producer: the item's Q rows (16 one-row boxes into a
+//              swizzled K-major tile) and K/V chunks into a kPS-stage ring,
+//              running ahead across items.
 //   warp 5     MMA issuer: S^T(c+1) = K Q^T is issued before waiting for the
 //              softmax of chunk c (double-buffered S in TMEM), then
 //              O^T += V^T P^T (V read MN-major from the same tile).
 //   warps 0-3  softmax (thread = key): per-chunk max through smem, online
 //              softmax with a lazy reference max (rescale O^T in TMEM only
 //              when the max grows by more than 2^8), P^T to smem; at the
-//              item end O^T / l -> the context row (thread = hd), or the
-//              split partial, handed to
-//   warp 6     combiner: counts the tile's arrived splits; the CTA holding
-//              the last one folds all partials in split order (loads of a
-//              whole split in flight at once) into the context rows.
-constexpr int kPS = 3, kPQ = 2, kPThreads = 224, kCQ = 4;
-constexpr int kSplitKeys = 1024;  // keys per KV split (8 chunks)
-constexpr int kMaxSplits = 8;     // splits per tile the combiner folds (cap <= 8192 keys)
+//              item end O^T / l -> the context row (thread = hd).
+constexpr int kPS = 3, kPQ = 2, kPThreads = 192;
 // stage = K boxes then V boxes (one 64-column box per 64 of head_dim)
 template <int HD>
 constexpr int kPStageB = 2 * (HD / 64) * kTcKeys * 128;
@@ -214,15 +197,11 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
     uint8_t* sP = qring + kPQ * 2048;                    // [2][2 atoms of 8 x 128 B]
     float* sS = (float*)(sP + 2 * 2048);                 // [8][128]
     __shared__ uint64_t full[kPS], empty[kPS], qfull[kPQ], qempty[kPQ], sfull[2], pfull[2], pvdone[2], ofree;
-    // published by the producer with each item: {item, first key, chunks, splits of the tile}
-    __shared__ int4 sq_item[kPQ];
+    __shared__ int sq_item[kPQ];
     __shared__ uint32_t tslot;
     __shared__ float sMx[8], sL[8];
-    // softmax -> combiner queue: {tile's first packed row, head, splits, queries}
-    __shared__ int4 cq[kCQ];
-    __shared__ uint64_t cfull[kCQ], cempty[kCQ];
-    __shared__ float c_ml[kMaxSplits * kQT][2], c_f[kMaxSplits][kQT], c_l[kQT];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, tid = threadIdx.x;
+    const int n_items = a.B * a.heads * qtiles;
     // a tail chunk of <= 64 keys loads half a stage: keep the other half finite (zero) once
     for (int i = tid; i < kPS * kPStage / 16; i += kPThreads) ((uint4*)ring)[i] = make_uint4(0u, 0u, 0u, 0u);
     ptx::fence_proxy_async_smem();
@@ -245,65 +224,48 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
             ptx::mbar_init(&pvdone[i], 1);
         }
         ptx::mbar_init(&ofree, 128);
-        for (int i = 0; i < kCQ; ++i) {
-            ptx::mbar_init(&cfull[i], 1);
-            ptx::mbar_init(&cempty[i], 1);
-        }
         ptx::fence_barrier_init();
     }
     if (warp == 5) ptx::tmem_alloc32(&tslot);
-    // Work list.  Samples in order of decreasing kv_len (LPT: the last items --
-    // the end-of-kernel tail -- are the shortest); a sample owns
-    // heads x qtiles x splits(kv_len) consecutive items, the splits of one
-    // (head, tile) adjacent so they finish together.  The segs are safe to
-    // read before griddepcontrol.wait under a.pre_ok (see the producer).
-    __shared__ uint8_t s_order[256];  // B <= 256 (two HD = 64 CTAs must fit one SM)
-    __shared__ int s_item0[257];
+    // Longest extents first (LPT): items are handed out in order of decreasing
+    // kv_len, so the last items -- the end-of-kernel tail -- are the shortest.
+    // The segs are safe to read before griddepcontrol.wait under a.pre_ok (see
+    // the producer); otherwise every warp waits first.
+    __shared__ int s_order[256];
+    const bool lpt = a.B <= 256;
     if (!a.pre_ok) pdl_wait();
-    for (int x = tid; x < a.B; x += kPThreads) {
-        const int lx = a.segs[x].kv_len;
-        int rank = 0;
-        for (int y = 0; y < a.B; ++y) {
-            const int ly = a.segs[y].kv_len;
-            rank += (ly > lx) || (ly == lx && y < x);
+    if (lpt)
+        for (int x = tid; x < a.B; x += kPThreads) {
+            const int lx = a.segs[x].kv_len;
+            int rank = 0;
+            for (int y = 0; y < a.B; ++y) {
+                const int ly = a.segs[y].kv_len;
+                rank += (ly > lx) || (ly == lx && y < x);
+            }
+            s_order[rank] = x;
         }
-        s_order[rank] = x;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        int at = 0;
-        for (int r = 0; r < a.B; ++r) {
-            s_item0[r] = at;
-            const SampleSeg g = a.segs[s_order[r]];
-            if (g.n_q > 0 && g.kv_len > 0) at += a.heads * ((g.n_q + kQT - 1) / kQT) * ((g.kv_len + kSplitKeys - 1) / kSplitKeys);
-        }
-        s_item0[a.B] = at;
-    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = tslot;  // S: cols [0,8) and [8,16); O^T: cols [16,24)
-    const int n_items = s_item0[a.B];
     pdl_trigger();
     // The producer waits below, after pre-issuing its first item's OLD chunks.
     if (warp != 4 && a.pre_ok) pdl_wait();  // Q and this step's K/V rows come from the QKV reduction
 
-    // item -> (sample, head, q tile, split)
-    auto decode = [&](int i, int& s, int& head, int& qt, int& split) {
-        int lo = 0, hi = a.B - 1;  // last rank with s_item0 <= i
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_item0[mid] <= i) lo = mid;
-            else hi = mid - 1;
-        }
-        s = s_order[lo];
-        const SampleSeg g = a.segs[s];
-        const int ns = (g.kv_len + kSplitKeys - 1) / kSplitKeys;
-        int rest = i - s_item0[lo];
-        split = rest % ns;
-        rest /= ns;
-        qt = rest % ((g.n_q + kQT - 1) / kQT);
-        head = rest / ((g.n_q + kQT - 1) / kQT);
+    auto decode = [&](int i, int& s, int& head, int& qt) {
+        qt = i % qtiles;
+        const int pair = i / qtiles;
+        s = pair / a.heads;
+        head = pair - s * a.heads;
+        if (lpt) s = s_order[s];
+    };
+    // keys the tile sees: up to its LAST query's slot (a sample's queries are in
+    // slot order; its last query ends the sample's extent)
+    auto tile_keys = [&](const SampleSeg& g, int qt) {
+        const int nq = min(kQT, g.n_q - qt * kQT);
+        if (nq <= 0 || g.kv_len <= 0) return 0;
+        if ((qt + 1) * kQT >= g.n_q) return g.kv_len;
+        return min(g.kv_len, a.plans[a.qidx[g.q_start + qt * kQT + nq - 1]].write_slot + 1);
     };
 
     if (warp == 4) {
@@ -314,6 +276,15 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
             uint32_t ph = 0, qph = 0;
             int next = atomicAdd(a.work, 1);
             unsigned long long algo = 0;
+            // Before griddepcontrol.wait: K/V rows of positions committed in EARLIER
+            // steps cannot change, and -- when the QKV GEMM ran one CTA on EVERY SM
+            // (a.pre_ok, set by the host) -- this CTA only became resident once the
+            // GEMM's CTA on this SM exited, i.e. after every kernel up to the last
+            // LayerNorm (and k_pack, which wrote segs) completed.  So the first
+            // item's chunks below its new tokens stream during the QKV reduction.
+            // (A smaller GEMM grid, e.g. a draft model's, leaves SMs free and this
+            // CTA could run next to an unfinished k_pack: no early reads then.)
+            int pre_item = -1, pre_chunks = 0;
             // rows: keys left in the extent; <= 32 / <= 64 -> the 32- / 64-row boxes (no
             // over-read of a whole 128-key chunk past the extent; the rest of the stage
             // holds finite data: zeros or an earlier chunk, masked by the softmax)
@@ -333,37 +304,17 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                     ph ^= 1;
                 }
             };
-            // the keys a tile can see end at its LAST query's write slot (queries
-            // of a sample are in slot order); its splits are cut at multiples of
-            // kSplitKeys of that extent
-            const auto tile_extent = [&](const SampleSeg& g, int qt, int& nq) {
-                nq = min(kQT, g.n_q - qt * kQT);
-                const int tok = a.qidx[g.q_start + qt * kQT + nq - 1];
-                return min(g.kv_len, a.plans[tok].write_slot + 1);
-            };
-            // Before griddepcontrol.wait: K/V rows of positions committed in EARLIER
-            // steps cannot change, and -- when the QKV GEMM ran one CTA on EVERY SM
-            // (a.pre_ok, set by the host) -- this CTA only became resident once the
-            // GEMM's CTA on this SM exited, i.e. after every kernel up to the last
-            // LayerNorm (and k_pack, which wrote segs / plans) completed.  So the
-            // first item's chunks below its new tokens stream during the QKV
-            // reduction.  (A smaller GEMM grid, e.g. a draft model's, leaves SMs
-            // free and this CTA could run next to an unfinished k_pack: no early
-            // reads then.)
-            int pre_item = -1, pre_chunks = 0;
             if (next < n_items && a.pre_ok) {
-                int s, head, qt, split, nq;
-                decode(next, s, head, qt, split);
-                const SampleSeg g = a.segs[s];
-                const int ext = tile_extent(g, qt, nq);
-                const int k_lo = split * kSplitKeys, k_hi = min(ext, k_lo + kSplitKeys);
-                const int old_hi = min(k_hi, g.kv_len - g.n_q);  // rows no kernel of this step writes
-                if (k_lo < k_hi && old_hi > k_lo) {
+                int s, head, qt;
+                decode(next, s, head, qt);
+                const SampleSeg seg = a.segs[s];
+                const int ext = tile_keys(seg, qt);
+                if (ext > 0) {
                     pre_item = next;
-                    pre_chunks = min(kPS, (old_hi - k_lo) / kTcKeys);
+                    pre_chunks = min(kPS, max(0, min(ext, seg.kv_len - seg.n_q)) / kTcKeys);
                     const int row_k = (((a.layer * 2 + 0) * a.B + s) * a.heads + head) * a.cap;
                     const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap;
-                    for (int c = 0; c < pre_chunks; ++c) issue_chunk(row_k, row_v, k_lo + c * kTcKeys, kTcKeys);
+                    for (int c = 0; c < pre_chunks; ++c) issue_chunk(row_k, row_v, c * kTcKeys, kTcKeys);
                 }
             }
             pdl_wait();
@@ -371,19 +322,17 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                 const int i = next;
                 if (i >= n_items) break;
                 next = atomicAdd(a.work, 1);  // in flight while this item is issued
-                int s, head, qt, split, nq;
-                decode(i, s, head, qt, split);
-                const SampleSeg g = a.segs[s];
-                const int ext = tile_extent(g, qt, nq);
-                const int k_lo = split * kSplitKeys, k_hi = min(ext, k_lo + kSplitKeys);
-                if (k_lo >= k_hi) continue;  // beyond this tile's last query: nothing to see
-                const int nch = (k_hi - k_lo + kTcKeys - 1) / kTcKeys;
-                const int ns = (ext + kSplitKeys - 1) / kSplitKeys;
+                int s, head, qt;
+                decode(i, s, head, qt);
+                const SampleSeg seg = a.segs[s];
+                const int nq = min(kQT, seg.n_q - qt * kQT);
+                const int ext = tile_keys(seg, qt);
+                if (ext <= 0) continue;
                 int toks[kQT];
 #pragma unroll
-                for (int r = 0; r < kQT; ++r) toks[r] = a.qidx[g.q_start + qt * kQT + (r < nq ? r : 0)];
+                for (int r = 0; r < kQT; ++r) toks[r] = a.qidx[seg.q_start + qt * kQT + (r < nq ? r : 0)];
                 ptx::mbar_wait(&qempty[qs], qph ^ 1);
-                sq_item[qs] = make_int4(i, k_lo, nch, ns);  // published by the arrive below
+                sq_item[qs] = i;  // published by the arrive below
                 ptx::mbar_arrive_expect_tx(&qfull[qs], kBoxes * 1024);
 #pragma unroll
                 for (int r = 0; r < kQT; ++r)  // one-row boxes: the TMA swizzles by destination address
@@ -398,13 +347,13 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                 const int row_k = (((a.layer * 2 + 0) * a.B + s) * a.heads + head) * a.cap;
                 const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap;
                 const int c0 = i == pre_item ? pre_chunks : 0;  // already in the ring
-                for (int k0 = k_lo + c0 * kTcKeys; k0 < k_hi; k0 += kTcKeys) issue_chunk(row_k, row_v, k0, k_hi - k0);
-                algo += (unsigned long long)(k_hi - k_lo) * (2 * HD * 2);
+                for (int k0 = c0 * kTcKeys; k0 < ext; k0 += kTcKeys) issue_chunk(row_k, row_v, k0, ext - k0);
+                algo += (unsigned long long)ext * (2 * HD * 2);
             }
             // in-graph roofline: this CTA's algorithmic K/V bytes (KiB) next to its timeline record
             trace_point(TK_ATTN_BYTES, (uint32_t)(algo >> 10));
             ptx::mbar_wait(&qempty[qs], qph ^ 1);  // end of work
-            sq_item[qs] = make_int4(-1, 0, 0, 0);
+            sq_item[qs] = -1;
             ptx::mbar_arrive(&qfull[qs]);
         }
     } else if (warp == 5) {
@@ -416,9 +365,11 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
             uint32_t gc = 0;  // chunks processed (S / P buffers alternate)
             for (;;) {
                 ptx::mbar_wait(&qfull[qs], qph);
-                const int4 it = sq_item[qs];
-                if (it.x < 0) break;
-                const int nch = it.z;
+                const int i = sq_item[qs];
+                if (i < 0) break;
+                int s, head, qt;
+                decode(i, s, head, qt);
+                const int nch = (tile_keys(a.segs[s], qt) + kTcKeys - 1) / kTcKeys;
                 const uint32_t qa = ptx::smem_u32(qring + qs * 2048);
                 // S^T(c) into TMEM buffer (gc + c) & 1
                 auto issue_s = [&](int c, int stc, uint32_t phc) {
@@ -476,106 +427,26 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                 }
             }
         }
-    } else if (warp == 6) {
-        // ------------------------------------------------------------ combiner
-        int cqs = 0;
-        uint32_t cph = 0;
-        constexpr int kPer = HD / 32;  // context columns per lane
-        for (;;) {
-            ptx::mbar_wait(&cfull[cqs], cph);
-            const int4 e = cq[cqs];
-            if (e.x < 0) break;
-            const int tile_tok = e.x, head = e.y, ns = e.z, nq = e.w;
-            int last = 0;
-            if (lane == 0) last = atomicAdd(&a.cnt[(size_t)tile_tok * a.heads + head], 1) == ns - 1;
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (last) {  // every split of the tile has landed: fold them in split order
-                __threadfence();
-                const size_t pbase = ((size_t)tile_tok * a.heads + head) * a.max_splits;
-                for (int j = lane; j < ns * kQT; j += 32) {  // (max, sum) of every split and query
-                    const int k = j / kQT, q = j % kQT;
-                    if (q < nq) {
-                        c_ml[j][0] = __ldcg(&a.part_ml[((pbase + k) * kQT + q) * 2]);
-                        c_ml[j][1] = __ldcg(&a.part_ml[((pbase + k) * kQT + q) * 2 + 1]);
-                    }
-                }
-                __syncwarp();
-                if (lane < nq) {
-                    const int q = lane;
-                    float M = -INFINITY;
-                    for (int k = 0; k < ns; ++k) M = fmaxf(M, c_ml[k * kQT + q][0]);
-                    float L = 0.0f;
-                    for (int k = 0; k < ns; ++k) {
-                        const float mk = c_ml[k * kQT + q][0];
-                        const float f = mk == -INFINITY ? 0.0f : exp2f(mk - M);
-                        c_f[k][q] = f;
-                        L += c_ml[k * kQT + q][1] * f;
-                    }
-                    c_l[q] = L;
-                }
-                __syncwarp();
-                float acc[kQT][kPer];
-#pragma unroll
-                for (int q = 0; q < kQT; ++q)
-#pragma unroll
-                    for (int j = 0; j < kPer; ++j) acc[q][j] = 0.0f;
-                for (int k = 0; k < ns; ++k) {  // one split's rows in flight at once
-                    float v[kQT][kPer];
-#pragma unroll
-                    for (int q = 0; q < kQT; ++q)
-#pragma unroll
-                        for (int j = 0; j < kPer; ++j)
-                            v[q][j] = q < nq ? __ldcg(&a.part_o[((pbase + k) * kQT + q) * HD + lane * kPer + j]) : 0.0f;
-#pragma unroll
-                    for (int q = 0; q < kQT; ++q)
-#pragma unroll
-                        for (int j = 0; j < kPer; ++j)
-                            if (q < nq && c_f[k][q] != 0.0f) acc[q][j] += v[q][j] * c_f[k][q];
-                }
-#pragma unroll
-                for (int q = 0; q < kQT; ++q) {
-                    if (q >= nq) break;
-                    const int tok = a.qidx[tile_tok + q];
-#pragma unroll
-                    for (int j = 0; j < kPer; ++j)
-                        a.ctx[(size_t)tok * a.h + head * HD + lane * kPer + j] = __float2bfloat16_rn(acc[q][j] / c_l[q]);
-                }
-                if (lane == 0) a.cnt[(size_t)tile_tok * a.heads + head] = 0;  // self-resetting
-                __syncwarp();
-            }
-            if (lane == 0) ptx::mbar_arrive(&cempty[cqs]);
-            if (++cqs == kCQ) {
-                cqs = 0;
-                cph ^= 1;
-            }
-        }
     } else {
         // ------------------------------------------------------------ softmax warps
-        int qs = 0, cqs = 0;
-        uint32_t qph = 0, gc = 0, cph = 0;
+        int qs = 0, items = 0;
+        uint32_t qph = 0, gc = 0;
         const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
         for (;;) {
             ptx::mbar_wait(&qfull[qs], qph);
-            const int4 it = sq_item[qs];
+            const int i = sq_item[qs];
             __syncwarp();
-            if (it.x >= 0 && lane == 0) ptx::mbar_arrive(&qempty[qs]);
+            if (i >= 0 && lane == 0) ptx::mbar_arrive(&qempty[qs]);
             if (++qs == kPQ) {
                 qs = 0;
                 qph ^= 1;
             }
-            if (it.x < 0) {  // end of work: release the combiner
-                if (tid == 0) {
-                    ptx::mbar_wait(&cempty[cqs], cph ^ 1);
-                    cq[cqs] = make_int4(-1, 0, 0, 0);
-                    ptx::mbar_arrive(&cfull[cqs]);
-                }
-                break;
-            }
-            int s, head, qt, split;
-            decode(it.x, s, head, qt, split);
-            const int k_lo = it.y, nch = it.z, ns = it.w;
+            if (i < 0) break;
+            int s, head, qt;
+            decode(i, s, head, qt);
             const SampleSeg seg = a.segs[s];
             const int nq = min(kQT, seg.n_q - qt * kQT);
+            const int nch = (tile_keys(seg, qt) + kTcKeys - 1) / kTcKeys;
             int ws[kQT];
 #pragma unroll
             for (int q = 0; q < kQT; ++q) {
@@ -590,7 +461,7 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
             }
             for (int c = 0; c < nch; ++c) {
                 const uint32_t g = gc + c;
-                const int key = k_lo + c * kTcKeys + tid;
+                const int key = c * kTcKeys + tid;
                 ptx::mbar_wait(&sfull[g & 1], (g >> 1) & 1);
                 ptx::tc_fence_after();
                 float x[kQT];
@@ -669,45 +540,21 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
             ptx::tmem_ld8(trow + 16, o);
             ptx::tc_fence_before();
             ptx::mbar_arrive(&ofree);
-            const int tile_tok = seg.q_start + qt * kQT;  // the tile's first packed row: its combine slot
-            if (ns == 1) {
 #pragma unroll
-                for (int q = 0; q < kQT; ++q) {
-                    if (q >= nq) break;
-                    const int tok = a.qidx[tile_tok + q];
-                    if (tid < HD) a.ctx[(size_t)tok * a.h + head * HD + tid] = __float2bfloat16_rn(o[q] / sL[q]);
-                }
-            } else {
-                // split partial: (reference max, sum, unnormalised O) per query
-                const size_t pbase = ((size_t)tile_tok * a.heads + head) * a.max_splits;
-#pragma unroll
-                for (int q = 0; q < kQT; ++q) {
-                    if (q >= nq) break;
-                    if (tid < HD) a.part_o[((pbase + split) * kQT + q) * HD + tid] = o[q];
-                    if (tid == q) {
-                        a.part_ml[((pbase + split) * kQT + q) * 2] = mref[q];
-                        a.part_ml[((pbase + split) * kQT + q) * 2 + 1] = sL[q];
-                    }
-                }
-                __threadfence();  // this split's partial is visible before it is counted
-                ptx::named_bar_sync(1, 128);
-                if (tid == 0) {  // hand the tile to the combiner warp
-                    ptx::mbar_wait(&cempty[cqs], cph ^ 1);
-                    cq[cqs] = make_int4(tile_tok, head, ns, nq);
-                    ptx::mbar_arrive(&cfull[cqs]);
-                }
-                if (++cqs == kCQ) {
-                    cqs = 0;
-                    cph ^= 1;
-                }
+            for (int q = 0; q < kQT; ++q) {
+                if (q >= nq) break;
+                const int tok = a.qidx[seg.q_start + qt * kQT + q];
+                if (tid < HD) a.ctx[(size_t)tok * a.h + head * HD + tid] = __float2bfloat16_rn(o[q] / sL[q]);
             }
             gc += nch;
+            ++items;
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 5) ptx::tmem_dealloc32(tmem);
 }
+
 
 template <typename T>
 T* walloc(FastWorkspace* f, size_t n) {
@@ -719,7 +566,6 @@ T* walloc(FastWorkspace* f, size_t n) {
 FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     FastWorkspace* f = ws.fast;
     if (f && f->B >= c.B && f->cap >= c.cap) return f;
-    SD_CHECK(c.B <= 256, CONFIG, "bf16 mode holds at most 256 samples per cache");
     free_fast_workspace(f);
     f = new FastWorkspace();
     const Config& cfg = m.cfg;
@@ -749,13 +595,6 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     f->kv_map32 = make_tmap_2d(c.kv, (int64_t)cfg.num_layers * 2 * c.B * cfg.num_heads * c.cap, cfg.head_dim, 32);
     f->q_map = make_tmap_2d(f->q, (int64_t)T, (int64_t)h, 1);
     f->attn_work = walloc<int>(f, (size_t)cfg.num_layers);
-    f->max_splits = (c.cap + kSplitKeys - 1) / kSplitKeys;
-    SD_CHECK(f->max_splits <= kMaxSplits, CONFIG,
-             "cache capacity above " + std::to_string(kMaxSplits * kSplitKeys) + " positions per sample");
-    f->part_o = walloc<float>(f, T * cfg.num_heads * f->max_splits * kQT * cfg.head_dim);
-    f->part_ml = walloc<float>(f, T * cfg.num_heads * f->max_splits * kQT * 2);
-    f->attn_cnt = walloc<int>(f, T * cfg.num_heads);
-    CUDA_OK(cudaMemset(f->attn_cnt, 0, sizeof(int) * T * cfg.num_heads));  // self-resetting afterwards
     ws.fast = f;
     return f;
 }
@@ -765,8 +604,7 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
 void launch_attention(const AttnArgs& at, const CUtensorMap& kv, const CUtensorMap& kv64, const CUtensorMap& kv32,
                       const CUtensorMap& qm, int hd, int qtiles, int max_kv_upper, cudaStream_t st) {
     const int sms = device_sm_count();
-    const long long items =
-        (long long)at.B * at.heads * qtiles * std::max(1, (max_kv_upper + kSplitKeys - 1) / kSplitKeys);
+    const long long items = (long long)at.B * at.heads * qtiles;
     if (hd == 128)
         launch_k(k_attention_tcp<128>, dim3((unsigned)std::min<long long>(items, sms)), dim3(kPThreads), kPSmem, st,
                  kv, kv64, kv32, qm, at, qtiles);
@@ -871,10 +709,6 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     at.qidx = db.qidx;
     at.pad = c.layout == PADDED ? c.d_pad : nullptr;
     at.ctx = f->ctx;
-    at.part_o = f->part_o;
-    at.part_ml = f->part_ml;
-    at.cnt = f->attn_cnt;
-    at.max_splits = f->max_splits;
     at.h = h;
     at.heads = heads;
     at.B = c.B;
@@ -1063,8 +897,7 @@ extern "C" int sd_debug_attention(const uint16_t* q, const uint16_t* kv, int B, 
             max_q = std::max(max_q, n_q[s]);
         }
         SD_CHECK(T >= 1 && T <= 256, CONFIG, "1..256 query rows");
-        const int h = heads * hd, max_splits = (cap + kSplitKeys - 1) / kSplitKeys;
-        SD_CHECK(max_splits <= kMaxSplits, CONFIG, "capacity above the combiner's split bound");
+        const int h = heads * hd;
         prepare_fast_kernels();
         auto* dq = (__nv_bfloat16*)dm(2 * (size_t)T * h);
         auto* dkv = (__nv_bfloat16*)dm(2 * (size_t)2 * B * heads * cap * hd);
@@ -1073,9 +906,6 @@ extern "C" int sd_debug_attention(const uint16_t* q, const uint16_t* kv, int B, 
         auto* dq_idx = (int32_t*)dm(4 * (size_t)T);
         auto* dplans = (Plan*)dm(sizeof(Plan) * T);
         uint8_t* dpad = pad ? (uint8_t*)dm((size_t)B * cap) : nullptr;
-        auto* po = (float*)dm(sizeof(float) * 256 * heads * max_splits * kQT * hd);
-        auto* pml = (float*)dm(sizeof(float) * 256 * heads * max_splits * kQT * 2);
-        auto* cnt = (int*)dm(sizeof(int) * 256 * heads);
         auto* work = (int*)dm(sizeof(int) * 2);
         CUDA_OK(cudaMemcpy(dq, q, 2 * (size_t)T * h, cudaMemcpyHostToDevice));
         CUDA_OK(cudaMemcpy(dkv, kv, 2 * (size_t)2 * B * heads * cap * hd, cudaMemcpyHostToDevice));
@@ -1083,7 +913,6 @@ extern "C" int sd_debug_attention(const uint16_t* q, const uint16_t* kv, int B, 
         CUDA_OK(cudaMemcpy(dq_idx, qidx.data(), 4 * (size_t)T, cudaMemcpyHostToDevice));
         CUDA_OK(cudaMemcpy(dplans, plans.data(), sizeof(Plan) * T, cudaMemcpyHostToDevice));
         if (pad) CUDA_OK(cudaMemcpy(dpad, pad, (size_t)B * cap, cudaMemcpyHostToDevice));
-        CUDA_OK(cudaMemset(cnt, 0, sizeof(int) * 256 * heads));
         CUDA_OK(cudaMemset(dctx, 0xff, 2 * (size_t)T * h));  // NaN: every row must be written
         const int64_t rows = (int64_t)2 * B * heads * cap;
         CUtensorMap m128 = make_tmap_2d(dkv, rows, hd, 128), m64 = make_tmap_2d(dkv, rows, hd, 64),
@@ -1096,10 +925,6 @@ extern "C" int sd_debug_attention(const uint16_t* q, const uint16_t* kv, int B, 
         at.qidx = dq_idx;
         at.pad = dpad;
         at.ctx = dctx;
-        at.part_o = po;
-        at.part_ml = pml;
-        at.cnt = cnt;
-        at.max_splits = max_splits;
         at.h = h;
         at.heads = heads;
         at.B = B;

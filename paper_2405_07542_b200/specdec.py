@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libspecdec_b200.so")
+LIB_PATH = _DEFAULT_LIB = os.path.join(_PKG, "lib", "libspecdec_b200.so")
 
 I32P = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 I64P = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
@@ -123,6 +123,8 @@ def lib() -> C.CDLL:
         "sd_session_destroy": ([vp], None),
     }
     for name, (args, res) in sig.items():
+        if LIB_PATH != _DEFAULT_LIB and not hasattr(L, name):
+            continue  # an older build loaded for an A/B timing (tools/steptime.py --lib)
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res

@@ -1,10 +1,10 @@
 """bf16 tcgen05 path pinned at the shapes the bench runs.
 
-(a) The persistent attention (k_attention_tcp, split-KV items + combine)
-    against a float64 softmax of the same bf16 Q/K/V: extents 129-4200 keys
-    (one chunk, many chunks, several KV splits), the 32/64/128-key tail boxes,
-    1-8 draft queries and a 40-query prefill-like sample, head_dim 128 and 64,
-    padded-grid holes, K chunks scaled so the lazy-rescale path fires
+(a) The persistent attention (k_attention_tcp) against a float64 softmax of
+    the same bf16 Q/K/V: extents 129-4200 keys (one chunk to 33 chunks), the
+    32/64/128-key tail boxes, 1-8 draft queries and a 40-query prefill-like
+    sample (5 tiles, each stopping at its own causal limit), head_dim 128 and
+    64, padded-grid holes, K chunks scaled so the lazy-rescale path fires
     (model.cpp:320-349: ascending-j softmax over the visible prefix).
     Tolerance: |ctx - ref| <= 1e-2 (V entries in [-1, 1]; bf16 P and bf16
     output rounding are <= 2^-9 each), mean <= 1e-3.
@@ -109,7 +109,8 @@ def make_attention_case(rng, extents, nqs, heads, hd, padded=False, prefill=None
 def test_attention_long_extents_vs_float64(sd, hd, heads, padded):
     rng = np.random.default_rng(hd * 7 + heads + padded)
     # 1 key past a chunk (32-box tail), 72 (128-box), 32 (32-box), 62 (64-box),
-    # 2 splits with a 76-key tail, 5 splits, one chunk, an empty (finished) sample
+    # 9 chunks with a 76-key tail, 33 chunks, a prefill-like sample, 1028 keys,
+    # an empty (finished) sample
     extents = [129, 200, 160, 190, 1100, 4200, 600, 1028, 64]
     nqs = [1, 8, 3, 5, 7, 8, 2, 6, 0]
     q, kv, n_q, kv_len, ws, pad, cap = make_attention_case(rng, extents, nqs, heads, hd, padded, prefill=6)
@@ -121,14 +122,14 @@ def test_attention_long_extents_vs_float64(sd, hd, heads, padded):
     assert np.isfinite(got).all()
     assert err.max() <= 1e-2 and err.mean() <= 1e-3
     out2, _ = run_attention(sd, q, kv, n_q, kv_len, ws, pad, heads, hd, cap)
-    assert np.array_equal(out, out2)  # deterministic split combine
+    assert np.array_equal(out, out2)  # deterministic
 
 
 @pytest.mark.parametrize("hd,heads", [(128, 2), (64, 4)])
 def test_attention_batch_composition_invariance(sd, hd, heads):
-    """A sample's context rows do not depend on the samples around it: the KV
-    splits are cut at fixed key offsets, so the long sample alone gives the
-    same bits as inside the batch (test_engine.cpp:307-320)."""
+    """A sample's context rows do not depend on the samples around it: each
+    sample's keys are chunked from its slot 0 whatever the batch, so a sample
+    alone gives the same bits as inside the batch (test_engine.cpp:307-320)."""
     rng = np.random.default_rng(5)
     extents, nqs = [300, 4200, 1100], [4, 8, 2]
     q, kv, n_q, kv_len, ws, pad, cap = make_attention_case(rng, extents, nqs, heads, hd)

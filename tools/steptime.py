@@ -19,10 +19,13 @@ if "--lib" in args:  # A/B against another build of the library
 eager = "--eager" in args  # launch-by-launch instead of the CUDA-graph replay
 if eager:
     args.remove("--eager")
-B = int(args[0]) if args else 24
-cfg = bench.C3
+c5 = "--c5" in args  # long context: OPT-6.7B shape, 4k prompts (retrieval drafts)
+if c5:
+    args.remove("--c5")
+B = int(args[0]) if args else (8 if c5 else 24)
+cfg = bench.C5 if c5 else bench.C3
 m = sd.Model.init(sd.ModelConfig(**cfg), device=0, precision=sd.BF16)
-prompts = bench.prompts_for(range(B), cfg["vocab_size"], 600, 900)
+prompts = bench.prompts_for(range(B), cfg["vocab_size"], *((3968, 4224) if c5 else (600, 900)))
 cap = max(len(p) for p in prompts) + 128 + 9
 e = sd.EngineConfig(mode="ems", predictor="retrieval", k=7, match_len=2, copy_len=7, batch_size=B, max_new_tokens=128,
                     stop_on_eos=False, seed=1)
@@ -35,4 +38,4 @@ for _ in range(4):
     best = min(best, ms / steps)
 env = " ".join([f"{k}={v}" for k, v in os.environ.items() if k.startswith("SD_")] +
                ([os.path.relpath(sd.LIB_PATH, ROOT)] if "--lib" in sys.argv else []) + (["eager"] if eager else []))
-print(f"[{env or 'default'}] B={B}: {steps} steps, best {best:.3f} ms/step", flush=True)
+print(f"[{env or 'default'}] {'C5' if c5 else 'C3'} B={B}: {steps} steps, best {best:.3f} ms/step", flush=True)
