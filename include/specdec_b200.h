@@ -76,7 +76,9 @@ int64_t sd_kernel_launches(void);
 /* Per-launch CUDA-event timing of the bf16 forward (eager runs only; graphs
  * are not instrumented).  sd_profile_read fills out[kinds][3] = {launches,
  * total_ms, algorithmic_bytes} for kinds 0 gemm_qkv, 1 gemm_o, 2 gemm_fc,
- * 3 gemm_proj, 4 gemm_lm, 5 attention, 6 layernorm/embed, 7 misc. */
+ * 3 gemm_proj, 4 gemm_lm (each a whole GEMM stage: streaming kernel + split-K
+ * reduction + epilogue), 5 attention, 6 layernorm/embed, 7 misc, 8 the
+ * streaming GEMM kernel alone (all classes; weights + token operand bytes). */
 int sd_profile_enable(int on);
 int sd_profile_read(double* out, int kinds);
 

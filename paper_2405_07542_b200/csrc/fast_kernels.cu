@@ -622,10 +622,12 @@ void ensure_fast_workspace(const Model& m, Cache& c, Workspace& ws) { ensure_fas
 // launching stream and charge it the ALGORITHMIC bytes it must move
 // (weights + activations + KV it reads/writes once).  bench.py reads this
 // to report the dominant kernel's achieved bandwidth.
-enum ProfKind { PK_QKV, PK_O, PK_FC, PK_PROJ, PK_LM, PK_ATTN, PK_ROW, PK_MISC, PK_N };
+// PK_STREAM: the k_gemm streaming kernel alone (every GEMM class), timed from
+// the launch to an event recorded between it and its split-K reduction.
+enum ProfKind { PK_QKV, PK_O, PK_FC, PK_PROJ, PK_LM, PK_ATTN, PK_ROW, PK_MISC, PK_STREAM, PK_N };
 struct ProfRec {
     int kind;
-    cudaEvent_t a, b;
+    cudaEvent_t a, b, mid;  // mid: after the GEMM's streaming kernel (GEMM classes only)
 };
 static bool g_prof = false;
 static std::vector<ProfRec> g_prof_pending;
@@ -634,7 +636,7 @@ static double g_prof_acc[PK_N][3];  // launches, ms, bytes
 #define PROF(kind, ...)                                    \
     do {                                                   \
         if (g_prof) {                                      \
-            ProfRec r__{kind, nullptr, nullptr};           \
+            ProfRec r__{kind, nullptr, nullptr, nullptr};  \
             CUDA_OK(cudaEventCreate(&r__.a));              \
             CUDA_OK(cudaEventCreate(&r__.b));              \
             CUDA_OK(cudaEventRecord(r__.a, st));           \
@@ -644,6 +646,23 @@ static double g_prof_acc[PK_N][3];  // launches, ms, bytes
         } else {                                           \
             __VA_ARGS__;                                   \
         }                                                  \
+    } while (0)
+// a GEMM stage: the kind's time is the whole stage (stream + reduction +
+// epilogue kernels); `mid` splits off the streaming kernel
+#define PROF_GEMM(kind, epi, g, mp)                                       \
+    do {                                                                  \
+        if (g_prof) {                                                     \
+            ProfRec r__{kind, nullptr, nullptr, nullptr};                 \
+            CUDA_OK(cudaEventCreate(&r__.a));                             \
+            CUDA_OK(cudaEventCreate(&r__.b));                             \
+            CUDA_OK(cudaEventCreate(&r__.mid));                           \
+            CUDA_OK(cudaEventRecord(r__.a, st));                          \
+            gemm_launch(epi, g, mp, n, st, r__.mid);                      \
+            CUDA_OK(cudaEventRecord(r__.b, st));                          \
+            g_prof_pending.push_back(r__);                                \
+        } else {                                                          \
+            gemm_launch(epi, g, mp, n, st);                               \
+        }                                                                 \
     } while (0)
 
 bool profile_on() { return g_prof; }
@@ -731,7 +750,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         gemm_plan(g, sms);
         GemmMaps mp = f->map_xb;
         mp.A = fm->qkv[l].A;
-        PROF(PK_QKV, gemm_launch(EPI_QKV, g, mp, n, st));
+        PROF_GEMM(PK_QKV, EPI_QKV, g, mp);
         // attention
         at.layer = l;
         at.work = f->attn_work + l;
@@ -753,7 +772,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         gemm_plan(g, sms);
         mp = f->map_ctx;
         mp.A = fm->o[l].A;
-        PROF(PK_O, gemm_launch(EPI_RESID_LN, g, mp, n, st));
+        PROF_GEMM(PK_O, EPI_RESID_LN, g, mp);
         // FC + GELU
         g = base;
         g.M = mm;
@@ -765,7 +784,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         gemm_plan(g, sms);
         mp = f->map_xb;
         mp.A = fm->fc[l].A;
-        PROF(PK_FC, gemm_launch(EPI_GELU, g, mp, n, st));
+        PROF_GEMM(PK_FC, EPI_GELU, g, mp);
         // PROJ + residual, fused with the next LN1 (or the final LN) -> xb
         g = base;
         g.M = h;
@@ -780,7 +799,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         gemm_plan(g, sms);
         mp = f->map_act;
         mp.A = fm->proj[l].A;
-        PROF(PK_PROJ, gemm_launch(EPI_RESID_LN, g, mp, n, st));
+        PROF_GEMM(PK_PROJ, EPI_RESID_LN, g, mp);
         launches += 8;
     }
     // LM head + greedy argmax
@@ -796,7 +815,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     gemm_plan(g, sms);
     GemmMaps mp = f->map_xb;
     mp.A = m.fast->lm.A;
-    PROF(PK_LM, gemm_launch(EPI_ARGMAX, g, mp, n, st));
+    PROF_GEMM(PK_LM, EPI_ARGMAX, g, mp);
     launches += 2;
     note_launches(launches);
     CUDA_OK(cudaGetLastError());
@@ -816,13 +835,25 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
                               V * H * 2 + Tt * H * 2,
                               kv * 2 * hd * 2 * heads + Tt * H * 4,
                               Tt * H * 6,
+                              0,
                               0};
+        // the streaming kernel alone: weights + token operand of each class
+        const double stream_bytes[5] = {3 * H * H * 2 + Tt * H * 2, H * H * 2 + Tt * H * 2, Mm * H * 2 + Tt * H * 2,
+                                        H * Mm * 2 + Tt * Mm * 2, V * H * 2 + Tt * H * 2};
         for (auto& r : g_prof_pending) {
             float ms = 0.0f;
             CUDA_OK(cudaEventElapsedTime(&ms, r.a, r.b));
             g_prof_acc[r.kind][0] += 1;
             g_prof_acc[r.kind][1] += ms;
             g_prof_acc[r.kind][2] += bytes[r.kind];
+            if (r.mid) {
+                float ms_s = 0.0f;
+                CUDA_OK(cudaEventElapsedTime(&ms_s, r.a, r.mid));
+                g_prof_acc[PK_STREAM][0] += 1;
+                g_prof_acc[PK_STREAM][1] += ms_s;
+                g_prof_acc[PK_STREAM][2] += stream_bytes[r.kind];
+                cudaEventDestroy(r.mid);
+            }
             cudaEventDestroy(r.a);
             cudaEventDestroy(r.b);
         }

@@ -63,7 +63,9 @@ void gemm_plan(GemmArgs& a, int sms);
 // floats the partial buffer needs for a shape (max over the model's GEMMs)
 size_t gemm_part_floats(int M, int K, int sms);
 // stream the weights (tcgen05 mainloop -> fp32 partials), then reduce + epilogue
-void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, cudaStream_t st);
+// (`after_stream`, if given, is recorded between the two: profiling)
+void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, cudaStream_t st,
+                 cudaEvent_t after_stream = nullptr);
 void gemm_prepare();  // one-time kernel attributes (before any graph capture)
 
 }  // namespace sdb

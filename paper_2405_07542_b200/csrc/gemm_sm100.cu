@@ -571,13 +571,15 @@ void gemm_prepare() {
         CUDA_OK(cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
 }
 
-void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, cudaStream_t st) {
+void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, cudaStream_t st,
+                 cudaEvent_t after_stream) {
     gemm_prepare();
     SD_CHECK(T_upper <= 256, INTERNAL, "GEMM token tile is at most 256");
     GemmArgs ab = a;
     ab.box = T_upper <= 32 ? 32 : T_upper <= 64 ? 64 : T_upper <= 128 ? 128 : 256;
     launch_k(k_gemm, dim3(a.grid), dim3(kThreads), kSmemBytes, st, maps.A, maps.B[0], maps.B[1], maps.B[2],
              maps.B[3], ab);
+    if (after_stream) CUDA_OK(cudaEventRecord(after_stream, st));
     RedInfo r{a.K / kBK, a.grid, (long long)a.m_tiles * (a.K / kBK)};
     const dim3 tg(a.m_tiles, (T_upper + kRT - 1) / kRT);
     switch (epi) {

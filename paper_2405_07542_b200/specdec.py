@@ -625,7 +625,8 @@ def results_json(config: EngineConfig, result: DecodeResult) -> str:
 
 
 # ---------------------------------------------------------------- sessions
-PROFILE_KINDS = ["gemm_qkv", "gemm_o", "gemm_fc", "gemm_proj", "gemm_lm", "attention", "layernorm", "misc"]
+PROFILE_KINDS = ["gemm_qkv", "gemm_o", "gemm_fc", "gemm_proj", "gemm_lm", "attention", "layernorm", "misc",
+                 "gemm_stream"]
 
 
 def profile_enable(on: bool) -> None:

@@ -40,6 +40,41 @@ def test_prompts_are_deterministic_and_in_range():
     assert bench.prompts_for([2, 3], 1000, 20, 30) == p1[2:]
 
 
+def test_reference_steps_fixture_is_the_c3_trajectory():
+    import json
+
+    fx = json.load(open(bench.STEPS_FIXTURE))
+    steps = fx["steps"]
+    assert 50 <= len(steps) <= 130 and all(1 <= len(st) <= 24 for st in steps)
+    for st in steps:
+        for c, k, tau in st:
+            assert 600 <= c <= 900 + 128 and 0 <= k <= 7 and 1 <= tau <= k + 1
+    assert sum(tau for st in steps for _, _, tau in st) == 24 * 127  # 128 new tokens, the first from prefill
+
+
+def test_run_metrics_padding_accounting():
+    st = dict(steps=2, avg_tau=1.5, avg_padding_ratio=0.25, useful_kv_writes=10, kv_padding=3, input_padding=4,
+              accepted=6)
+    v, e = bench.run_metrics("vanilla", st, 6, 1.0), bench.run_metrics("ems", st, 6, 1.0)
+    assert e["padding_kv_writes"] == 0 and v["padding_kv_writes"] == 3
+    assert v["total_tokens_processed"] - e["total_tokens_processed"] == 3 + 4
+
+
+def test_bench_csv_columns_extend_the_reference_schema():
+    ref = ("batch_size,mode,predictor,k,total_tokens,decode_steps,avg_acceptance_length,avg_padding_ratio,"
+           "total_input_padding,total_kv_padding,useful_kv_writes,padding_kv_writes,total_tokens_processed,"
+           "decode_seconds,tokens_per_second_decode,tokens_per_second_total")  # tools/specdec_main.cpp:161-164
+    assert bench.CSV_COLUMNS.startswith(ref + ",")
+    assert bench.CSV_COLUMNS.split(",")[16:] == ["accepted_tok_s", "hbm_gbs", "roof_frac", "gpus", "cpu_cores"]
+
+
+def test_gemm_algorithmic_bytes_cover_every_launch():
+    b = bench.gemm_algorithmic_bytes(100, 40, 5120, 50272)
+    assert len(b) == 4 * 40 + 1
+    assert abs(sum(b) - (40 * 12 * 5120 ** 2 * 2 + 50272 * 5120 * 2 + 100 * 40 * (3 * 5120 + 20480) * 2
+                         + 100 * 5120 * 2)) < 1
+
+
 def test_reference_extrapolation_scales_with_layers():
     cfg = dict(bench.C3)
     one = bench.extrapolate(cfg, 1.0, 1, 14, 256)

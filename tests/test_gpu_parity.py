@@ -24,7 +24,7 @@ import math
 import numpy as np
 import pytest
 
-from torch_ref import TorchRef, parity_stats
+from torch_ref import c3_truncated_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -169,43 +169,10 @@ def test_gemm_exact_shapes_vs_float64(sd, M, K):
 
 
 # ------------------------------------------------------------------ (c)
-C3_L2 = dict(num_layers=2, num_heads=40, head_dim=128, vocab_size=50272, max_positions=2048, init_seed=0xD5EED)
-
-
-def c3_truncated_parity(sd, cfg=C3_L2, B=4, seed=1):
-    """bf16 verify-step logits of a layer-truncated C3 model vs the float64
-    reference on the fp32 weights of the same seed.  Returns parity_stats."""
-    import torch
-
-    rng = np.random.default_rng(seed)
-    V = cfg["vocab_size"]
-    prompts = [[0] + rng.integers(3, V, size=int(rng.integers(600, 660))).tolist() for _ in range(B)]
-    drafts = [rng.integers(3, V, size=1 + (3 * s) % 8).tolist() for s in range(B)]
-    m32 = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.FP32_CHECK)
-    ref = TorchRef(cfg, m32.tensors(), device="cuda", dtype=torch.float64)
-    m32.close()
-    m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.BF16)
-    c = sd.UnpadArena(m, B, 1024)
-    slots = [sd.TokenSlot(s, i) for s in range(B) for i in range(len(prompts[s]))]
-    _, am = m.forward(sd.concatenate_inputs(prompts), c, slots, want_logits=False)
-    for s in range(B):
-        c.commit_accepted(s, len(prompts[s]))
-    ends = np.cumsum([len(p) for p in prompts]) - 1
-    per = [[int(am[ends[s]])] + drafts[s] for s in range(B)]
-    slots2 = [sd.TokenSlot(s, len(prompts[s]) + o) for s in range(B) for o in range(len(per[s]))]
-    lg, am2 = m.forward(sd.concatenate_inputs(per), c, slots2)
-    assert (am2 == lg.argmax(1)).all()
-    rows = [ref.logits(prompts[s] + per[s], rows=range(len(prompts[s]), len(prompts[s]) + len(per[s])))
-            for s in range(B)]
-    c.close()
-    m.close()
-    torch.cuda.empty_cache()
-    return parity_stats(lg, np.concatenate(rows))
-
-
 def test_c3_layer_truncated_forward_vs_float64(sd):
-    st = c3_truncated_parity(sd)
+    st = c3_truncated_parity(sd, greedy_tokens=12)
     print("C3 L=2 bf16 vs float64:", st)
     assert st["max_abs_over_std"] <= 0.15
     assert st["mean_abs_over_std"] <= 0.03
     assert st["argmax_agree"] >= 0.9
+    assert st["token_agree"] >= 0.75  # greedy streams, position-wise

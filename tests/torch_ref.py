@@ -115,3 +115,57 @@ def parity_stats(ours: np.ndarray, ref: np.ndarray) -> dict:
     scale = float(ref.std())
     return {"max_abs_over_std": float(d.max() / scale), "mean_abs_over_std": float(d.mean() / scale),
             "argmax_agree": float(np.mean(ours.argmax(1) == ref.argmax(1))), "rows": int(ref.shape[0])}
+
+
+C3_L2 = dict(num_layers=2, num_heads=40, head_dim=128, vocab_size=50272, max_positions=2048, init_seed=0xD5EED)
+
+
+def c3_truncated_parity(sd, cfg=C3_L2, B=4, seed=1, greedy_tokens=0) -> dict:
+    """bf16 verify-step logits of a layer-truncated C3 model (the library's
+    public API: prefill + one ragged verify forward) against this float64
+    reference on the fp32 weights of the same seed (an FP32_CHECK model of the
+    library, itself bit-exact with the compiled reference).  Optionally also
+    the greedy token agreement over `greedy_tokens` decoded tokens per sample
+    (bf16 sd.decode vs float64 argmax decoding)."""
+    import torch
+
+    rng = np.random.default_rng(seed)
+    V = cfg["vocab_size"]
+    prompts = [[0] + rng.integers(3, V, size=int(rng.integers(600, 660))).tolist() for _ in range(B)]
+    drafts = [rng.integers(3, V, size=1 + (3 * s) % 8).tolist() for s in range(B)]
+    m32 = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.FP32_CHECK)
+    ref = TorchRef(cfg, m32.tensors(), device="cuda", dtype=torch.float64)
+    m32.close()
+    m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.BF16)
+    c = sd.UnpadArena(m, B, 1024)
+    slots = [sd.TokenSlot(s, i) for s in range(B) for i in range(len(prompts[s]))]
+    _, am = m.forward(sd.concatenate_inputs(prompts), c, slots, want_logits=False)
+    for s in range(B):
+        c.commit_accepted(s, len(prompts[s]))
+    ends = np.cumsum([len(p) for p in prompts]) - 1
+    per = [[int(am[ends[s]])] + drafts[s] for s in range(B)]
+    slots2 = [sd.TokenSlot(s, len(prompts[s]) + o) for s in range(B) for o in range(len(per[s]))]
+    lg, am2 = m.forward(sd.concatenate_inputs(per), c, slots2)
+    assert (am2 == lg.argmax(1)).all()
+    rows = [ref.logits(prompts[s] + per[s], rows=range(len(prompts[s]), len(prompts[s]) + len(per[s])))
+            for s in range(B)]
+    c.close()
+    out = parity_stats(lg, np.concatenate(rows))
+    out["config"] = "C3 shape truncated to L=%d, B=%d, ~600-token contexts, drafts 1-8" % (cfg["num_layers"], B)
+    if greedy_tokens:
+        g = sd.decode(sd.EngineConfig(mode="greedy", batch_size=B, max_new_tokens=greedy_tokens, stop_on_eos=False),
+                      m, prompts).generated_tokens
+        same, prefix = 0, []
+        for s in range(B):
+            seq, ref_tok = list(prompts[s]), []
+            for _ in range(greedy_tokens):
+                ref_tok.append(int(ref.logits(seq, rows=[len(seq) - 1])[0].argmax()))
+                seq.append(ref_tok[-1])
+            same += sum(int(a == b) for a, b in zip(g[s], ref_tok))
+            prefix.append(next((i for i, (a, b) in enumerate(zip(g[s], ref_tok)) if a != b), greedy_tokens))
+        out["token_agree"] = same / (B * greedy_tokens)
+        out["greedy_prefix_agree"] = float(np.mean(prefix)) / greedy_tokens
+        out["greedy_tokens_per_sample"] = greedy_tokens
+    m.close()
+    torch.cuda.empty_cache()
+    return out

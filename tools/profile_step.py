@@ -1,7 +1,12 @@
 """Profile one C3 verify step: prefill outside the profiled range, then
 cuProfilerStart() / N eager device steps / cuProfilerStop() so that
-`ncu --profile-from-start off` captures exactly the step's kernels."""
+`ncu --profile-from-start off` captures exactly the step's kernels.
+
+META=path writes the profiled step's shape next to the launch list (token
+count T and each sample's KV extent), so bench.py charges the ncu DRAM bytes
+against the algorithmic bytes of the SAME step."""
 import ctypes as C
+import json
 import os
 import sys
 
@@ -23,8 +28,20 @@ L = sd.lib()
 L.sd_session_step.argtypes = [C.c_void_p, C.c_int]
 # advance into the generation so drafts exist, then profile
 assert L.sd_session_step(s._h, 20) == 0
+toks0, _, _ = s.outputs()
+committed = [len(p) + len(t) - 1 for p, t in zip(prompts, toks0)]  # ctx_len - 1 (engine.cpp:465-470)
 cuda = C.CDLL("libcuda.so.1")
 cuda.cuProfilerStart()
 assert L.sd_session_step(s._h, steps) == 0
 cuda.cuProfilerStop()
 print("profiled", steps, "step(s)")
+if os.environ.get("META") and steps == 1:
+    _, lk, _ = s.outputs()
+    k = lk[20].tolist()
+    meta = {"config": "C3", "batch": B, "mode": e.mode, "step_index": 20, "k": k,
+            "T": int(sum(1 + x for x in k if x >= 0)),
+            "kv_len": [c + 1 + x if x >= 0 else 0 for c, x in zip(committed, k)],
+            "num_layers": cfg["num_layers"], "hidden": cfg["num_heads"] * cfg["head_dim"],
+            "vocab": cfg["vocab_size"]}
+    json.dump(meta, open(os.environ["META"], "w"), indent=1)
+    print("meta", meta["T"], "tokens")
