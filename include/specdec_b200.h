@@ -138,7 +138,54 @@ int sd_cache_ledger(const sd_cache* c, int64_t* useful, int64_t* padding);
  * k_out / v_out are [upto+1][hidden] fp32. */
 int sd_cache_gather_visible(const sd_cache* c, int sample, int upto, int layer, float* k_out,
                             float* v_out, int32_t* count);
+/* A model-less arena, CacheArena(num_layers, batch, capacity, kv_dim)
+ * (kv_cache.hpp:68-73, kv_cache.cpp:78-88): K/V rows can be stored with
+ * sd_cache_write_kv and read back with sd_cache_gather_visible; the first
+ * forward binds a model of the same depth and width (the arena then takes
+ * the model's head split, precision and device, which requires that no row
+ * was stored yet if they differ).  precision: SD_FP32_CHECK or SD_BF16. */
+int sd_cache_create_dims(int num_layers, int batch, int capacity, int kv_dim, int layout, int device,
+                         int precision, sd_cache** out);
+/* CacheArena::write_kv (kv_cache.hpp:82-83; kv_cache.cpp:128-138, 203-213):
+ * store one token's key and value ([kv_dim] fp32 each; rounded to bf16 in a
+ * bf16 arena) for one layer.  The ledger counts the slot once, on layer 0. */
+int sd_cache_write_kv(sd_cache* c, int sample, int position, int layer, const float* k_vec,
+                      const float* v_vec);
 void sd_cache_destroy(sd_cache* c);
+
+/* ---- write ledger (WriteLedger, kv_cache.hpp:13-57) ----------------------- */
+/* Useful / padding KV slot writes per sample and the per-step grouping of one
+ * decode iteration (begin_step, note_tau per committed sample, end_step).
+ * Every cache owns one (sd_cache_ledger_handle, valid while the cache lives):
+ * forwards count useful slots, commit_padded counts its filler rows and notes
+ * each tau -- it therefore needs an open step, as in the reference -- and
+ * sd_verify_step records one whole step (it opens and closes the step itself
+ * unless the caller holds one open).  sd_ledger_create makes a standalone
+ * WriteLedger(batch). */
+typedef struct sd_ledger sd_ledger;
+int sd_ledger_create(int batch, sd_ledger** out);
+void sd_ledger_destroy(sd_ledger* l); /* no-op for a cache's own ledger */
+int sd_cache_ledger_handle(sd_cache* c, sd_ledger** out);
+int sd_ledger_note_useful(sd_ledger* l, int sample);
+int sd_ledger_note_padding(sd_ledger* l, int sample);
+int sd_ledger_begin_step(sd_ledger* l);
+int sd_ledger_note_tau(sd_ledger* l, int tau);
+int sd_ledger_end_step(sd_ledger* l);
+int sd_ledger_batch(const sd_ledger* l, int32_t* batch);
+/* useful_total / padding_total (either pointer may be NULL) */
+int sd_ledger_totals(const sd_ledger* l, int64_t* useful, int64_t* padding);
+/* useful_by_sample / padding_by_sample: [batch] each, either may be NULL */
+int sd_ledger_by_sample(const sd_ledger* l, int64_t* useful, int64_t* padding);
+int sd_ledger_num_steps(const sd_ledger* l, int64_t* n);
+/* LedgerStep i: tau_list (up to cap entries; n_tau = its full length), tau_max,
+ * pad_writes, useful_writes */
+int sd_ledger_step(const sd_ledger* l, int64_t i, int32_t* tau_list, int32_t cap, int32_t* n_tau,
+                   int32_t* tau_max, int64_t* pad_writes, int64_t* useful_writes);
+/* WriteLedger::dump_json (kv_cache.cpp:53-62), byte-identical to nlohmann's
+ * compact dump; *len = full length, buf gets at most cap-1 bytes + NUL */
+int sd_ledger_dump_json(const sd_ledger* l, char* buf, int64_t cap, int64_t* len);
+/* padding_ratio (kv_cache.cpp:64-76); SD_CONTRACT when no step was recorded */
+int sd_ledger_padding_ratio(const sd_ledger* l, double* out);
 
 /* ---- ragged batching (ragged.cpp:6-36) ----------------------------------- */
 int sd_restore_indices(const int32_t* counts, int batch, int flat_index, int32_t* sample,

@@ -11,14 +11,23 @@
 //   specdec::CacheArena, UnpadArena, PaddedGrid                               kv_cache.hpp:68-168
 //   specdec::VerifyResult, verify                                             engine.hpp:82-90
 //
+//   specdec::LedgerStep, WriteLedger, padding_ratio                           kv_cache.hpp:13-62
+//   specdec::softmax, LayerWeights, Model weight accessors                     model.hpp:27-32, 48, 81-87
+//   specdec::SplitMix64, mix_seed                                              rng.hpp
+//   specdec::tok::tokenize / detokenize                                        tokenizer.hpp
+//
 // Differences, all at the boundary: a Model lives on one GPU (precision
 // SD_FP32_CHECK -- bit-exact with the reference -- unless SD_BF16 is asked
-// for); a cache arena binds to the first Model that runs a forward over it
-// (its device buffers are created then, the dimensions must match); K/V rows
-// are written by the forward on the device (there is no host write_kv), and
-// the ledger exposes the useful / padding totals.
+// for); a cache arena is a device arena on device 0 from construction (fp32),
+// and the first Model that runs a forward over it binds it (same depth and
+// width; the arena then takes the model's head split, precision and device,
+// which needs it to be still unwritten if they differ).  Weight accessors
+// download the tensors on first use (bf16 models return their bf16 values
+// widened to fp32).
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -33,12 +42,27 @@ using TokenId = int32_t;
 using TokenSequence = std::vector<TokenId>;
 using LogitsRow = std::vector<float>;
 
-namespace tok {
-constexpr TokenId kBos = 0;
-constexpr TokenId kEos = 1;
-constexpr TokenId kPad = 2;
-constexpr int kVocabSize = 259;
-}  // namespace tok
+// ------------------------------------------------------------ SplitMix64 (rng.hpp)
+class SplitMix64 {
+public:
+    explicit SplitMix64(uint64_t seed) : state_(seed) {}
+    uint64_t next_u64() {
+        uint64_t z = (state_ += 0x9E3779B97F4A7C15ULL);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        return z ^ (z >> 31);
+    }
+    float next_unit_float() { return static_cast<float>(next_u64() >> 40) * 0x1.0p-24f; }
+    double next_unit_double() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+    float next_symmetric(float limit) { return (2.0f * next_unit_float() - 1.0f) * limit; }
+
+private:
+    uint64_t state_;
+};
+inline uint64_t mix_seed(uint64_t a, uint64_t b = 0, uint64_t c = 0) {
+    SplitMix64 r(a ^ (b * 0xD1B54A32D192ED03ULL) ^ (c * 0x8CB92BA72F3D8DD7ULL));
+    return r.next_u64();
+}
 
 // ------------------------------------------------------------ errors (common.hpp:13-34)
 struct Error : std::runtime_error {
@@ -77,6 +101,30 @@ inline void check(int rc) {
 }
 }  // namespace b200
 
+// ------------------------------------------------------------ byte tokenizer (tokenizer.hpp)
+namespace tok {
+constexpr TokenId kBos = 0;
+constexpr TokenId kEos = 1;
+constexpr TokenId kPad = 2;
+constexpr TokenId kByteOffset = 3;
+constexpr int kVocabSize = 259;
+inline TokenSequence tokenize(const std::string& text) {
+    TokenSequence out;
+    for (unsigned char ch : text) out.push_back(static_cast<TokenId>(ch) + kByteOffset);
+    return out;
+}
+inline std::string detokenize(const TokenSequence& tokens) {
+    std::string out;
+    for (TokenId id : tokens) {
+        if (id < 0 || id >= kVocabSize) throw ContractError("token id " + std::to_string(id) + " outside vocabulary");
+        if (id < kByteOffset) throw ContractError("special token " + std::to_string(id) + " has no byte form");
+        out.push_back(static_cast<char>(id - kByteOffset));
+    }
+    return out;
+}
+inline bool is_special(TokenId id) { return id >= 0 && id < kByteOffset; }
+}  // namespace tok
+
 // ------------------------------------------------------------ ragged batching (ragged.hpp)
 struct RaggedBatch {
     std::vector<TokenId> concatenated_tokens;
@@ -94,6 +142,7 @@ struct TokenSlot {
 namespace ragged {
 // Algorithm 1 (ragged.cpp:6-17): flatten in order, zero-length samples keep their entry.
 inline RaggedBatch concatenate_inputs(const std::vector<TokenSequence>& per_sample) {
+    if (per_sample.empty()) throw ContractError("batch must have at least one sample");
     RaggedBatch b;
     for (const TokenSequence& s : per_sample) {
         b.concatenated_tokens.insert(b.concatenated_tokens.end(), s.begin(), s.end());
@@ -141,25 +190,132 @@ struct TokenPlan {
     bool store = true;
 };
 
+// Numerically safe softmax (model.cpp:20-32), host-side helper of the tests.
+inline std::vector<float> softmax(const std::vector<float>& scores) {
+    if (scores.empty()) throw ContractError("softmax over an empty set");
+    float mx = scores[0];
+    for (float v : scores) mx = std::max(mx, v);
+    std::vector<float> out(scores.size());
+    float denom = 0.0f;
+    for (size_t i = 0; i < scores.size(); ++i) {
+        out[i] = std::exp(scores[i] - mx);
+        denom += out[i];
+    }
+    for (float& w : out) w /= denom;
+    return out;
+}
+
 // Argmax with ties toward the lowest id (model.cpp:34-41).
 inline TokenId greedy_next(const LogitsRow& row) {
-    if (row.empty()) throw ContractError("greedy_next on an empty row");
+    if (row.empty()) throw ContractError("argmax over an empty row");
     TokenId best = 0;
     for (size_t i = 1; i < row.size(); ++i)
         if (row[i] > row[best]) best = static_cast<TokenId>(i);
     return best;
 }
 
-class Model;
+// ------------------------------------------------------------ write ledger (kv_cache.hpp:13-62)
+struct LedgerStep {
+    std::vector<int> tau_list;
+    int tau_max = 0;
+    int64_t pad_writes = 0;
+    int64_t useful_writes = 0;
+};
 
-// Read contract shared by both layouts (kv_cache.hpp:68-101).  The device
-// arena is created when a Model first runs a forward over it.
+// A standalone WriteLedger(batch) owns its library ledger; a cache's ledger()
+// is a view of the ledger the library keeps for that cache.
+class WriteLedger {
+public:
+    explicit WriteLedger(int batch_size) {
+        sd_ledger* l = nullptr;
+        b200::check(sd_ledger_create(batch_size, &l));
+        h_.reset(l, sd_ledger_destroy);
+    }
+    explicit WriteLedger(sd_ledger* view) : h_(view, [](sd_ledger*) {}) {}
+
+    void note_useful(int sample) { b200::check(sd_ledger_note_useful(h_.get(), sample)); }
+    void note_padding(int sample) { b200::check(sd_ledger_note_padding(h_.get(), sample)); }
+    void begin_step() { b200::check(sd_ledger_begin_step(h_.get())); }
+    void note_tau(int tau) { b200::check(sd_ledger_note_tau(h_.get(), tau)); }
+    void end_step() { b200::check(sd_ledger_end_step(h_.get())); }
+
+    int64_t useful_total() const { return totals().first; }
+    int64_t padding_total() const { return totals().second; }
+    int64_t total() const { return useful_total() + padding_total(); }
+    const std::vector<int64_t>& useful_by_sample() const {
+        by_sample();
+        return useful_by_;
+    }
+    const std::vector<int64_t>& padding_by_sample() const {
+        by_sample();
+        return padding_by_;
+    }
+    const std::vector<LedgerStep>& steps() const {
+        int64_t n = 0;
+        b200::check(sd_ledger_num_steps(h_.get(), &n));
+        steps_.assign(static_cast<size_t>(n), LedgerStep{});
+        for (int64_t i = 0; i < n; ++i) {
+            LedgerStep& st = steps_[static_cast<size_t>(i)];
+            int32_t nt = 0, tm = 0;
+            std::vector<int32_t> buf(64);
+            b200::check(sd_ledger_step(h_.get(), i, buf.data(), 64, &nt, &tm, &st.pad_writes, &st.useful_writes));
+            if (nt > 64) {
+                buf.resize(static_cast<size_t>(nt));
+                b200::check(sd_ledger_step(h_.get(), i, buf.data(), nt, &nt, &tm, &st.pad_writes, &st.useful_writes));
+            }
+            st.tau_list.assign(buf.begin(), buf.begin() + nt);
+            st.tau_max = tm;
+        }
+        return steps_;
+    }
+    std::string dump_json() const {
+        int64_t n = 0;
+        b200::check(sd_ledger_dump_json(h_.get(), nullptr, 0, &n));
+        std::string out(static_cast<size_t>(n) + 1, '\0');
+        b200::check(sd_ledger_dump_json(h_.get(), out.data(), n + 1, &n));
+        out.resize(static_cast<size_t>(n));
+        return out;
+    }
+    const sd_ledger* handle() const { return h_.get(); }
+
+private:
+    std::pair<int64_t, int64_t> totals() const {
+        int64_t u = 0, p = 0;
+        b200::check(sd_ledger_totals(h_.get(), &u, &p));
+        return {u, p};
+    }
+    void by_sample() const {
+        int32_t b = 0;
+        b200::check(sd_ledger_batch(h_.get(), &b));
+        useful_by_.assign(static_cast<size_t>(b), 0);
+        padding_by_.assign(static_cast<size_t>(b), 0);
+        b200::check(sd_ledger_by_sample(h_.get(), useful_by_.data(), padding_by_.data()));
+    }
+    std::shared_ptr<sd_ledger> h_;
+    mutable std::vector<int64_t> useful_by_, padding_by_;
+    mutable std::vector<LedgerStep> steps_;
+};
+
+// padding_ratio (kv_cache.cpp:64-76); ContractError without steps.
+inline double padding_ratio(const WriteLedger& ledger) {
+    double r = 0.0;
+    b200::check(sd_ledger_padding_ratio(ledger.handle(), &r));
+    return r;
+}
+
+// ------------------------------------------------------------ KV arenas (kv_cache.hpp:65-168)
+// Read contract shared by both layouts.  The device arena exists from
+// construction; the first Model::forward over it binds the model.
 class CacheArena {
 public:
     CacheArena(int num_layers, int batch_size, int capacity, int kv_dim, int layout)
-        : num_layers_(num_layers), batch_size_(batch_size), capacity_(capacity), kv_dim_(kv_dim), layout_(layout) {
-        if (num_layers <= 0 || batch_size <= 0 || capacity <= 0 || kv_dim <= 0)
-            throw ConfigError("cache dimensions must be positive");
+        : num_layers_(num_layers), batch_size_(batch_size), capacity_(capacity), kv_dim_(kv_dim) {
+        sd_cache* c = nullptr;
+        b200::check(sd_cache_create_dims(num_layers, batch_size, capacity, kv_dim, layout, 0, SD_FP32_CHECK, &c));
+        h_.reset(c, sd_cache_destroy);
+        sd_ledger* l = nullptr;
+        b200::check(sd_cache_ledger_handle(c, &l));
+        ledger_ = std::make_unique<WriteLedger>(l);
     }
     virtual ~CacheArena() = default;
     CacheArena(const CacheArena&) = delete;
@@ -171,61 +327,35 @@ public:
     int kv_dim() const { return kv_dim_; }
 
     int committed_len(int sample) const {
-        check_sample(sample);
-        if (!h_) return 0;
         int32_t v = 0;
         b200::check(sd_cache_committed_len(h_.get(), sample, &v));
         return v;
     }
     int logical_len(int sample) const {
-        check_sample(sample);
-        if (!h_) return 0;
         int32_t v = 0;
         b200::check(sd_cache_logical_len(h_.get(), sample, &v));
         return v;
     }
-    virtual void mark_hole(int sample, int position) {
-        b200::check(sd_cache_mark_hole(bound(), sample, position));
+    // Store a real token's key/value for one layer; counted once, on layer 0.
+    void write_kv(int sample, int position, int layer, const float* k_vec, const float* v_vec) {
+        b200::check(sd_cache_write_kv(h_.get(), sample, position, layer, k_vec, v_vec));
     }
+    virtual void mark_hole(int sample, int position) { b200::check(sd_cache_mark_hole(h_.get(), sample, position)); }
     // Copies the visible real K/V rows [0, upto] of (sample, layer), ascending.
     int gather_visible(int sample, int upto, int layer, float* k_out, float* v_out) const {
-        if (!h_) return 0;
         int32_t n = 0;
         b200::check(sd_cache_gather_visible(h_.get(), sample, upto, layer, k_out, v_out, &n));
         return n;
     }
-    // Ledger totals (kv_cache.hpp:21-45): useful / padding slot writes.
-    int64_t useful_writes() const { return totals().first; }
-    int64_t padding_writes() const { return totals().second; }
+    const WriteLedger& ledger() const { return *ledger_; }
+    WriteLedger& ledger() { return *ledger_; }
 
-    // The C handle (binds on first forward; see Model::forward).
     sd_cache* handle() const { return h_.get(); }
-    void bind(const sd_model* m) {
-        if (h_) return;
-        sd_model_config cfg{};
-        b200::check(sd_model_get_config(m, &cfg));
-        if (cfg.num_layers != num_layers_ || cfg.num_heads * cfg.head_dim != kv_dim_)
-            throw ContractError("cache dimensions do not match the model");
-        sd_cache* c = nullptr;
-        b200::check(sd_cache_create(m, batch_size_, capacity_, layout_, &c));
-        h_.reset(c, sd_cache_destroy);
-    }
 
 protected:
-    sd_cache* bound() const {
-        if (!h_) throw ContractError("cache arena not bound to a model yet (run a forward first)");
-        return h_.get();
-    }
-    void check_sample(int s) const {
-        if (s < 0 || s >= batch_size_) throw ContractError("cache sample out of range");
-    }
-    std::pair<int64_t, int64_t> totals() const {
-        int64_t u = 0, p = 0;
-        if (h_) b200::check(sd_cache_ledger(h_.get(), &u, &p));
-        return {u, p};
-    }
-    int num_layers_, batch_size_, capacity_, kv_dim_, layout_;
+    int num_layers_, batch_size_, capacity_, kv_dim_;
     std::shared_ptr<sd_cache> h_;
+    std::unique_ptr<WriteLedger> ledger_;
 };
 
 // EMS-SD layout (kv_cache.hpp:105-128).
@@ -234,10 +364,11 @@ public:
     UnpadArena(int num_layers, int batch_size, int capacity, int kv_dim)
         : CacheArena(num_layers, batch_size, capacity, kv_dim, SD_UNPAD) {}
     int start_offset(int sample) const {
-        check_sample(sample);
-        return sample * capacity_;  // kv_cache.cpp:116-120
+        int32_t v = 0;
+        b200::check(sd_cache_start_offset(h_.get(), sample, &v));
+        return v;
     }
-    void commit_accepted(int sample, int tau) { b200::check(sd_cache_commit_accepted(bound(), sample, tau)); }
+    void commit_accepted(int sample, int tau) { b200::check(sd_cache_commit_accepted(h_.get(), sample, tau)); }
 };
 
 // Vanilla (aligned) layout (kv_cache.hpp:133-168).
@@ -247,19 +378,28 @@ public:
         : CacheArena(num_layers, batch_size, capacity, kv_dim, SD_PADDED) {}
     bool is_pad(int sample, int row) const {
         int32_t v = 0;
-        b200::check(sd_cache_is_pad(bound(), sample, row, &v));
+        b200::check(sd_cache_is_pad(h_.get(), sample, row, &v));
         return v != 0;
     }
     void commit_prefill(const std::vector<int>& samples, const std::vector<int>& prompt_lens) {
         if (samples.size() != prompt_lens.size()) throw ContractError("commit_prefill: mismatched lists");
         std::vector<int32_t> s(samples.begin(), samples.end()), l(prompt_lens.begin(), prompt_lens.end());
-        b200::check(sd_cache_commit_prefill(bound(), s.data(), l.data(), static_cast<int>(s.size())));
+        b200::check(sd_cache_commit_prefill(h_.get(), s.data(), l.data(), static_cast<int>(s.size())));
     }
     void commit_padded(const std::vector<int>& samples, const std::vector<int>& taus) {
-        if (samples.size() != taus.size()) throw ContractError("commit_padded: mismatched lists");
+        if (samples.empty() || samples.size() != taus.size())
+            throw ContractError("padded commit needs matching sample and tau lists");
         std::vector<int32_t> s(samples.begin(), samples.end()), t(taus.begin(), taus.end());
-        b200::check(sd_cache_commit_padded(bound(), s.data(), t.data(), static_cast<int>(s.size())));
+        b200::check(sd_cache_commit_padded(h_.get(), s.data(), t.data(), static_cast<int>(s.size())));
     }
+};
+
+// One layer's tensors (model.hpp:27-32), declaration order.
+struct LayerWeights {
+    std::vector<float> ln1_gain, ln1_bias;
+    std::vector<float> wq, bq, wk, bk, wv, bv, wo, bo;
+    std::vector<float> ln2_gain, ln2_bias;
+    std::vector<float> w_fc, b_fc, w_proj, b_proj;
 };
 
 // Decoder-only transformer resident on one B200 (model.hpp:54-103).
@@ -293,7 +433,6 @@ public:
     // restore_indices(batch.token_nums_per_sample, i) at the sample's committed extent.
     std::vector<LogitsRow> forward(const RaggedBatch& batch, CacheArena& cache,
                                    const std::vector<TokenSlot>& slots) const {
-        cache.bind(h_.get());
         const int T = batch.total_input_token_nums;
         if (static_cast<int>(slots.size()) != T || static_cast<int>(batch.concatenated_tokens.size()) != T)
             throw ContractError("forward: slots / tokens do not match the batch");
@@ -312,7 +451,6 @@ public:
     // Plan-level entry point (model.cpp:256-373).
     std::vector<LogitsRow> forward_planned(const std::vector<TokenId>& tokens, const std::vector<TokenPlan>& plans,
                                            CacheArena& cache) const {
-        cache.bind(h_.get());
         const int T = static_cast<int>(tokens.size());
         if (static_cast<int>(plans.size()) != T) throw ContractError("forward_planned: tokens / plans mismatch");
         std::vector<int32_t> s(T), lp(T), ws(T), st(T);
@@ -328,10 +466,34 @@ public:
         return rows(flat, T);
     }
 
+    // Weight access for independent reimplementations in tests (model.hpp:81-87).
+    const std::vector<float>& token_embedding() const { return tensor(-1, 0); }
+    const std::vector<float>& position_embedding() const { return tensor(-1, 1); }
+    const std::vector<float>& final_ln_gain() const { return tensor(-1, 2); }
+    const std::vector<float>& final_ln_bias() const { return tensor(-1, 3); }
+    const std::vector<float>& lm_head() const { return tensor(-1, 4); }
+    const LayerWeights& layer(int i) const {
+        if (i < 0 || i >= config_.num_layers) throw std::out_of_range("layer index out of range");
+        auto& lw = weights_->layers;
+        if (lw.empty()) lw.resize(static_cast<size_t>(config_.num_layers));
+        LayerWeights& w = lw[static_cast<size_t>(i)];
+        if (w.ln1_gain.empty()) {
+            std::vector<float>* t[16] = {&w.ln1_gain, &w.ln1_bias, &w.wq, &w.bq, &w.wk, &w.bk, &w.wv, &w.bv,
+                                         &w.wo, &w.bo, &w.ln2_gain, &w.ln2_bias, &w.w_fc, &w.b_fc, &w.w_proj,
+                                         &w.b_proj};
+            for (int k = 0; k < 16; ++k) fetch(i, k, *t[k]);
+        }
+        return w;
+    }
+
     sd_model* handle() const { return h_.get(); }
 
 private:
-    Model(sd_model* m, const ModelConfig& c) : h_(m, sd_model_destroy), config_(c) {}
+    struct Weights {
+        std::vector<float> model_level[5];
+        std::vector<LayerWeights> layers;
+    };
+    Model(sd_model* m, const ModelConfig& c) : h_(m, sd_model_destroy), config_(c), weights_(std::make_shared<Weights>()) {}
     std::vector<LogitsRow> rows(const std::vector<float>& flat, int T) const {
         std::vector<LogitsRow> out(T);
         for (int i = 0; i < T; ++i)
@@ -339,8 +501,28 @@ private:
                           flat.begin() + static_cast<size_t>(i + 1) * config_.vocab_size);
         return out;
     }
+    int64_t tensor_size(int layer, int k) const {
+        const int64_t h = config_.hidden(), m = config_.mlp_hidden(), V = config_.vocab_size,
+                      P = config_.max_positions;
+        if (layer < 0) {
+            const int64_t sz[5] = {V * h, P * h, h, h, V * h};
+            return sz[k];
+        }
+        const int64_t sz[16] = {h, h, h * h, h, h * h, h, h * h, h, h * h, h, h, h, m * h, m, h * m, h};
+        return sz[k];
+    }
+    void fetch(int layer, int k, std::vector<float>& out) const {
+        out.resize(static_cast<size_t>(tensor_size(layer, k)));
+        b200::check(sd_model_get_tensor(h_.get(), layer, k, out.data(), static_cast<int64_t>(out.size())));
+    }
+    const std::vector<float>& tensor(int layer, int k) const {
+        std::vector<float>& t = weights_->model_level[k];
+        if (t.empty()) fetch(layer, k, t);
+        return t;
+    }
     std::shared_ptr<sd_model> h_;
     ModelConfig config_;
+    std::shared_ptr<Weights> weights_;  // lazily downloaded copies
 };
 
 // ------------------------------------------------------------ verify (engine.hpp:82-90)

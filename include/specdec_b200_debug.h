@@ -9,7 +9,10 @@ extern "C" {
 /* Y[T][M] = X[T][K] . W[M][K]^T with bf16 inputs (raw bits) and fp32 output,
  * through the stream-K tcgen05 kernel on `grid` CTAs (0 = one per SM).
  * Returns the kernel time in microseconds in *usec (CUDA events). */
-/* flags bit 3: time the streaming kernel alone (no split-K reduction; Y untouched) */
+/* flags bit 3: time the streaming kernel alone (no split-K reduction; Y untouched);
+ * bit 7: time ten launches back to back (mean); bits 4-6 select bottleneck
+ * probes (skip MMAs / token loads / partial stores) that only a probe build of
+ * the kernel (-DSD_GEMM_PROBE, tools/gemm_probe.py --probe) honours */
 int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K, int T, int grid, int flags, float* Y,
                   float* usec);
 /* In-graph kernel timeline (tools/timeline.py): while on, every CTA of every

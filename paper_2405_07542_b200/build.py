@@ -10,6 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "lib")
 LIB = os.path.join(OUT, "libspecdec_b200.so")
+PROBE_LIB = os.path.join(OUT, "probe", "libspecdec_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
@@ -59,5 +60,26 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+def build_probe() -> str:
+    """A measurement-only variant of the library whose GEMM honours the
+    bottleneck probes of sd_debug_gemm (-DSD_GEMM_PROBE); tools/ load it with
+    --lib.  The library itself never contains them."""
+    build()
+    os.makedirs(os.path.dirname(PROBE_LIB), exist_ok=True)
+    po = os.path.join(OUT, "probe", "gemm_sm100.cu.o")
+    cmd = [NVCC, *ARCH, *FLAGS, "-DSD_GEMM_PROBE", "-c", os.path.join(CSRC, "gemm_sm100.cu"), "-o", po]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    objs = [po if s == "gemm_sm100.cu" else _obj(s) for s in SOURCES]
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-o", PROBE_LIB, *objs], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    return PROBE_LIB
+
+
 if __name__ == "__main__":
-    build(verbose=True)
+    if "--probe" in sys.argv:
+        print("built", build_probe())
+    else:
+        build(verbose=True)

@@ -173,41 +173,99 @@ sd_model* create_model(const Config& cfg, int device, int precision, const float
     return h;
 }
 
-sd_cache* create_cache(sd_model* mh, int batch, int capacity, int layout) {
-    const Model& m = mh->m;
-    SD_CHECK(batch >= 1 && capacity >= 1, CONFIG, "cache dimensions must be positive");
+// (re)allocate the device arena and descriptors for the current geometry
+static void alloc_arena(sd_cache* h) {
+    Cache& c = h->c;
+    set_device(h->device);
+    dfree(c.kv);
+    dfree(c.d_committed);
+    dfree(c.d_logical);
+    dfree(c.d_pad);
+    c.kv = nullptr;
+    c.d_committed = c.d_logical = nullptr;
+    c.d_pad = nullptr;
+    size_t bytes = (size_t)c.L * 2 * c.B * c.heads * (size_t)c.cap * c.hd * c.elem_bytes;
+    c.kv = dmalloc(bytes);
+    CUDA_OK(cudaMemset(c.kv, 0, bytes));
+    c.d_committed = (int32_t*)dmalloc(4 * (size_t)c.B);
+    c.d_logical = (int32_t*)dmalloc(4 * (size_t)c.B);
+    c.d_pad = (uint8_t*)dmalloc((size_t)c.B * c.cap);
+    CUDA_OK(cudaMemset(c.d_committed, 0, 4 * (size_t)c.B));
+    CUDA_OK(cudaMemset(c.d_logical, 0, 4 * (size_t)c.B));
+    CUDA_OK(cudaMemset(c.d_pad, 0, (size_t)c.B * c.cap));
+}
+
+static sd_cache* new_cache(int layers, int batch, int capacity, int heads, int hd, int layout, int device,
+                           int precision) {
+    // CacheArena::CacheArena (kv_cache.cpp:78-88)
+    SD_CHECK(layers >= 1 && batch >= 1 && capacity >= 1 && heads >= 1 && hd >= 1, CONFIG,
+             "cache dimensions must be positive");
     SD_CHECK(layout == UNPAD || layout == PADDED, CONFIG, "unknown cache layout");
-    set_device(m.device);
+    SD_CHECK(precision == FP32_CHECK || precision == BF16, CONFIG, "unknown precision");
     auto* h = new sd_cache();
     try {
         Cache& c = h->c;
         c.layout = layout;
-        c.L = m.cfg.num_layers;
+        c.L = layers;
         c.B = batch;
         c.cap = capacity;
-        c.heads = m.cfg.num_heads;
-        c.hd = m.cfg.head_dim;
-        c.elem_bytes = m.precision == FP32_CHECK ? 4 : 2;
-        c.model = &m;
-        h->model = mh;
-        size_t bytes = (size_t)c.L * 2 * c.B * c.heads * (size_t)c.cap * c.hd * c.elem_bytes;
-        c.kv = dmalloc(bytes);
-        CUDA_OK(cudaMemset(c.kv, 0, bytes));
-        c.d_committed = (int32_t*)dmalloc(4 * (size_t)batch);
-        c.d_logical = (int32_t*)dmalloc(4 * (size_t)batch);
-        c.d_pad = (uint8_t*)dmalloc((size_t)batch * capacity);
-        CUDA_OK(cudaMemset(c.d_committed, 0, 4 * (size_t)batch));
-        CUDA_OK(cudaMemset(c.d_logical, 0, 4 * (size_t)batch));
-        CUDA_OK(cudaMemset(c.d_pad, 0, (size_t)batch * capacity));
+        c.heads = heads;
+        c.hd = hd;
+        c.elem_bytes = precision == FP32_CHECK ? 4 : 2;
+        h->device = device;
+        h->precision = precision;
+        h->lh.l = &c.ledger;
+        alloc_arena(h);
         c.committed.assign(batch, 0);
         c.logical.assign(batch, 0);
         c.staged.assign(batch, 0);
         c.pad.assign((size_t)batch * capacity, 0);
+        c.ledger.reset(batch);
     } catch (...) {
         delete h;
         throw;
     }
     return h;
+}
+
+sd_cache* create_cache(sd_model* mh, int batch, int capacity, int layout) {
+    const Model& m = mh->m;
+    set_device(m.device);
+    sd_cache* h = new_cache(m.cfg.num_layers, batch, capacity, m.cfg.num_heads, m.cfg.head_dim, layout, m.device,
+                            m.precision);
+    h->c.model = &m;
+    h->model = mh;
+    return h;
+}
+
+sd_cache* create_cache_dims(int layers, int batch, int capacity, int kv_dim, int layout, int device, int precision) {
+    set_device(device);
+    return new_cache(layers, batch, capacity, 1, kv_dim, layout, device, precision);
+}
+
+// A dims-only arena meets its first model (Model::forward on a freshly built
+// CacheArena, model.cpp:273-276): the depth and width must match; the arena
+// takes the model's head split, element type and device.  Slots written
+// through write_kv before that would have to move, so that is refused.
+void bind_cache(sd_cache* h, sd_model* mh) {
+    Cache& c = h->c;
+    const Model& m = mh->m;
+    if (h->model) return;
+    SD_CHECK(c.heads * c.hd == m.cfg.hidden(), CONTRACT, "cache width does not match the model");
+    SD_CHECK(c.L == m.cfg.num_layers, CONTRACT, "cache depth does not match the model");
+    const int eb = m.precision == FP32_CHECK ? 4 : 2;
+    if (c.heads != m.cfg.num_heads || c.elem_bytes != eb || h->device != m.device) {
+        // masked holes are metadata only; stored rows would have to move
+        SD_CHECK(!h->kv_stored, CONTRACT, "cache holds write_kv rows in a layout this model cannot read");
+        c.heads = m.cfg.num_heads;
+        c.hd = m.cfg.head_dim;
+        c.elem_bytes = eb;
+        h->device = m.device;
+        h->precision = m.precision;
+        alloc_arena(h);
+    }
+    c.model = &m;
+    h->model = mh;
 }
 
 void reset_cache(sd_cache* h) {
@@ -216,16 +274,17 @@ void reset_cache(sd_cache* h) {
     std::fill(c.logical.begin(), c.logical.end(), 0);
     std::fill(c.staged.begin(), c.staged.end(), 0);
     std::fill(c.pad.begin(), c.pad.end(), 0);
-    c.useful = c.padding = 0;
-    CUDA_OK(cudaMemsetAsync(c.d_committed, 0, 4 * (size_t)c.B, h->model->st));
-    CUDA_OK(cudaMemsetAsync(c.d_logical, 0, 4 * (size_t)c.B, h->model->st));
-    CUDA_OK(cudaMemsetAsync(c.d_pad, 0, (size_t)c.B * c.cap, h->model->st));
+    c.ledger.reset(c.B);
+    cudaStream_t st = cache_stream(h);
+    CUDA_OK(cudaMemsetAsync(c.d_committed, 0, 4 * (size_t)c.B, st));
+    CUDA_OK(cudaMemsetAsync(c.d_logical, 0, 4 * (size_t)c.B, st));
+    CUDA_OK(cudaMemsetAsync(c.d_pad, 0, (size_t)c.B * c.cap, st));
 }
 
 // ------------------------------------------------------------------ forward
 static void sync_descriptors_to_device(sd_cache* h) {
     Cache& c = h->c;
-    cudaStream_t st = h->model->st;
+    cudaStream_t st = cache_stream(h);
     CUDA_OK(cudaMemcpyAsync(c.d_committed, c.committed.data(), 4 * (size_t)c.B, cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(c.d_logical, c.logical.data(), 4 * (size_t)c.B, cudaMemcpyHostToDevice, st));
     if (c.layout == PADDED)
@@ -263,6 +322,7 @@ void forward_planned_host(sd_model* mh, sd_cache* h, const int32_t* tokens, cons
     set_device(m.device);
     // model.cpp:266-285
     SD_CHECK(n > 0, CONTRACT, "forward pass over zero tokens");
+    bind_cache(h, mh);
     SD_CHECK(c.model == &m && c.heads * c.hd == cfg.hidden(), CONTRACT, "cache width does not match the model");
     SD_CHECK(c.L == cfg.num_layers, CONTRACT, "cache depth does not match the model");
     for (int t = 0; t < n; ++t) {
@@ -297,7 +357,7 @@ void forward_planned_host(sd_model* mh, sd_cache* h, const int32_t* tokens, cons
         if (!p.store) continue;
         if (c.layout == PADDED) c.pad[(size_t)p.sample * c.cap + p.write_slot] = 0;
         c.staged[p.sample] = std::max(c.staged[p.sample], p.write_slot + 1);
-        c.useful += 1;
+        c.ledger.note_useful(p.sample);  // once per slot, the layer-0 write (kv_cache.cpp:134-137)
     }
     // phase-2 gather checks (kv_cache.cpp:140-150): unpad reads stay below `written`
     if (c.layout == UNPAD)
@@ -357,6 +417,7 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
     const Config& cfg = m.cfg;
     const int B = c.B;
     set_device(m.device);
+    bind_cache(h, mh);
     // the cache must have been created for this model (model.cpp:273-276)
     SD_CHECK(c.model == &m && c.heads * c.hd == cfg.hidden(), CONTRACT, "cache width does not match the model");
     SD_CHECK(c.L == cfg.num_layers, CONTRACT, "cache depth does not match the model");
@@ -522,23 +583,28 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
         for (int j = 0; j < W; ++j) accepted[s * W + j] = active[s] && j < tau[s] ? hs[o_acc + (size_t)s * K1 + j] : -1;
         tmax = std::max(tmax, tau[s]);
     }
+    // the ledger step of one decode iteration (engine.cpp:398-487): opened here
+    // unless the caller holds one open around this call
+    const bool own_step = !c.ledger.open;
+    if (own_step) c.ledger.begin_step();
     for (int s = 0; s < B; ++s) {
         if (!active[s]) continue;
+        c.ledger.note_useful(s, 1 + counts[s]);  // the real input rows; PAD rows are holes
         if (c.layout == UNPAD) {
-            c.useful += 1 + counts[s];
             c.committed[s] += tau[s];
             c.logical[s] = c.committed[s];
             c.staged[s] = c.committed[s];
         } else {
-            c.useful += 1 + counts[s];
             for (int o = 0; o <= kmax; ++o) c.pad[(size_t)s * c.cap + base + o] = o <= counts[s] ? 0 : 1;
             for (int r = base + tau[s]; r < base + tmax; ++r) c.pad[(size_t)s * c.cap + r] = 1;
-            c.padding += tmax - tau[s];
+            c.ledger.note_padding(s, tmax - tau[s]);  // commit_padded's filler rows
             c.committed[s] = base + tmax;
             c.logical[s] += tau[s];
             c.staged[s] = c.committed[s];
         }
+        c.ledger.note_tau(tau[s]);
     }
+    if (own_step) c.ledger.end_step();
     return kmax;
 }
 
@@ -856,6 +922,7 @@ int sd_cache_commit_padded(sd_cache* h, const int32_t* samples, const int32_t* t
             SD_CHECK(taus[i] >= 1, CONTRACT, "commit needs tau >= 1");
             tmax = std::max(tmax, taus[i]);
         }
+        c.ledger.check_tau(tmax);  // commit_padded notes every tau (kv_cache.cpp:312): a step must be open
         int base = -1;
         for (int i = 0; i < n; ++i) {
             int s = samples[i];
@@ -867,8 +934,8 @@ int sd_cache_commit_padded(sd_cache* h, const int32_t* samples, const int32_t* t
             for (int r = base; r < base + taus[i]; ++r)
                 SD_CHECK(!c.pad[(size_t)s * c.cap + r], CONTRACT, "accepted row was never written");
         }
-        set_device(h->model->m.device);
-        cudaStream_t st = h->model->st;
+        set_device(h->device);
+        cudaStream_t st = cache_stream(h);
         // the filler rows of every sample and layer in ONE launch (kv_cache.cpp:295-307)
         std::vector<int32_t> rows(2 * (size_t)n);
         for (int i = 0; i < n; ++i) {
@@ -890,11 +957,12 @@ int sd_cache_commit_padded(sd_cache* h, const int32_t* samples, const int32_t* t
             int s = samples[i];
             for (int r = base + taus[i]; r < base + tmax; ++r) {
                 c.pad[(size_t)s * c.cap + r] = 1;
-                c.padding += 1;
+                c.ledger.note_padding(s);
             }
             c.committed[s] += tmax;
             c.logical[s] += taus[i];
             c.staged[s] = c.committed[s];
+            c.ledger.note_tau(taus[i]);
         }
     });
 }
@@ -916,8 +984,8 @@ int sd_cache_is_pad(const sd_cache* h, int s, int row, int32_t* out) {
 
 int sd_cache_ledger(const sd_cache* c, int64_t* useful, int64_t* padding) {
     return guarded([&] {
-        *useful = c->c.useful;
-        *padding = c->c.padding;
+        *useful = c->c.ledger.useful();
+        *padding = c->c.ledger.padding();
     });
 }
 
@@ -930,7 +998,7 @@ int sd_cache_gather_visible(const sd_cache* h, int s, int upto, int layer, float
         SD_CHECK(upto >= 0, CONTRACT, "cache position negative");
         SD_CHECK(upto < c.cap, CAPACITY, "cache position " + std::to_string(upto) + " exceeds capacity " + std::to_string(c.cap));
         if (c.layout == UNPAD) SD_CHECK(upto < c.staged[s], CONTRACT, "read past the written extent");
-        set_device(h->model->m.device);
+        set_device(h->device);
         int hidden = c.heads * c.hd, n = 0;
         std::vector<float> kh((size_t)(upto + 1) * c.hd), vh(kh.size());
         std::vector<uint16_t> kb(kh.size()), vb(kh.size());
@@ -962,9 +1030,152 @@ int sd_cache_gather_visible(const sd_cache* h, int s, int upto, int layer, float
     });
 }
 
+int sd_cache_create_dims(int num_layers, int batch, int capacity, int kv_dim, int layout, int device,
+                         int precision, sd_cache** out) {
+    return guarded([&] { *out = create_cache_dims(num_layers, batch, capacity, kv_dim, layout, device, precision); });
+}
+
+int sd_cache_write_kv(sd_cache* h, int s, int pos, int layer, const float* k_vec, const float* v_vec) {
+    return guarded([&] {  // UnpadArena / PaddedGrid::write_kv (kv_cache.cpp:93-103, 128-138, 203-213)
+        Cache& c = h->c;
+        SD_CHECK(s >= 0 && s < c.B, CONTRACT, "cache sample out of range");
+        SD_CHECK(layer >= 0 && layer < c.L, CONTRACT, "cache layer out of range");
+        SD_CHECK(pos >= 0, CONTRACT, "cache position negative");
+        SD_CHECK(pos < c.cap, CAPACITY, "cache position " + std::to_string(pos) + " exceeds capacity " +
+                                            std::to_string(c.cap));
+        set_device(h->device);
+        const size_t eb = c.elem_bytes, row = (size_t)c.hd * eb, pitch = (size_t)c.cap * c.hd * eb;
+        const int kv_dim = c.heads * c.hd;
+        std::vector<uint16_t> b16(eb == 2 ? (size_t)kv_dim : 0);
+        for (int w = 0; w < 2; ++w) {
+            const float* src = w == 0 ? k_vec : v_vec;
+            const void* hsrc = src;
+            if (eb == 2) {  // the bf16 arena stores round-to-nearest-even bf16
+                for (int i = 0; i < kv_dim; ++i) {
+                    uint32_t u;
+                    std::memcpy(&u, &src[i], 4);
+                    b16[i] = (u & 0x7fffffffu) > 0x7f800000u ? (uint16_t)((u >> 16) | 0x40)
+                                                             : (uint16_t)((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+                }
+                hsrc = b16.data();
+            }
+            char* dst = (char*)c.kv + c.kv_offset(layer, w, s, 0, pos) * eb;
+            CUDA_OK(cudaMemcpy2D(dst, pitch, hsrc, row, row, c.heads, cudaMemcpyHostToDevice));
+        }
+        h->kv_stored = true;
+        if (layer == 0) {  // the slot is counted once, on its layer-0 write
+            if (c.layout == PADDED) c.pad[(size_t)s * c.cap + pos] = 0;
+            c.staged[s] = std::max(c.staged[s], pos + 1);
+            c.ledger.note_useful(s);
+        }
+    });
+}
+
+// ---- WriteLedger (kv_cache.hpp:13-57) ----------------------------------------
+int sd_ledger_create(int batch, sd_ledger** out) {
+    return guarded([&] {
+        SD_CHECK(batch >= 0, CONFIG, "ledger batch must be >= 0");
+        auto* l = new sd_ledger();
+        l->own.reset(batch);
+        *out = l;
+    });
+}
+void sd_ledger_destroy(sd_ledger* l) {
+    if (l && l->l == &l->own) delete l;  // a cache's ledger view is owned by the cache
+}
+int sd_cache_ledger_handle(sd_cache* c, sd_ledger** out) {
+    return guarded([&] { *out = &c->lh; });
+}
+int sd_ledger_note_useful(sd_ledger* l, int sample) {
+    return guarded([&] { l->l->note_useful(sample); });
+}
+int sd_ledger_note_padding(sd_ledger* l, int sample) {
+    return guarded([&] { l->l->note_padding(sample); });
+}
+int sd_ledger_begin_step(sd_ledger* l) {
+    return guarded([&] { l->l->begin_step(); });
+}
+int sd_ledger_note_tau(sd_ledger* l, int tau) {
+    return guarded([&] { l->l->note_tau(tau); });
+}
+int sd_ledger_end_step(sd_ledger* l) {
+    return guarded([&] { l->l->end_step(); });
+}
+int sd_ledger_totals(const sd_ledger* l, int64_t* useful, int64_t* padding) {
+    return guarded([&] {
+        if (useful) *useful = l->l->useful();
+        if (padding) *padding = l->l->padding();
+    });
+}
+int sd_ledger_batch(const sd_ledger* l, int32_t* batch) {
+    return guarded([&] { *batch = (int32_t)l->l->useful_by.size(); });
+}
+int sd_ledger_by_sample(const sd_ledger* l, int64_t* useful, int64_t* padding) {
+    return guarded([&] {
+        const Ledger& g = *l->l;
+        if (useful) std::memcpy(useful, g.useful_by.data(), 8 * g.useful_by.size());
+        if (padding) std::memcpy(padding, g.padding_by.data(), 8 * g.padding_by.size());
+    });
+}
+int sd_ledger_num_steps(const sd_ledger* l, int64_t* n) {
+    return guarded([&] { *n = (int64_t)l->l->steps.size(); });
+}
+int sd_ledger_step(const sd_ledger* l, int64_t i, int32_t* tau_list, int32_t cap, int32_t* n_tau, int32_t* tau_max,
+                   int64_t* pad_writes, int64_t* useful_writes) {
+    return guarded([&] {
+        const Ledger& g = *l->l;
+        SD_CHECK(i >= 0 && i < (int64_t)g.steps.size(), CONTRACT, "ledger step out of range");
+        const LedgerStep& st = g.steps[(size_t)i];
+        *n_tau = (int32_t)st.taus.size();
+        for (int32_t j = 0; j < *n_tau && j < cap; ++j) tau_list[j] = st.taus[j];
+        *tau_max = st.tau_max;
+        *pad_writes = st.pad_writes;
+        *useful_writes = st.useful_writes;
+    });
+}
+// WriteLedger::dump_json (kv_cache.cpp:53-62): [{tau_list, tau_max, pad_writes,
+// useful_writes}, ...] in nlohmann's compact key order (sorted keys).  len
+// receives the full length; at most cap-1 bytes plus a NUL are written.
+int sd_ledger_dump_json(const sd_ledger* l, char* buf, int64_t cap, int64_t* len) {
+    return guarded([&] {
+        std::string o = "[";
+        bool first = true;
+        for (const LedgerStep& st : l->l->steps) {
+            o += first ? "{" : ",{";
+            first = false;
+            o += "\"pad_writes\":" + std::to_string(st.pad_writes) + ",\"tau_list\":[";
+            for (size_t j = 0; j < st.taus.size(); ++j) o += (j ? "," : "") + std::to_string(st.taus[j]);
+            o += "],\"tau_max\":" + std::to_string(st.tau_max) + ",\"useful_writes\":" +
+                 std::to_string(st.useful_writes) + "}";
+        }
+        o += "]";
+        *len = (int64_t)o.size();
+        if (buf && cap > 0) {
+            size_t n = std::min((size_t)cap - 1, o.size());
+            std::memcpy(buf, o.data(), n);
+            buf[n] = 0;
+        }
+    });
+}
+// padding_ratio (kv_cache.cpp:64-76): mean over steps of (tau_max - mean tau) / tau_max
+int sd_ledger_padding_ratio(const sd_ledger* l, double* out) {
+    return guarded([&] {
+        const Ledger& g = *l->l;
+        SD_CHECK(!g.steps.empty(), CONTRACT, "padding ratio undefined without steps");
+        double sum = 0.0;
+        for (const LedgerStep& st : g.steps) {
+            double mean = 0.0;
+            for (int32_t t : st.taus) mean += t;
+            mean /= (double)st.taus.size();
+            sum += ((double)st.tau_max - mean) / (double)st.tau_max;
+        }
+        *out = sum / (double)g.steps.size();
+    });
+}
+
 void sd_cache_destroy(sd_cache* c) {
     if (c) {
-        cudaSetDevice(c->model->m.device);
+        cudaSetDevice(c->device);
         delete c;
     }
 }

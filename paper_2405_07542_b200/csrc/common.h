@@ -88,6 +88,67 @@ void free_fast_model(FastModelState* f);
 void free_fast_workspace(FastWorkspace* f);
 void build_fast_model(Model& m);
 
+// WriteLedger (kv_cache.hpp:13-57, kv_cache.cpp:11-76): KV slot writes per
+// sample split into useful / padding, and the per-step grouping the engine
+// opens around one verify step (begin_step / note_tau / end_step).  Checks and
+// messages follow the reference; the per-step counters only move while a
+// step is open.
+struct LedgerStep {
+    std::vector<int32_t> taus;
+    int32_t tau_max = 0;
+    int64_t pad_writes = 0, useful_writes = 0;
+};
+struct Ledger {
+    std::vector<int64_t> useful_by, padding_by;
+    std::vector<LedgerStep> steps;
+    bool open = false;
+    void reset(int batch) {
+        useful_by.assign(batch, 0);
+        padding_by.assign(batch, 0);
+        steps.clear();
+        open = false;
+    }
+    void note_useful(int s, int64_t n = 1) {
+        SD_CHECK(s >= 0 && s < (int)useful_by.size(), CONTRACT, "ledger sample out of range");
+        useful_by[s] += n;
+        if (open) steps.back().useful_writes += n;
+    }
+    void note_padding(int s, int64_t n = 1) {
+        SD_CHECK(s >= 0 && s < (int)padding_by.size(), CONTRACT, "ledger sample out of range");
+        padding_by[s] += n;
+        if (open) steps.back().pad_writes += n;
+    }
+    void begin_step() {
+        SD_CHECK(!open, CONTRACT, "ledger step already open");
+        steps.emplace_back();
+        open = true;
+    }
+    void check_tau(int tau) const {
+        SD_CHECK(open, CONTRACT, "note_tau outside a step");
+        SD_CHECK(tau >= 1, CONTRACT, "acceptance length must be >= 1");
+    }
+    void note_tau(int tau) {
+        check_tau(tau);
+        steps.back().taus.push_back(tau);
+        if (tau > steps.back().tau_max) steps.back().tau_max = tau;
+    }
+    void end_step() {
+        SD_CHECK(open, CONTRACT, "no ledger step open");
+        SD_CHECK(!steps.back().taus.empty(), CONTRACT, "ledger step closed without any acceptance length");
+        open = false;
+    }
+    int64_t useful() const {
+        int64_t t = 0;
+        for (int64_t v : useful_by) t += v;
+        return t;
+    }
+    int64_t padding() const {
+        int64_t t = 0;
+        for (int64_t v : padding_by) t += v;
+        return t;
+    }
+};
+
 // Per-sample KV arena.  K and V live in [L][2][B][heads][cap][head_dim]
 // (head-major per sample so the attention kernel streams one contiguous
 // extent per (sample, head)).  Slot coordinates follow the reference: sample s
@@ -103,7 +164,7 @@ struct Cache {
     // host mirrors (the host validates every call exactly like the reference)
     std::vector<int32_t> committed, logical, staged;
     std::vector<uint8_t> pad;
-    int64_t useful = 0, padding = 0;
+    Ledger ledger;
     const Model* model = nullptr;
     ~Cache();
     size_t kv_offset(int layer, int which, int s, int head, int pos) const {

@@ -172,7 +172,7 @@ int decode_impl(const sd_engine_config& e, sd_model* target, sd_model* draft, co
                 S.generated += 1;
             }
             timing[1] += since(t0);
-            ledger[0] += cache->c.useful;
+            ledger[0] += cache->c.ledger.useful();
         }
         return finish(), 0;
     }
@@ -278,8 +278,8 @@ int decode_impl(const sd_engine_config& e, sd_model* target, sd_model* draft, co
         }
     }
     timing[1] = since(t0);
-    ledger[0] = cache->c.useful;
-    ledger[1] = cache->c.padding;
+    ledger[0] = cache->c.ledger.useful();
+    ledger[1] = cache->c.ledger.padding();
     finish();
     return 0;
 }

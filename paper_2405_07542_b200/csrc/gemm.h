@@ -49,6 +49,7 @@ struct GemmArgs {
     float* logits;            // optional [T][vocab]
     int* flag;                // non-finite flag
     ArgmaxScratch am;
+    int probe;                // 0 in the library; tools/micro probe builds (-DSD_GEMM_PROBE) only
 };
 
 struct GemmMaps {

@@ -37,6 +37,12 @@
 
 SD_TRACE_TU(gemm)
 
+#ifdef SD_GEMM_PROBE  // bottleneck probes (tools/gemm_probe.py --probe): never in the library build
+#define PROBE(bit) ((a.probe & (bit)) != 0)
+#else
+#define PROBE(bit) false
+#endif
+
 namespace sdb {
 namespace {
 
@@ -146,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const CUtensorMap* tmB = box_d == 32 ? &tmB32 : box_d == 64 ? &tmB64 : box_d == 128 ? &tmB128 : &tmB256;
         const int nbuf = box_d <= 128 ? 2 : 1;  // TMEM accumulator buffers
         if (warp == 3) {
-            if (lane == 0 && !idle) {  // ---------------- TMA producer B: the token tile of each k-block
+            if (lane == 0 && !idle && !PROBE(2)) {  // ---------------- TMA producer B: the token tile of each k-block
                 const uint64_t pol_x = ptx::policy_evict_last();  // tokens: re-read by every tile
                 int stage = 0;
                 uint32_t phase = 0;
@@ -178,12 +184,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int kb = kb0; kb < kb1; ++kb) {
                         ptx::mbar_wait(&fullA[sa_i], pa);
                         if (!idle) {
-                            ptx::mbar_wait(&fullB[sb_i], pb);
+                            if (!PROBE(2)) ptx::mbar_wait(&fullB[sb_i], pb);
                             ptx::tc_fence_after();
                             uint32_t sa = ptx::smem_u32(a_base + sa_i * kABytes);
                             uint32_t sb = ptx::smem_u32(b_base + sb_i * b_bytes);
 #pragma unroll
-                            for (int k = 0; k < kBK / 16; ++k) {
+                            for (int k = 0; k < (PROBE(1) ? 0 : kBK / 16); ++k) {
                                 uint64_t bdesc = ptx::umma_desc_kmajor_sw128(sb + k * 32);
 #pragma unroll
                                 for (int acc = 0; acc < 2; ++acc) {
@@ -228,8 +234,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j0 = 0; j0 < BN; j0 += 16) {
                         float v[16];
                         ptx::tmem_ld16(trow + acc * (nbuf == 2 ? 128 : 256) + j0, v);
+                        if (!PROBE(4)) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) ptx::st_f32_hint(dcol + (size_t)(j0 + i) * 256, v[i], pol_keep);
+                            for (int i = 0; i < 16; ++i)
+                                ptx::st_f32_hint(dcol + (size_t)(j0 + i) * 256, v[i], pol_keep);
+                        }
                     }
                 }
                 ptx::tc_fence_before();
@@ -639,14 +648,17 @@ extern "C" int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K,
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
+        a.probe = flags >> 4;  // only a -DSD_GEMM_PROBE build reads it
         gemm_launch(epi, a, maps, T, 0);  // warm-up / configure
         CUDA_OK(cudaDeviceSynchronize());
+        const int reps = (flags & 128) ? 10 : 1;  // bit 7: ten launches back to back, mean
         cudaEventRecord(e0);
-        gemm_launch(epi, a, maps, T, 0);
+        for (int r = 0; r < reps; ++r) gemm_launch(epi, a, maps, T, 0);
         cudaEventRecord(e1);
         CUDA_OK(cudaDeviceSynchronize());
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
+        ms /= reps;
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         if (usec) *usec = ms * 1000.0f;

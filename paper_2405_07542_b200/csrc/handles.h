@@ -14,9 +14,20 @@ struct sd_model {
     ~sd_model();
 };
 
+// A WriteLedger handle: standalone (sd_ledger_create) or a view of a cache's
+// own ledger (sd_cache_ledger_handle; lives and dies with the cache).
+struct sd_ledger {
+    sdb::Ledger own;
+    sdb::Ledger* l = &own;
+};
+
 struct sd_cache {
     sdb::Cache c;
-    sd_model* model = nullptr;
+    sd_model* model = nullptr;  // null for a dims-only arena until a forward binds a model
+    int device = 0;
+    int precision = 0;          // element type of the arena (sd_precision)
+    sd_ledger lh;               // lh.l -> c.ledger
+    bool kv_stored = false;     // a write_kv stored K/V bytes (a dims-only arena can no longer re-lay out)
     sdb::Workspace ws;
     // verify-step device buffers
     int kcap = 0;                 // drafts per sample the buffers hold
@@ -67,6 +78,12 @@ std::vector<int32_t> retrieval_predict(const std::vector<int32_t>& ctx, int matc
 
 sd_model* create_model(const Config& cfg, int device, int precision, const float* host_weights);
 sd_cache* create_cache(sd_model* m, int batch, int capacity, int layout);
+// A model-less arena (CacheArena(num_layers, batch, capacity, kv_dim),
+// kv_cache.cpp:78-88): one kv_dim-wide head per slot until a forward binds a
+// model, which re-lays the (still unwritten) arena out for its heads.
+sd_cache* create_cache_dims(int layers, int batch, int capacity, int kv_dim, int layout, int device, int precision);
+void bind_cache(sd_cache* c, sd_model* m);
+inline cudaStream_t cache_stream(const sd_cache* c) { return c->model ? c->model->st : nullptr; }
 
 // forward for the bf16 performance mode (fast_kernels.cu)
 void forward_fast(const Model& m, Cache& c, Workspace& ws, int T, bool want_logits, cudaStream_t st);

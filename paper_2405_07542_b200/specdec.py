@@ -102,6 +102,24 @@ def lib() -> C.CDLL:
         "sd_cache_ledger": ([vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
         "sd_cache_gather_visible": ([vp, C.c_int, C.c_int, C.c_int, F32P, F32P, C.POINTER(C.c_int32)], C.c_int),
         "sd_cache_destroy": ([vp], None),
+        "sd_cache_create_dims": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, pp], C.c_int),
+        "sd_cache_write_kv": ([vp, C.c_int, C.c_int, C.c_int, F32P, F32P], C.c_int),
+        "sd_ledger_create": ([C.c_int, pp], C.c_int),
+        "sd_ledger_destroy": ([vp], None),
+        "sd_cache_ledger_handle": ([vp, pp], C.c_int),
+        "sd_ledger_note_useful": ([vp, C.c_int], C.c_int),
+        "sd_ledger_note_padding": ([vp, C.c_int], C.c_int),
+        "sd_ledger_begin_step": ([vp], C.c_int),
+        "sd_ledger_note_tau": ([vp, C.c_int], C.c_int),
+        "sd_ledger_end_step": ([vp], C.c_int),
+        "sd_ledger_batch": ([vp, C.POINTER(C.c_int32)], C.c_int),
+        "sd_ledger_totals": ([vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
+        "sd_ledger_by_sample": ([vp, I64P, I64P], C.c_int),
+        "sd_ledger_num_steps": ([vp, C.POINTER(C.c_int64)], C.c_int),
+        "sd_ledger_step": ([vp, C.c_int64, I32P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                            C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
+        "sd_ledger_dump_json": ([vp, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
+        "sd_ledger_padding_ratio": ([vp, C.POINTER(C.c_double)], C.c_int),
         "sd_restore_indices": ([I32P, C.c_int, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int),
         "sd_forward": ([vp, vp, I32P, I32P, C.c_int, I32P, I32P, vp, vp], C.c_int),
         "sd_forward_planned": ([vp, vp, I32P, C.c_int, I32P, I32P, I32P, I32P, vp, vp], C.c_int),
@@ -357,8 +375,116 @@ class Model:
 
 
 # ---------------------------------------------------------------- caches
+@dataclass
+class LedgerStep:
+    """kv_cache.hpp:13-18"""
+
+    tau_list: list
+    tau_max: int
+    pad_writes: int
+    useful_writes: int
+
+
+class WriteLedger:
+    """WriteLedger (kv_cache.hpp:21-57): a standalone ledger (WriteLedger(batch))
+    or, from CacheArena.ledger(), the view of a cache's own ledger."""
+
+    def __init__(self, batch_size: int = 0, _cache=None):
+        h = C.c_void_p()
+        if _cache is None:
+            _check(lib().sd_ledger_create(batch_size, C.byref(h)))
+        else:
+            _check(lib().sd_cache_ledger_handle(_cache._h, C.byref(h)))
+        self._h, self._cache = h.value, _cache  # a view keeps its cache alive
+
+    def __del__(self):
+        try:
+            if self._h and self._cache is None:
+                lib().sd_ledger_destroy(self._h)
+        except Exception:
+            pass
+
+    def note_useful(self, sample: int) -> None:
+        _check(lib().sd_ledger_note_useful(self._h, sample))
+
+    def note_padding(self, sample: int) -> None:
+        _check(lib().sd_ledger_note_padding(self._h, sample))
+
+    def begin_step(self) -> None:
+        _check(lib().sd_ledger_begin_step(self._h))
+
+    def note_tau(self, tau: int) -> None:
+        _check(lib().sd_ledger_note_tau(self._h, tau))
+
+    def end_step(self) -> None:
+        _check(lib().sd_ledger_end_step(self._h))
+
+    def _totals(self):
+        u, p = C.c_int64(), C.c_int64()
+        _check(lib().sd_ledger_totals(self._h, C.byref(u), C.byref(p)))
+        return u.value, p.value
+
+    def useful_total(self) -> int:
+        return self._totals()[0]
+
+    def padding_total(self) -> int:
+        return self._totals()[1]
+
+    def total(self) -> int:
+        return sum(self._totals())
+
+    def _by_sample(self):
+        b = C.c_int32()
+        _check(lib().sd_ledger_batch(self._h, C.byref(b)))
+        u = np.zeros(max(1, b.value), np.int64)
+        p = np.zeros_like(u)
+        _check(lib().sd_ledger_by_sample(self._h, u, p))
+        return u[: b.value].tolist(), p[: b.value].tolist()
+
+    def useful_by_sample(self) -> list:
+        return self._by_sample()[0]
+
+    def padding_by_sample(self) -> list:
+        return self._by_sample()[1]
+
+    def steps(self) -> list:
+        n = C.c_int64()
+        _check(lib().sd_ledger_num_steps(self._h, C.byref(n)))
+        out = []
+        for i in range(n.value):
+            buf = np.zeros(1024, np.int32)
+            nt, tm, pw, uw = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
+            _check(lib().sd_ledger_step(self._h, i, buf, len(buf), C.byref(nt), C.byref(tm), C.byref(pw),
+                                        C.byref(uw)))
+            if nt.value > len(buf):
+                buf = np.zeros(nt.value, np.int32)
+                _check(lib().sd_ledger_step(self._h, i, buf, len(buf), C.byref(nt), C.byref(tm), C.byref(pw),
+                                            C.byref(uw)))
+            out.append(LedgerStep(buf[: nt.value].tolist(), tm.value, pw.value, uw.value))
+        return out
+
+    def dump_json(self) -> str:
+        n = C.c_int64()
+        _check(lib().sd_ledger_dump_json(self._h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib().sd_ledger_dump_json(self._h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
+
+def padding_ratio(ledger: WriteLedger) -> float:
+    """padding_ratio (kv_cache.cpp:64-76)"""
+    v = C.c_double()
+    _check(lib().sd_ledger_padding_ratio(ledger._h, C.byref(v)))
+    return v.value
+
+
 class CacheArena:
-    """CacheArena read contract (kv_cache.hpp:65-100) over the device arena."""
+    """CacheArena read contract (kv_cache.hpp:65-100) over the device arena.
+
+    CacheArena(model, batch, capacity) builds the arena for a model;
+    CacheArena.from_dims(num_layers, batch, capacity, kv_dim) is the
+    reference's model-less constructor (kv_cache.cpp:78-88): rows can be stored
+    with write_kv, and the first forward binds a model of that depth and width."""
 
     layout = UNPAD
 
@@ -369,6 +495,23 @@ class CacheArena:
         self.model = model
         self._batch = batch_size
         self._capacity = capacity
+
+    @classmethod
+    def from_dims(cls, num_layers: int, batch_size: int, capacity: int, kv_dim: int, precision: int = 0,
+                  device: int = 0):
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        _check(lib().sd_cache_create_dims(num_layers, batch_size, capacity, kv_dim, cls.layout, device, precision,
+                                          C.byref(h)))
+        self._h, self.model, self._batch, self._capacity = h.value, None, batch_size, capacity
+        self._kv_dim = kv_dim
+        return self
+
+    def write_kv(self, sample: int, position: int, layer: int, k_vec, v_vec) -> None:
+        """CacheArena::write_kv (kv_cache.cpp:128-138, 203-213)"""
+        k = np.ascontiguousarray(k_vec, dtype=np.float32)
+        v = np.ascontiguousarray(v_vec, dtype=np.float32)
+        _check(lib().sd_cache_write_kv(self._h, sample, position, layer, k, v))
 
     def batch_size(self) -> int:
         return self._batch
@@ -400,13 +543,12 @@ class CacheArena:
     def mark_hole(self, sample: int, position: int) -> None:
         _check(lib().sd_cache_mark_hole(self._h, sample, position))
 
-    def ledger(self) -> tuple[int, int]:
-        u, p = C.c_int64(), C.c_int64()
-        _check(lib().sd_cache_ledger(self._h, C.byref(u), C.byref(p)))
-        return u.value, p.value
+    def ledger(self) -> WriteLedger:
+        """The cache's own WriteLedger (kv_cache.hpp:95-96)."""
+        return WriteLedger(_cache=self)
 
     def gather_visible(self, sample: int, upto: int, layer: int):
-        hidden = self.model.config.hidden()
+        hidden = self.model.config.hidden() if self.model is not None else self._kv_dim
         k = np.zeros((upto + 1) * hidden, dtype=np.float32)
         v = np.zeros_like(k)
         n = C.c_int32()

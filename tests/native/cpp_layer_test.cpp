@@ -75,7 +75,7 @@ int main() {
             std::printf("tau %d %d %d %d\n", step + 1, s, v.tau, arena.committed_len(s));
         }
     }
-    std::printf("ledger %lld %lld\n", (long long)arena.useful_writes(), (long long)arena.padding_writes());
+    std::printf("ledger %lld %lld\n", (long long)arena.ledger().useful_total(), (long long)arena.ledger().padding_total());
     // the array forms of the C ABI: all lengths at once, batched commit
     int32_t com[3], so[3];
     b200::check(sd_cache_get_lengths(arena.handle(), com, so));
@@ -99,14 +99,18 @@ int main() {
         stage(0, 0, 1, 0);
         stage(1, 0, 1, 0);
         grid.commit_prefill({0, 1}, {1, 1});
+        grid.ledger().begin_step();
         stage(0, 1, 6, 1);
         stage(1, 1, 3, 1);
         grid.commit_padded({0, 1}, {4, 1});
-        const long long after1 = grid.padding_writes();
+        grid.ledger().end_step();
+        const long long after1 = grid.ledger().padding_total();
+        grid.ledger().begin_step();
         stage(0, 5, 3, 5);
         stage(1, 5, 6, 2);
         grid.commit_padded({0, 1}, {2, 6});
-        std::printf("grid_padding %lld %lld %d %d %d\n", after1, (long long)grid.padding_writes(),
+        grid.ledger().end_step();
+        std::printf("grid_padding %lld %lld %d %d %d\n", after1, (long long)grid.ledger().padding_total(),
                     grid.committed_len(0), grid.logical_len(1), grid.is_pad(1, 2) ? 1 : 0);
     }
 

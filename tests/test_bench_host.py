@@ -80,3 +80,29 @@ def test_reference_extrapolation_scales_with_layers():
     one = bench.extrapolate(cfg, 1.0, 1, 14, 256)
     two = bench.extrapolate(cfg, 1.0, 2, 14, 256)
     assert one > two > 0  # timing more layers per sample means fewer extrapolated
+
+
+def test_reference_bench_checks_follow_specdec_main():
+    """The seven checks of tools/specdec_main.cpp:197-220 on hand-made runs:
+    Table-1-like trajectory (taus (4, 1) then (2, 2)), identical across layouts."""
+    from types import SimpleNamespace as NS
+
+    steps = [{"samples": [{"sample": 0, "k": 3, "tau": 4, "clipped": False},
+                          {"sample": 1, "k": 0, "tau": 1, "clipped": False}]},
+             {"samples": [{"sample": 0, "k": 1, "tau": 2, "clipped": False},
+                          {"sample": 1, "k": 1, "tau": 2, "clipped": False}]}]
+    toks = [[5, 6, 7, 8, 9, 10], [5, 6, 7]]
+    met = lambda useful, pad_w, in_pad, kv_pad, extra: {
+        "useful_kv_writes": useful, "padding_kv_writes": pad_w, "total_input_padding": in_pad,
+        "total_kv_padding": kv_pad, "total_tokens_processed": useful + extra}
+    res = {"greedy": (NS(generated_tokens=toks, steps=[]), met(0, 0, 0, 0, 0)),
+           "vanilla": (NS(generated_tokens=toks, steps=steps), met(8, 3, 3, 3, 6)),
+           "ems": (NS(generated_tokens=toks, steps=steps), met(8, 0, 3, 3, 0))}
+    chk = bench.reference_bench_checks(res)
+    assert all(chk.values()), chk
+    # a vanilla run that diverged fails exactly the cross-layout checks
+    res["vanilla"] = (NS(generated_tokens=[toks[0], [5, 6, 4]], steps=steps[:1]), met(7, 3, 3, 3, 6))
+    chk = bench.reference_bench_checks(res)
+    assert not chk["aligned_output_matches_greedy"] and not chk["aligned_and_unpad_step_records_agree"]
+    assert not chk["useful_writes_agree_across_layouts"]
+    assert chk["unpad_output_matches_greedy"] and chk["unpad_wrote_zero_padding_slots"]

@@ -90,6 +90,7 @@ def test_gpu_fused_verify_step_c1_bit_exact(sd, oracle):
     toks = [prompts[s] + [int(am[rows[s]])] for s in range(B)]
     gen = [1] * B
     at_row = 0
+    step_taus = []
     for step, T in enumerate(g["step_T"]):
         active = [int(x < 128) for x in gen]
         drafts = [oracle.retrieval_predict(toks[s], 2, 4) if active[s] else [] for s in range(B)]
@@ -98,6 +99,7 @@ def test_gpu_fused_verify_step_c1_bit_exact(sd, oracle):
         tau, acc, clipped, lg = c.verify_step([t[-1] for t in toks], counts, [x for d in drafts for x in d],
                                               [128 - x for x in gen], active, False, want_logits=True)
         assert tau.tolist() == g["step_tau"][step].tolist(), f"step {step}"
+        step_taus.append([int(t) for t, a in zip(tau, active) if a])
         assert (P.fnv_rows(lg) == g["step_fnv"][at_row: at_row + T]).all()
         at_row += T
         for s in range(B):
@@ -105,7 +107,10 @@ def test_gpu_fused_verify_step_c1_bit_exact(sd, oracle):
             gen[s] += int(tau[s])
         assert [c.committed_len(s) for s in range(B)] == g["step_committed"][step].tolist()
     assert [t[len(p):] for t, p in zip(toks, prompts)] == g["generated"].tolist()
-    assert c.ledger() == (int(g["step_T"].sum()) + int(g["prompt_lens"].sum()), 0)
+    led = c.ledger()
+    assert (led.useful_total(), led.padding_total()) == (int(g["step_T"].sum()) + int(g["prompt_lens"].sum()), 0)
+    # one ledger step per sd_verify_step call, its taus in sample order (engine.cpp:398-487)
+    assert [st.tau_list for st in led.steps()] == step_taus
 
 
 @pytest.mark.parametrize("name", ["c1_ems_decode", "c1_vanilla_decode"] +
@@ -346,46 +351,67 @@ def test_gpu_results_json_matches_reference(sd, mode):
 
 
 def test_gpu_table1_scripted_trace_ledgers(sd):
-    """The same script driven through the device arenas (KV rows written by
-    forward_planned, commits through the C ABI): the aligned grid writes 3 + 4
-    PAD filler rows, the unpadded arena none (acceptance.cpp:125-176)."""
-    m = sd.Model.init(sd.ModelConfig())
+    """acceptance.cpp:125-176 (check 2, the paper's Table 1) on the device
+    arenas, through the reference's own calls: write_kv rows, commit_prefill,
+    ledger steps around commit_padded / commit_accepted + note_tau.  The
+    aligned grid writes 3 + 4 PAD filler rows, the unpadded arena none."""
+    vec = np.full(4, 0.25, np.float32)
 
-    def stage(cache, sample, start, count, logical0=None):
-        lp0 = start if logical0 is None else logical0
-        plans = [sd.TokenPlan(sample=sample, logical_pos=lp0 + i, write_slot=start + i, store=True)
-                 for i in range(count)]
-        m.forward_planned([5] * count, plans, cache, want_logits=False)
+    def stage(arena, sample, start, count):
+        for pos in range(start, start + count):
+            arena.write_kv(sample, pos, 0, vec, vec)
 
-    grid = sd.PaddedGrid(m, 2, 32)
+    grid = sd.PaddedGrid.from_dims(1, 2, 32, 4)
     stage(grid, 0, 0, 1)
     stage(grid, 1, 0, 1)
     grid.commit_prefill([0, 1], [1, 1])
+    grid.ledger().begin_step()
     stage(grid, 0, 1, 6)
     stage(grid, 1, 1, 3)
     grid.commit_padded([0, 1], [4, 1])
-    assert grid.ledger()[1] == 3
-    stage(grid, 0, 5, 3, logical0=5)
-    stage(grid, 1, 5, 6, logical0=2)
+    grid.ledger().end_step()
+    grid.ledger().begin_step()
+    stage(grid, 0, 5, 3)
+    stage(grid, 1, 5, 6)
     grid.commit_padded([0, 1], [2, 6])
-    assert grid.ledger()[1] == 3 + 4
+    grid.ledger().end_step()
+    led = grid.ledger()
+    assert [st.pad_writes for st in led.steps()] == [3, 4]
+    assert led.padding_by_sample() == [4, 3]
+    assert [st.tau_list for st in led.steps()] == [[4, 1], [2, 6]]
     assert [grid.committed_len(s) for s in (0, 1)] == [11, 11]
+    assert [grid.logical_len(s) for s in (0, 1)] == [7, 8]
+    # the filler rows are real zero writes on the device, skipped by reads
+    k, v = grid.gather_visible(1, 10, 0)
+    assert len(k) == 8 and np.all(k == 0.25)
 
-    arena = sd.UnpadArena(m, 2, 32)
+    arena = sd.UnpadArena.from_dims(1, 2, 32, 4)
     stage(arena, 0, 0, 1)
     stage(arena, 1, 0, 1)
     arena.commit_accepted(0, 1)
     arena.commit_accepted(1, 1)
+    arena.ledger().begin_step()
     stage(arena, 0, 1, 6)
     stage(arena, 1, 1, 3)
     arena.commit_accepted(0, 4)
     arena.commit_accepted(1, 1)
+    arena.ledger().note_tau(4)
+    arena.ledger().note_tau(1)
+    arena.ledger().end_step()
+    arena.ledger().begin_step()
     stage(arena, 0, 5, 3)
     stage(arena, 1, 2, 6)
     arena.commit_accepted(0, 2)
     arena.commit_accepted(1, 6)
-    assert arena.ledger()[1] == 0
+    arena.ledger().note_tau(2)
+    arena.ledger().note_tau(6)
+    arena.ledger().end_step()
+    led = arena.ledger()
+    assert led.padding_total() == 0 and [st.pad_writes for st in led.steps()] == [0, 0]
     assert [arena.committed_len(s) for s in (0, 1)] == [7, 8]
+    assert sd.padding_ratio(grid.ledger()) == pytest.approx(sd.padding_ratio(arena.ledger()), abs=1e-15)
+    with pytest.raises(sd.ContractError):  # commit_padded notes its taus: a ledger step must be open
+        grid.commit_padded([0, 1], [1, 1])
 
 
 def test_gpu_write_gap_is_the_padding_shortfall(sd):

@@ -1,0 +1,47 @@
+"""The reference's own hot-path unit suites (proj/tests/test_ragged.cpp,
+test_kv_cache.cpp, test_model.cpp + support/naive_model.cpp), recompiled
+unmodified against our C++ layer include/specdec_b200.hpp with a
+doctest-compatible harness (tests/native/Makefile, binaries in
+tests/native/_reftests/, built by __graft_entry__.build() where the reference
+sources exist).  Every TEST_CASE must pass on the B200; the host-only cases
+(ragged batching, the WriteLedger protocol) also run here without a GPU."""
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+BIN = os.path.join(ROOT, "tests", "native", "_reftests")
+
+
+def run_suite(name, timeout=600):
+    exe = os.path.join(BIN, name)
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (make -C tests/native reftests needs /root/reference)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=timeout)
+    cases = {}
+    for line in r.stdout.splitlines():
+        if line.startswith("[PASS] ") or line.startswith("[FAIL] "):
+            cases[line[7:]] = line.startswith("[PASS]")
+    return r, cases
+
+
+def test_ragged_suite_passes_without_gpu(sd):
+    r, cases = run_suite("test_ragged")
+    assert r.returncode == 0 and len(cases) == 7 and all(cases.values()), r.stdout
+
+
+def test_kv_cache_ledger_cases_pass_without_gpu(sd):
+    _, cases = run_suite("test_kv_cache")
+    for name in ("ledger step bookkeeping enforces its protocol", "padding ratio averages per-step shortfall ratios",
+                 "ledger dump is valid JSON with per-step fields"):
+        assert cases.get(name), name
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite,n_cases", [("test_ragged", 7), ("test_kv_cache", 18), ("test_model", 15)])
+def test_reference_suite_passes_on_b200(sd, suite, n_cases):
+    r, cases = run_suite(suite)
+    assert len(cases) == n_cases, r.stdout
+    assert r.returncode == 0 and all(cases.values()), r.stdout[-4000:]
