@@ -264,6 +264,9 @@ int sd_session_run_host(sd_session* s, int32_t* steps, float* gpu_ms, int64_t* h
  * of draft counts k (-1 inactive) and tau (| 0x10000 when clipped) */
 int sd_session_outputs(sd_session* s, int32_t* gen_tokens, int32_t* gen_counts, int32_t* log_k,
                        int32_t* log_tau, int max_steps);
+/* the drafts each verify step checked: [max_steps][B][kcap] (kcap = k, or
+ * copy_len for the retrieval predictor); entry j < log_k[step][s] is valid */
+int sd_session_draft_log(sd_session* s, int32_t* drafts, int max_steps);
 int sd_session_cache(sd_session* s, sd_cache** out);
 /* run n device steps eagerly (no graph, no completion loop) -- profiling */
 int sd_session_step(sd_session* s, int n);

@@ -28,7 +28,7 @@ struct sd_session {
     int B = 0, ctx_cap = 0, kcap = 0, max_steps = 0;
     // device state
     int32_t *ctx = nullptr, *ctx_len = nullptr, *gen = nullptr, *active = nullptr, *counts = nullptr,
-            *drafts = nullptr, *n_active = nullptr, *step = nullptr, *log_k = nullptr, *log_tau = nullptr,
+            *drafts = nullptr, *n_active = nullptr, *step = nullptr, *log_k = nullptr, *log_tau = nullptr, *log_drafts = nullptr,
             *traj = nullptr, *first_row = nullptr, *draft_off = nullptr, *scalars = nullptr, *tau = nullptr,
             *accepted = nullptr, *clipped = nullptr;
     int traj_stride = 0;
@@ -86,6 +86,8 @@ StepArgs step_args(sd_session* s) {
     a.n_active = s->n_active;
     a.log_k = s->log_k;
     a.log_tau = s->log_tau;
+    a.log_drafts = s->log_drafts;
+    a.log_kcap = s->kcap;
     a.step = s->step;
     a.max_steps = s->max_steps;
     a.committed = c.d_committed;
@@ -217,6 +219,7 @@ sd_session* session_create(sd_model* m, const sd_engine_config& e, int capacity,
         s->step = ialloc(s, 4);
         s->log_k = ialloc(s, (size_t)s->max_steps * B);
         s->log_tau = ialloc(s, (size_t)s->max_steps * B);
+        s->log_drafts = ialloc(s, (size_t)s->max_steps * B * std::max(1, s->kcap));
         s->first_row = ialloc(s, B);
         s->draft_off = ialloc(s, B);
         s->scalars = ialloc(s, 8);
@@ -655,6 +658,13 @@ int sd_session_outputs(sd_session* s, int32_t* gen_tokens, int32_t* gen_counts, 
         int n = std::min(max_steps, s->max_steps);
         if (log_k) CUDA_OK(cudaMemcpy(log_k, s->log_k, 4 * (size_t)n * B, cudaMemcpyDeviceToHost));
         if (log_tau) CUDA_OK(cudaMemcpy(log_tau, s->log_tau, 4 * (size_t)n * B, cudaMemcpyDeviceToHost));
+    });
+}
+int sd_session_draft_log(sd_session* s, int32_t* drafts, int max_steps) {
+    return sguard([&] {
+        int n = std::min(max_steps, s->max_steps);
+        CUDA_OK(cudaMemcpy(drafts, s->log_drafts, 4 * (size_t)n * s->B * std::max(1, s->kcap),
+                           cudaMemcpyDeviceToHost));
     });
 }
 int sd_session_cache(sd_session* s, sd_cache** out) {

@@ -27,6 +27,8 @@ struct StepArgs {
     int32_t* n_active;       // scalar: samples still active after this step
     int32_t* log_k;          // [max_steps][B] step records (or null)
     int32_t* log_tau;
+    int32_t* log_drafts;     // [max_steps][B][log_kcap] the drafts each step verified (or null)
+    int log_kcap;
     int32_t* step;           // scalar step counter
     int max_steps;
     // cache descriptors (mutated by k_accept) --------------------------------

@@ -165,6 +165,9 @@ __global__ void k_accept(StepArgs a) {
         if (logging) {
             a.log_tau[(size_t)s_step * B + s] = tau + (a.clipped[s] ? 0x10000 : 0);
             a.log_k[(size_t)s_step * B + s] = ks;
+            if (a.log_drafts)
+                for (int j = 0; j < ks && j < a.log_kcap; ++j)
+                    a.log_drafts[((size_t)s_step * B + s) * a.log_kcap + j] = draft_at(a, s, d0, j);
         }
     }
     __syncthreads();

@@ -139,6 +139,7 @@ def lib() -> C.CDLL:
                                  C.POINTER(C.c_int64)], C.c_int),
         "sd_session_outputs": ([vp, I32P, I32P, vp, vp, C.c_int], C.c_int),
         "sd_session_destroy": ([vp], None),
+        "sd_session_draft_log": ([vp, I32P, C.c_int], C.c_int),
     }
     for name, (args, res) in sig.items():
         if LIB_PATH != _DEFAULT_LIB and not hasattr(L, name):
@@ -845,3 +846,12 @@ class Session:
         _scheck(lib().sd_session_outputs(self._h, gen, cnt, lk.ctypes.data, lt.ctypes.data, steps))
         tokens = [gen[s * mx: s * mx + min(cnt[s], mx)].tolist() for s in range(B)]
         return tokens, lk.reshape(steps, B), lt.reshape(steps, B)
+
+    def draft_log(self) -> np.ndarray:
+        """[steps][B][kcap] drafts each verify step checked (valid below log_k)."""
+        B = self.config.batch_size
+        kcap = max(1, self.config.copy_len if self.config.predictor == "retrieval" else self.config.k)
+        steps = self.config.max_new_tokens + 2
+        out = np.zeros(steps * B * kcap, dtype=np.int32)
+        _scheck(lib().sd_session_draft_log(self._h, out, steps))
+        return out.reshape(steps, B, kcap)

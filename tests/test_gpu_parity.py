@@ -176,3 +176,20 @@ def test_c3_layer_truncated_forward_vs_float64(sd):
     assert st["mean_abs_over_std"] <= 0.03
     assert st["argmax_agree"] >= 0.9
     assert st["token_agree"] >= 0.75  # greedy streams, position-wise
+
+
+# ------------------------------------------------------------------ (d)
+def test_long_prompt_prefill_vs_float64(sd):
+    """(d) Prefill of 600-700-token prompts (3 forward chunks of 256 tokens;
+    attention items of 8 queries, each tile stopping at its own causal
+    limit) on the unpadded arena and on the left-padded vanilla grid,
+    at the C3 width (L = 2): the stated bf16 tolerance on sampled rows and
+    argmax agreement over every prompt row."""
+    from torch_ref import prefill_parity
+
+    st = prefill_parity(sd)
+    print("prefill bf16 vs float64:", st)
+    for layout, s in st.items():
+        assert s["max_abs_over_std"] <= 0.15, layout
+        assert s["mean_abs_over_std"] <= 0.03, layout
+        assert s["argmax_agree"] >= 0.9 and s["argmax_agree_all_rows"] >= 0.9, layout

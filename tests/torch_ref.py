@@ -169,3 +169,50 @@ def c3_truncated_parity(sd, cfg=C3_L2, B=4, seed=1, greedy_tokens=0) -> dict:
     m.close()
     torch.cuda.empty_cache()
     return out
+
+
+def prefill_parity(sd, cfg=C3_L2, B=2, lo=600, hi=700, seed=3, every=9) -> dict:
+    """Long-prompt prefill (engine.cpp:330-385) through the bf16 kernels in
+    256-token chunks, on both layouts -- the unpadded arena and the vanilla
+    padded grid with its left-pad holes (engine.cpp:335-357) -- against the
+    float64 reference: every `every`-th prompt row's logits, and the argmax of
+    every row."""
+    import torch
+
+    rng = np.random.default_rng(seed)
+    V = cfg["vocab_size"]
+    prompts = [[0] + rng.integers(3, V, size=int(rng.integers(lo, hi))).tolist() for _ in range(B)]
+    m32 = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.FP32_CHECK)
+    ref = TorchRef(cfg, m32.tensors(), device="cuda", dtype=torch.float64)
+    m32.close()
+    want = [list(range(0, len(p), every)) + [len(p) - 1] for p in prompts]
+    ref_rows = np.concatenate([ref.logits(p, rows=w) for p, w in zip(prompts, want)])
+    ref_am = np.concatenate([ref.logits(p).argmax(1) for p in prompts])
+    m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.BF16)
+    out = {}
+    for layout in ("unpad", "padded"):
+        rows_needed = max(map(len, prompts))
+        if layout == "unpad":
+            c = sd.UnpadArena(m, B, rows_needed + 8)
+            lg, am = m.forward(sd.concatenate_inputs(prompts), c,
+                               [sd.TokenSlot(s, i) for s in range(B) for i in range(len(prompts[s]))])
+        else:
+            c = sd.PaddedGrid(m, B, rows_needed + 8)
+            toks, plans = [], []
+            for s, p in enumerate(prompts):
+                holes = rows_needed - len(p)
+                for r in range(holes):
+                    c.mark_hole(s, r)
+                toks += p
+                plans += [sd.TokenPlan(sample=s, logical_pos=i, write_slot=holes + i, store=True) for i in range(len(p))]
+            lg, am = m.forward_planned(toks, plans, c)
+        c.close()
+        offs = np.cumsum([0] + [len(p) for p in prompts[:-1]])
+        pick = np.concatenate([o + np.asarray(w) for o, w in zip(offs, want)])
+        st = parity_stats(lg[pick], ref_rows)
+        st["argmax_agree_all_rows"] = float(np.mean(am == ref_am))
+        st["rows_total"] = int(len(am))
+        out[layout] = st
+    m.close()
+    torch.cuda.empty_cache()
+    return out
