@@ -221,6 +221,25 @@ int sd_verify_step(sd_model* m, sd_cache* c, const int32_t* last_tokens,
                    const int32_t* budget_left, const int32_t* active, int stop_on_eos,
                    int32_t* tau, int32_t* accepted, int32_t* clipped, float* logits);
 
+/* The same step, asynchronous (calls are stream-ordered and
+ * async until outputs are read).  sd_verify_step_async validates on the host
+ * (errors are returned before anything is enqueued, nothing mutated), copies
+ * the inputs to pinned staging and enqueues H2D -> pack -> forward -> accept
+ * [-> pad_fill] -> D2H on `stream` (a cudaStream_t; NULL = the cache's stream,
+ * see sd_cache_set_stream), then returns.  sd_verify_step_wait blocks until
+ * that work is done, raises device-side errors (non-finite logit) and applies
+ * the commit to the cache's host mirrors and ledger; accepted is
+ * [B][k_max + 1] with k_max the largest active draft count of that step.
+ * Between the two calls every other call on the cache returns SD_CONTRACT.
+ * Logits are not available on this path. */
+int sd_verify_step_async(sd_model* m, sd_cache* c, const int32_t* last_tokens,
+                         const int32_t* draft_counts, const int32_t* drafts,
+                         const int32_t* budget_left, const int32_t* active, int stop_on_eos, void* stream);
+int sd_verify_step_wait(sd_cache* c, int32_t* tau, int32_t* accepted, int32_t* clipped);
+/* Order all of this cache's device work on `stream` (a cudaStream_t; NULL
+ * restores the model's internal stream). */
+int sd_cache_set_stream(sd_cache* c, void* stream);
+
 /* ---- engine (decode_speculative / decode_greedy, engine.cpp:206-489) ------ */
 /* prompts: concatenated token ids (BOS included), prompt_lens[B].
  * gen_tokens[B][max_new_tokens], gen_counts[B]; step records as rows of
@@ -271,6 +290,28 @@ int sd_session_cache(sd_session* s, sd_cache** out);
 /* run n device steps eagerly (no graph, no completion loop) -- profiling */
 int sd_session_step(sd_session* s, int n);
 void sd_session_destroy(sd_session* s);
+
+/* ---- multi-GPU: samples sharded over the GPUs of one box */
+/* Weights are replicated and every rank runs its own verify loop (global
+ * sample ids: sd_engine_config.sample_id_base); the step has no collective.
+ * The per-sample outputs are all-gathered once at the end over NCCL
+ * (libnccl.so.2, opened at first use).  Bootstrap for C++ hosts: rank 0 calls
+ * sd_nccl_unique_id and ships the 128 bytes to every rank out of band; each
+ * rank then calls sd_comm_init on its own GPU. */
+typedef struct sd_comm sd_comm;
+const char* sd_comm_last_error(void);
+int sd_nccl_unique_id(uint8_t* id /* [128] */);
+int sd_comm_init(const uint8_t* id, int world, int rank, int device, sd_comm** out);
+int sd_comm_size(const sd_comm* c, int* world, int* rank);
+void sd_comm_destroy(sd_comm* c);
+/* every rank sends `count` int32 (same count on all ranks), every rank
+ * receives world * count of them in rank order; host buffers */
+int sd_comm_allgather_i32(sd_comm* c, const int32_t* local, int64_t count, int32_t* all);
+/* A finished session's outputs gathered over all ranks in global sample
+ * order (rank r holds samples [r B, (r+1) B)): gen_tokens [world B][max_new],
+ * gen_counts [world B]; every rank's session must have the same B and
+ * max_new_tokens. */
+int sd_session_gather_outputs(sd_session* s, sd_comm* c, int32_t* gen_tokens, int32_t* gen_counts);
 
 #ifdef __cplusplus
 }

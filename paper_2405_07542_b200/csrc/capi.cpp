@@ -282,9 +282,8 @@ void reset_cache(sd_cache* h) {
 }
 
 // ------------------------------------------------------------------ forward
-static void sync_descriptors_to_device(sd_cache* h) {
+static void sync_descriptors_to_device(sd_cache* h, cudaStream_t st) {
     Cache& c = h->c;
-    cudaStream_t st = cache_stream(h);
     CUDA_OK(cudaMemcpyAsync(c.d_committed, c.committed.data(), 4 * (size_t)c.B, cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(c.d_logical, c.logical.data(), 4 * (size_t)c.B, cudaMemcpyHostToDevice, st));
     if (c.layout == PADDED)
@@ -293,7 +292,7 @@ static void sync_descriptors_to_device(sd_cache* h) {
 
 static void run_forward(sd_model* mh, sd_cache* h, int T, float* logits, int32_t* argmax) {
     Model& m = mh->m;
-    cudaStream_t st = mh->st;
+    cudaStream_t st = cache_stream(h);
     if (m.precision == FP32_CHECK) {
         forward_check(m, h->c, h->ws, T, true, st);
         note_launches(3 + 11 * (int64_t)m.cfg.num_layers + 3);
@@ -322,6 +321,7 @@ void forward_planned_host(sd_model* mh, sd_cache* h, const int32_t* tokens, cons
     set_device(m.device);
     // model.cpp:266-285
     SD_CHECK(n > 0, CONTRACT, "forward pass over zero tokens");
+    check_idle(h);
     bind_cache(h, mh);
     SD_CHECK(c.model == &m && c.heads * c.hd == cfg.hidden(), CONTRACT, "cache width does not match the model");
     SD_CHECK(c.L == cfg.num_layers, CONTRACT, "cache depth does not match the model");
@@ -365,8 +365,8 @@ void forward_planned_host(sd_model* mh, sd_cache* h, const int32_t* tokens, cons
             SD_CHECK(plans[t].write_slot < c.staged[plans[t].sample], CONTRACT, "read past the written extent");
 
     h->ws.ensure(m, c, n);
-    cudaStream_t st = mh->st;
-    sync_descriptors_to_device(h);
+    cudaStream_t st = cache_stream(h);
+    sync_descriptors_to_device(h, st);
     CUDA_OK(cudaMemcpyAsync(h->ws.d_tokens, tokens, 4 * (size_t)n, cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaMemcpyAsync(h->ws.d_plans, plans, sizeof(Plan) * (size_t)n, cudaMemcpyHostToDevice, st));
     run_forward(mh, h, n, logits, argmax);
@@ -398,6 +398,7 @@ void forward_ragged_host(sd_model* mh, sd_cache* h, const int32_t* tokens, const
 }
 
 void commit_accepted_host(sd_cache* h, int s, int tau) {  // kv_cache.cpp:152-161
+    check_idle(h);
     Cache& c = h->c;
     SD_CHECK(c.layout == UNPAD, CONTRACT, "not an unpad arena");
     SD_CHECK(s >= 0 && s < c.B, CONTRACT, "cache sample out of range");
@@ -409,9 +410,16 @@ void commit_accepted_host(sd_cache* h, int s, int tau) {  // kv_cache.cpp:152-16
 }
 
 // --------------------------------------------------------------- verify step
-int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32_t* counts,
-                     const int32_t* drafts, const int32_t* budget, const int32_t* active, int stop_on_eos,
-                     int32_t* tau, int32_t* accepted, int32_t* clipped, float* logits) {
+// The step is split in two so that it can run asynchronously on a caller's
+// stream: verify_step_enqueue validates on the host (before any state
+// changes), stages the inputs in pinned memory and enqueues H2D -> pack ->
+// forward -> accept [-> pad_fill] -> D2H on `st`; verify_step_finish waits
+// for it, raises the device flags and applies the commit to the host mirrors
+// and the ledger.  While a step is in flight the cache refuses other calls.
+void verify_step_enqueue(sd_model* mh, sd_cache* h, const int32_t* last, const int32_t* counts,
+                         const int32_t* drafts, const int32_t* budget, const int32_t* active, int stop_on_eos,
+                         float* logits, cudaStream_t st) {
+    SD_CHECK(!h->inflight.on, CONTRACT, "a verify step is already in flight on this cache");
     Model& m = mh->m;
     Cache& c = h->c;
     const Config& cfg = m.cfg;
@@ -482,8 +490,7 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
     // the graph path below sizes its grids for B x (kcap + 1): allocate for that
     // bound up front (a reallocation would move buffers the StepArgs point at)
     h->ws.ensure(m, c, m.precision != FP32_CHECK && !logits && B * K1 <= 256 ? std::max(T, B * K1) : T);
-    cudaStream_t st = mh->st;
-    sync_descriptors_to_device(h);
+    sync_descriptors_to_device(h, st);
     CUDA_OK(cudaMemcpyAsync(ds, hs, 4 * (o_drafts + ndraft), cudaMemcpyHostToDevice, st));
     StepArgs a{};
     a.B = B;
@@ -563,12 +570,38 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
             note_launches(1);
         }
     }
-    int32_t flag = 0;
-    CUDA_OK(cudaMemcpyAsync(&flag, h->ws.d_flag, 4, cudaMemcpyDeviceToHost, st));
+    // device flag + outputs into the pinned step block (o_scal + 7 holds the flag)
+    CUDA_OK(cudaMemcpyAsync(hs + o_scal + 7, h->ws.d_flag, 4, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaMemcpyAsync(hs + o_tau, ds + o_tau, 4 * ((size_t)2 * B + (size_t)B * K1), cudaMemcpyDeviceToHost, st));
     if (logits)
         CUDA_OK(cudaMemcpyAsync(logits, h->ws.d_logits, 4 * (size_t)T * cfg.vocab_size, cudaMemcpyDeviceToHost, st));
-    CUDA_OK(cudaStreamSynchronize(st));
+    if (!h->done_ev) CUDA_OK(cudaEventCreateWithFlags(&h->done_ev, cudaEventDisableTiming));
+    CUDA_OK(cudaEventRecord(h->done_ev, st));
+    VerifyInflight& f = h->inflight;
+    f.on = true;
+    f.kmax = kmax;
+    f.base = base;
+    f.counts.assign(counts, counts + B);
+    f.active.assign(active, active + B);
+    f.o_tau = o_tau;
+    f.o_clip = o_clip;
+    f.o_acc = o_acc;
+    f.o_flag = o_scal + 7;
+    f.K1 = K1;
+}
+
+int verify_step_finish(sd_cache* h, int32_t* tau, int32_t* accepted, int32_t* clipped) {
+    SD_CHECK(h->inflight.on, CONTRACT, "no verify step in flight on this cache");
+    VerifyInflight& f = h->inflight;
+    Cache& c = h->c;
+    const int B = c.B, kmax = f.kmax, base = f.base, K1 = f.K1;
+    const int32_t* counts = f.counts.data();
+    const int32_t* active = f.active.data();
+    const int32_t* hs = h->h_step;
+    const size_t o_tau = f.o_tau, o_clip = f.o_clip, o_acc = f.o_acc;
+    f.on = false;  // the step is consumed whatever happens below
+    CUDA_OK(cudaEventSynchronize(h->done_ev));
+    const int32_t flag = hs[f.o_flag];
     if (flag != 0) {
         CUDA_OK(cudaMemset(h->ws.d_flag, 0, 4));
         if (flag == 3) throw Error(CONTRACT, prefixed(CONTRACT, "token with an empty visible set"));
@@ -608,7 +641,15 @@ int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32
     return kmax;
 }
 
+int verify_step_host(sd_model* mh, sd_cache* h, const int32_t* last, const int32_t* counts,
+                     const int32_t* drafts, const int32_t* budget, const int32_t* active, int stop_on_eos,
+                     int32_t* tau, int32_t* accepted, int32_t* clipped, float* logits) {
+    verify_step_enqueue(mh, h, last, counts, drafts, budget, active, stop_on_eos, logits, cache_stream(h));
+    return verify_step_finish(h, tau, accepted, clipped);
+}
+
 void commit_prefill_host(sd_cache* h, const int32_t* samples, const int32_t* lens, int n) {  // kv_cache.cpp:237-267
+        check_idle(h);
         Cache& c = h->c;
         SD_CHECK(c.layout == PADDED, CONTRACT, "not a padded grid");
         SD_CHECK(n >= 1, CONTRACT, "prefill commit needs matching sample and length lists");
@@ -633,6 +674,7 @@ void commit_prefill_host(sd_cache* h, const int32_t* samples, const int32_t* len
 }
 
 void mark_hole_host(sd_cache* h, int s, int pos) {  // kv_cache.cpp:215-219
+        check_idle(h);
         Cache& c = h->c;
         SD_CHECK(c.layout == PADDED, CONTRACT, "this cache layout has no masked holes");
         SD_CHECK(s >= 0 && s < c.B, CONTRACT, "cache sample out of range");
@@ -648,6 +690,8 @@ sd_model::~sd_model() {
     if (st) cudaStreamDestroy(st);
 }
 sd_cache::~sd_cache() {
+    if (inflight.on && done_ev) cudaEventSynchronize(done_ev);  // never free buffers under a running step
+    if (done_ev) cudaEventDestroy(done_ev);
     if (vgraph) cudaGraphExecDestroy(vgraph);
     sdb::dfree(d_step);
     if (h_step) cudaFreeHost(h_step);
@@ -914,6 +958,7 @@ int sd_cache_commit_prefill(sd_cache* h, const int32_t* samples, const int32_t* 
 
 int sd_cache_commit_padded(sd_cache* h, const int32_t* samples, const int32_t* taus, int n) {
     return guarded([&] {  // kv_cache.cpp:269-314
+        check_idle(h);
         Cache& c = h->c;
         SD_CHECK(c.layout == PADDED, CONTRACT, "not a padded grid");
         SD_CHECK(n >= 1, CONTRACT, "padded commit needs matching sample and tau lists");
@@ -992,6 +1037,7 @@ int sd_cache_ledger(const sd_cache* c, int64_t* useful, int64_t* padding) {
 int sd_cache_gather_visible(const sd_cache* h, int s, int upto, int layer, float* k_out, float* v_out,
                             int32_t* count) {
     return guarded([&] {
+        check_idle(h);
         const Cache& c = h->c;
         SD_CHECK(s >= 0 && s < c.B, CONTRACT, "cache sample out of range");
         SD_CHECK(layer >= 0 && layer < c.L, CONTRACT, "cache layer out of range");
@@ -1037,6 +1083,7 @@ int sd_cache_create_dims(int num_layers, int batch, int capacity, int kv_dim, in
 
 int sd_cache_write_kv(sd_cache* h, int s, int pos, int layer, const float* k_vec, const float* v_vec) {
     return guarded([&] {  // UnpadArena / PaddedGrid::write_kv (kv_cache.cpp:93-103, 128-138, 203-213)
+        check_idle(h);
         Cache& c = h->c;
         SD_CHECK(s >= 0 && s < c.B, CONTRACT, "cache sample out of range");
         SD_CHECK(layer >= 0 && layer < c.L, CONTRACT, "cache layer out of range");
@@ -1173,6 +1220,13 @@ int sd_ledger_padding_ratio(const sd_ledger* l, double* out) {
     });
 }
 
+int sd_cache_set_stream(sd_cache* c, void* stream) {
+    return guarded([&] {
+        check_idle(c);
+        c->user_stream = (cudaStream_t)stream;
+    });
+}
+
 void sd_cache_destroy(sd_cache* c) {
     if (c) {
         cudaSetDevice(c->device);
@@ -1229,6 +1283,22 @@ int sd_verify_step(sd_model* m, sd_cache* c, const int32_t* last, const int32_t*
                    int32_t* accepted, int32_t* clipped, float* logits) {
     return guarded([&] {
         verify_step_host(m, c, last, counts, drafts, budget, active, stop_on_eos, tau, accepted, clipped, logits);
+    });
+}
+
+int sd_verify_step_async(sd_model* m, sd_cache* c, const int32_t* last, const int32_t* counts, const int32_t* drafts,
+                         const int32_t* budget, const int32_t* active, int stop_on_eos, void* stream) {
+    return guarded([&] {
+        set_device(m->m.device);
+        verify_step_enqueue(m, c, last, counts, drafts, budget, active, stop_on_eos, nullptr,
+                            stream ? (cudaStream_t)stream : cache_stream(c));
+    });
+}
+
+int sd_verify_step_wait(sd_cache* c, int32_t* tau, int32_t* accepted, int32_t* clipped) {
+    return guarded([&] {
+        set_device(c->device);
+        verify_step_finish(c, tau, accepted, clipped);
     });
 }
 

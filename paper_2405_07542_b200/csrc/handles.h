@@ -21,6 +21,15 @@ struct sd_ledger {
     sdb::Ledger* l = &own;
 };
 
+// The host-side half of a verify step enqueued by verify_step_enqueue and
+// not yet consumed by verify_step_finish.
+struct VerifyInflight {
+    bool on = false;
+    int kmax = 0, base = 0, K1 = 0;
+    size_t o_tau = 0, o_clip = 0, o_acc = 0, o_flag = 0;
+    std::vector<int32_t> counts, active;
+};
+
 struct sd_cache {
     sdb::Cache c;
     sd_model* model = nullptr;  // null for a dims-only arena until a forward binds a model
@@ -28,6 +37,9 @@ struct sd_cache {
     int precision = 0;          // element type of the arena (sd_precision)
     sd_ledger lh;               // lh.l -> c.ledger
     bool kv_stored = false;     // a write_kv stored K/V bytes (a dims-only arena can no longer re-lay out)
+    cudaStream_t user_stream = nullptr;  // sd_cache_set_stream: all of this cache's work is ordered on it
+    cudaEvent_t done_ev = nullptr;       // end of the in-flight verify step
+    VerifyInflight inflight;
     sdb::Workspace ws;
     // verify-step device buffers
     int kcap = 0;                 // drafts per sample the buffers hold
@@ -83,7 +95,19 @@ sd_cache* create_cache(sd_model* m, int batch, int capacity, int layout);
 // model, which re-lays the (still unwritten) arena out for its heads.
 sd_cache* create_cache_dims(int layers, int batch, int capacity, int kv_dim, int layout, int device, int precision);
 void bind_cache(sd_cache* c, sd_model* m);
-inline cudaStream_t cache_stream(const sd_cache* c) { return c->model ? c->model->st : nullptr; }
+inline cudaStream_t cache_stream(const sd_cache* c) {
+    return c->user_stream ? c->user_stream : c->model ? c->model->st : nullptr;
+}
+// every call that reads or mutates a cache first checks that no asynchronous
+// verify step is still in flight on it (sd_verify_step_async / _wait)
+inline void check_idle(const sd_cache* c) {
+    if (c->inflight.on)
+        throw sdb::Error(sdb::CONTRACT, sdb::prefixed(sdb::CONTRACT, "a verify step is in flight on this cache"));
+}
+void verify_step_enqueue(sd_model* mh, sd_cache* h, const int32_t* last, const int32_t* counts,
+                         const int32_t* drafts, const int32_t* budget, const int32_t* active, int stop_on_eos,
+                         float* logits, cudaStream_t st);
+int verify_step_finish(sd_cache* h, int32_t* tau, int32_t* accepted, int32_t* clipped);
 
 // forward for the bf16 performance mode (fast_kernels.cu)
 void forward_fast(const Model& m, Cache& c, Workspace& ws, int T, bool want_logits, cudaStream_t st);

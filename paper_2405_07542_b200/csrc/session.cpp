@@ -667,6 +667,26 @@ int sd_session_draft_log(sd_session* s, int32_t* drafts, int max_steps) {
                            cudaMemcpyDeviceToHost));
     });
 }
+int sd_session_gather_outputs(sd_session* s, sd_comm* comm, int32_t* gen_tokens, int32_t* gen_counts) {
+    return sguard([&] {
+        const int B = s->B, mx = s->e.max_new_tokens;
+        // one int32 block per rank: [B][max_new] tokens then [B] counts
+        std::vector<int32_t> mine((size_t)B * mx + B);
+        CUDA_OK(cudaSetDevice(s->model->m.device));
+        if (sd_session_outputs(s, mine.data(), mine.data() + (size_t)B * mx, nullptr, nullptr, 0) != 0)
+            throw Error(INTERNAL, "session outputs unavailable");
+        int world = 0, rank = 0;
+        if (sd_comm_size(comm, &world, &rank) != 0) throw Error(INTERNAL, sd_comm_last_error());
+        std::vector<int32_t> all(mine.size() * (size_t)world);
+        if (sd_comm_allgather_i32(comm, mine.data(), (int64_t)mine.size(), all.data()) != 0)
+            throw Error(INTERNAL, sd_comm_last_error());
+        for (int r = 0; r < world; ++r) {
+            const int32_t* blk = all.data() + (size_t)r * mine.size();
+            std::memcpy(gen_tokens + (size_t)r * B * mx, blk, 4 * (size_t)B * mx);
+            std::memcpy(gen_counts + (size_t)r * B, blk + (size_t)B * mx, 4 * (size_t)B);
+        }
+    });
+}
 int sd_session_cache(sd_session* s, sd_cache** out) {
     return sguard([&] { *out = s->cache.get(); });
 }

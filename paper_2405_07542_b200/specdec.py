@@ -140,6 +140,16 @@ def lib() -> C.CDLL:
         "sd_session_outputs": ([vp, I32P, I32P, vp, vp, C.c_int], C.c_int),
         "sd_session_destroy": ([vp], None),
         "sd_session_draft_log": ([vp, I32P, C.c_int], C.c_int),
+        "sd_verify_step_async": ([vp, vp, I32P, I32P, I32P, I32P, I32P, C.c_int, vp], C.c_int),
+        "sd_verify_step_wait": ([vp, I32P, I32P, I32P], C.c_int),
+        "sd_cache_set_stream": ([vp, vp], C.c_int),
+        "sd_comm_last_error": ([], C.c_char_p),
+        "sd_nccl_unique_id": ([np.ctypeslib.ndpointer(np.uint8)], C.c_int),
+        "sd_comm_init": ([np.ctypeslib.ndpointer(np.uint8), C.c_int, C.c_int, C.c_int, pp], C.c_int),
+        "sd_comm_size": ([vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+        "sd_comm_destroy": ([vp], None),
+        "sd_comm_allgather_i32": ([vp, I32P, C.c_int64, I32P], C.c_int),
+        "sd_session_gather_outputs": ([vp, vp, I32P, I32P], C.c_int),
     }
     for name, (args, res) in sig.items():
         if LIB_PATH != _DEFAULT_LIB and not hasattr(L, name):
@@ -574,6 +584,31 @@ class CacheArena:
         return tau, acc.reshape(B, kmax + 1), clipped.astype(bool), (logits[:T] if want_logits else None)
 
 
+    def verify_step_async(self, last_tokens, draft_counts, drafts, budget_left, active, stop_on_eos: bool,
+                          stream: int | None = None) -> None:
+        """sd_verify_step_async: enqueue one verify step on `stream` (a raw
+        cudaStream_t, e.g. torch.cuda.Stream().cuda_stream; None = the cache's
+        stream) and return; collect it with verify_step_wait."""
+        counts = _i32(draft_counts)
+        self._inflight_kmax = int(max([c for c, a in zip(counts, active) if a] or [0]))
+        _check(lib().sd_verify_step_async(self.model._h, self._h, _i32(last_tokens), counts,
+                                          _i32(drafts) if len(drafts) else np.zeros(1, np.int32),
+                                          _i32(budget_left), _i32(active), int(stop_on_eos), stream))
+
+    def verify_step_wait(self):
+        """sd_verify_step_wait -> (tau, accepted [B][k_max+1], clipped)"""
+        B, kmax = self._batch, self._inflight_kmax
+        tau = np.zeros(B, dtype=np.int32)
+        clipped = np.zeros(B, dtype=np.int32)
+        acc = np.full(B * (kmax + 1), -1, dtype=np.int32)
+        _check(lib().sd_verify_step_wait(self._h, tau, acc, clipped))
+        return tau, acc.reshape(B, kmax + 1), clipped.astype(bool)
+
+    def set_stream(self, stream: int | None) -> None:
+        """sd_cache_set_stream: order this cache's device work on `stream`."""
+        _check(lib().sd_cache_set_stream(self._h, stream))
+
+
 class UnpadArena(CacheArena):
     """kv_cache.hpp:105-128"""
 
@@ -788,6 +823,44 @@ def _scheck(rc: int) -> None:
         raise _ERRORS.get(rc, SpecdecError)(lib().sd_session_last_error().decode())
 
 
+def _ccheck(rc: int) -> None:
+    if rc != 0:
+        raise _ERRORS.get(rc, SpecdecError)(lib().sd_comm_last_error().decode())
+
+
+def nccl_unique_id() -> bytes:
+    """sd_nccl_unique_id: the 128-byte NCCL bootstrap id rank 0 ships to the others."""
+    out = np.zeros(128, np.uint8)
+    _ccheck(lib().sd_nccl_unique_id(out))
+    return out.tobytes()
+
+
+class Comm:
+    """sd_comm: one rank's NCCL communicator for the end-of-run gather."""
+
+    def __init__(self, uid: bytes, world: int, rank: int, device: int = 0):
+        h = C.c_void_p()
+        _ccheck(lib().sd_comm_init(np.frombuffer(uid, np.uint8).copy(), world, rank, device, C.byref(h)))
+        self._h, self.world, self.rank = h.value, world, rank
+
+    def allgather_i32(self, local) -> np.ndarray:
+        x = np.ascontiguousarray(local, dtype=np.int32).ravel()
+        out = np.zeros(x.size * self.world, np.int32)
+        _ccheck(lib().sd_comm_allgather_i32(self._h, x, x.size, out))
+        return out.reshape(self.world, -1)
+
+    def close(self) -> None:
+        if self._h:
+            lib().sd_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Session:
     """A prefilled batch whose decode loop (engine.cpp:391-489) runs on the GPU."""
 
@@ -846,6 +919,14 @@ class Session:
         _scheck(lib().sd_session_outputs(self._h, gen, cnt, lk.ctypes.data, lt.ctypes.data, steps))
         tokens = [gen[s * mx: s * mx + min(cnt[s], mx)].tolist() for s in range(B)]
         return tokens, lk.reshape(steps, B), lt.reshape(steps, B)
+
+    def gather_outputs(self, comm: "Comm"):
+        """sd_session_gather_outputs: every rank's generated tokens, global sample order."""
+        B, mx = self.config.batch_size, self.config.max_new_tokens
+        gen = np.zeros(comm.world * B * mx, np.int32)
+        cnt = np.zeros(comm.world * B, np.int32)
+        _scheck(lib().sd_session_gather_outputs(self._h, comm._h, gen, cnt))
+        return [gen[i * mx: i * mx + min(cnt[i], mx)].tolist() for i in range(comm.world * B)]
 
     def draft_log(self) -> np.ndarray:
         """[steps][B][kcap] drafts each verify step checked (valid below log_k)."""

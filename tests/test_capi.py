@@ -120,3 +120,10 @@ def test_table1_scripted_trace_step_records(sd):
     assert [x["input_padding"] for x in st[1]["samples"]] == [3, 0]
     assert [x["kv_padding"] for x in st[0]["samples"]] == [0, 3]
     assert [x["kv_padding"] for x in st[1]["samples"]] == [4, 0]
+
+
+def test_nccl_bootstrap_id_without_gpu(sd):
+    """sd_nccl_unique_id (libnccl.so.2 opened on first use): the 128-byte
+    bootstrap id a C++ host ships from rank 0 to the other ranks."""
+    a, b = sd.nccl_unique_id(), sd.nccl_unique_id()
+    assert len(a) == 128 and any(a) and a != b

@@ -183,3 +183,80 @@ def test_global_sample_ids_reproduce_the_unsharded_run(sd, mode):
     k0, t0 = s.outputs()[1:]
     assert [(k0[:n, j] >= 0).sum() for j in range(3)] != [(lk[:steps, 3 + j] >= 0).sum() for j in range(3)] or \
         not all(((t0[:n, j][k0[:n, j] >= 0] & 0xFFFF).tolist() == per_sample[3 + j][1]) for j in range(3))
+
+
+def test_async_verify_step_on_caller_streams(sd):
+    """sd_verify_step_async / _wait (stream-ordered, async
+    until outputs are read): two caches' steps enqueued on two caller streams
+    before either is collected give exactly the synchronous results; calls
+    on a cache with a step in flight are refused (contract), and a bad step is
+    rejected before anything is enqueued."""
+    import torch
+
+    cfg = dict(num_layers=2, num_heads=4, head_dim=128, vocab_size=900, max_positions=512, init_seed=0xA5)
+    m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.BF16)
+    rng = np.random.default_rng(3)
+    B = 3
+    prompts = [[0] + rng.integers(3, 900, size=int(rng.integers(20, 60))).tolist() for _ in range(B)]
+
+    def prefilled():
+        c = sd.UnpadArena(m, B, 256)
+        _, am = m.forward(sd.concatenate_inputs(prompts), c,
+                          [sd.TokenSlot(s, i) for s in range(B) for i in range(len(prompts[s]))], want_logits=False)
+        for s in range(B):
+            c.commit_accepted(s, len(prompts[s]))
+        ends = np.cumsum([len(p) for p in prompts]) - 1
+        return c, [int(am[e]) for e in ends]
+
+    drafts = [rng.integers(3, 900, size=k).tolist() for k in (1, 4, 2)]
+    args = lambda last: (last, [len(d) for d in drafts], [t for d in drafts for t in d], [10] * B, [1] * B, False)
+    ref, last = prefilled()
+    tau_r, acc_r, clip_r, _ = ref.verify_step(*args(last))
+    c1, _ = prefilled()
+    c2, _ = prefilled()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    c1.verify_step_async(*args(last), stream=s1.cuda_stream)
+    c2.verify_step_async(*args(last), stream=s2.cuda_stream)
+    with pytest.raises(sd.ContractError):
+        c1.commit_accepted(0, 1)  # a step is in flight
+    for c in (c2, c1):
+        tau, acc, clip = c.verify_step_wait()
+        assert tau.tolist() == tau_r.tolist() and acc.tolist() == acc_r.tolist() and clip.tolist() == clip_r.tolist()
+        assert [c.committed_len(s) for s in range(B)] == [ref.committed_len(s) for s in range(B)]
+        assert [st.tau_list for st in c.ledger().steps()] == [tau_r.tolist()]
+    with pytest.raises(sd.ContractError):
+        c1.verify_step_wait()  # nothing in flight any more
+    bad = args(last)
+    with pytest.raises(sd.ContractError):  # out-of-vocabulary draft: refused before enqueue
+        c1.verify_step_async(bad[0], bad[1], [10 ** 6] * len(bad[2]), *bad[3:], stream=s1.cuda_stream)
+    c1.set_stream(s1.cuda_stream)  # the synchronous step on a caller stream
+    tau, acc, _, _ = c1.verify_step([int(a[t - 1]) for a, t in zip(acc_r, tau_r)], [0] * B, [], [9] * B, [1] * B,
+                                    False)
+    assert (tau == 1).all()
+    for c in (ref, c1, c2):
+        c.close()
+    m.close()
+
+
+def test_nccl_gather_of_session_outputs(sd):
+    """The run's only collective through the library (sd_comm_*, NCCL): a
+    world-1 communicator on this GPU all-gathers int32 blocks in rank order
+    and sd_session_gather_outputs returns the session's own outputs.  (The
+    box has one GPU; NCCL refuses two ranks on one device, so N > 1 is
+    covered by the host-side sharding tests and the bench's torchrun path.)"""
+    cfg = dict(num_layers=2, num_heads=4, head_dim=128, vocab_size=700, max_positions=512, init_seed=0xC0)
+    m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.BF16)
+    rng = np.random.default_rng(2)
+    prompts = [[0] + rng.integers(3, 700, size=30).tolist() for _ in range(3)]
+    e = sd.EngineConfig(mode="ems", predictor="retrieval", k=4, copy_len=4, batch_size=3, max_new_tokens=12,
+                        stop_on_eos=False)
+    s = sd.Session(m, e, 128)
+    s.prefill(prompts)
+    s.run()
+    comm = sd.Comm(sd.nccl_unique_id(), 1, 0, 0)
+    x = np.arange(37, dtype=np.int32)
+    assert (comm.allgather_i32(x) == x[None, :]).all()
+    assert s.gather_outputs(comm) == s.outputs()[0]
+    comm.close()
+    s.close()
+    m.close()
