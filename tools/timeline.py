@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--cap", type=int, default=6_000_000)
     ap.add_argument("--mode", default="ems")
     ap.add_argument("--draft", action="store_true", help="C4: OPT-125m-shaped draft model, k=4")
+    ap.add_argument("--config", default="c3", choices=["c3", "c2"],
+                    help="c2: OPT-125m shape, B=8, 512-id prompts, synthetic p=0.7 drafts (bench --config c2)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "timeline.txt"))
     a = ap.parse_args()
     import bench
@@ -41,15 +43,25 @@ def main():
     L = sd.lib()
     L.sd_debug_trace_begin.argtypes = [C.c_int]
     L.sd_debug_trace_end.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int)]
-    cfg = bench.C3
+    cfg = bench.C2 if a.config == "c2" else bench.C3
+    if a.config == "c2" and "--batch" not in sys.argv:
+        a.batch = 8
     m = sd.Model.init(sd.ModelConfig(**cfg), device=0, precision=sd.BF16)
-    prompts = bench.prompts_for(range(a.batch), cfg["vocab_size"], 600, 900)
+    lo_hi = (512, 512) if a.config == "c2" else (600, 900)
+    prompts = bench.prompts_for(range(a.batch), cfg["vocab_size"], *lo_hi)
     cap = max(len(p) for p in prompts) + 128 + 9 if a.mode == "ems" else cfg["max_positions"]
     if a.draft:
         d = sd.Model.init(sd.ModelConfig(**dict(bench.C2, init_seed=cfg["init_seed"] + 1)), device=0, precision=sd.BF16)
         e = sd.EngineConfig(mode=a.mode, predictor="draft", k=4, batch_size=a.batch, max_new_tokens=128,
                             stop_on_eos=False)
         s = sd.Session(m, e, cap, draft=d)
+    elif a.config == "c2":
+        e = sd.EngineConfig(mode=a.mode, predictor="synthetic", k=7, batch_size=a.batch, max_new_tokens=128,
+                            stop_on_eos=False, seed=1, synthetic_accuracy=0.7)
+        s = sd.Session(m, e, cap)
+        g = sd.decode(sd.EngineConfig(mode="greedy", batch_size=a.batch, max_new_tokens=128 + 9, stop_on_eos=False),
+                      m, prompts)
+        s.set_trajectory(np.array(g.generated_tokens, dtype=np.int32))
     else:
         e = sd.EngineConfig(mode=a.mode, predictor="retrieval", k=7, match_len=2, copy_len=7, batch_size=a.batch,
                             max_new_tokens=128, stop_on_eos=False, seed=1)
