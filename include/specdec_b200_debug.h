@@ -29,6 +29,12 @@ int sd_debug_attention(const uint16_t* q, const uint16_t* kv, int B, int heads, 
                        const int32_t* kv_len, const int32_t* write_slot, const uint8_t* pad, uint16_t* ctx,
                        float* usec);
 int sd_debug_trace_end(void* out, int cap, int* n);
+/* 1 if the bf16 model runs its layer GEMMs as cluster split-K launches with
+ * fused reductions / LayerNorms (small models, gemm_cluster.cu), 0 if through
+ * the stream-K GEMM + reduction kernels, negative on error.  SD_COMPACT=0 in
+ * the environment when the model is created forces the stream-K path. */
+struct sd_model;
+int sd_debug_model_compact(const struct sd_model* m);
 #ifdef __cplusplus
 }
 #endif

@@ -15,7 +15,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "--expt-relaxed-constexpr"]
-SOURCES = ["model.cu", "check_kernels.cu", "step_kernels.cu", "fast_kernels.cu", "gemm_sm100.cu", "capi.cpp",
+SOURCES = ["model.cu", "check_kernels.cu", "step_kernels.cu", "fast_kernels.cu", "gemm_sm100.cu", "gemm_cluster.cu", "capi.cpp",
            "engine.cpp", "session.cpp", "comm.cpp"]
 
 

@@ -830,6 +830,11 @@ int sd_model_checksum(const sd_model* m, uint64_t* out) {
     });
 }
 
+int sd_debug_model_compact(const sd_model* m) {
+    if (!m) return -SD_CONTRACT;
+    return m->m.fast && fast_model_compact(m->m) ? 1 : 0;
+}
+
 int sd_model_get_config(const sd_model* m, sd_model_config* out) {
     return guarded([&] {
         const Config& c = m->m.cfg;

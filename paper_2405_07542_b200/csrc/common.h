@@ -87,6 +87,7 @@ struct FastWorkspace;
 void free_fast_model(FastModelState* f);
 void free_fast_workspace(FastWorkspace* f);
 void build_fast_model(Model& m);
+bool fast_model_compact(const Model& m);  // layer GEMMs as cluster split-K launches
 
 // WriteLedger (kv_cache.hpp:13-57, kv_cache.cpp:11-76): KV slot writes per
 // sample split into useful / padding, and the per-step grouping the engine

@@ -31,12 +31,17 @@ constexpr int kQT = 8;             // queries per attention item (the S^T MMA's 
 struct FastModelState {
     std::vector<GemmMaps> qkv, o, fc, proj;  // per layer (A map only used)
     GemmMaps lm;
+    // small models: every layer GEMM as one cluster split-K launch
+    // (gemm_cluster.cu) over 128-row weight boxes
+    bool compact = false;
+    std::vector<CUtensorMap> cqkv, co, cfc, cproj;
 };
 
 struct FastWorkspace {
     int cap_tokens = 0, B = 0, cap = 0;
     __nv_bfloat16 *xb = nullptr, *q = nullptr, *ctx = nullptr, *act = nullptr;
     float* part = nullptr;     // stream-K partial sums (largest GEMM of the model)
+    float2* stats = nullptr;   // compact models: per-(token, 128-row tile) residual (sum, M2)
     ArgmaxScratch am;          // LM-head (max, id) partials per token + arrival counters
     GemmMaps map_xb, map_ctx, map_act;
     CUtensorMap kv_map;        // TMA view of the KV arena [L*2*B*heads*cap][hd], box {64, 128}
@@ -72,8 +77,30 @@ void build_fast_model(Model& m) {
         f->proj.push_back(g);
     }
     f->lm.A = make_tmap_2d(m.lm16, m.vocab_pad, h, 256);
+    // Small models (the C2 target, the C4 draft) run each layer GEMM as one
+    // cluster split-K launch with the reductions and LayerNorms fused (five
+    // launches per layer instead of eleven).  The choice depends on the model
+    // shape only, so every forward of a model takes the same path.
+    const char* env = getenv("SD_COMPACT");  // "0": stream-K path for every model (A/B measurement)
+    bool compact = h <= 1024 && h % 128 == 0 && !(env && env[0] == '0');
+    const int sms = device_sm_count();
+    for (auto mk : {std::make_pair(3 * h, h), std::make_pair(h, h), std::make_pair(mm, h), std::make_pair(h, mm)}) {
+        if (!compact) break;
+        ClPlan p = gemm_cl_plan((int)mk.first, (int)mk.second, 256, sms);
+        compact = p.ok && gemm_cl_schedulable(p);
+    }
+    f->compact = compact;
+    if (compact)
+        for (const FastLayer& L : m.layers) {
+            f->cqkv.push_back(make_tmap_2d(L.wqkv, 3 * h, h, 128));
+            f->co.push_back(make_tmap_2d(L.wo, h, h, 128));
+            f->cfc.push_back(make_tmap_2d(L.wfc, mm, h, 128));
+            f->cproj.push_back(make_tmap_2d(L.wproj, h, mm, 128));
+        }
     m.fast = f;
 }
+
+bool fast_model_compact(const Model& m) { return m.fast && m.fast->compact; }
 
 namespace {
 
@@ -117,7 +144,7 @@ __global__ void __launch_bounds__(kRowThreads) k_embed_ln(const __nv_bfloat16* _
                                                           const Plan* __restrict__ plans, int h,
                                                           float* __restrict__ resid, const float* __restrict__ g,
                                                           const float* __restrict__ b, __nv_bfloat16* __restrict__ y,
-                                                          const int* __restrict__ dT) {
+                                                          const int* __restrict__ dT, float2* __restrict__ stats) {
     CtaTrace trace__(TK_EMBED_LN);
     pdl_trigger();
     pdl_wait();
@@ -129,6 +156,20 @@ __global__ void __launch_bounds__(kRowThreads) k_embed_ln(const __nv_bfloat16* _
     float* r = resid + (size_t)t * h;
     for (int i = threadIdx.x; i < h; i += kRowThreads) r[i] = __bfloat162float(e[i]) + __bfloat162float(p[i]);
     __syncthreads();
+    if (stats) {  // compact models: per-128-row-tile (sum, M2), the cluster GEMM's LN_IN input
+        const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+        for (int c = w; c < h / 128; c += kRowThreads / 32) {
+            const float4 x = ((const float4*)(r + c * 128))[l];
+            float sm = x.x + x.y + x.z + x.w;
+            for (int o = 16; o > 0; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+            const float mu = sm * (1.0f / 128.0f);
+            float q = (x.x - mu) * (x.x - mu) + (x.y - mu) * (x.y - mu) + (x.z - mu) * (x.z - mu) +
+                      (x.w - mu) * (x.w - mu);
+            for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+            if (l == 0) stats[(size_t)t * (h / 128) + c] = make_float2(sm, q);
+        }
+        return;  // the QKV GEMM applies LN1 itself
+    }
     ln_row(r, g, b, h, y + (size_t)t * h, scratch);
 }
 
@@ -583,6 +624,7 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
                     std::make_pair(m.vocab_pad, (int)h)})
         part = std::max(part, gemm_part_floats(mk.first, mk.second, device_sm_count()));
     f->part = walloc<float>(f, part);
+    f->stats = walloc<float2>(f, T * (h / 128 + 1));
     f->am.val = walloc<float>(f, (size_t)T * kArgmaxGroups);
     f->am.idx = walloc<int>(f, (size_t)T * kArgmaxGroups);
     f->am.cnt = walloc<int>(f, T);
@@ -718,7 +760,8 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     CUDA_OK(cudaMemsetAsync(f->attn_work, 0, sizeof(int) * (size_t)cfg.num_layers, st));
     PROF(PK_ROW, launch_k(k_embed_ln, dim3(n), dim3(kRowThreads), 0, st, (const __nv_bfloat16*)m.tok16,
                           (const __nv_bfloat16*)m.pos16, tokens, dplans, h, resid, (const float*)m.layers[0].ln1_g,
-                          (const float*)m.layers[0].ln1_b, f->xb, (const int*)db.dT));
+                          (const float*)m.layers[0].ln1_b, f->xb, (const int*)db.dT,
+                          m.fast->compact ? f->stats : nullptr));
     launches++;
     AttnArgs at{};
     at.q = f->q;
@@ -736,7 +779,86 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     const int qtiles = std::max(1, (db.max_q_upper + kQT - 1) / kQT);
     const int sms = device_sm_count();
 
-    for (int l = 0; l < cfg.num_layers; ++l) {
+    const FastModelState* fmc = m.fast;
+    ClArgs cb{};
+    cb.T = n;
+    cb.dT = db.dT;
+    cb.x_resid = resid;
+    cb.stats_in = f->stats;
+    cb.hidden = h;
+    cb.n_stat = h / 128;
+    cb.h = h;
+    cb.hd = hd;
+    cb.heads = heads;
+    cb.B = c.B;
+    cb.cap = c.cap;
+    cb.plans = dplans;
+    cb.kv = (__nv_bfloat16*)c.kv;
+    for (int l = 0; fmc->compact && l < cfg.num_layers; ++l) {
+        const FastLayer& L = m.layers[l];
+        // QKV (LN1 applied while building the token operand) + scatter
+        ClArgs g = cb;
+        g.M = 3 * h;
+        g.K = h;
+        g.bias = L.bqkv;
+        g.ln_g = L.ln1_g;
+        g.ln_b = L.ln1_b;
+        g.out_bf16 = f->q;
+        g.layer = l;
+        GemmMaps mp = f->map_xb;
+        mp.A = fmc->cqkv[l];
+        PROF(PK_QKV, gemm_cl_launch(EPI_QKV, g, mp, n, st));
+        at.layer = l;
+        at.work = f->attn_work + l;
+        at.pre_ok = 0;
+        PROF(PK_ATTN, launch_attention(at, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, hd, qtiles, db.max_kv_upper,
+                                       st));
+        // O projection + residual -> residual tile statistics
+        g = cb;
+        g.M = h;
+        g.K = h;
+        g.bias = L.bo;
+        g.resid = resid;
+        g.stats_out = f->stats;
+        mp = f->map_ctx;
+        mp.A = fmc->co[l];
+        PROF(PK_O, gemm_cl_launch(EPI_RESID_LN, g, mp, n, st));
+        // FC (LN2 applied to the operand) + GELU
+        g = cb;
+        g.M = mm;
+        g.K = h;
+        g.bias = L.bfc;
+        g.ln_g = L.ln2_g;
+        g.ln_b = L.ln2_b;
+        g.out_bf16 = f->act;
+        g.ld_out = mm;
+        mp = f->map_xb;
+        mp.A = fmc->cfc[l];
+        PROF(PK_FC, gemm_cl_launch(EPI_GELU, g, mp, n, st));
+        // PROJ + residual -> statistics for the next layer's LN1
+        g = cb;
+        g.M = h;
+        g.K = mm;
+        g.bias = L.bproj;
+        g.resid = resid;
+        g.stats_out = f->stats;
+        mp = f->map_act;
+        mp.A = fmc->cproj[l];
+        PROF(PK_PROJ, gemm_cl_launch(EPI_RESID_LN, g, mp, n, st));
+        launches += 5;
+    }
+    if (fmc->compact) {  // final LayerNorm -> xb for the LM head
+        GemmArgs g = base;
+        g.M = h;
+        g.out_f32 = resid;
+        g.ld_out = h;
+        g.ln_g = m.lnf_g;
+        g.ln_b = m.lnf_b;
+        g.ln_out = f->xb;
+        PROF(PK_ROW, ln_rows_launch(g, n, st));
+        launches++;
+    }
+    for (int l = 0; !fmc->compact && l < cfg.num_layers; ++l) {
         const FastLayer& L = m.layers[l];
         const FastModelState* fm = m.fast;
         // QKV + scatter (Q -> q16, K/V -> the arena at each token's write slot)

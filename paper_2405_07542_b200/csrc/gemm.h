@@ -68,5 +68,42 @@ size_t gemm_part_floats(int M, int K, int sms);
 void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, cudaStream_t st,
                  cudaEvent_t after_stream = nullptr);
 void gemm_prepare();  // one-time kernel attributes (before any graph capture)
+// LayerNorm rows of the residual stream (a.out_f32, width a.M) -> a.ln_out
+void ln_rows_launch(const GemmArgs& a, int T_upper, cudaStream_t st);
+
+// ---- cluster split-K GEMM for small models (gemm_cluster.cu)
+struct ClArgs {
+    int M, K;                  // W is [M][K] bf16, M % 128 == 0, K % 64 == 0
+    int T;                     // token count when dT == nullptr
+    const int* dT;             // device token count
+    int CS, nkb_max, box;      // set by gemm_cl_launch
+    const float* bias;         // [M]
+    // LN_IN (QKV / FC): the token operand is LayerNorm(x_resid) built in shared memory
+    const float* x_resid;      // [T][hidden] fp32 residual stream
+    const float2* stats_in;    // [T][n_stat] per-(token, 128-row tile) (sum, M2) of x_resid
+    const float *ln_g, *ln_b;
+    int hidden, n_stat;        // n_stat = hidden / 128
+    // EPI_RESID_LN: resid[t][m] += y + b, then stats_out[t][tile] = (sum, M2) of the new rows
+    float* resid;
+    float2* stats_out;
+    // EPI_GELU activations / EPI_QKV queries
+    __nv_bfloat16* out_bf16;
+    int ld_out;
+    // EPI_QKV scatter into the KV arena [L][2][B][heads][cap][hd]
+    __nv_bfloat16* kv;
+    const Plan* plans;
+    int h, hd, heads, B, cap, layer;
+};
+struct ClPlan {
+    bool ok;
+    int CS, nkb_max, tiles;
+    size_t smem;
+};
+// cluster size / k-blocks per CTA for a shape: a function of (M, K, SMs) only
+ClPlan gemm_cl_plan(int M, int K, int box, int sms);
+bool gemm_cl_schedulable(const ClPlan& p);
+void gemm_cl_prepare();
+// epi: EPI_QKV (LN_IN), EPI_GELU (LN_IN) or EPI_RESID_LN (TMA token operand, stats out)
+void gemm_cl_launch(int epi, const ClArgs& a, const GemmMaps& maps, int T_upper, cudaStream_t st);
 
 }  // namespace sdb

@@ -1,0 +1,375 @@
+// Cluster split-K tcgen05 GEMM for small models (hidden <= 1024, e.g. the
+// OPT-125m-shaped C2 target and the C4 draft).
+//
+//   Y[t][m] = sum_k W[m][k] * X[t][k]       (W = weights [M][K], X = tokens [T][K])
+//
+// At these sizes a verify step is a chain of latency-bound launches, not a
+// bandwidth problem (C2 streams ~0.4 GB per step): the stream-K GEMM of
+// gemm_sm100.cu spends more on its separate split-K reduction and LayerNorm
+// launches than on the weights.  Here one launch does the whole GEMM stage:
+//
+//   * a 128-row weight tile is split over the CS CTAs of one thread-block
+//     cluster along K (CS <= 16, each CTA holds its whole k-range in shared
+//     memory: no ring), every CTA issuing tcgen05.mma into its own TMEM
+//     accumulator (M = 128 rows, N = the packed tokens);
+//   * the CS fp32 partial tiles are summed inside the cluster through
+//     distributed shared memory in fixed rank order (deterministic, no global
+//     partials), CTA r owning tokens t = r (mod CS), one warp per token;
+//   * the epilogue is fused: bias + Q/K/V scatter into the unpadded KV arena,
+//     bias + GELU, or bias + residual update plus the per-(token, 128-row tile)
+//     LayerNorm statistics (sum, M2) of the new residual rows;
+//   * the NEXT GEMM applies that LayerNorm while it builds its token operand
+//     (LN_IN): per-token mean / rstd Chan-combined from the tile statistics in
+//     fixed order, (x - mean) * rstd * gamma + beta packed to bf16 straight
+//     into the 128B-swizzled K-major layout the MMA reads.
+//
+// A transformer layer is therefore QKV -> attention -> O -> FC -> PROJ: five
+// launches instead of eleven.  The split (CS, k-range per CTA) depends only on
+// the GEMM shape and the SM count, never on the token count, so a token's
+// result does not depend on the batch it is verified in.
+//
+// Warp roles (256 threads): thread 0 TMA (weights before griddepcontrol.wait,
+// tokens after), warp 1 TMEM allocation + lane 0 MMA issue, warps 4-7 TMEM ->
+// shared-memory partial tile, all 8 warps the LN_IN operand build and the
+// in-cluster reduction + epilogue.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "gemm.h"
+#include "pdl.cuh"
+#include "sm100_ptx.cuh"
+#include "trace.cuh"
+
+SD_TRACE_TU(gemmcl)
+
+namespace sdb {
+namespace {
+
+constexpr int kClThreads = 256;
+constexpr int kClABytes = 128 * 64 * 2;  // one 128-row x 64-k bf16 weight block (16 KB)
+constexpr int kClMaxKb = 4;              // k-blocks per CTA (whole k-range resident)
+constexpr int kClMaxCS = 16;
+constexpr int kClSmemMax = 220 * 1024;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(ptx::smem_u32(local)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void tmem_alloc_n(uint32_t* dst, uint32_t cols) {  // whole warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_u32(dst)),
+                 "r"(cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc_n(uint32_t taddr, uint32_t cols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols));
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float gelu_tanh(float x) {  // model.cpp:71-74, hardware tanh
+    const float c = 0.7978845608028654f;
+    float u = c * (x + 0.044715f * x * x * x);
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+    return 0.5f * x * (1.0f + t);
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int EPI, bool LN_IN>
+__global__ void __launch_bounds__(kClThreads, 1)
+    k_gemm_cl(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB32,
+              const __grid_constant__ CUtensorMap tmB64, const __grid_constant__ CUtensorMap tmB128,
+              const __grid_constant__ CUtensorMap tmB256, const ClArgs a) {
+    CtaTrace trace__(TK_GEMM_CL);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ uint64_t s_full_a[kClMaxKb], s_full_b, s_tmem_full;
+    __shared__ uint32_t s_tmem;
+    __shared__ float s_mu[256], s_rs[256];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int CS = a.CS;
+    const int rank = (int)cluster_rank();
+    const int tile = blockIdx.x / CS;
+    const int KB = a.K / 64;
+    const int kb0 = rank * KB / CS, nkb = (rank + 1) * KB / CS - kb0;
+    const int bstride = a.box * 128;              // bytes per token k-block (host bound)
+    uint8_t* A = smem;                            // [nkb_max][128 rows][128 B]
+    uint8_t* Bt = smem + a.nkb_max * kClABytes;   // [nkb_max][box rows][128 B]
+    float* red = (float*)smem;                    // [BN tokens][128 rows] fp32, after the MMAs
+
+    if (threadIdx.x == 0) {
+        ptx::prefetch_tmap(&tmA);
+        for (int i = 0; i < nkb; ++i) ptx::mbar_init(&s_full_a[i], 1);
+        ptx::mbar_init(&s_full_b, 1);
+        ptx::mbar_init(&s_tmem_full, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_n(&s_tmem, (uint32_t)a.box);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = s_tmem;
+    pdl_trigger();
+    if (threadIdx.x == 0) {  // weights do not depend on the predecessor: load them before the wait
+        const uint64_t pol_w = ptx::policy_evict_first();
+        for (int i = 0; i < nkb; ++i) {
+            ptx::mbar_arrive_expect_tx(&s_full_a[i], kClABytes);
+            ptx::tma_load_2d(A + i * kClABytes, &tmA, &s_full_a[i], (kb0 + i) * 64, tile * 128, pol_w);
+        }
+    }
+    pdl_wait();
+    const int T = a.dT ? *a.dT : a.T;
+    const int BN = T <= 16 ? 16 : ((T + 15) / 16) * 16;
+    const bool idle = T <= 0 || BN > a.box;
+    if (!idle) {
+        if constexpr (LN_IN) {
+            // per-token LayerNorm statistics: Chan combination of the producer's
+            // per-tile (sum, M2) in tile order (deterministic)
+            for (int t = threadIdx.x; t < BN; t += kClThreads) {
+                float mu = 0.0f, rs = 0.0f;
+                if (t < T) {
+                    const float2* p = a.stats_in + (size_t)t * a.n_stat;
+                    float s = 0.0f;
+                    for (int i = 0; i < a.n_stat; ++i) s += p[i].x;
+                    mu = s / a.hidden;
+                    float m2 = 0.0f;
+                    for (int i = 0; i < a.n_stat; ++i) {
+                        const float d = p[i].x * (1.0f / 128.0f) - mu;
+                        m2 += p[i].y + 128.0f * d * d;
+                    }
+                    rs = rsqrtf(m2 / a.hidden + 1e-5f);
+                }
+                s_mu[t] = mu;
+                s_rs[t] = rs;
+            }
+            __syncthreads();
+            // LN(x) -> bf16, written in the 128B-swizzled K-major layout TMA
+            // would produce (16-byte chunk c of row t at chunk c ^ (t & 7))
+            const int per = BN * 8;
+            for (int idx = threadIdx.x; idx < nkb * per; idx += kClThreads) {
+                const int i = idx / per, r = idx - i * per, t = r >> 3, c = r & 7;
+                uint4 o = make_uint4(0u, 0u, 0u, 0u);
+                if (t < T) {
+                    const int k = (kb0 + i) * 64 + c * 8;
+                    const float4* x = (const float4*)(a.x_resid + (size_t)t * a.hidden + k);
+                    const float4* g = (const float4*)(a.ln_g + k);
+                    const float4* b = (const float4*)(a.ln_b + k);
+                    const float4 x0 = x[0], x1 = x[1], g0 = g[0], g1 = g[1], b0 = b[0], b1 = b[1];
+                    const float mu = s_mu[t], rs = s_rs[t];
+                    o.x = pack_bf16((x0.x - mu) * rs * g0.x + b0.x, (x0.y - mu) * rs * g0.y + b0.y);
+                    o.y = pack_bf16((x0.z - mu) * rs * g0.z + b0.z, (x0.w - mu) * rs * g0.w + b0.w);
+                    o.z = pack_bf16((x1.x - mu) * rs * g1.x + b1.x, (x1.y - mu) * rs * g1.y + b1.y);
+                    o.w = pack_bf16((x1.z - mu) * rs * g1.z + b1.z, (x1.w - mu) * rs * g1.w + b1.w);
+                }
+                *(uint4*)(Bt + i * bstride + t * 128 + ((c ^ (t & 7)) << 4)) = o;
+            }
+            ptx::fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
+            __syncthreads();
+        } else if (threadIdx.x == 0) {
+            const int box_d = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+            const CUtensorMap* tmB = box_d == 32 ? &tmB32 : box_d == 64 ? &tmB64 : box_d == 128 ? &tmB128 : &tmB256;
+            const uint64_t pol_x = ptx::policy_evict_last();
+            ptx::mbar_arrive_expect_tx(&s_full_b, (uint32_t)(nkb * box_d * 128));
+            for (int i = 0; i < nkb; ++i)
+                ptx::tma_load_2d(Bt + i * bstride, tmB, &s_full_b, (kb0 + i) * 64, 0, pol_x);
+        }
+        if (threadIdx.x == 32) {  // ---------------- MMA issuer
+            const uint32_t idesc = ptx::umma_idesc_bf16(128, BN);
+            if (!LN_IN) ptx::mbar_wait(&s_full_b, 0);
+            for (int i = 0; i < nkb; ++i) {
+                ptx::mbar_wait(&s_full_a[i], 0);
+                ptx::tc_fence_after();
+                const uint32_t sa = ptx::smem_u32(A + i * kClABytes), sb = ptx::smem_u32(Bt + i * bstride);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    ptx::umma_bf16(tmem, ptx::umma_desc_kmajor_sw128(sa + k * 32), ptx::umma_desc_kmajor_sw128(sb + k * 32),
+                                   idesc, (i > 0 || k > 0) ? 1u : 0u);
+            }
+            ptx::umma_commit(&s_tmem_full);
+        }
+        if (warp >= 4) {  // ---------------- TMEM -> shared partial tile [token][row]
+            ptx::mbar_wait(&s_tmem_full, 0);
+            ptx::tc_fence_after();
+            const int row = (warp - 4) * 32 + lane;
+            const uint32_t trow = tmem + ((uint32_t)((warp - 4) * 32) << 16);
+            for (int j0 = 0; j0 < BN; j0 += 16) {
+                float v[16];
+                ptx::tmem_ld16(trow + j0, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) red[(j0 + i) * 128 + row] = v[i];
+            }
+        }
+    } else if (threadIdx.x == 0) {
+        for (int i = 0; i < nkb; ++i) ptx::mbar_wait(&s_full_a[i], 0);  // no TMA in flight at exit
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();  // every CTA's partial tile is in its shared memory
+    if (!idle) {
+        const int m0 = tile * 128 + lane * 4;
+        const float4 bias = a.bias ? *(const float4*)(a.bias + m0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int t = rank + CS * warp; t < T; t += CS * (kClThreads / 32)) {
+            float4 v[kClMaxCS];  // every peer's load in flight before the first add
+#pragma unroll
+            for (int p = 0; p < kClMaxCS; ++p)
+                if (p < CS) v[p] = ld_dsmem_f4(dsmem_addr(red + t * 128 + lane * 4, p));
+            float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int p = 0; p < kClMaxCS; ++p)  // fixed rank order: deterministic
+                if (p < CS) {
+                    s.x += v[p].x;
+                    s.y += v[p].y;
+                    s.z += v[p].z;
+                    s.w += v[p].w;
+                }
+            if constexpr (EPI == EPI_RESID_LN) {
+                float4* rp = (float4*)(a.resid + (size_t)t * a.hidden + m0);
+                const float4 o = *rp;
+                const float4 x = make_float4(o.x + (s.x + bias.x), o.y + (s.y + bias.y), o.z + (s.z + bias.z),
+                                             o.w + (s.w + bias.w));
+                *rp = x;
+                const float sum = warp_sum(x.x + x.y + x.z + x.w);
+                const float mu = sum * (1.0f / 128.0f);
+                const float dx = x.x - mu, dy = x.y - mu, dz = x.z - mu, dw = x.w - mu;
+                const float m2 = warp_sum(dx * dx + dy * dy + dz * dz + dw * dw);
+                if (lane == 0) a.stats_out[(size_t)t * a.n_stat + tile] = make_float2(sum, m2);
+            } else if constexpr (EPI == EPI_GELU) {
+                uint2 o;
+                o.x = pack_bf16(gelu_tanh(s.x + bias.x), gelu_tanh(s.y + bias.y));
+                o.y = pack_bf16(gelu_tanh(s.z + bias.z), gelu_tanh(s.w + bias.w));
+                *(uint2*)(a.out_bf16 + (size_t)t * a.ld_out + m0) = o;
+            } else {  // EPI_QKV
+                uint2 o;
+                o.x = pack_bf16(s.x + bias.x, s.y + bias.y);
+                o.y = pack_bf16(s.z + bias.z, s.w + bias.w);
+                const int which = m0 / a.h, hm = m0 - which * a.h;
+                if (which == 0) {
+                    *(uint2*)(a.out_bf16 + (size_t)t * a.h + hm) = o;
+                } else {
+                    const Plan pl = a.plans[t];
+                    if (pl.store) {
+                        const int head = hm / a.hd, d = hm - head * a.hd;
+                        const size_t off = ((((size_t)a.layer * 2 + (which - 1)) * a.B + pl.sample) * a.heads + head) *
+                                               (size_t)a.cap * a.hd +
+                                           (size_t)pl.write_slot * a.hd + d;
+                        *(uint2*)(a.kv + off) = o;
+                    }
+                }
+            }
+        }
+    }
+    cluster_sync_all();  // peers have finished reading this CTA's partial tile
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        tmem_dealloc_n(tmem, (uint32_t)a.box);
+    }
+}
+
+template <int EPI, bool LN_IN>
+void prepare_one() {
+    auto k = k_gemm_cl<EPI, LN_IN>;
+    CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kClSmemMax));
+    CUDA_OK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
+
+}  // namespace
+
+ClPlan gemm_cl_plan(int M, int K, int box, int sms) {
+    ClPlan p{};
+    if (M % 128 || K % 64 || box < 32 || box > 256) return p;
+    const int tiles = M / 128, KB = K / 64;
+    int cs = std::max((KB + kClMaxKb - 1) / kClMaxKb, std::min({8, sms / std::max(1, tiles), KB}));
+    if (cs < 1 || cs > kClMaxCS || cs > KB || (long long)tiles * cs > sms) return p;
+    const int nkb = (KB + cs - 1) / cs;
+    const size_t ab = (size_t)nkb * kClABytes + (size_t)nkb * box * 128;
+    const size_t smem = std::max(ab, (size_t)128 * box * 4) + 1024;
+    if (smem > (size_t)kClSmemMax) return p;
+    p.ok = true;
+    p.CS = cs;
+    p.nkb_max = nkb;
+    p.tiles = tiles;
+    p.smem = smem;
+    return p;
+}
+
+void gemm_cl_prepare() {
+    if (!first_use_on_device(3)) return;
+    prepare_one<EPI_QKV, true>();
+    prepare_one<EPI_GELU, true>();
+    prepare_one<EPI_RESID_LN, false>();
+}
+
+bool gemm_cl_schedulable(const ClPlan& p) {
+    gemm_cl_prepare();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.tiles * p.CS);
+    cfg.blockDim = dim3(kClThreads);
+    cfg.dynamicSmemBytes = p.smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_gemm_cl<EPI_RESID_LN, false>, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return n >= 1;
+}
+
+void gemm_cl_launch(int epi, const ClArgs& a0, const GemmMaps& maps, int T_upper, cudaStream_t st) {
+    gemm_cl_prepare();
+    SD_CHECK(T_upper >= 1 && T_upper <= 256, INTERNAL, "cluster GEMM token tile is at most 256");
+    ClArgs a = a0;
+    a.box = T_upper <= 32 ? 32 : T_upper <= 64 ? 64 : T_upper <= 128 ? 128 : 256;
+    const ClPlan p = gemm_cl_plan(a.M, a.K, a.box, device_sm_count());
+    SD_CHECK(p.ok, INTERNAL, "cluster GEMM plan infeasible for this shape");
+    a.CS = p.CS;
+    a.nkb_max = p.nkb_max;
+    const dim3 grid(p.tiles * p.CS);
+    switch (epi) {
+        case EPI_QKV:
+            launch_kc(k_gemm_cl<EPI_QKV, true>, grid, dim3(kClThreads), p.smem, st, p.CS, maps.A, maps.B[0],
+                      maps.B[1], maps.B[2], maps.B[3], a);
+            break;
+        case EPI_GELU:
+            launch_kc(k_gemm_cl<EPI_GELU, true>, grid, dim3(kClThreads), p.smem, st, p.CS, maps.A, maps.B[0],
+                      maps.B[1], maps.B[2], maps.B[3], a);
+            break;
+        case EPI_RESID_LN:
+            launch_kc(k_gemm_cl<EPI_RESID_LN, false>, grid, dim3(kClThreads), p.smem, st, p.CS, maps.A, maps.B[0],
+                      maps.B[1], maps.B[2], maps.B[3], a);
+            break;
+        default:
+            throw Error(INTERNAL, "cluster GEMM epilogue not supported");
+    }
+    CUDA_OK(cudaGetLastError());
+}
+
+}  // namespace sdb

@@ -614,6 +614,11 @@ void gemm_launch(int epi, const GemmArgs& a, const GemmMaps& maps, int T_upper, 
     CUDA_OK(cudaGetLastError());
 }
 
+void ln_rows_launch(const GemmArgs& a, int T_upper, cudaStream_t st) {
+    SD_CHECK(a.M % 4 == 0 && a.M <= 8192, CONFIG, "bf16 mode needs hidden % 4 == 0 and <= 8192");
+    launch_k(k_ln_rows, dim3(T_upper), dim3(256), 0, st, a);
+}
+
 }  // namespace sdb
 
 // --------------------------------------------------------------- test hook
@@ -678,6 +683,7 @@ extern "C" int sd_debug_gemm(const uint16_t* W, const uint16_t* X, int M, int K,
 namespace sdb {
 void trace_set_fast(const TraceBuf& b);
 void trace_set_step(const TraceBuf& b);
+void trace_set_gemmcl(const TraceBuf& b);
 }  // namespace sdb
 namespace {
 sdb::TraceBuf g_host_trace{nullptr, nullptr, 0};
@@ -685,6 +691,7 @@ void trace_set_all(const sdb::TraceBuf& b) {
     sdb::trace_set_gemm(b);
     sdb::trace_set_fast(b);
     sdb::trace_set_step(b);
+    sdb::trace_set_gemmcl(b);
 }
 }  // namespace
 extern "C" int sd_debug_trace_begin(int cap) {

@@ -5,6 +5,7 @@
 #include <memory>
 
 #include "../../include/specdec_b200.h"
+#include "../../include/specdec_b200_debug.h"
 #include "common.h"
 #include "step.h"
 

@@ -20,7 +20,7 @@ struct TraceRec {
 enum TraceKid : uint32_t {
     TK_GEMM = 1, TK_RED_STORE, TK_RED_GELU, TK_RED_QKV, TK_RED_RESID, TK_LN_ROWS, TK_ARGMAX,
     TK_EMBED_LN, TK_ATTN, TK_ATTN_COMBINE, TK_PREDICT, TK_PACK, TK_ACCEPT, TK_PAD_FILL,
-    TK_DRAFT_PACK, TK_DRAFT_TAKE, TK_DRAFT_COMMIT,
+    TK_DRAFT_PACK, TK_DRAFT_TAKE, TK_DRAFT_COMMIT, TK_GEMM_CL,
     // trace points (kid >= 100): one record, tag = payload
     TK_ATTN_BYTES = 110,  // per attention CTA: algorithmic K/V bytes >> 10
 };

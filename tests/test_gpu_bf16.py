@@ -328,3 +328,60 @@ def test_device_draft_loop_drafts_vs_oracle(sd, oracle):
     oracle.model_free(dm)
     print(f"draft agreement over {n} (step, sample) pairs: first {first / n:.3f}, whole {whole / n:.3f}")
     assert n >= steps and first / n >= 0.9 and whole / n >= 0.75
+
+
+def compact_flag(sd, m):
+    fn = sd.lib().sd_debug_model_compact
+    fn.argtypes = [C.c_void_p]
+    return fn(m._h)
+
+
+@pytest.mark.parametrize("cfg", [
+    # C2 / C4-draft shape (OPT-125m: h 768, hd 64, V 50272), layer-truncated
+    dict(num_layers=2, num_heads=12, head_dim=64, vocab_size=50272, max_positions=2048, init_seed=7),
+    # hd 128, h 1024 (the largest compact width), 16 heads
+    dict(num_layers=2, num_heads=8, head_dim=128, vocab_size=3000, max_positions=1024, init_seed=21),
+])
+def test_compact_layer_path_vs_oracle_and_stream_k(sd, oracle, cfg, monkeypatch):
+    """Small models run each layer GEMM as ONE cluster split-K launch with the
+    reduction in distributed shared memory and the LayerNorms fused
+    (gemm_cluster.cu).  Same stated bf16 tolerance against the fp32 oracle as
+    the stream-K path, and the two paths agree with each other closely."""
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SD_COMPACT", flag)
+        m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.BF16)
+        assert compact_flag(sd, m) == int(flag)
+        del m
+        lg, lo, am, amo = bf16_vs_oracle(sd, oracle, cfg, B=6, prompt_len=40, seed=cfg["init_seed"])
+        assert (am == lg.argmax(axis=1)).all()
+        d = np.abs(lg - lo)
+        scale = lo.std()
+        print(f"SD_COMPACT={flag}: max|d|/std={d.max() / scale:.4f} mean|d|/std={d.mean() / scale:.5f} "
+              f"argmax agree={np.mean(am == amo):.3f}")
+        assert d.max() <= 0.1 * scale
+        assert d.mean() <= 0.02 * scale
+        assert np.mean(am == amo) >= 0.9
+        out[flag] = lg
+    dd = np.abs(out["1"] - out["0"])
+    assert dd.max() <= 0.1 * out["0"].std() and dd.mean() <= 0.02 * out["0"].std()
+
+
+def test_compact_path_is_batch_composition_invariant(sd):
+    """The cluster split (CS, k-range per CTA) is a function of the shape
+    only: a sample verified alone and inside a batch of 13 produces the same
+    logits bit for bit (the property the EMS/greedy equality rests on)."""
+    cfg = dict(num_layers=2, num_heads=12, head_dim=64, vocab_size=4000, max_positions=1024, init_seed=5)
+    m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.BF16)
+    assert compact_flag(sd, m) == 1
+    rng = np.random.default_rng(5)
+    prompts = [rng.integers(3, 4000, size=int(rng.integers(5, 90))).tolist() for _ in range(13)]
+    full = sd.UnpadArena(m, 13, 256)
+    lg, _ = m.forward(sd.concatenate_inputs(prompts), full,
+                      [sd.TokenSlot(s, i) for s in range(13) for i in range(len(prompts[s]))])
+    off = np.cumsum([0] + [len(p) for p in prompts])
+    for s in (0, 7, 12):
+        one = sd.UnpadArena(m, 1, 256)
+        l1, _ = m.forward(sd.concatenate_inputs([prompts[s]]), one,
+                          [sd.TokenSlot(0, i) for i in range(len(prompts[s]))])
+        assert np.array_equal(l1.view(np.uint32), lg[off[s]:off[s + 1]].view(np.uint32)), s

@@ -23,7 +23,7 @@ sys.path.insert(0, ROOT)
 
 NAMES = {1: "gemm", 2: "red_store", 3: "red_gelu", 4: "red_qkv", 5: "red_resid", 6: "ln_rows", 7: "argmax",
          8: "embed_ln", 9: "attention", 10: "attn_combine", 11: "predict", 12: "pack", 13: "accept", 14: "pad_fill",
-         15: "draft_pack", 16: "draft_take", 17: "draft_commit"}
+         15: "draft_pack", 16: "draft_take", 17: "draft_commit", 18: "gemm_cl"}
 from bench import TRACE_REC as REC, trace_launches as launches  # noqa: E402
 
 
@@ -106,7 +106,7 @@ def main():
         n_steps += 1
         if si == 2:
             lines.append(f"--- step {si}: {len(st)} launches, {(t_b - t_a) / 1e3:.1f} us; layer 1 sequence:")
-            gemm_i = [i for i, l in enumerate(st) if l[0] == 1]
+            gemm_i = [i for i, l in enumerate(st) if l[0] in (1, 18)]
             lo, hi = (0, min(len(st), 60)) if a.draft else (gemm_i[4], min(len(st), gemm_i[8] + 3))
             prev_end = st[lo - 1][2]
             for l in st[lo:hi]:
