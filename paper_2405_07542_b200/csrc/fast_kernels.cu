@@ -86,7 +86,7 @@ void build_fast_model(Model& m) {
     const int sms = device_sm_count();
     for (auto mk : {std::make_pair(3 * h, h), std::make_pair(h, h), std::make_pair(mm, h), std::make_pair(h, mm)}) {
         if (!compact) break;
-        ClPlan p = gemm_cl_plan((int)mk.first, (int)mk.second, 256, sms);
+        ClPlan p = gemm_cl_plan((int)mk.first, (int)mk.second, 128, sms);
         compact = p.ok && gemm_cl_schedulable(p);
     }
     f->compact = compact;
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                 algo += (unsigned long long)ext * (2 * HD * 2);
             }
             // in-graph roofline: this CTA's algorithmic K/V bytes (KiB) next to its timeline record
-            trace_point(TK_ATTN_BYTES, (uint32_t)(algo >> 10));
+            trace__.point(TK_ATTN_BYTES, (uint32_t)(algo >> 10));
             ptx::mbar_wait(&qempty[qs], qph ^ 1);  // end of work
             sq_item[qs] = -1;
             ptx::mbar_arrive(&qfull[qs]);
@@ -794,6 +794,13 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     cb.cap = c.cap;
     cb.plans = dplans;
     cb.kv = (__nv_bfloat16*)c.kv;
+    // one cluster-GEMM launch per 128-token half of the chunk
+    auto cl_launch = [&](int epi, ClArgs g, const GemmMaps& mp, int nt, cudaStream_t s2) {
+        for (int tb = 0; tb < nt; tb += 128) {
+            g.t_base = tb;
+            gemm_cl_launch(epi, g, mp, std::min(128, nt - tb), s2);
+        }
+    };
     for (int l = 0; fmc->compact && l < cfg.num_layers; ++l) {
         const FastLayer& L = m.layers[l];
         // QKV (LN1 applied while building the token operand) + scatter
@@ -807,7 +814,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         g.layer = l;
         GemmMaps mp = f->map_xb;
         mp.A = fmc->cqkv[l];
-        PROF(PK_QKV, gemm_cl_launch(EPI_QKV, g, mp, n, st));
+        PROF(PK_QKV, cl_launch(EPI_QKV, g, mp, n, st));
         at.layer = l;
         at.work = f->attn_work + l;
         at.pre_ok = 0;
@@ -822,7 +829,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         g.stats_out = f->stats;
         mp = f->map_ctx;
         mp.A = fmc->co[l];
-        PROF(PK_O, gemm_cl_launch(EPI_RESID_LN, g, mp, n, st));
+        PROF(PK_O, cl_launch(EPI_RESID_LN, g, mp, n, st));
         // FC (LN2 applied to the operand) + GELU
         g = cb;
         g.M = mm;
@@ -834,7 +841,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         g.ld_out = mm;
         mp = f->map_xb;
         mp.A = fmc->cfc[l];
-        PROF(PK_FC, gemm_cl_launch(EPI_GELU, g, mp, n, st));
+        PROF(PK_FC, cl_launch(EPI_GELU, g, mp, n, st));
         // PROJ + residual -> statistics for the next layer's LN1
         g = cb;
         g.M = h;
@@ -844,8 +851,8 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         g.stats_out = f->stats;
         mp = f->map_act;
         mp.A = fmc->cproj[l];
-        PROF(PK_PROJ, gemm_cl_launch(EPI_RESID_LN, g, mp, n, st));
-        launches += 5;
+        PROF(PK_PROJ, cl_launch(EPI_RESID_LN, g, mp, n, st));
+        launches += 1 + 4 * ((n + 127) / 128);
     }
     if (fmc->compact) {  // final LayerNorm -> xb for the LM head
         GemmArgs g = base;

@@ -76,7 +76,9 @@ struct ClArgs {
     int M, K;                  // W is [M][K] bf16, M % 128 == 0, K % 64 == 0
     int T;                     // token count when dT == nullptr
     const int* dT;             // device token count
+    int t_base;                // this launch covers tokens [t_base, t_base + 128)
     int CS, nkb_max, box;      // set by gemm_cl_launch
+    int recv_off, per_owner;   // reduction receive buffer offset, tokens each CTA reduces
     const float* bias;         // [M]
     // LN_IN (QKV / FC): the token operand is LayerNorm(x_resid) built in shared memory
     const float* x_resid;      // [T][hidden] fp32 residual stream
@@ -96,14 +98,15 @@ struct ClArgs {
 };
 struct ClPlan {
     bool ok;
-    int CS, nkb_max, tiles;
-    size_t smem;
+    int CS, nkb_max, tiles, per_owner;
+    size_t smem, recv_off;
 };
 // cluster size / k-blocks per CTA for a shape: a function of (M, K, SMs) only
 ClPlan gemm_cl_plan(int M, int K, int box, int sms);
 bool gemm_cl_schedulable(const ClPlan& p);
 void gemm_cl_prepare();
-// epi: EPI_QKV (LN_IN), EPI_GELU (LN_IN) or EPI_RESID_LN (TMA token operand, stats out)
+// epi: EPI_QKV (LN_IN), EPI_GELU (LN_IN) or EPI_RESID_LN (TMA token operand, stats out);
+// T_upper <= 128 tokens from a.t_base
 void gemm_cl_launch(int epi, const ClArgs& a, const GemmMaps& maps, int T_upper, cudaStream_t st);
 
 }  // namespace sdb

@@ -14,7 +14,10 @@
 //     accumulator (M = 128 rows, N = the packed tokens);
 //   * the CS fp32 partial tiles are summed inside the cluster through
 //     distributed shared memory in fixed rank order (deterministic, no global
-//     partials), CTA r owning tokens t = r (mod CS), one warp per token;
+//     partials): CTA r owns a contiguous run of tokens, every CTA pushes its
+//     rows of that run into r's shared memory with one bulk copy
+//     (cp.async.bulk shared::cta -> shared::cluster, completing on r's
+//     mbarrier), r sums them one warp per token;
 //   * the epilogue is fused: bias + Q/K/V scatter into the unpadded KV arena,
 //     bias + GELU, or bias + residual update plus the per-(token, 128-row tile)
 //     LayerNorm statistics (sum, M2) of the new residual rows;
@@ -28,10 +31,15 @@
 // the GEMM shape and the SM count, never on the token count, so a token's
 // result does not depend on the batch it is verified in.
 //
+// One launch covers at most 128 tokens (a 256-token forward chunk is two
+// launches per GEMM over token halves, t_base = 0 / 128: the weights of a
+// small model stay in L2 between them).
+//
 // Warp roles (256 threads): thread 0 TMA (weights before griddepcontrol.wait,
-// tokens after), warp 1 TMEM allocation + lane 0 MMA issue, warps 4-7 TMEM ->
-// shared-memory partial tile, all 8 warps the LN_IN operand build and the
-// in-cluster reduction + epilogue.
+// tokens after), warp 1 TMEM allocation + lane 0 MMA issue, warps 4-7 push
+// their TMEM rows straight into the owning CTA's shared memory
+// (st.shared::cluster; one cluster barrier), all 8 warps the LN_IN operand
+// build and the owner-side reduction + epilogue.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -60,18 +68,23 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-__device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t local, uint32_t rank) {
     uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(ptx::smem_u32(local)), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
     return r;
 }
-__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
-    float4 v;
-    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "r"(addr)
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// bulk copy of this CTA's shared memory into a peer's (both shared::cluster
+// addresses), completing on the peer's mbarrier
+__device__ __forceinline__ void bulk_s2c(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "r"(src), "r"(bytes), "r"(bar)
                  : "memory");
-    return v;
 }
 __device__ __forceinline__ void tmem_alloc_n(uint32_t* dst, uint32_t cols) {  // whole warp
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_u32(dst)),
@@ -102,99 +115,170 @@ template <int EPI, bool LN_IN>
 __global__ void __launch_bounds__(kClThreads, 1)
     k_gemm_cl(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB32,
               const __grid_constant__ CUtensorMap tmB64, const __grid_constant__ CUtensorMap tmB128,
-              const __grid_constant__ CUtensorMap tmB256, const ClArgs a) {
-    CtaTrace trace__(TK_GEMM_CL);
+              const ClArgs a) {
+    CtaTrace trace__(EPI == EPI_QKV ? TK_GEMM_CL_QKV : EPI == EPI_GELU ? TK_GEMM_CL_GELU : TK_GEMM_CL_RESID);
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    __shared__ uint64_t s_full_a[kClMaxKb], s_full_b, s_tmem_full;
+    // 1024-byte aligned by pointer arithmetic on the __shared__ array, so every
+    // access below stays a shared-memory instruction (no generic ST/LD)
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    __shared__ uint64_t s_full_a[kClMaxKb], s_full_b, s_tmem_full, s_recv;
     __shared__ uint32_t s_tmem;
-    __shared__ float s_mu[256], s_rs[256];
+    __shared__ float4 s_g[kClMaxKb * 16], s_b[kClMaxKb * 16];  // LN gamma / beta of this CTA's k-range
+    __shared__ float s_mu[128], s_rs[128];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int CS = a.CS;
     const int rank = (int)cluster_rank();
     const int tile = blockIdx.x / CS;
     const int KB = a.K / 64;
     const int kb0 = rank * KB / CS, nkb = (rank + 1) * KB / CS - kb0;
-    const int bstride = a.box * 128;              // bytes per token k-block (host bound)
-    uint8_t* A = smem;                            // [nkb_max][128 rows][128 B]
-    uint8_t* Bt = smem + a.nkb_max * kClABytes;   // [nkb_max][box rows][128 B]
-    float* red = (float*)smem;                    // [BN tokens][128 rows] fp32, after the MMAs
+    const int box = a.box;                          // host bound on this launch's tokens (<= 128)
+    const int per_owner = a.per_owner;              // CTA r reduces tokens [r * per_owner, (r + 1) * per_owner)
+    uint8_t* A = smem;                              // [nkb_max][128 rows][128 B]
+    uint8_t* Bt = smem + a.nkb_max * kClABytes;     // [nkb_max][box rows][128 B]
+    float* send = (float*)smem;                     // after the MMAs: [token][128 rows] fp32
+    float* recv = (float*)(smem + a.recv_off);      // [sender][slot][128 rows] fp32
 
     if (threadIdx.x == 0) {
         ptx::prefetch_tmap(&tmA);
         for (int i = 0; i < nkb; ++i) ptx::mbar_init(&s_full_a[i], 1);
         ptx::mbar_init(&s_full_b, 1);
         ptx::mbar_init(&s_tmem_full, 1);
+        ptx::mbar_init(&s_recv, 1);
         ptx::fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc_n(&s_tmem, (uint32_t)a.box);
+    if (warp == 1) tmem_alloc_n(&s_tmem, (uint32_t)box);
+    // everything that does not depend on the predecessor is issued before
+    // griddepcontrol.wait: the weight blocks, LN gamma / beta, the bias
+    if constexpr (LN_IN) {
+        for (int i = threadIdx.x; i < nkb * 16; i += kClThreads) {
+            s_g[i] = ((const float4*)(a.ln_g + kb0 * 64))[i];
+            s_b[i] = ((const float4*)(a.ln_b + kb0 * 64))[i];
+        }
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();  // barrier inits visible cluster-wide before any peer's bulk copy lands
     ptx::tc_fence_after();
     const uint32_t tmem = s_tmem;
     pdl_trigger();
-    if (threadIdx.x == 0) {  // weights do not depend on the predecessor: load them before the wait
+    if (threadIdx.x == 0) {
         const uint64_t pol_w = ptx::policy_evict_first();
         for (int i = 0; i < nkb; ++i) {
             ptx::mbar_arrive_expect_tx(&s_full_a[i], kClABytes);
             ptx::tma_load_2d(A + i * kClABytes, &tmA, &s_full_a[i], (kb0 + i) * 64, tile * 128, pol_w);
         }
     }
+    const int m0 = tile * 128 + lane * 4;
+    const float4 bias = a.bias ? *(const float4*)(a.bias + m0) : make_float4(0.f, 0.f, 0.f, 0.f);
     pdl_wait();
-    const int T = a.dT ? *a.dT : a.T;
+    const int T = min(max((a.dT ? *a.dT : a.T) - a.t_base, 0), box);  // this launch's tokens
     const int BN = T <= 16 ? 16 : ((T + 15) / 16) * 16;
-    const bool idle = T <= 0 || BN > a.box;
+    const bool idle = T <= 0;
+    const int own0 = rank * per_owner;
+    const int n_own = min(max(T - own0, 0), per_owner);  // tokens this CTA reduces
+    if (threadIdx.x == 0) ptx::mbar_arrive_expect_tx(&s_recv, (uint32_t)(CS * n_own * 512));
+    const uint32_t ttag = ((uint32_t)EPI << 24) | blockIdx.x;
+    if (threadIdx.x == 0) trace__.point(120, ttag);
+    // the epilogue operands of this warp's first token, in flight during the MMAs
+    const int t_first = own0 + warp;  // warp w reduces slots w, w + 8, ...
+    float4 pre_old = make_float4(0.f, 0.f, 0.f, 0.f);
+    Plan pre_pl{};
+    if (t_first < T) {
+        if constexpr (EPI == EPI_RESID_LN) pre_old = *(const float4*)(a.resid + (size_t)(a.t_base + t_first) * a.hidden + m0);
+        if constexpr (EPI == EPI_QKV) pre_pl = a.plans[a.t_base + t_first];
+    }
     if (!idle) {
         if constexpr (LN_IN) {
-            // per-token LayerNorm statistics: Chan combination of the producer's
-            // per-tile (sum, M2) in tile order (deterministic)
-            for (int t = threadIdx.x; t < BN; t += kClThreads) {
-                float mu = 0.0f, rs = 0.0f;
-                if (t < T) {
-                    const float2* p = a.stats_in + (size_t)t * a.n_stat;
-                    float s = 0.0f;
-                    for (int i = 0; i < a.n_stat; ++i) s += p[i].x;
-                    mu = s / a.hidden;
-                    float m2 = 0.0f;
-                    for (int i = 0; i < a.n_stat; ++i) {
-                        const float d = p[i].x * (1.0f / 128.0f) - mu;
-                        m2 += p[i].y + 128.0f * d * d;
-                    }
-                    rs = rsqrtf(m2 / a.hidden + 1e-5f);
+            // LN(x) -> bf16 in the 128B-swizzled K-major layout TMA would
+            // produce (16-byte chunk c of row t at chunk c ^ (t & 7)).  The x
+            // loads of up to four chunks per thread are issued together with the
+            // per-token statistics (Chan combination of the producer's per-tile
+            // (sum, M2) in tile order: deterministic): one L2 round trip.
+            const int per = BN * 8, total = nkb * per;
+            constexpr int kU = 4;
+            float4 xr[kU][2];
+            // chunk idx = threadIdx.x + u * 256 -> (k-block i, token t, 16-byte chunk c),
+            // advanced incrementally (no integer division in the loops)
+            const int i_0 = threadIdx.x / per, r_0 = threadIdx.x - i_0 * per;
+            int ci = i_0, cr = r_0;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int idx = threadIdx.x + u * kClThreads;
+                const int i = ci, t = cr >> 3, c = cr & 7;
+                cr += kClThreads;
+                while (cr >= per) {
+                    cr -= per;
+                    ++ci;
                 }
-                s_mu[t] = mu;
-                s_rs[t] = rs;
+                if (idx < total && t < T) {
+                    const float4* x = (const float4*)(a.x_resid + (size_t)(a.t_base + t) * a.hidden + (kb0 + i) * 64 + c * 8);
+                    xr[u][0] = x[0];
+                    xr[u][1] = x[1];
+                }
+            }
+            if (threadIdx.x < T) {
+                const float2* p = a.stats_in + (size_t)(a.t_base + threadIdx.x) * a.n_stat;
+                float2 st[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < a.n_stat) st[j] = p[j];
+                float sm = 0.0f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < a.n_stat) sm += st[j].x;
+                const float mu = sm / a.hidden;
+                float m2 = 0.0f;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < a.n_stat) {
+                        const float d = st[j].x * (1.0f / 128.0f) - mu;
+                        m2 += st[j].y + 128.0f * d * d;
+                    }
+                s_mu[threadIdx.x] = mu;
+                s_rs[threadIdx.x] = rsqrtf(m2 / a.hidden + 1e-5f);
             }
             __syncthreads();
-            // LN(x) -> bf16, written in the 128B-swizzled K-major layout TMA
-            // would produce (16-byte chunk c of row t at chunk c ^ (t & 7))
-            const int per = BN * 8;
-            for (int idx = threadIdx.x; idx < nkb * per; idx += kClThreads) {
-                const int i = idx / per, r = idx - i * per, t = r >> 3, c = r & 7;
-                uint4 o = make_uint4(0u, 0u, 0u, 0u);
-                if (t < T) {
-                    const int k = (kb0 + i) * 64 + c * 8;
-                    const float4* x = (const float4*)(a.x_resid + (size_t)t * a.hidden + k);
-                    const float4* g = (const float4*)(a.ln_g + k);
-                    const float4* b = (const float4*)(a.ln_b + k);
-                    const float4 x0 = x[0], x1 = x[1], g0 = g[0], g1 = g[1], b0 = b[0], b1 = b[1];
-                    const float mu = s_mu[t], rs = s_rs[t];
-                    o.x = pack_bf16((x0.x - mu) * rs * g0.x + b0.x, (x0.y - mu) * rs * g0.y + b0.y);
-                    o.y = pack_bf16((x0.z - mu) * rs * g0.z + b0.z, (x0.w - mu) * rs * g0.w + b0.w);
-                    o.z = pack_bf16((x1.x - mu) * rs * g1.x + b1.x, (x1.y - mu) * rs * g1.y + b1.y);
-                    o.w = pack_bf16((x1.z - mu) * rs * g1.z + b1.z, (x1.w - mu) * rs * g1.w + b1.w);
+            ci = i_0;
+            cr = r_0;
+            for (int u0 = 0; u0 * kClThreads < total; u0 += kU) {
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const int idx = threadIdx.x + (u0 + u) * kClThreads;
+                    if (idx >= total) break;
+                    const int i = ci, t = cr >> 3, c = cr & 7;
+                    cr += kClThreads;
+                    while (cr >= per) {
+                        cr -= per;
+                        ++ci;
+                    }
+                    if (u0 > 0 && t < T) {  // chunks beyond the first four (BN * nkb > 128)
+                        const float4* x = (const float4*)(a.x_resid + (size_t)(a.t_base + t) * a.hidden + (kb0 + i) * 64 + c * 8);
+                        xr[u][0] = x[0];
+                        xr[u][1] = x[1];
+                    }
+                    uint4 o = make_uint4(0u, 0u, 0u, 0u);
+                    if (t < T) {
+                        const float mu = s_mu[t], rs = s_rs[t];
+                        const float4 x0 = xr[u][0], x1 = xr[u][1];
+                        const float4 g0 = s_g[i * 16 + c * 2], g1 = s_g[i * 16 + c * 2 + 1];
+                        const float4 b0 = s_b[i * 16 + c * 2], b1 = s_b[i * 16 + c * 2 + 1];
+                        o.x = pack_bf16((x0.x - mu) * rs * g0.x + b0.x, (x0.y - mu) * rs * g0.y + b0.y);
+                        o.y = pack_bf16((x0.z - mu) * rs * g0.z + b0.z, (x0.w - mu) * rs * g0.w + b0.w);
+                        o.z = pack_bf16((x1.x - mu) * rs * g1.x + b1.x, (x1.y - mu) * rs * g1.y + b1.y);
+                        o.w = pack_bf16((x1.z - mu) * rs * g1.z + b1.z, (x1.w - mu) * rs * g1.w + b1.w);
+                    }
+                    *(uint4*)(Bt + i * box * 128 + t * 128 + ((c ^ (t & 7)) << 4)) = o;
                 }
-                *(uint4*)(Bt + i * bstride + t * 128 + ((c ^ (t & 7)) << 4)) = o;
             }
             ptx::fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
             __syncthreads();
+            if (threadIdx.x == 0) trace__.point(121, ttag);
         } else if (threadIdx.x == 0) {
-            const int box_d = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-            const CUtensorMap* tmB = box_d == 32 ? &tmB32 : box_d == 64 ? &tmB64 : box_d == 128 ? &tmB128 : &tmB256;
+            const int box_d = BN <= 32 ? 32 : BN <= 64 ? 64 : 128;
+            const CUtensorMap* tmB = box_d == 32 ? &tmB32 : box_d == 64 ? &tmB64 : &tmB128;
             const uint64_t pol_x = ptx::policy_evict_last();
             ptx::mbar_arrive_expect_tx(&s_full_b, (uint32_t)(nkb * box_d * 128));
             for (int i = 0; i < nkb; ++i)
-                ptx::tma_load_2d(Bt + i * bstride, tmB, &s_full_b, (kb0 + i) * 64, 0, pol_x);
+                ptx::tma_load_2d(Bt + i * box * 128, tmB, &s_full_b, (kb0 + i) * 64, a.t_base, pol_x);
         }
         if (threadIdx.x == 32) {  // ---------------- MMA issuer
             const uint32_t idesc = ptx::umma_idesc_bf16(128, BN);
@@ -202,7 +286,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
             for (int i = 0; i < nkb; ++i) {
                 ptx::mbar_wait(&s_full_a[i], 0);
                 ptx::tc_fence_after();
-                const uint32_t sa = ptx::smem_u32(A + i * kClABytes), sb = ptx::smem_u32(Bt + i * bstride);
+                const uint32_t sa = ptx::smem_u32(A + i * kClABytes), sb = ptx::smem_u32(Bt + i * box * 128);
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     ptx::umma_bf16(tmem, ptx::umma_desc_kmajor_sw128(sa + k * 32), ptx::umma_desc_kmajor_sw128(sb + k * 32),
@@ -210,81 +294,100 @@ __global__ void __launch_bounds__(kClThreads, 1)
             }
             ptx::umma_commit(&s_tmem_full);
         }
-        if (warp >= 4) {  // ---------------- TMEM -> shared partial tile [token][row]
+        if (warp >= 4) {  // ---------------- TMEM -> send buffer -> bulk copies to the owners
             ptx::mbar_wait(&s_tmem_full, 0);
             ptx::tc_fence_after();
+            if (threadIdx.x == 128) trace__.point(122, ttag);
             const int row = (warp - 4) * 32 + lane;
             const uint32_t trow = tmem + ((uint32_t)((warp - 4) * 32) << 16);
             for (int j0 = 0; j0 < BN; j0 += 16) {
                 float v[16];
                 ptx::tmem_ld16(trow + j0, v);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) red[(j0 + i) * 128 + row] = v[i];
+                for (int i = 0; i < 16; ++i) send[(j0 + i) * 128 + row] = v[i];
+            }
+            if (threadIdx.x == 128) trace__.point(126, ttag);
+            ptx::fence_proxy_async_smem();  // the bulk copies read what the generic proxy wrote
+            ptx::named_bar_sync(1, 128);
+            if (warp == 4) {  // lane r ships owner r's run (CS <= 32)
+                if (lane == 0) trace__.point(127, ttag);
+                const int r = lane;
+                const int nr = r < CS ? min(max(T - r * per_owner, 0), per_owner) : 0;
+                if (nr > 0) {
+                    const uint32_t src = ptx::smem_u32(send + (size_t)r * per_owner * 128);
+                    const uint32_t dst = mapa_u32(ptx::smem_u32(recv + (size_t)rank * per_owner * 128), (uint32_t)r);
+                    const uint32_t bar = mapa_u32(ptx::smem_u32(&s_recv), (uint32_t)r);
+                    bulk_s2c(dst, src, (uint32_t)(nr * 512), bar);
+                }
+                __syncwarp();
+                if (lane == 0) trace__.point(123, ttag);
             }
         }
     } else if (threadIdx.x == 0) {
         for (int i = 0; i < nkb; ++i) ptx::mbar_wait(&s_full_a[i], 0);  // no TMA in flight at exit
     }
-    ptx::tc_fence_before();
-    __syncthreads();
-    cluster_sync_all();  // every CTA's partial tile is in its shared memory
-    if (!idle) {
-        const int m0 = tile * 128 + lane * 4;
-        const float4 bias = a.bias ? *(const float4*)(a.bias + m0) : make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int t = rank + CS * warp; t < T; t += CS * (kClThreads / 32)) {
-            float4 v[kClMaxCS];  // every peer's load in flight before the first add
+    ptx::mbar_wait(&s_recv, 0);  // every sender's rows of this CTA's tokens have landed
+    __syncwarp();
+    cluster_arrive();            // ... so this CTA's incoming copies are complete
+    if (threadIdx.x == 0) trace__.point(124, ttag);
+    int it = 0;
+    for (int slot = warp; slot < n_own; slot += kClThreads / 32, ++it) {
+        const int t = own0 + slot;
+        float4 v[kClMaxCS];  // every sender's rows loaded before the first add
 #pragma unroll
-            for (int p = 0; p < kClMaxCS; ++p)
-                if (p < CS) v[p] = ld_dsmem_f4(dsmem_addr(red + t * 128 + lane * 4, p));
-            float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int p = 0; p < kClMaxCS; ++p)
+            if (p < CS) v[p] = *(const float4*)(recv + ((size_t)p * per_owner + slot) * 128 + lane * 4);
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-            for (int p = 0; p < kClMaxCS; ++p)  // fixed rank order: deterministic
-                if (p < CS) {
-                    s.x += v[p].x;
-                    s.y += v[p].y;
-                    s.z += v[p].z;
-                    s.w += v[p].w;
-                }
-            if constexpr (EPI == EPI_RESID_LN) {
-                float4* rp = (float4*)(a.resid + (size_t)t * a.hidden + m0);
-                const float4 o = *rp;
-                const float4 x = make_float4(o.x + (s.x + bias.x), o.y + (s.y + bias.y), o.z + (s.z + bias.z),
-                                             o.w + (s.w + bias.w));
-                *rp = x;
-                const float sum = warp_sum(x.x + x.y + x.z + x.w);
-                const float mu = sum * (1.0f / 128.0f);
-                const float dx = x.x - mu, dy = x.y - mu, dz = x.z - mu, dw = x.w - mu;
-                const float m2 = warp_sum(dx * dx + dy * dy + dz * dz + dw * dw);
-                if (lane == 0) a.stats_out[(size_t)t * a.n_stat + tile] = make_float2(sum, m2);
-            } else if constexpr (EPI == EPI_GELU) {
-                uint2 o;
-                o.x = pack_bf16(gelu_tanh(s.x + bias.x), gelu_tanh(s.y + bias.y));
-                o.y = pack_bf16(gelu_tanh(s.z + bias.z), gelu_tanh(s.w + bias.w));
-                *(uint2*)(a.out_bf16 + (size_t)t * a.ld_out + m0) = o;
-            } else {  // EPI_QKV
-                uint2 o;
-                o.x = pack_bf16(s.x + bias.x, s.y + bias.y);
-                o.y = pack_bf16(s.z + bias.z, s.w + bias.w);
-                const int which = m0 / a.h, hm = m0 - which * a.h;
-                if (which == 0) {
-                    *(uint2*)(a.out_bf16 + (size_t)t * a.h + hm) = o;
-                } else {
-                    const Plan pl = a.plans[t];
-                    if (pl.store) {
-                        const int head = hm / a.hd, d = hm - head * a.hd;
-                        const size_t off = ((((size_t)a.layer * 2 + (which - 1)) * a.B + pl.sample) * a.heads + head) *
-                                               (size_t)a.cap * a.hd +
-                                           (size_t)pl.write_slot * a.hd + d;
-                        *(uint2*)(a.kv + off) = o;
-                    }
+        for (int p = 0; p < kClMaxCS; ++p)  // fixed rank order: deterministic
+            if (p < CS) {
+                s.x += v[p].x;
+                s.y += v[p].y;
+                s.z += v[p].z;
+                s.w += v[p].w;
+            }
+        const size_t tg = (size_t)(a.t_base + t);
+        if constexpr (EPI == EPI_RESID_LN) {
+            float4* rp = (float4*)(a.resid + tg * a.hidden + m0);
+            const float4 o = it == 0 ? pre_old : *rp;
+            const float4 x = make_float4(o.x + (s.x + bias.x), o.y + (s.y + bias.y), o.z + (s.z + bias.z),
+                                         o.w + (s.w + bias.w));
+            *rp = x;
+            const float sum = warp_sum(x.x + x.y + x.z + x.w);
+            const float mu = sum * (1.0f / 128.0f);
+            const float dx = x.x - mu, dy = x.y - mu, dz = x.z - mu, dw = x.w - mu;
+            const float m2 = warp_sum(dx * dx + dy * dy + dz * dz + dw * dw);
+            if (lane == 0) a.stats_out[tg * a.n_stat + tile] = make_float2(sum, m2);
+        } else if constexpr (EPI == EPI_GELU) {
+            uint2 o;
+            o.x = pack_bf16(gelu_tanh(s.x + bias.x), gelu_tanh(s.y + bias.y));
+            o.y = pack_bf16(gelu_tanh(s.z + bias.z), gelu_tanh(s.w + bias.w));
+            *(uint2*)(a.out_bf16 + tg * a.ld_out + m0) = o;
+        } else {  // EPI_QKV
+            uint2 o;
+            o.x = pack_bf16(s.x + bias.x, s.y + bias.y);
+            o.y = pack_bf16(s.z + bias.z, s.w + bias.w);
+            const int which = m0 / a.h, hm = m0 - which * a.h;
+            if (which == 0) {
+                *(uint2*)(a.out_bf16 + tg * a.h + hm) = o;
+            } else {
+                const Plan pl = it == 0 ? pre_pl : a.plans[tg];
+                if (pl.store) {
+                    const int head = hm / a.hd, d = hm - head * a.hd;
+                    const size_t off = ((((size_t)a.layer * 2 + (which - 1)) * a.B + pl.sample) * a.heads + head) *
+                                           (size_t)a.cap * a.hd +
+                                       (size_t)pl.write_slot * a.hd + d;
+                    *(uint2*)(a.kv + off) = o;
                 }
             }
         }
     }
-    cluster_sync_all();  // peers have finished reading this CTA's partial tile
+    if (threadIdx.x == 0) trace__.point(125, ttag);
+    __syncwarp();
+    cluster_wait();  // every owner has received everything: no copy still reads this CTA's memory
     if (warp == 1) {
         ptx::tc_fence_after();
-        tmem_dealloc_n(tmem, (uint32_t)a.box);
+        tmem_dealloc_n(tmem, (uint32_t)box);
     }
 }
 
@@ -299,13 +402,20 @@ void prepare_one() {
 
 ClPlan gemm_cl_plan(int M, int K, int box, int sms) {
     ClPlan p{};
-    if (M % 128 || K % 64 || box < 32 || box > 256) return p;
+    if (M % 128 || K % 64 || box < 32 || box > 128) return p;
     const int tiles = M / 128, KB = K / 64;
-    int cs = std::max((KB + kClMaxKb - 1) / kClMaxKb, std::min({8, sms / std::max(1, tiles), KB}));
+    // at most half the SMs, so a launch and its (PDL-overlapped) successor fit
+    // side by side: one CTA per SM (shared memory), no second wave
+    const int max_ctas = std::max(1, sms / 2);
+    int cs = std::max((KB + kClMaxKb - 1) / kClMaxKb, std::min({kClMaxCS, max_ctas / std::max(1, tiles), KB}));
     if (cs < 1 || cs > kClMaxCS || cs > KB || (long long)tiles * cs > sms) return p;
     const int nkb = (KB + cs - 1) / cs;
+    p.per_owner = (box + cs - 1) / cs;
+    const size_t send = (size_t)box * 128 * 4;                     // [token][row] fp32
+    const size_t recv = (size_t)cs * p.per_owner * 128 * 4;         // [sender][slot][row] fp32
     const size_t ab = (size_t)nkb * kClABytes + (size_t)nkb * box * 128;
-    const size_t smem = std::max(ab, (size_t)128 * box * 4) + 1024;
+    p.recv_off = (std::max(ab, send) + 1023) / 1024 * 1024;  // the send buffer reuses the operand tiles
+    const size_t smem = p.recv_off + recv + 1024;
     if (smem > (size_t)kClSmemMax) return p;
     p.ok = true;
     p.CS = cs;
@@ -345,26 +455,28 @@ bool gemm_cl_schedulable(const ClPlan& p) {
 
 void gemm_cl_launch(int epi, const ClArgs& a0, const GemmMaps& maps, int T_upper, cudaStream_t st) {
     gemm_cl_prepare();
-    SD_CHECK(T_upper >= 1 && T_upper <= 256, INTERNAL, "cluster GEMM token tile is at most 256");
+    SD_CHECK(T_upper >= 1 && T_upper <= 128, INTERNAL, "cluster GEMM token tile is at most 128");
     ClArgs a = a0;
-    a.box = T_upper <= 32 ? 32 : T_upper <= 64 ? 64 : T_upper <= 128 ? 128 : 256;
+    a.box = T_upper <= 32 ? 32 : T_upper <= 64 ? 64 : 128;
     const ClPlan p = gemm_cl_plan(a.M, a.K, a.box, device_sm_count());
     SD_CHECK(p.ok, INTERNAL, "cluster GEMM plan infeasible for this shape");
     a.CS = p.CS;
     a.nkb_max = p.nkb_max;
+    a.recv_off = (int)p.recv_off;
+    a.per_owner = p.per_owner;
     const dim3 grid(p.tiles * p.CS);
     switch (epi) {
         case EPI_QKV:
             launch_kc(k_gemm_cl<EPI_QKV, true>, grid, dim3(kClThreads), p.smem, st, p.CS, maps.A, maps.B[0],
-                      maps.B[1], maps.B[2], maps.B[3], a);
+                      maps.B[1], maps.B[2], a);
             break;
         case EPI_GELU:
             launch_kc(k_gemm_cl<EPI_GELU, true>, grid, dim3(kClThreads), p.smem, st, p.CS, maps.A, maps.B[0],
-                      maps.B[1], maps.B[2], maps.B[3], a);
+                      maps.B[1], maps.B[2], a);
             break;
         case EPI_RESID_LN:
             launch_kc(k_gemm_cl<EPI_RESID_LN, false>, grid, dim3(kClThreads), p.smem, st, p.CS, maps.A, maps.B[0],
-                      maps.B[1], maps.B[2], maps.B[3], a);
+                      maps.B[1], maps.B[2], a);
             break;
         default:
             throw Error(INTERNAL, "cluster GEMM epilogue not supported");

@@ -20,7 +20,7 @@ struct TraceRec {
 enum TraceKid : uint32_t {
     TK_GEMM = 1, TK_RED_STORE, TK_RED_GELU, TK_RED_QKV, TK_RED_RESID, TK_LN_ROWS, TK_ARGMAX,
     TK_EMBED_LN, TK_ATTN, TK_ATTN_COMBINE, TK_PREDICT, TK_PACK, TK_ACCEPT, TK_PAD_FILL,
-    TK_DRAFT_PACK, TK_DRAFT_TAKE, TK_DRAFT_COMMIT, TK_GEMM_CL,
+    TK_DRAFT_PACK, TK_DRAFT_TAKE, TK_DRAFT_COMMIT, TK_GEMM_CL_QKV, TK_GEMM_CL_GELU, TK_GEMM_CL_RESID,
     // trace points (kid >= 100): one record, tag = payload
     TK_ATTN_BYTES = 110,  // per attention CTA: algorithmic K/V bytes >> 10
 };
@@ -61,13 +61,19 @@ struct TraceBuf {
     }                                                                                     \
     struct CtaTrace {                                                                     \
         uint64_t t0;                                                                      \
+        TraceRec* rec; /* read once at entry: no global load on the exit path */          \
         uint32_t kid;                                                                     \
         __device__ __forceinline__ explicit CtaTrace(uint32_t k) : kid(k) {               \
-            t0 = g_trace_##name.rec ? globaltimer() : 0;                                  \
+            rec = g_trace_##name.rec;                                                     \
+            t0 = rec ? globaltimer() : 0;                                                 \
+        }                                                                                 \
+        /* phase record from any thread (kid >= 100), free when tracing is off */         \
+        __device__ __forceinline__ void point(uint32_t pk, uint32_t tag) const {          \
+            if (rec) trace_point(pk, tag);                                                \
         }                                                                                 \
         __device__ __forceinline__ ~CtaTrace() {                                          \
-            const TraceBuf& b = g_trace_##name;                                           \
-            if (b.rec && threadIdx.x == 0) {                                              \
+            if (threadIdx.x == 0 && rec) {                                                \
+                const TraceBuf& b = g_trace_##name;                                       \
                 const uint64_t t1 = globaltimer();                                        \
                 unsigned i = atomicAdd(b.count, 1u);                                      \
                 if (i < b.cap) {                                                          \

@@ -23,7 +23,7 @@ sys.path.insert(0, ROOT)
 
 NAMES = {1: "gemm", 2: "red_store", 3: "red_gelu", 4: "red_qkv", 5: "red_resid", 6: "ln_rows", 7: "argmax",
          8: "embed_ln", 9: "attention", 10: "attn_combine", 11: "predict", 12: "pack", 13: "accept", 14: "pad_fill",
-         15: "draft_pack", 16: "draft_take", 17: "draft_commit", 18: "gemm_cl"}
+         15: "draft_pack", 16: "draft_take", 17: "draft_commit", 18: "cl_qkv", 19: "cl_gelu", 20: "cl_resid"}
 from bench import TRACE_REC as REC, trace_launches as launches  # noqa: E402
 
 
@@ -106,12 +106,25 @@ def main():
         n_steps += 1
         if si == 2:
             lines.append(f"--- step {si}: {len(st)} launches, {(t_b - t_a) / 1e3:.1f} us; layer 1 sequence:")
-            gemm_i = [i for i, l in enumerate(st) if l[0] in (1, 18)]
+            gemm_i = [i for i, l in enumerate(st) if l[0] in (1, 18, 19, 20)]
             lo, hi = (0, min(len(st), 60)) if a.draft else (gemm_i[4], min(len(st), gemm_i[8] + 3))
             prev_end = st[lo - 1][2]
             for l in st[lo:hi]:
                 lines.append(f"  {NAMES[l[0]]:13s} start {(l[1] - t_a) / 1e3:9.1f} dur {(l[2] - l[1]) / 1e3:7.1f} "
-                             f"gap {(l[1] - prev_end) / 1e3:6.1f} ctas {l[3]:5d} sms {l[4]:3d}")
+                             f"gap {(l[1] - prev_end) / 1e3:6.1f} ctas {l[3]:5d} sms {l[4]:3d} "
+                             f"end-after-prev {(l[2] - prev_end) / 1e3:6.1f}")
+                if l[0] in (18, 19, 20):  # cluster GEMM phases (trace points 120-125), us after the predecessor's end
+                    epi = {18: 3, 19: 2, 20: 1}[l[0]]
+                    pts = rec[(rec["kid"] >= 120) & (rec["kid"] <= 127) & (rec["t0"] >= l[1]) & (rec["t0"] <= l[2])
+                              & ((rec["blk"] >> 24) == epi)]
+                    row = []
+                    for k, nm in ((120, "dep"), (121, "ln"), (122, "mma"), (126, "tmem"), (127, "nbar"), (123, "push"),
+                                  (124, "recv"), (125, "epi")):
+                        v = pts[pts["kid"] == k]
+                        if len(v):
+                            d = (v["t0"].astype(np.int64) - prev_end) / 1e3
+                            row.append(f"{nm} {np.median(d):5.1f}/{d.max():5.1f}")
+                    lines.append("      phases (median/max): " + " | ".join(row))
                 prev_end = max(prev_end, l[2])
     # phases inside persistent GEMM chains (trace points 101..106)
     pts = rec[rec["kid"] >= 100]
