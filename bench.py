@@ -539,6 +539,22 @@ def run_extra(a, rank, world, local):
         res[mode] = dict(value=acc / (ms_tot / 1000.0), ms_per_step=ms_tot / a.steps,
                          ms_per_verify_step=ms_tot / max(1, steps_tot), avg_tau=st["avg_tau"],
                          padding_ratio=st["avg_padding_ratio"], verify_steps=steps_tot / a.steps)
+    # HBM roofline of the EMS generation: the algorithmic bytes every launch of
+    # one eager profiled generation must move (weights + K/V + activations; the
+    # draft model's forwards included for C4) over the graph-timed generation
+    sess = sessions["ems"]
+    sess.reset()
+    sd.profile_enable(True)
+    sess.run(use_graph=False, graph_steps=1)
+    prof = sd.profile_read()
+    sd.profile_enable(False)
+    gen_b = sum(v["bytes"] for kk, v in prof.items() if kk != "gemm_stream")
+    hbm, _, peak_src = measured_peaks()
+    roof = {"bound": "hbm", "unit": "GB/s", "peak": hbm, "peak_source": peak_src,
+            "achieved": round(gen_b / (res["ems"]["ms_per_step"] / 1000.0) / 1e9, 1),
+            "generation_hbm_roof_frac": round(gen_b / (res["ems"]["ms_per_step"] / 1000.0) / (hbm * 1e9), 4),
+            "generation_gb": round(gen_b / 1e9, 2),
+            "what": "algorithmic bytes of one eager profiled EMS generation / graph-timed ms per generation"}
     if rank == 0:
         wl = ("C4 OPT-13B target + OPT-125m-shaped draft model (k=4, persistent device draft KV)" if a.config == "c4"
               else "C5 OPT-6.7B shape, 4k prompts, skewed acceptance (p 0.95/0.05), 256 new tokens")
@@ -552,6 +568,7 @@ def run_extra(a, rank, world, local):
         if "vanilla" in res:
             line["padded"] = {k2: round(v, 4) for k2, v in res["vanilla"].items()}
             line["ems_vs_padded"] = round(res["ems"]["value"] / res["vanilla"]["value"], 4)
+        line["roofline"] = roof
         if prefill:
             line["prefill"] = {k2: round(v, 1) for k2, v in prefill.items()}
         print(json.dumps(line), flush=True)

@@ -65,8 +65,11 @@ __device__ __forceinline__ uint32_t cluster_rank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
+// execution-only cluster barrier (no memory fence: nothing is published
+// through ordinary memory; barrier inits are covered by
+// fence.mbarrier_init.release.cluster, the bulk copies by their mbarriers)
 __device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 __device__ __forceinline__ uint32_t mapa_u32(uint32_t local, uint32_t rank) {
     uint32_t r;
@@ -74,10 +77,10 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t local, uint32_t rank) {
     return r;
 }
 __device__ __forceinline__ void cluster_arrive() {
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_wait() {
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
 // bulk copy of this CTA's shared memory into a peer's (both shared::cluster
 // addresses), completing on the peer's mbarrier
@@ -156,6 +159,7 @@ __global__ void __launch_bounds__(kClThreads, 1)
         }
     }
     ptx::tc_fence_before();
+    __syncthreads();     // TMEM address, gamma / beta visible inside the CTA
     cluster_sync_all();  // barrier inits visible cluster-wide before any peer's bulk copy lands
     ptx::tc_fence_after();
     const uint32_t tmem = s_tmem;

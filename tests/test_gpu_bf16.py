@@ -123,11 +123,21 @@ def test_bf16_decode_agrees_with_oracle(sd, oracle, mode):
         agree.append(k / len(a))
     print(f"{mode}: prefix agreement per sample {np.round(agree, 2).tolist()}")
     assert np.mean(agree) >= 0.25
-    # losslessness inside the bf16 model: vanilla and ems give the same streams
+    # The other layout on the same bf16 model.  The padded grid shifts each
+    # sample's keys by its left padding, which regroups the bf16 attention sums
+    # into different 128-key chunks, so the two layouts are NOT bit-identical
+    # in bf16 (they are in the fp32 check mode: test_gpu_check.py); each is
+    # lossless against greedy decoding on its own layout (test_device_loop_*).
+    # Stated bound: the streams agree on at least half their length on
+    # average, and most samples agree on the first 16 tokens.
     r2 = sd.decode(sd.EngineConfig(mode="ems" if mode == "vanilla" else "vanilla", predictor="retrieval",
                                    copy_len=7, batch_size=B, max_new_tokens=48, stop_on_eos=False), m, prompts)
     same = np.mean([a == b for a, b in zip(r.generated_tokens, r2.generated_tokens)])
-    print(f"{mode}: vanilla/ems identical streams fraction {same:.2f}")
+    pre = [next((i for i, (x, y) in enumerate(zip(a, b)) if x != y), len(a)) for a, b in
+           zip(r.generated_tokens, r2.generated_tokens)]
+    print(f"{mode}: vanilla/ems identical streams fraction {same:.2f}, common prefix per sample {pre}")
+    assert np.mean(pre) >= 24
+    assert np.mean([p >= 16 for p in pre]) >= 0.5
 
 
 @pytest.mark.parametrize("mode", ["ems", "vanilla"])
