@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--cap", type=int, default=6_000_000)
     ap.add_argument("--mode", default="ems")
     ap.add_argument("--draft", action="store_true", help="C4: OPT-125m-shaped draft model, k=4")
+    ap.add_argument("--tail", action="store_true", help="print the step's head and tail launches instead of layer 1")
     ap.add_argument("--config", default="c3", choices=["c3", "c2"],
                     help="c2: OPT-125m shape, B=8, 512-id prompts, synthetic p=0.7 drafts (bench --config c2)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "timeline.txt"))
@@ -109,7 +110,11 @@ def main():
             gemm_i = [i for i, l in enumerate(st) if l[0] in (1, 18, 19, 20)]
             lo, hi = (0, min(len(st), 60)) if a.draft else (gemm_i[4], min(len(st), gemm_i[8] + 3))
             prev_end = st[lo - 1][2]
-            for l in st[lo:hi]:
+            seq = list(range(lo, hi))
+            if a.tail:  # the step's first 4 and last 10 launches (embed / LM head / accept)
+                seq = list(range(0, 4)) + list(range(max(4, len(st) - 10), len(st)))
+                prev_end = t_a
+            for l in [st[j] for j in seq]:
                 lines.append(f"  {NAMES[l[0]]:13s} start {(l[1] - t_a) / 1e3:9.1f} dur {(l[2] - l[1]) / 1e3:7.1f} "
                              f"gap {(l[1] - prev_end) / 1e3:6.1f} ctas {l[3]:5d} sms {l[4]:3d} "
                              f"end-after-prev {(l[2] - prev_end) / 1e3:6.1f}")
