@@ -428,31 +428,53 @@ __global__ void __launch_bounds__(256) k_reduce_argmax(const GemmArgs a, const R
     float bv[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
     int bi[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
     bool bad = false;
-    for (int k = 0; k < kArgTiles; ++k) {  // ascending ids per thread: strict > keeps the lowest
-        const int tile = grp * kArgTiles + k;
-        const int m = tile * 256 + row;
-        if (tile >= a.m_tiles) break;
-        int nc;
-        tile_contrib(r, tile, nc);
-        const float* p = a.part + ((size_t)tile * a.max_contrib * 256 + t0) * 256 + row;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int c = 0; c < nc; ++c) {
-            const float* q = p + (size_t)c * 65536;
-            v.x += __ldcg(q);
-            if (nt > 1) v.y += __ldcg(q + 256);
-            if (nt > 2) v.z += __ldcg(q + 512);
-            if (nt > 3) v.w += __ldcg(q + 768);
-        }
-        if (m >= a.vocab) continue;
-        const float vv[4] = {v.x, v.y, v.z, v.w};
+    // Partials of kTB tiles x <= kCB contributors x 4 tokens are loaded before the
+    // first add (one L2 round trip per kTB tiles instead of one per tile and
+    // contributor); each tile still sums its contributors in order from 0
+    constexpr int kTB = 4, kCB = 4;
+    for (int k0 = 0; k0 < kArgTiles; k0 += kTB) {
+        float x[kTB][kCB][4];
+        int ncs[kTB];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            if (i >= nt) break;
-            if (a.logits) a.logits[(size_t)(t0 + i) * a.vocab + m] = vv[i];
-            if (!isfinite(vv[i])) bad = true;
-            if (vv[i] > bv[i]) {
-                bv[i] = vv[i];
-                bi[i] = m;
+        for (int kk = 0; kk < kTB; ++kk) {
+            const int tile = grp * kArgTiles + k0 + kk;
+            ncs[kk] = 0;
+            if (tile < a.m_tiles) tile_contrib(r, tile, ncs[kk]);
+            const float* p = a.part + ((size_t)tile * a.max_contrib * 256 + t0) * 256 + row;
+#pragma unroll
+            for (int c = 0; c < kCB; ++c)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    x[kk][c][i] = (c < ncs[kk] && i < nt) ? __ldcg(p + (size_t)c * 65536 + i * 256) : 0.0f;
+        }
+#pragma unroll
+        for (int kk = 0; kk < kTB; ++kk) {  // ascending ids per thread: strict > keeps the lowest
+            const int tile = grp * kArgTiles + k0 + kk;
+            const int m = tile * 256 + row;
+            if (tile >= a.m_tiles) break;
+            float vv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+            for (int c = 0; c < kCB; ++c)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (c < ncs[kk]) vv[i] += x[kk][c][i];
+            if (ncs[kk] > kCB) {  // more contributors than one batch (not at C2-C5 shapes)
+                const float* p = a.part + ((size_t)tile * a.max_contrib * 256 + t0) * 256 + row;
+                for (int c = kCB; c < ncs[kk]; ++c)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (i < nt) vv[i] += __ldcg(p + (size_t)c * 65536 + i * 256);
+            }
+            if (m >= a.vocab) continue;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (i >= nt) break;
+                if (a.logits) a.logits[(size_t)(t0 + i) * a.vocab + m] = vv[i];
+                if (!isfinite(vv[i])) bad = true;
+                if (vv[i] > bv[i]) {
+                    bv[i] = vv[i];
+                    bi[i] = m;
+                }
             }
         }
     }
