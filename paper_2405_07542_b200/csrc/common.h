@@ -182,9 +182,11 @@ struct Plan {
 // Per-sample ragged descriptor consumed by the attention kernel: the sample's
 // query tokens are qidx[q_start .. q_start + n_q) of the packed stream and its
 // visible KV extent is slots [0, kv_len) (each query still sees only slots
-// <= its own write_slot).
+// <= its own write_slot).  `wide`: the sample's queries are one contiguous run
+// of >= kWideMin tokens (a prompt chunk), attended by the 128-query prefill
+// kernel instead of the 8-query verification kernel (host-planned forwards only).
 struct SampleSeg {
-    int q_start, n_q, kv_len, pad_;
+    int q_start, n_q, kv_len, wide;
 };
 
 // Where a device-described batch lives (written by k_pack or uploaded by the
@@ -195,7 +197,8 @@ struct DeviceBatch {
     const int32_t* dT;   // device token count
     int T_upper;         // grid bound for token-parallel kernels (<= 256)
     int max_kv_upper;    // bound on any sample's kv_len
-    int max_q_upper;     // bound on any sample's query count
+    int max_q_upper;     // bound on any (non-wide) sample's query count
+    int max_wide_q = 0;  // bound on a wide sample's query count (0: no wide samples)
 };
 
 // ---- device entry points (defined in the .cu files) -------------------------

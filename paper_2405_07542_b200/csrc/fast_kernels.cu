@@ -48,7 +48,8 @@ struct FastWorkspace {
     CUtensorMap kv_map64;      // ... with box {64, 64} (attention tail chunks)
     CUtensorMap kv_map32;      // ... with box {64, 32}
     CUtensorMap q_map;         // TMA view of the queries [256][h], one-row boxes {64, 1}
-    int* attn_work = nullptr;  // persistent attention item counters [num_layers], zeroed per forward
+    CUtensorMap q_map128;      // ... with 128-row boxes (prefill kernel)
+    int* attn_work = nullptr;  // persistent attention item counters [2][num_layers], zeroed per forward
     std::vector<void*> allocs;
 };
 
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
     // slot order; its last query ends the sample's extent)
     auto tile_keys = [&](const SampleSeg& g, int qt) {
         const int nq = min(kQT, g.n_q - qt * kQT);
-        if (nq <= 0 || g.kv_len <= 0) return 0;
+        if (nq <= 0 || g.kv_len <= 0 || g.wide) return 0;  // wide runs: k_attention_wide
         if ((qt + 1) * kQT >= g.n_q) return g.kv_len;
         return min(g.kv_len, a.plans[a.qidx[g.q_start + qt * kQT + nq - 1]].write_slot + 1);
     };
@@ -597,6 +598,334 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
 }
 
 
+// ------------------------------------------------------------- prefill attention
+// Long query runs (a prompt chunk: >= kWideMin queries of one sample, packed
+// contiguously) get their own persistent tcgen05 kernel in the usual
+// flash-attention orientation: an item is (sample, head, 128-query tile), the
+// tile's 128 queries are the MMA's M, so every K/V chunk of its causal extent
+// is streamed once per 128 queries instead of once per 8 (the verification
+// kernel above puts the <= 8 queries on N).  A 4k-token prompt re-read its
+// KV 512x per head with 8-query tiles; here 32x.
+//   S = Q K^T     M = 128 queries, N = 128 keys, K = hd   (TMEM, double-buffered)
+//   O += P V      M = 128 queries, N = hd,       K = 128 keys (V read MN-major)
+//   warps 0-3     softmax, thread = query row: two TMEM passes over its S row
+//                 (masked max, then exp2 / row sum / bf16 P into the swizzled
+//                 K-major A tile); lazy reference max (O rescaled in TMEM only
+//                 when the row max grows by more than 2^8); at the item end
+//                 O / l -> the context row.
+//   warp 4        TMA producer: the tile's Q rows (one 128-row box per 64
+//                 columns) and 128-key K/V chunks into a 2-stage ring.
+//   warp 5        TMEM allocation; lane 0 issues S(c+1) before waiting for
+//                 P(c), then O += P(c) V(c).
+// A sample uses this kernel iff its query run in the forward chunk has >=
+// kWideMin tokens and is contiguous (SampleSeg::wide, set on the host), a
+// function of the sample alone: host chunking never splits a sample at a
+// place that depends on the batch (forward_fast).
+constexpr int kWideMin = 64;   // queries of one sample in a chunk -> the prefill kernel
+constexpr int kWQ = 128;       // queries per prefill item (M)
+constexpr int kWStages = 2;
+template <int HD>
+constexpr int kWStageB = 2 * (HD / 64) * kTcKeys * 128;  // K boxes then V boxes
+template <int HD>
+constexpr int kWSmemB = 1024 + (HD / 64) * kWQ * 128 + kWStages * kWStageB<HD> + kWQ * kTcKeys * 2;
+constexpr int kWThreads = 192;
+
+template <int HD>
+__global__ void __launch_bounds__(kWThreads, 1)
+    k_attention_wide(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q128,
+                     AttnArgs a, int qtiles) {
+    CtaTrace trace__(TK_ATTN_WIDE);
+    constexpr int kBoxes = HD / 64;
+    constexpr int kStage = kWStageB<HD>;
+    constexpr int kVOff = kBoxes * kTcKeys * 128;
+    extern __shared__ uint8_t smraw[];
+    uint8_t* sm = smraw + ((1024u - (ptx::smem_u32(smraw) & 1023u)) & 1023u);
+    uint8_t* sQ = sm;                               // [kBoxes][128 rows][128 B]
+    uint8_t* ring = sQ + kBoxes * kWQ * 128;        // [kWStages][K boxes | V boxes]
+    uint8_t* sP = ring + kWStages * kStage;         // [2 k-blocks][128 rows][128 B]
+    __shared__ uint64_t full[kWStages], empty[kWStages], qfull, qempty, sfull[2], pfull, pvdone, ofree;
+    __shared__ int4 s_item;  // {item, chunks, -, -} published by the producer with qfull
+    __shared__ uint32_t tslot;
+    __shared__ uint8_t s_pad[kTcKeys];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, tid = threadIdx.x;
+    const int n_items = a.B * a.heads * qtiles;
+    if (tid == 0) {
+        ptx::prefetch_tmap(&tm_kv);
+        ptx::prefetch_tmap(&tm_q128);
+        for (int i = 0; i < kWStages; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        ptx::mbar_init(&qfull, 1);
+        ptx::mbar_init(&qempty, 5);  // the MMA (its last S read Q) + the 4 softmax warps (read s_item)
+        ptx::mbar_init(&sfull[0], 1);
+        ptx::mbar_init(&sfull[1], 1);
+        ptx::mbar_init(&pfull, 128);
+        ptx::mbar_init(&pvdone, 1);
+        ptx::mbar_init(&ofree, 128);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 5) ptx::tmem_alloc<512>(&tslot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tslot;  // S: cols [0, 128) and [128, 256); O: [256, 256 + HD)
+    pdl_trigger();
+    pdl_wait();  // Q and the chunk's K/V rows come from the QKV epilogue
+
+    // item -> (sample, head, 128-query tile); a tile's keys end at its last query's slot
+    auto decode = [&](int i, int& s, int& head, int& qt) {
+        qt = i % qtiles;
+        const int pair = i / qtiles;
+        s = pair / a.heads;
+        head = pair - s * a.heads;
+    };
+    auto tile_keys = [&](const SampleSeg& g, int qt, int& nq) {
+        nq = min(kWQ, g.n_q - qt * kWQ);
+        if (!g.wide || nq <= 0 || g.kv_len <= 0) return 0;
+        return min(g.kv_len, a.plans[a.qidx[g.q_start + qt * kWQ + nq - 1]].write_slot + 1);
+    };
+
+    if (warp == 4) {
+        if (lane == 0) {  // ------------------------------------------------ producer
+            const uint64_t pol = ptx::policy_evict_first();
+            int st = 0;
+            uint32_t ph = 0, qph = 0;
+            for (int i = atomicAdd(a.work, 1); i < n_items; i = atomicAdd(a.work, 1)) {
+                int s, head, qt, nq;
+                decode(i, s, head, qt);
+                const SampleSeg seg = a.segs[s];
+                const int ext = tile_keys(seg, qt, nq);
+                if (ext <= 0) continue;
+                const int nch = (ext + kTcKeys - 1) / kTcKeys;
+                const int tok0 = a.qidx[seg.q_start + qt * kWQ];  // the run is contiguous (SampleSeg::wide)
+                ptx::mbar_wait(&qempty, qph ^ 1);
+                qph ^= 1;
+                s_item = make_int4(i, nch, 0, 0);
+                ptx::mbar_arrive_expect_tx(&qfull, kBoxes * kWQ * 128);
+#pragma unroll
+                for (int hx = 0; hx < kBoxes; ++hx)
+                    ptx::tma_load_2d(sQ + hx * kWQ * 128, &tm_q128, &qfull, head * HD + hx * 64, tok0, pol);
+                const int row_k = (((a.layer * 2 + 0) * a.B + s) * a.heads + head) * a.cap;
+                const int row_v = (((a.layer * 2 + 1) * a.B + s) * a.heads + head) * a.cap;
+                for (int c = 0; c < nch; ++c) {
+                    ptx::mbar_wait(&empty[st], ph ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[st], 2 * kBoxes * kTcKeys * 128);
+                    uint8_t* b = ring + st * kStage;
+#pragma unroll
+                    for (int bx = 0; bx < kBoxes; ++bx) {
+                        ptx::tma_load_2d(b + bx * kTcKeys * 128, &tm_kv, &full[st], bx * 64, row_k + c * kTcKeys, pol);
+                        ptx::tma_load_2d(b + kVOff + bx * kTcKeys * 128, &tm_kv, &full[st], bx * 64,
+                                         row_v + c * kTcKeys, pol);
+                    }
+                    if (++st == kWStages) {
+                        st = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+            ptx::mbar_wait(&qempty, qph ^ 1);  // end of work
+            s_item = make_int4(-1, 0, 0, 0);
+            ptx::mbar_arrive(&qfull);
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {  // ------------------------------------------------ MMA issuer
+            const uint32_t id_s = ptx::umma_idesc_bf16(kWQ, kTcKeys);
+            const uint32_t id_o = ptx::umma_idesc_bf16(kWQ, HD) | (1u << 16);  // B = V, MN-major
+            const uint32_t qa = ptx::smem_u32(sQ), pa = ptx::smem_u32(sP);
+            int st = 0, items = 0;
+            uint32_t ph = 0, qph = 0, g = 0;  // g: chunks issued so far (S buffers alternate)
+            for (;;) {
+                ptx::mbar_wait(&qfull, qph);
+                qph ^= 1;
+                const int4 it = s_item;
+                if (it.x < 0) break;
+                const int nch = it.y;
+                auto issue_s = [&](int stc, uint32_t phc, uint32_t gg) {
+                    ptx::mbar_wait(&full[stc], phc);
+                    ptx::tc_fence_after();
+                    const uint32_t ka = ptx::smem_u32(ring + stc * kStage);
+#pragma unroll
+                    for (int k = 0; k < HD / 16; ++k)
+                        ptx::umma_bf16(tmem + (gg & 1) * kTcKeys,
+                                       ptx::umma_desc_kmajor_sw128(qa + (k / 4) * (kWQ * 128) + (k % 4) * 32),
+                                       ptx::umma_desc_kmajor_sw128(ka + (k / 4) * (kTcKeys * 128) + (k % 4) * 32),
+                                       id_s, k > 0 ? 1u : 0u);
+                    ptx::umma_commit(&sfull[gg & 1]);
+                };
+                int stn = st;
+                uint32_t phn = ph;
+                issue_s(stn, phn, g);
+                if (++stn == kWStages) {
+                    stn = 0;
+                    phn ^= 1;
+                }
+                for (int c = 0; c < nch; ++c) {
+                    const uint32_t gc = g + c;
+                    if (c + 1 < nch) {  // S(c+1) overlaps the softmax of chunk c
+                        issue_s(stn, phn, gc + 1);
+                        if (++stn == kWStages) {
+                            stn = 0;
+                            phn ^= 1;
+                        }
+                    } else {
+                        ptx::umma_commit(&qempty);  // every S of the item issued: Q may be replaced
+                    }
+                    ptx::mbar_wait(&pfull, gc & 1);  // P(c) written (and S(c) read)
+                    if (c == 0 && items > 0) ptx::mbar_wait(&ofree, (items - 1) & 1);  // O of the last item read
+                    ptx::tc_fence_after();
+                    const uint32_t va = ptx::smem_u32(ring + st * kStage + kVOff);
+#pragma unroll
+                    for (int k = 0; k < kTcKeys / 16; ++k)
+                        ptx::umma_bf16(tmem + 256, ptx::umma_desc_kmajor_sw128(pa + (k / 4) * (kWQ * 128) + (k % 4) * 32),
+                                       ptx::umma_desc_mn_sw128(va + k * 16 * 128, kTcKeys * 128, 1024), id_o,
+                                       (c > 0 || k > 0) ? 1u : 0u);
+                    ptx::umma_commit(&empty[st]);
+                    ptx::umma_commit(&pvdone);
+                    if (++st == kWStages) {
+                        st = 0;
+                        ph ^= 1;
+                    }
+                }
+                g += nch;
+                ++items;
+            }
+        }
+    } else {  // ------------------------------------------------------------ softmax warps
+        uint32_t qph = 0, g = 0;
+        int items = 0;
+        const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+        const int r = tid;  // query row of the tile
+        for (;;) {
+            ptx::mbar_wait(&qfull, qph);
+            qph ^= 1;
+            const int4 it = s_item;
+            __syncwarp();
+            if (it.x >= 0 && lane == 0) ptx::mbar_arrive(&qempty);
+            if (it.x < 0) break;
+            int s, head, qt, nq;
+            decode(it.x, s, head, qt);
+            const SampleSeg seg = a.segs[s];
+            const int nch = it.y;
+            tile_keys(seg, qt, nq);
+            const int tok = r < nq ? a.qidx[seg.q_start + qt * kWQ + r] : -1;
+            const int ws = tok >= 0 ? a.plans[tok].write_slot : -1;  // sees keys <= its own slot
+            const int lim = min(ws + 1, seg.kv_len);
+            float mref = -INFINITY, l = 0.0f;
+            for (int c = 0; c < nch; ++c) {
+                const uint32_t gc = g + c;
+                const int k0 = c * kTcKeys;
+                if (a.pad) {  // padded grid: this chunk's hole flags
+                    ptx::named_bar_sync(1, 128);  // the previous chunk's flags were read
+                    s_pad[r] = (k0 + r < a.cap) ? a.pad[(size_t)s * a.cap + k0 + r] : 1;
+                    ptx::named_bar_sync(1, 128);
+                }
+                ptx::mbar_wait(&sfull[gc & 1], (gc >> 1) & 1);
+                ptx::tc_fence_after();
+                const uint32_t sb = trow + (gc & 1) * kTcKeys;
+                // pass 1: masked row max
+                float cm = -INFINITY;
+#pragma unroll
+                for (int j0 = 0; j0 < kTcKeys; j0 += 16) {
+                    float x[16];
+                    ptx::tmem_ld16(sb + j0, x);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int kk = k0 + j0 + j;
+                        if (kk < lim && !(a.pad && s_pad[j0 + j])) cm = fmaxf(cm, x[j] * a.scale_log2);
+                    }
+                }
+                float alpha = 1.0f;
+                bool rescale = false;
+                if (cm > mref + 8.0f) {  // lazy: keep the reference unless the max grows by > 2^8
+                    if (mref != -INFINITY) {
+                        alpha = exp2f(mref - cm);
+                        rescale = true;
+                    }
+                    mref = cm;
+                }
+                if (c > 0) ptx::mbar_wait(&pvdone, (gc - 1) & 1);  // PV(c-1) done: P free, O current
+                // O row *= alpha.  tcgen05.ld / st are warp-collective (.sync.aligned):
+                // the whole warp takes the branch when any of its rows rescales
+                if (__any_sync(0xffffffffu, rescale) && c > 0) {
+                    ptx::tc_fence_after();
+#pragma unroll
+                    for (int d0 = 0; d0 < HD; d0 += 8) {
+                        float o[8];
+                        ptx::tmem_ld8(trow + 256 + d0, o);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) o[j] *= alpha;
+                        ptx::tmem_st8(trow + 256 + d0, o);
+                    }
+                }
+                // pass 2: p = 2^(s - mref) (0 where masked) -> bf16 P row, row sum
+                float ls = 0.0f;
+#pragma unroll
+                for (int j0 = 0; j0 < kTcKeys; j0 += 16) {
+                    float x[16];
+                    ptx::tmem_ld16(sb + j0, x);
+                    uint32_t pk[8];
+#pragma unroll
+                    for (int j = 0; j < 16; j += 2) {
+                        float p2[2];
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int kk = k0 + j0 + j + u;
+                            const bool ok = kk < lim && !(a.pad && s_pad[j0 + j + u]);
+                            p2[u] = ok ? exp2f(x[j + u] * a.scale_log2 - mref) : 0.0f;
+                            ls += p2[u];
+                        }
+                        __nv_bfloat162 b2 = __floats2bfloat162_rn(p2[0], p2[1]);
+                        pk[j / 2] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                    // keys j0..j0+15 = 16-byte chunks (j0 % 64) / 8 and +1 of k-block j0 / 64
+                    uint8_t* rowp = sP + (j0 / 64) * (kWQ * 128) + r * 128;
+                    const int c0 = (j0 % 64) / 8;
+                    *(uint4*)(rowp + (((c0) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    *(uint4*)(rowp + (((c0 + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                }
+                l = l * alpha + ls;
+                ptx::fence_proxy_async_smem();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&pfull);
+            }
+            // item end: O / l -> the context row
+            const uint32_t gl = g + nch - 1;
+            ptx::mbar_wait(&pvdone, gl & 1);
+            ptx::tc_fence_after();
+            float o[HD];
+#pragma unroll
+            for (int d0 = 0; d0 < HD; d0 += 8) {
+                float t8[8];
+                ptx::tmem_ld8(trow + 256 + d0, t8);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) o[d0 + j] = t8[j];
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&ofree);
+            if (tok >= 0) {
+                const float inv = 1.0f / l;
+                uint4* dst = (uint4*)(a.ctx + (size_t)tok * a.h + head * HD);
+#pragma unroll
+                for (int d0 = 0; d0 < HD; d0 += 8) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int j = 0; j < 8; j += 2) {
+                        __nv_bfloat162 b2 = __floats2bfloat162_rn(o[d0 + j] * inv, o[d0 + j + 1] * inv);
+                        w[j / 2] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                    dst[d0 / 8] = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            }
+            g += nch;
+            ++items;
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 5) ptx::tmem_dealloc<512>(tmem);
+}
+
 template <typename T>
 T* walloc(FastWorkspace* f, size_t n) {
     T* p = (T*)dmalloc(sizeof(T) * (n ? n : 1));
@@ -636,7 +965,8 @@ FastWorkspace* ensure_fast(const Model& m, const Cache& c, Workspace& ws) {
     f->kv_map64 = make_tmap_2d(c.kv, (int64_t)cfg.num_layers * 2 * c.B * cfg.num_heads * c.cap, cfg.head_dim, 64);
     f->kv_map32 = make_tmap_2d(c.kv, (int64_t)cfg.num_layers * 2 * c.B * cfg.num_heads * c.cap, cfg.head_dim, 32);
     f->q_map = make_tmap_2d(f->q, (int64_t)T, (int64_t)h, 1);
-    f->attn_work = walloc<int>(f, (size_t)cfg.num_layers);
+    f->q_map128 = make_tmap_2d(f->q, (int64_t)T, (int64_t)h, 128);
+    f->attn_work = walloc<int>(f, 2 * (size_t)cfg.num_layers);  // [verify kernel | prefill kernel] per layer
     ws.fast = f;
     return f;
 }
@@ -653,6 +983,17 @@ void launch_attention(const AttnArgs& at, const CUtensorMap& kv, const CUtensorM
     else
         launch_k(k_attention_tcp<64>, dim3((unsigned)std::min<long long>(items, 2LL * sms)), dim3(kPThreads),
                  kPSmemB<64>, st, kv, kv64, kv32, qm, at, qtiles);
+}
+
+// Prefill kernel over the batch's wide samples (grid: one CTA per SM at most).
+void launch_attention_wide(const AttnArgs& at, const CUtensorMap& kv, const CUtensorMap& q128, int hd, int wtiles,
+                           cudaStream_t st) {
+    const long long items = (long long)at.B * at.heads * wtiles;
+    const unsigned grid = (unsigned)std::min<long long>(items, device_sm_count());
+    if (hd == 128)
+        launch_k(k_attention_wide<128>, dim3(grid), dim3(kWThreads), kWSmemB<128>, st, kv, q128, at, wtiles);
+    else
+        launch_k(k_attention_wide<64>, dim3(grid), dim3(kWThreads), kWSmemB<64>, st, kv, q128, at, wtiles);
 }
 
 }  // namespace
@@ -724,6 +1065,8 @@ void prepare_fast_kernels() {
     if (!first_use_on_device(1)) return;
     CUDA_OK(cudaFuncSetAttribute(k_attention_tcp<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
     CUDA_OK(cudaFuncSetAttribute(k_attention_tcp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmemB<64>));
+    CUDA_OK(cudaFuncSetAttribute(k_attention_wide<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmemB<128>));
+    CUDA_OK(cudaFuncSetAttribute(k_attention_wide<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmemB<64>));
     gemm_prepare();
 }
 
@@ -757,7 +1100,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     base.plans = dplans;
     base.kv = (__nv_bfloat16*)c.kv;
 
-    CUDA_OK(cudaMemsetAsync(f->attn_work, 0, sizeof(int) * (size_t)cfg.num_layers, st));
+    CUDA_OK(cudaMemsetAsync(f->attn_work, 0, sizeof(int) * 2 * (size_t)cfg.num_layers, st));
     PROF(PK_ROW, launch_k(k_embed_ln, dim3(n), dim3(kRowThreads), 0, st, (const __nv_bfloat16*)m.tok16,
                           (const __nv_bfloat16*)m.pos16, tokens, dplans, h, resid, (const float*)m.layers[0].ln1_g,
                           (const float*)m.layers[0].ln1_b, f->xb, (const int*)db.dT,
@@ -820,6 +1163,12 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         at.pre_ok = 0;
         PROF(PK_ATTN, launch_attention(at, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, hd, qtiles, db.max_kv_upper,
                                        st));
+        if (db.max_wide_q > 0) {  // prompt runs of >= kWideMin queries: the 128-query prefill kernel
+            AttnArgs aw = at;
+            aw.work = f->attn_work + cfg.num_layers + l;
+            PROF(PK_ATTN, launch_attention_wide(aw, f->kv_map, f->q_map128, hd, (db.max_wide_q + kWQ - 1) / kWQ, st));
+            launches++;
+        }
         // O projection + residual -> residual tile statistics
         g = cb;
         g.M = h;
@@ -886,6 +1235,12 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         at.pre_ok = g.grid == sms ? 1 : 0;  // the QKV GEMM above held every SM
         PROF(PK_ATTN, launch_attention(at, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, hd, qtiles, db.max_kv_upper,
                                        st));
+        if (db.max_wide_q > 0) {  // prompt runs of >= kWideMin queries: the 128-query prefill kernel
+            AttnArgs aw = at;
+            aw.work = f->attn_work + cfg.num_layers + l;
+            PROF(PK_ATTN, launch_attention_wide(aw, f->kv_map, f->q_map128, hd, (db.max_wide_q + kWQ - 1) / kWQ, st));
+            launches++;
+        }
         launches++;
         // O projection + residual, fused with LN2 -> xb
         g = base;
@@ -998,27 +1353,74 @@ void forward_fast(const Model& m, Cache& c, Workspace& ws, int T, bool want_logi
     std::vector<Plan> plans(T);
     CUDA_OK(cudaMemcpyAsync(plans.data(), ws.d_plans, sizeof(Plan) * T, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
-    for (int t0 = 0; t0 < T; t0 += kChunkTokens) {
-        int n = std::min(kChunkTokens, T - t0);
+    // Chunks of <= kChunkTokens tokens.  When every sample's tokens form one
+    // contiguous run of the stream (every prefill, concatenate_inputs), chunks
+    // break only between samples or at multiples of kChunkTokens from a
+    // sample's own first token, so how a sample is cut -- and so which
+    // attention kernel sees each of its runs (SampleSeg::wide) -- depends on
+    // the sample alone, never on the batch around it.  Otherwise: fixed cuts.
+    std::vector<int> cuts{0};
+    {
+        std::vector<int> first(c.B, -1), last(c.B, -1);
+        bool contiguous = true;
+        for (int i = 0; i < T && contiguous; ++i) {
+            const int s = plans[i].sample;
+            if (first[s] < 0) first[s] = i;
+            else if (last[s] != i - 1) contiguous = false;
+            last[s] = i;
+        }
+        if (contiguous) {
+            int start = 0;  // current chunk start
+            for (int i = 0; i < T;) {
+                const int s = plans[i].sample, run_end = last[s] + 1;
+                int p = i;
+                while (p < run_end) {
+                    const int piece = std::min(kChunkTokens, run_end - p);
+                    if (p + piece - start > kChunkTokens) {  // does not fit: close the chunk first
+                        cuts.push_back(p);
+                        start = p;
+                    }
+                    p += piece;
+                    if (piece == kChunkTokens) {  // a full piece of a long run is a chunk of its own
+                        cuts.push_back(p);
+                        start = p;
+                    }
+                }
+                i = run_end;
+            }
+        } else {
+            for (int t0 = kChunkTokens; t0 < T; t0 += kChunkTokens) cuts.push_back(t0);
+        }
+        if (cuts.back() != T) cuts.push_back(T);
+    }
+    for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+        const int t0 = cuts[k], n = cuts[k + 1] - t0;
+        if (n <= 0) continue;
         std::vector<SampleSeg> segs(c.B, SampleSeg{0, 0, 0, 0});
         std::vector<std::vector<int>> per(c.B);
         for (int i = 0; i < n; ++i) per[plans[t0 + i].sample].push_back(i);
         std::vector<int32_t> qidx;
-        int max_kv = 0, max_q = 0;
+        int max_kv = 0, max_q = 0, max_wide = 0;
         for (int s = 0; s < c.B; ++s) {
             segs[s].q_start = (int)qidx.size();
             segs[s].n_q = (int)per[s].size();
-            for (int i : per[s]) {
+            bool run = segs[s].n_q >= kWideMin;
+            for (size_t j = 0; j < per[s].size(); ++j) {
+                const int i = per[s][j];
                 qidx.push_back(i);
                 segs[s].kv_len = std::max(segs[s].kv_len, plans[t0 + i].write_slot + 1);
+                if (j > 0 && (i != per[s][j - 1] + 1 || plans[t0 + i].write_slot <= plans[t0 + i - 1].write_slot))
+                    run = false;  // the prefill kernel needs a contiguous run in slot order
             }
+            segs[s].wide = run ? 1 : 0;
             max_kv = std::max(max_kv, segs[s].kv_len);
-            max_q = std::max(max_q, segs[s].n_q);
+            if (run) max_wide = std::max(max_wide, segs[s].n_q);
+            else max_q = std::max(max_q, segs[s].n_q);
         }
         CUDA_OK(cudaMemcpyAsync(ws.d_segs, segs.data(), sizeof(SampleSeg) * c.B, cudaMemcpyHostToDevice, st));
         CUDA_OK(cudaMemcpyAsync(ws.d_qidx, qidx.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
         CUDA_OK(cudaMemcpyAsync(ws.d_T, &n, sizeof(int), cudaMemcpyHostToDevice, st));
-        DeviceBatch db{ws.d_segs, ws.d_qidx, ws.d_T, n, max_kv, max_q};
+        DeviceBatch db{ws.d_segs, ws.d_qidx, ws.d_T, n, max_kv, std::max(1, max_q), max_wide};
         forward_fast_dev(m, c, ws, db, t0, want_logits, st);
         CUDA_OK(cudaStreamSynchronize(st));  // host vectors above are reused per chunk
     }
@@ -1043,18 +1445,22 @@ extern "C" int sd_debug_attention(const uint16_t* q, const uint16_t* kv, int B, 
     };
     try {
         SD_CHECK(hd == 64 || hd == 128, CONFIG, "head_dim 64 or 128");
-        int T = 0, max_kv = 0, max_q = 0;
+        int T = 0, max_kv = 0, max_q = 0, max_wide = 0;
         std::vector<SampleSeg> segs(B);
         std::vector<int32_t> qidx;
         std::vector<Plan> plans;
         for (int s = 0; s < B; ++s) {
-            segs[s] = SampleSeg{T, n_q[s], kv_len[s], 0};
+            // a run of >= kWideMin queries in slot order goes to the prefill kernel, as in forward_fast
+            bool wide = n_q[s] >= kWideMin;
+            for (int i = 1; i < n_q[s]; ++i) wide = wide && write_slot[T + i] > write_slot[T + i - 1];
+            segs[s] = SampleSeg{T, n_q[s], kv_len[s], wide ? 1 : 0};
             for (int i = 0; i < n_q[s]; ++i, ++T) {
                 qidx.push_back(T);
                 plans.push_back(Plan{s, write_slot[T], write_slot[T], 1});
             }
             max_kv = std::max(max_kv, kv_len[s]);
-            max_q = std::max(max_q, n_q[s]);
+            if (wide) max_wide = std::max(max_wide, n_q[s]);
+            else max_q = std::max(max_q, n_q[s]);
         }
         SD_CHECK(T >= 1 && T <= 256, CONFIG, "1..256 query rows");
         const int h = heads * hd;
@@ -1091,7 +1497,8 @@ extern "C" int sd_debug_attention(const uint16_t* q, const uint16_t* kv, int B, 
         at.cap = cap;
         at.layer = 0;
         at.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
-        const int qtiles = (max_q + kQT - 1) / kQT;
+        const int qtiles = std::max(1, (max_q + kQT - 1) / kQT);
+        const CUtensorMap mq128 = make_tmap_2d(dq, T, h, 128);
         cudaEvent_t e0, e1;
         CUDA_OK(cudaEventCreate(&e0));
         CUDA_OK(cudaEventCreate(&e1));
@@ -1100,6 +1507,11 @@ extern "C" int sd_debug_attention(const uint16_t* q, const uint16_t* kv, int B, 
             at.work = work;
             CUDA_OK(cudaEventRecord(e0));
             launch_attention(at, m128, m64, m32, mq, hd, qtiles, max_kv, 0);
+            if (max_wide > 0) {
+                AttnArgs aw = at;
+                aw.work = work + 1;
+                launch_attention_wide(aw, m128, mq128, hd, (max_wide + kWQ - 1) / kWQ, 0);
+            }
             CUDA_OK(cudaEventRecord(e1));
             CUDA_OK(cudaDeviceSynchronize());
         }

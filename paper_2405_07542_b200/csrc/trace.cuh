@@ -20,7 +20,7 @@ struct TraceRec {
 enum TraceKid : uint32_t {
     TK_GEMM = 1, TK_RED_STORE, TK_RED_GELU, TK_RED_QKV, TK_RED_RESID, TK_LN_ROWS, TK_ARGMAX,
     TK_EMBED_LN, TK_ATTN, TK_ATTN_COMBINE, TK_PREDICT, TK_PACK, TK_ACCEPT, TK_PAD_FILL,
-    TK_DRAFT_PACK, TK_DRAFT_TAKE, TK_DRAFT_COMMIT, TK_GEMM_CL_QKV, TK_GEMM_CL_GELU, TK_GEMM_CL_RESID,
+    TK_DRAFT_PACK, TK_DRAFT_TAKE, TK_DRAFT_COMMIT, TK_GEMM_CL_QKV, TK_GEMM_CL_GELU, TK_GEMM_CL_RESID, TK_ATTN_WIDE,
     // trace points (kid >= 100): one record, tag = payload
     TK_ATTN_BYTES = 110,  // per attention CTA: algorithmic K/V bytes >> 10
 };
@@ -68,7 +68,7 @@ struct TraceBuf {
             t0 = rec ? globaltimer() : 0;                                                 \
         }                                                                                 \
         /* phase record from any thread (kid >= 100), free when tracing is off */         \
-        __device__ __forceinline__ void point(uint32_t pk, uint32_t tag) const {          \
+        template <int = 0> __device__ __forceinline__ void point(uint32_t pk, uint32_t tag) const { \
             if (rec) trace_point(pk, tag);                                                \
         }                                                                                 \
         __device__ __forceinline__ ~CtaTrace() {                                          \

@@ -141,6 +141,38 @@ def test_attention_batch_composition_invariance(sd, hd, heads):
         assert np.array_equal(alone, whole[r0:r0 + n_q[s]]), s
 
 
+@pytest.mark.parametrize("hd,heads", [(128, 2), (64, 4)])
+@pytest.mark.parametrize("padded", [False, True])
+def test_prefill_attention_wide_runs_vs_float64(sd, hd, heads, padded):
+    """(a') Prompt runs of >= 64 queries go to the 128-query prefill kernel
+    (k_attention_wide: queries as the MMA's M, each K/V chunk streamed once per
+    128 queries) in the same launch sequence as the verification kernel's
+    samples: a full 128-query tile at the end of a 4200-key extent (33
+    chunks, lazy rescale), a 64-query run that spans a chunk boundary, next
+    to 40-, 8- and 1-query samples (verification kernel) and an empty one.  Same float64 reference
+    and tolerance as (a); deterministic; a wide sample alone gives the same
+    bits as inside the batch."""
+    rng = np.random.default_rng(hd + 3 * heads + padded)
+    extents = [4200, 700, 1100, 129, 64, 600]
+    nqs = [128, 64, 8, 1, 0, 40]
+    q, kv, n_q, kv_len, ws, pad, cap = make_attention_case(rng, extents, nqs, heads, hd, padded)
+    out, us = run_attention(sd, q, kv, n_q, kv_len, ws, pad, heads, hd, cap)
+    ref = attention_ref(q, kv, n_q, kv_len, ws, pad, heads, hd)
+    got = from_bf16_bits(out).astype(np.float64)
+    err = np.abs(got - ref)
+    print(f"wide hd={hd} padded={padded}: max|err|={err.max():.2e} mean={err.mean():.2e} ({us:.1f} us)")
+    assert np.isfinite(got).all()
+    assert err.max() <= 1e-2 and err.mean() <= 1e-3
+    out2, _ = run_attention(sd, q, kv, n_q, kv_len, ws, pad, heads, hd, cap)
+    assert np.array_equal(out, out2)
+    if not padded:
+        for s in (0, 1):
+            r0 = sum(n_q[:s])
+            alone, _ = run_attention(sd, q[r0:r0 + n_q[s]], np.ascontiguousarray(kv[:, s:s + 1]), [n_q[s]],
+                                     [kv_len[s]], ws[r0:r0 + n_q[s]], None, heads, hd, cap)
+            assert np.array_equal(alone, out[r0:r0 + n_q[s]]), s
+
+
 # ------------------------------------------------------------------ (b)
 SHAPES = [(15360, 5120), (5120, 5120), (20480, 5120), (5120, 20480), (50432, 5120), (12288, 4096), (4096, 16384)]
 
@@ -180,9 +212,10 @@ def test_c3_layer_truncated_forward_vs_float64(sd):
 
 # ------------------------------------------------------------------ (d)
 def test_long_prompt_prefill_vs_float64(sd):
-    """(d) Prefill of 600-700-token prompts (3 forward chunks of 256 tokens;
-    attention items of 8 queries, each tile stopping at its own causal
-    limit) on the unpadded arena and on the left-padded vanilla grid,
+    """(d) Prefill of 600-700-token prompts (forward chunks of <= 256 tokens cut
+    at multiples of 256 from each prompt's start; the 128-query prefill
+    attention kernel on runs of >= 64 queries) on the unpadded arena and on
+    the left-padded vanilla grid,
     at the C3 width (L = 2): the stated bf16 tolerance on sampled rows and
     argmax agreement over every prompt row."""
     from torch_ref import prefill_parity

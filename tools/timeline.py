@@ -118,6 +118,13 @@ def main():
                 lines.append(f"  {NAMES[l[0]]:13s} start {(l[1] - t_a) / 1e3:9.1f} dur {(l[2] - l[1]) / 1e3:7.1f} "
                              f"gap {(l[1] - prev_end) / 1e3:6.1f} ctas {l[3]:5d} sms {l[4]:3d} "
                              f"end-after-prev {(l[2] - prev_end) / 1e3:6.1f}")
+                if l[0] in (2, 3, 4, 5, 6, 7, 9):  # per-CTA entry / exit spread (us after the predecessor's end)
+                    r = rec[(rec["kid"] == l[0]) & (rec["t0"] >= l[1]) & (rec["t1"] <= l[2])]
+                    if len(r):
+                        en = (r["t0"].astype(np.int64) - prev_end) / 1e3
+                        ex = (r["t1"].astype(np.int64) - prev_end) / 1e3
+                        q = lambda v: "/".join(f"{x:.1f}" for x in np.percentile(v, [10, 50, 90, 100]))
+                        lines.append(f"      ctas {len(r)}: entry p10/50/90/max {q(en)} | exit {q(ex)}")
                 if l[0] in (18, 19, 20):  # cluster GEMM phases (trace points 120-125), us after the predecessor's end
                     epi = {18: 3, 19: 2, 20: 1}[l[0]]
                     pts = rec[(rec["kid"] >= 120) & (rec["kid"] <= 127) & (rec["t0"] >= l[1]) & (rec["t0"] <= l[2])
