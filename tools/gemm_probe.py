@@ -35,7 +35,7 @@ variants = ([("gemm", 0), ("stream", 8)] if not probe else
 for name in only:
     M, K = shapes[name]
     W = rng.integers(0, 1 << 15, size=(M, K), dtype=np.uint16) & 0x3FFF
-    for T in (48, 112, 192):
+    for T in [int(x) for x in os.environ.get("TS", "48,112,192").split(",")]:
         X = rng.integers(0, 1 << 15, size=(T, K), dtype=np.uint16) & 0x3FFF
         Y = np.zeros((T, M), np.float32)
         res = []
