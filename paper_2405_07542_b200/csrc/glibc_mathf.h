@@ -16,6 +16,18 @@
 //   * tanhf — fdlibm s_tanhf.c as shipped in glibc 2.39 (no ifunc variant).
 //   * expm1f — fdlibm s_expm1f.c as shipped in glibc 2.39 (no ifunc variant).
 //
+// Upstream notices for the restated algorithms and constants:
+//   * expf: ARM optimized-routines (github.com/ARM-software/optimized-routines,
+//     math/expf.c, math/exp2f_data.c), Copyright (c) 2017-2018 Arm Limited,
+//     SPDX-License-Identifier: MIT OR Apache-2.0 WITH LLVM-exception -- the
+//     upstream glibc imports; the 32-entry 2^(i/32) table below is its
+//     __exp2f_data.tab.
+//   * tanhf, expm1f: fdlibm, "Copyright (C) 1993 by Sun Microsystems, Inc.
+//     All rights reserved.  Developed at SunPro, a Sun Microsystems, Inc.
+//     business.  Permission to use, copy, modify, and distribute this software
+//     is freely granted, provided that this notice is preserved."  (float
+//     versions by Ian Lance Taylor, Cygnus Support.)
+//
 // Every operation is spelled out with explicit round-to-nearest intrinsics on
 // the device (no FMA contraction) so the result does not depend on nvcc's
 // -fmad setting.  The same header compiles as plain C on the host; the host
