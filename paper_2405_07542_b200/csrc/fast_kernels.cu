@@ -233,7 +233,9 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
     // O^T rows 64-127 duplicate rows 0-63 and are never stored
     constexpr uint32_t kVLbo = HD == 128 ? kTcKeys * 128 : 0;
     extern __shared__ uint8_t smraw[];
-    uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+    // 1024-aligned by pointer arithmetic on the __shared__ array: the softmax's
+    // sS / sP accesses stay shared-memory instructions (not generic LD / ST)
+    uint8_t* sm = smraw + ((1024u - (ptx::smem_u32(smraw) & 1023u)) & 1023u);
     uint8_t* ring = sm;                                  // [kPS][K 2 boxes | V 2 boxes]
     uint8_t* qring = ring + kPS * kPStage;               // [kPQ][2 atoms of 8 x 128 B]
     uint8_t* sP = qring + kPQ * 2048;                    // [2][2 atoms of 8 x 128 B]

@@ -1,7 +1,7 @@
 """Untraced ms per verify step of the C2 device loop (OPT-125m shape, B=8,
 512-id prompts, synthetic p=0.7 drafts): same-box A/B of SD_* settings.
 
-  python tools/c2time.py [--draft]     # --draft: the C4 draft model's own forward, B=24
+  python tools/c2time.py [--lib path/to/other/libspecdec_b200.so]
 """
 import os
 import sys
@@ -13,6 +13,10 @@ sys.path.insert(0, ROOT)
 from paper_2405_07542_b200 import specdec as sd  # noqa: E402
 import bench  # noqa: E402
 
+args = sys.argv[1:]
+if "--lib" in args:  # A/B against another build of the library
+    i = args.index("--lib")
+    sd.LIB_PATH = os.path.abspath(args[i + 1])
 cfg, B = bench.C2, 8
 m = sd.Model.init(sd.ModelConfig(**cfg), device=0, precision=sd.BF16)
 prompts = bench.prompts_for(range(B), cfg["vocab_size"], 512, 512)
@@ -27,5 +31,6 @@ for _ in range(6):
     s.reset()
     steps, ms = s.run()
     best = min(best, ms / steps)
-env = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("SD_"))
+env = " ".join([f"{k}={v}" for k, v in os.environ.items() if k.startswith("SD_")] +
+               ([os.path.relpath(sd.LIB_PATH, ROOT)] if "--lib" in args else []))
 print(f"[{env or 'default'}] C2 B={B}: {steps} steps, best {best:.4f} ms/step", flush=True)
