@@ -362,6 +362,7 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                 }
             }
             pdl_wait();
+            trace__.point(130, blockIdx.x);  // phase records (timeline.py): dependency released
             for (;;) {
                 const int i = next;
                 if (i >= n_items) break;
@@ -431,6 +432,7 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                 int stn = st;  // ring position of the next S
                 uint32_t phn = ph;
                 issue_s(0, stn, phn);
+                if (items == 0) trace__.point(131, blockIdx.x);  // first S issued (Q and K chunk 0 landed)
                 if (++stn == kPS) {
                     stn = 0;
                     phn ^= 1;
@@ -507,6 +509,7 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                 const uint32_t g = gc + c;
                 const int key = c * kTcKeys + tid;
                 ptx::mbar_wait(&sfull[g & 1], (g >> 1) & 1);
+                if (g == 0 && tid == 0) trace__.point(132, blockIdx.x);  // first S ready
                 ptx::tc_fence_after();
                 float x[kQT];
                 ptx::tmem_ld8(trow + (g & 1) * 8, x);
@@ -590,6 +593,7 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
                 const int tok = a.qidx[seg.q_start + qt * kQT + q];
                 if (tid < HD) a.ctx[(size_t)tok * a.h + head * HD + tid] = __float2bfloat16_rn(o[q] / sL[q]);
             }
+            if (items == 0 && tid == 0) trace__.point(133, (uint32_t)nch << 20 | blockIdx.x);  // first item done
             gc += nch;
             ++items;
         }

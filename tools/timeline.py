@@ -125,6 +125,18 @@ def main():
                         ex = (r["t1"].astype(np.int64) - prev_end) / 1e3
                         q = lambda v: "/".join(f"{x:.1f}" for x in np.percentile(v, [10, 50, 90, 100]))
                         lines.append(f"      ctas {len(r)}: entry p10/50/90/max {q(en)} | exit {q(ex)}")
+                if l[0] == 9:  # attention phases of each CTA's first item (trace points 130-133)
+                    pts = rec[(rec["kid"] >= 130) & (rec["kid"] <= 133) & (rec["t0"] >= l[1]) & (rec["t0"] <= l[2])]
+                    row = []
+                    for k, nm in ((130, "dep"), (131, "S0 issued"), (132, "S0 ready"), (133, "item done")):
+                        v = pts[pts["kid"] == k]
+                        if len(v):
+                            d = (v["t0"].astype(np.int64) - prev_end) / 1e3
+                            row.append(f"{nm} {np.median(d):5.1f}/{d.max():5.1f}")
+                    v = pts[pts["kid"] == 133]
+                    if len(v):
+                        row.append(f"chunks/item {np.median(v['blk'] >> 20):.0f}")
+                    lines.append("      phases (median/max): " + " | ".join(row))
                 if l[0] in (18, 19, 20):  # cluster GEMM phases (trace points 120-125), us after the predecessor's end
                     epi = {18: 3, 19: 2, 20: 1}[l[0]]
                     pts = rec[(rec["kid"] >= 120) & (rec["kid"] <= 127) & (rec["t0"] >= l[1]) & (rec["t0"] <= l[2])
