@@ -174,7 +174,50 @@ __global__ void __launch_bounds__(kClThreads, 1)
     const int m0 = tile * 128 + lane * 4;
     const float4 bias = a.bias ? *(const float4*)(a.bias + m0) : make_float4(0.f, 0.f, 0.f, 0.f);
     pdl_wait();
-    const int T = min(max((a.dT ? *a.dT : a.T) - a.t_base, 0), box);  // this launch's tokens
+    // The token count and the token operand are fetched in the same round trip:
+    // operand rows are read up to the host bound on this launch's tokens (rows
+    // >= T are stale and never leave the CTA: the MMA uses N = BN, the owners
+    // reduce only t < T)
+    const int T_raw = a.dT ? *a.dT : a.T;
+    constexpr int kU = 4;
+    float4 xr[kU][2];
+    float2 st[8];
+    const int per_h = box * 8, total_h = nkb * per_h;  // 16-byte chunks of the LN_IN operand
+    const int T_h = min(box, a.T - a.t_base);  // host bound on the rows that exist in this chunk
+    const int i_0 = threadIdx.x / per_h, r_0 = threadIdx.x - i_0 * per_h;
+    if constexpr (LN_IN) {
+        // chunk idx = threadIdx.x + u * 256 -> (k-block i, token t, 16-byte chunk c),
+        // advanced incrementally (no integer division in the loops)
+        int ci = i_0, cr = r_0;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int idx = threadIdx.x + u * kClThreads;
+            const int i = ci, t = cr >> 3, c = cr & 7;
+            cr += kClThreads;
+            while (cr >= per_h) {
+                cr -= per_h;
+                ++ci;
+            }
+            if (idx < total_h && t < T_h) {
+                const float4* x = (const float4*)(a.x_resid + (size_t)(a.t_base + t) * a.hidden + (kb0 + i) * 64 + c * 8);
+                xr[u][0] = x[0];
+                xr[u][1] = x[1];
+            }
+        }
+        if (threadIdx.x < T_h) {
+            const float2* p = a.stats_in + (size_t)(a.t_base + threadIdx.x) * a.n_stat;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < a.n_stat) st[j] = p[j];
+        }
+    } else if (threadIdx.x == 0) {
+        const CUtensorMap* tmB = box == 32 ? &tmB32 : box == 64 ? &tmB64 : &tmB128;
+        const uint64_t pol_x = ptx::policy_evict_last();
+        ptx::mbar_arrive_expect_tx(&s_full_b, (uint32_t)(nkb * box * 128));
+        for (int i = 0; i < nkb; ++i)
+            ptx::tma_load_2d(Bt + i * box * 128, tmB, &s_full_b, (kb0 + i) * 64, a.t_base, pol_x);
+    }
+    const int T = min(max(T_raw - a.t_base, 0), box);  // this launch's tokens
     const int BN = T <= 16 ? 16 : ((T + 15) / 16) * 16;
     const bool idle = T <= 0;
     const int own0 = rank * per_owner;
@@ -193,38 +236,10 @@ __global__ void __launch_bounds__(kClThreads, 1)
     if (!idle) {
         if constexpr (LN_IN) {
             // LN(x) -> bf16 in the 128B-swizzled K-major layout TMA would
-            // produce (16-byte chunk c of row t at chunk c ^ (t & 7)).  The x
-            // loads of up to four chunks per thread are issued together with the
-            // per-token statistics (Chan combination of the producer's per-tile
-            // (sum, M2) in tile order: deterministic): one L2 round trip.
-            const int per = BN * 8, total = nkb * per;
-            constexpr int kU = 4;
-            float4 xr[kU][2];
-            // chunk idx = threadIdx.x + u * 256 -> (k-block i, token t, 16-byte chunk c),
-            // advanced incrementally (no integer division in the loops)
-            const int i_0 = threadIdx.x / per, r_0 = threadIdx.x - i_0 * per;
-            int ci = i_0, cr = r_0;
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const int idx = threadIdx.x + u * kClThreads;
-                const int i = ci, t = cr >> 3, c = cr & 7;
-                cr += kClThreads;
-                while (cr >= per) {
-                    cr -= per;
-                    ++ci;
-                }
-                if (idx < total && t < T) {
-                    const float4* x = (const float4*)(a.x_resid + (size_t)(a.t_base + t) * a.hidden + (kb0 + i) * 64 + c * 8);
-                    xr[u][0] = x[0];
-                    xr[u][1] = x[1];
-                }
-            }
+            // produce (16-byte chunk c of row t at chunk c ^ (t & 7)); per-token
+            // statistics: Chan combination of the producer's per-tile (sum, M2)
+            // in tile order (deterministic)
             if (threadIdx.x < T) {
-                const float2* p = a.stats_in + (size_t)(a.t_base + threadIdx.x) * a.n_stat;
-                float2 st[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (j < a.n_stat) st[j] = p[j];
                 float sm = 0.0f;
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
@@ -241,20 +256,19 @@ __global__ void __launch_bounds__(kClThreads, 1)
                 s_rs[threadIdx.x] = rsqrtf(m2 / a.hidden + 1e-5f);
             }
             __syncthreads();
-            ci = i_0;
-            cr = r_0;
-            for (int u0 = 0; u0 * kClThreads < total; u0 += kU) {
+            int ci = i_0, cr = r_0;
+            for (int u0 = 0; u0 * kClThreads < total_h; u0 += kU) {
 #pragma unroll
                 for (int u = 0; u < kU; ++u) {
                     const int idx = threadIdx.x + (u0 + u) * kClThreads;
-                    if (idx >= total) break;
+                    if (idx >= total_h) break;
                     const int i = ci, t = cr >> 3, c = cr & 7;
                     cr += kClThreads;
-                    while (cr >= per) {
-                        cr -= per;
+                    while (cr >= per_h) {
+                        cr -= per_h;
                         ++ci;
                     }
-                    if (u0 > 0 && t < T) {  // chunks beyond the first four (BN * nkb > 128)
+                    if (u0 > 0 && t < T) {  // chunks beyond the first four per thread (box * nkb > 128)
                         const float4* x = (const float4*)(a.x_resid + (size_t)(a.t_base + t) * a.hidden + (kb0 + i) * 64 + c * 8);
                         xr[u][0] = x[0];
                         xr[u][1] = x[1];
@@ -276,13 +290,6 @@ __global__ void __launch_bounds__(kClThreads, 1)
             ptx::fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
             __syncthreads();
             if (threadIdx.x == 0) trace__.point(121, ttag);
-        } else if (threadIdx.x == 0) {
-            const int box_d = BN <= 32 ? 32 : BN <= 64 ? 64 : 128;
-            const CUtensorMap* tmB = box_d == 32 ? &tmB32 : box_d == 64 ? &tmB64 : &tmB128;
-            const uint64_t pol_x = ptx::policy_evict_last();
-            ptx::mbar_arrive_expect_tx(&s_full_b, (uint32_t)(nkb * box_d * 128));
-            for (int i = 0; i < nkb; ++i)
-                ptx::tma_load_2d(Bt + i * box * 128, tmB, &s_full_b, (kb0 + i) * 64, a.t_base, pol_x);
         }
         if (threadIdx.x == 32) {  // ---------------- MMA issuer
             const uint32_t idesc = ptx::umma_idesc_bf16(128, BN);
@@ -327,8 +334,9 @@ __global__ void __launch_bounds__(kClThreads, 1)
                 if (lane == 0) trace__.point(123, ttag);
             }
         }
-    } else if (threadIdx.x == 0) {
-        for (int i = 0; i < nkb; ++i) ptx::mbar_wait(&s_full_a[i], 0);  // no TMA in flight at exit
+    } else if (threadIdx.x == 0) {  // no TMA in flight at exit
+        for (int i = 0; i < nkb; ++i) ptx::mbar_wait(&s_full_a[i], 0);
+        if (!LN_IN) ptx::mbar_wait(&s_full_b, 0);
     }
     ptx::mbar_wait(&s_recv, 0);  // every sender's rows of this CTA's tokens have landed
     __syncwarp();
