@@ -378,7 +378,10 @@ def cpu_reference_steps(cfg, n_steps, procs, warmup=0, layers=1):
 
     fx = json.load(open(STEPS_FIXTURE))
     steps = fx["steps"]
-    pick = [steps[int(i)] for i in np.linspace(0, len(steps) - 1, n_steps + warmup).round()]
+    # timed steps spread evenly over the whole trajectory (early steps: every sample
+    # active, short contexts; late ones: long contexts), warm-up on the first step
+    timed = [steps[int(i)] for i in np.linspace(0, len(steps) - 1, n_steps).round()]
+    pick = [timed[0]] * warmup + timed
     lib, kind = _ref_lib()  # loaded in the parent, inherited by the forked workers
     _REF_STATE.clear()
     _REF_STATE["lib"] = lib
