@@ -35,11 +35,18 @@
 // launches per GEMM over token halves, t_base = 0 / 128: the weights of a
 // small model stay in L2 between them).
 //
+// At most half the SMs per launch (so a launch and its PDL-overlapped
+// successor fit side by side, one CTA per SM); C2: QKV 18 tiles x CS 4, O 6 x
+// 12, FC 24 x 3, PROJ 6 x 12.
+//
 // Warp roles (256 threads): thread 0 TMA (weights before griddepcontrol.wait,
-// tokens after), warp 1 TMEM allocation + lane 0 MMA issue, warps 4-7 push
-// their TMEM rows straight into the owning CTA's shared memory
-// (st.shared::cluster; one cluster barrier), all 8 warps the LN_IN operand
-// build and the owner-side reduction + epilogue.
+// tokens after, fetched with the token count in one round trip), warp 1 TMEM
+// allocation + lane 0 MMA issue, warps 4-7 copy their TMEM rows to shared
+// memory and lane r of warp 4 ships owner r's run with one bulk copy, all 8
+// warps the LN_IN operand build and the owner-side reduction + epilogue.  A
+// relaxed cluster barrier at entry (barrier inits visible) and an
+// arrive (all incoming copies landed) / wait (before exit) pair are the only
+// cluster-wide synchronisation.
 #include <cuda_bf16.h>
 
 #include <algorithm>
