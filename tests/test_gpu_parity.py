@@ -226,3 +226,19 @@ def test_long_prompt_prefill_vs_float64(sd):
         assert s["max_abs_over_std"] <= 0.15, layout
         assert s["mean_abs_over_std"] <= 0.03, layout
         assert s["argmax_agree"] >= 0.9 and s["argmax_agree_all_rows"] >= 0.9, layout
+
+
+def test_compact_model_long_prompt_prefill_vs_float64(sd):
+    """(d') The same on a small model (C2 / C4-draft shape, L = 2): the
+    cluster-GEMM layer path (two 128-token launches per 256-token chunk) and
+    the 128-query prefill attention at head_dim 64, unpadded arena and the
+    left-padded vanilla grid, against the float64 reference."""
+    from torch_ref import prefill_parity
+
+    cfg = dict(num_layers=2, num_heads=12, head_dim=64, vocab_size=50272, max_positions=2048, init_seed=7)
+    st = prefill_parity(sd, cfg=cfg, B=3, lo=150, hi=300, seed=5, every=7)
+    print("compact prefill bf16 vs float64:", st)
+    for layout, s in st.items():
+        assert s["max_abs_over_std"] <= 0.15, layout
+        assert s["mean_abs_over_std"] <= 0.03, layout
+        assert s["argmax_agree"] >= 0.9 and s["argmax_agree_all_rows"] >= 0.9, layout
