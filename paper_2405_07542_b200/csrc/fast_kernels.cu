@@ -277,6 +277,10 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
     // the producer); otherwise every warp waits first.
     __shared__ int s_order[256];
     const bool lpt = a.B <= 256;
+    // the producer's first work item: the counter is zeroed before the forward
+    // (not by a predecessor kernel), so its round trip overlaps the dependency wait
+    int first_item = 0;
+    if (tid == 128) first_item = atomicAdd(a.work, 1);
     if (!a.pre_ok) pdl_wait();
     if (lpt)
         for (int x = tid; x < a.B; x += kPThreads) {
@@ -318,7 +322,7 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
             const uint64_t pol = ptx::policy_evict_first();
             int st = 0, qs = 0;
             uint32_t ph = 0, qph = 0;
-            int next = atomicAdd(a.work, 1);
+            int next = first_item;
             unsigned long long algo = 0;
             // Before griddepcontrol.wait: K/V rows of positions committed in EARLIER
             // steps cannot change, and -- when the QKV GEMM ran one CTA on EVERY SM
