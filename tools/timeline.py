@@ -34,7 +34,7 @@ def main():
     ap.add_argument("--mode", default="ems")
     ap.add_argument("--draft", action="store_true", help="C4: OPT-125m-shaped draft model, k=4")
     ap.add_argument("--tail", action="store_true", help="print the step's head and tail launches instead of layer 1")
-    ap.add_argument("--config", default="c3", choices=["c3", "c2"],
+    ap.add_argument("--config", default="c3", choices=["c3", "c2", "c5"],
                     help="c2: OPT-125m shape, B=8, 512-id prompts, synthetic p=0.7 drafts (bench --config c2)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "timeline.txt"))
     a = ap.parse_args()
@@ -44,11 +44,11 @@ def main():
     L = sd.lib()
     L.sd_debug_trace_begin.argtypes = [C.c_int]
     L.sd_debug_trace_end.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_int)]
-    cfg = bench.C2 if a.config == "c2" else bench.C3
-    if a.config == "c2" and "--batch" not in sys.argv:
+    cfg = {"c2": bench.C2, "c5": bench.C5}.get(a.config, bench.C3)
+    if a.config in ("c2", "c5") and "--batch" not in sys.argv:
         a.batch = 8
     m = sd.Model.init(sd.ModelConfig(**cfg), device=0, precision=sd.BF16)
-    lo_hi = (512, 512) if a.config == "c2" else (600, 900)
+    lo_hi = {"c2": (512, 512), "c5": (3968, 4224)}.get(a.config, (600, 900))
     prompts = bench.prompts_for(range(a.batch), cfg["vocab_size"], *lo_hi)
     cap = max(len(p) for p in prompts) + 128 + 9 if a.mode == "ems" else cfg["max_positions"]
     if a.draft:
