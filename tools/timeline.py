@@ -125,6 +125,14 @@ def main():
                         ex = (r["t1"].astype(np.int64) - prev_end) / 1e3
                         q = lambda v: "/".join(f"{x:.1f}" for x in np.percentile(v, [10, 50, 90, 100]))
                         lines.append(f"      ctas {len(r)}: entry p10/50/90/max {q(en)} | exit {q(ex)}")
+                        if l[0] in (3, 4, 5) and len(r) > 20:  # reductions: who is slow (grid x = tile, y = group)
+                            gx = {4: 60, 3: 80, 5: 20}[l[0]] if a.config == "c3" else None
+                            if gx:
+                                slow = r[ex >= np.percentile(ex, 90)]
+                                ys = (slow["blk"] // gx).astype(int)
+                                xs = (slow["blk"] % gx).astype(int)
+                                lines.append(f"      slowest 10%: y {np.bincount(ys).nonzero()[0].tolist()} "
+                                             f"x {sorted(set(xs.tolist()))[:40]} sms {len(set(slow['smid'].tolist()))}")
                 if l[0] == 9:  # attention phases of each CTA's first item (trace points 130-133)
                     pts = rec[(rec["kid"] >= 130) & (rec["kid"] <= 133) & (rec["t0"] >= l[1]) & (rec["t0"] <= l[2])]
                     row = []
