@@ -10,6 +10,9 @@
 //   specdec::ModelConfig, TokenPlan, greedy_next, Model                       model.hpp:14-103
 //   specdec::CacheArena, UnpadArena, PaddedGrid                               kv_cache.hpp:68-168
 //   specdec::VerifyResult, verify                                             engine.hpp:82-90
+//   specdec::Mode, PredictorKind, EngineConfig, SampleStep, StepRecord,
+//     RunMetrics, DecodeResult, make_step_record, compute_metrics,
+//     decode_greedy, decode_speculative, results_json                         engine.hpp:15-110
 //
 //   specdec::LedgerStep, WriteLedger, padding_ratio                           kv_cache.hpp:13-62
 //   specdec::softmax, LayerWeights, Model weight accessors                     model.hpp:27-32, 48, 81-87
@@ -29,6 +32,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -544,6 +548,386 @@ inline VerifyResult verify(const std::vector<LogitsRow>& rows, const TokenSequen
     }
     r.tau = static_cast<int>(r.accepted.size());
     return r;
+}
+
+// ------------------------------------------------------------ engine (engine.hpp:15-110)
+// The reference's decoding entry points over sd_decode (the library's engine:
+// prefill, then the verify-step loop of engine.cpp:391-489 with the
+// predictors on the host, every forward on the GPU), plus the host-side
+// bookkeeping of engine.cpp (step records, metrics, the JSON run report).
+enum class Mode { greedy, vanilla, ems };
+enum class PredictorKind { draft, retrieval, synthetic };
+
+inline Mode mode_from_string(const std::string& name) {
+    if (name == "greedy") return Mode::greedy;
+    if (name == "vanilla") return Mode::vanilla;
+    if (name == "ems") return Mode::ems;
+    throw ConfigError("unknown mode '" + name + "' (greedy, vanilla, ems)");
+}
+inline std::string to_string(Mode mode) {
+    return mode == Mode::greedy ? "greedy" : mode == Mode::vanilla ? "vanilla" : "ems";
+}
+inline PredictorKind predictor_from_string(const std::string& name) {
+    if (name == "draft") return PredictorKind::draft;
+    if (name == "retrieval") return PredictorKind::retrieval;
+    if (name == "synthetic") return PredictorKind::synthetic;
+    throw ConfigError("unknown predictor '" + name + "' (draft, retrieval, synthetic)");
+}
+inline std::string to_string(PredictorKind kind) {
+    return kind == PredictorKind::draft ? "draft" : kind == PredictorKind::retrieval ? "retrieval" : "synthetic";
+}
+
+struct EngineConfig {
+    Mode mode = Mode::ems;
+    PredictorKind predictor = PredictorKind::draft;
+    int k = 4;
+    int match_len = 2;
+    int copy_len = 7;
+    int batch_size = 1;
+    int max_new_tokens = 64;
+    bool stop_on_eos = true;
+    uint64_t seed = 1;
+    double synthetic_accuracy = 0.8;
+
+    // engine.cpp:48-58
+    void validate() const {
+        if (predictor != PredictorKind::retrieval && k < 1) throw ConfigError("k must be >= 1");
+        if (match_len < 1) throw ConfigError("match_len must be >= 1");
+        if (copy_len < 1) throw ConfigError("copy_len must be >= 1");
+        if (batch_size < 1) throw ConfigError("batch_size must be >= 1");
+        if (max_new_tokens < 0) throw ConfigError("max_new_tokens must be >= 0");
+        if (!(synthetic_accuracy >= 0.0 && synthetic_accuracy < 1.0))
+            throw ConfigError("synthetic accuracy must lie in [0, 1)");
+    }
+    sd_engine_config c() const {
+        sd_engine_config e{};
+        e.mode = static_cast<int32_t>(mode);
+        e.predictor = static_cast<int32_t>(predictor);
+        e.k = k;
+        e.match_len = match_len;
+        e.copy_len = copy_len;
+        e.batch_size = batch_size;
+        e.max_new_tokens = max_new_tokens;
+        e.stop_on_eos = stop_on_eos ? 1 : 0;
+        e.seed = seed;
+        e.synthetic_accuracy = synthetic_accuracy;
+        e.sample_id_base = 0;
+        return e;
+    }
+};
+
+struct SampleStep {
+    int sample = 0;
+    int k = 0;
+    int input_padding = 0;
+    int tau = 0;
+    int kv_padding = 0;
+    bool clipped = false;
+};
+
+struct StepRecord {
+    std::vector<SampleStep> samples;
+    int tau_max = 0;
+    double delta_bar = 0.0;
+    double r_bar = 0.0;
+};
+
+struct RunMetrics {
+    int decode_steps = 0;
+    std::vector<int64_t> tokens_generated;
+    int64_t total_tokens_generated = 0;
+    double avg_acceptance_length = 0.0;
+    double avg_padding_ratio = 0.0;
+    int64_t total_input_padding = 0;
+    int64_t total_kv_padding = 0;
+    int64_t useful_kv_writes = 0;
+    int64_t padding_kv_writes = 0;
+    int64_t real_tokens_processed = 0;
+    int64_t pad_tokens_processed = 0;
+    int64_t total_tokens_processed = 0;
+    double prefill_seconds = 0.0;
+    double decode_seconds = 0.0;
+    double tokens_per_second_decode = 0.0;
+    double tokens_per_second_total = 0.0;
+};
+
+struct DecodeResult {
+    std::vector<TokenSequence> generated_tokens;
+    std::vector<std::string> texts;
+    std::vector<StepRecord> steps;
+    RunMetrics metrics;
+    std::string ledger_json;
+};
+
+// engine.cpp:78-105
+inline StepRecord make_step_record(const std::vector<int>& sample_ids, const std::vector<int>& ks,
+                                   const std::vector<int>& taus, const std::vector<bool>& clipped) {
+    const size_t n = sample_ids.size();
+    if (n < 1) throw ContractError("a step needs at least one sample");
+    if (ks.size() != n || taus.size() != n || clipped.size() != n)
+        throw ContractError("per-sample step lists differ in length");
+    int k_max = 0, tau_max = 0;
+    double tau_sum = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        if (ks[i] < 0) throw ContractError("negative draft count");
+        if (taus[i] < 1 || taus[i] > ks[i] + 1) throw ContractError("acceptance length outside [1, k + 1]");
+        k_max = std::max(k_max, ks[i]);
+        tau_max = std::max(tau_max, taus[i]);
+        tau_sum += taus[i];
+    }
+    StepRecord r;
+    r.samples.resize(n);
+    for (size_t i = 0; i < n; ++i)
+        r.samples[i] = SampleStep{sample_ids[i], ks[i], k_max - ks[i], taus[i], tau_max - taus[i], clipped[i]};
+    r.tau_max = tau_max;
+    r.delta_bar = tau_max - tau_sum / static_cast<double>(n);
+    r.r_bar = r.delta_bar / static_cast<double>(tau_max);
+    return r;
+}
+
+// engine.cpp:107-126
+inline RunMetrics compute_metrics(const std::vector<StepRecord>& records) {
+    RunMetrics m;
+    m.decode_steps = static_cast<int>(records.size());
+    if (records.empty()) return m;
+    int64_t events = 0;
+    double tau_sum = 0.0, ratio_sum = 0.0;
+    for (const StepRecord& rec : records) {
+        for (const SampleStep& s : rec.samples) {
+            tau_sum += s.tau;
+            m.total_input_padding += s.input_padding;
+            m.total_kv_padding += s.kv_padding;
+            ++events;
+        }
+        ratio_sum += rec.r_bar;
+    }
+    m.avg_acceptance_length = tau_sum / static_cast<double>(events);
+    m.avg_padding_ratio = ratio_sum / static_cast<double>(records.size());
+    return m;
+}
+
+namespace b200 {
+inline std::string text_without_specials(const TokenSequence& tokens) {  // engine.cpp:148-155
+    TokenSequence bytes;
+    for (TokenId t : tokens)
+        if (!tok::is_special(t)) bytes.push_back(t);
+    return tok::detokenize(bytes);
+}
+
+// sd_decode, then the reference's result assembly (engine.cpp:206-289, 291-528)
+inline DecodeResult run_decode(const std::vector<std::string>& prompts, const EngineConfig& config,
+                               const Model& target, const Model* draft) {
+    const int b = config.batch_size;
+    std::vector<int32_t> flat, lens;
+    for (const std::string& p : prompts) {  // engine.cpp:136-145: BOS + byte tokens
+        flat.push_back(tok::kBos);
+        for (TokenId t : tok::tokenize(p)) flat.push_back(t);
+        lens.push_back(static_cast<int32_t>(tok::tokenize(p).size() + 1));
+    }
+    const int mx = std::max(config.max_new_tokens, 1);
+    std::vector<int32_t> gen(static_cast<size_t>(b) * mx), cnt(b);
+    const int64_t cap = static_cast<int64_t>(b) * (config.max_new_tokens + 2) + 16;
+    std::vector<int32_t> rec(static_cast<size_t>(cap) * 6);
+    int64_t n_rec = 0, ledger[2] = {0, 0};
+    double timing[2] = {0.0, 0.0};
+    const sd_engine_config c = config.c();
+    check(sd_decode(&c, target.handle(), draft ? draft->handle() : nullptr, flat.data(), lens.data(), gen.data(),
+                    cnt.data(), rec.data(), cap, &n_rec, ledger, timing));
+
+    DecodeResult out;
+    out.metrics.tokens_generated.assign(b, 0);
+    for (int s = 0; s < b; ++s) {
+        TokenSequence g(gen.begin() + static_cast<size_t>(s) * mx, gen.begin() + static_cast<size_t>(s) * mx + cnt[s]);
+        out.texts.push_back(text_without_specials(g));
+        out.generated_tokens.push_back(std::move(g));
+        out.metrics.tokens_generated[s] = cnt[s];
+        out.metrics.total_tokens_generated += cnt[s];
+    }
+    RunMetrics& m = out.metrics;
+    m.prefill_seconds = timing[0];
+    m.decode_seconds = timing[1];
+    m.useful_kv_writes = ledger[0];
+    m.padding_kv_writes = ledger[1];
+    std::string led = "[]";
+    if (config.max_new_tokens > 0 && config.mode == Mode::greedy) {  // engine.cpp:259-287
+        for (int s = 0; s < b; ++s) {
+            m.real_tokens_processed += lens[s] + cnt[s] - 1;
+            m.decode_steps = std::max(m.decode_steps, cnt[s] - 1);
+        }
+        m.avg_acceptance_length = 1.0;
+        m.total_tokens_processed = m.real_tokens_processed;
+    } else if (config.max_new_tokens > 0) {  // engine.cpp:486-528
+        // step records: rows {step, sample, k, tau, clipped, 0}, grouped by step
+        for (int64_t i = 0; i < n_rec;) {
+            const int step = rec[i * 6];
+            std::vector<int> ids, ks, taus;
+            std::vector<bool> clips;
+            for (; i < n_rec && rec[i * 6] == step; ++i) {
+                ids.push_back(rec[i * 6 + 1]);
+                ks.push_back(rec[i * 6 + 2]);
+                taus.push_back(rec[i * 6 + 3]);
+                clips.push_back(rec[i * 6 + 4] != 0);
+            }
+            out.steps.push_back(make_step_record(ids, ks, taus, clips));
+        }
+        const RunMetrics agg = compute_metrics(out.steps);
+        m.decode_steps = agg.decode_steps;
+        m.avg_acceptance_length = agg.avg_acceptance_length;
+        m.avg_padding_ratio = agg.avg_padding_ratio;
+        m.total_input_padding = agg.total_input_padding;
+        m.total_kv_padding = agg.total_kv_padding;
+        for (int s = 0; s < b; ++s) m.real_tokens_processed += lens[s];
+        led = "[";
+        for (size_t i = 0; i < out.steps.size(); ++i) {  // WriteLedger::dump_json (kv_cache.cpp:53-62)
+            const StepRecord& r = out.steps[i];
+            int64_t pad = 0, useful = 0;
+            std::string taus = "[";
+            for (size_t j = 0; j < r.samples.size(); ++j) {
+                const SampleStep& x = r.samples[j];
+                m.real_tokens_processed += 1 + x.k;
+                useful += 1 + x.k;
+                if (config.mode == Mode::vanilla) pad += x.kv_padding;
+                taus += (j ? "," : "") + std::to_string(x.tau);
+            }
+            led += std::string(i ? "," : "") + "{\"tau_list\":" + taus + "],\"tau_max\":" + std::to_string(r.tau_max) +
+                   ",\"pad_writes\":" + std::to_string(pad) + ",\"useful_writes\":" + std::to_string(useful) + "}";
+        }
+        led += "]";
+        if (config.mode == Mode::vanilla) m.pad_tokens_processed = m.total_input_padding + m.total_kv_padding;
+        m.total_tokens_processed = m.real_tokens_processed + m.pad_tokens_processed;
+    }
+    if (m.decode_seconds > 0.0) m.tokens_per_second_decode = m.total_tokens_generated / m.decode_seconds;
+    const double wall = m.prefill_seconds + m.decode_seconds;
+    if (wall > 0.0) m.tokens_per_second_total = m.total_tokens_generated / wall;
+    out.ledger_json = led;
+    return out;
+}
+
+// JSON string: controls escaped, valid UTF-8 passed through, every byte that
+// does not start a well-formed sequence replaced by U+FFFD (what the
+// reference's dump does with error_handler_t::replace)
+inline std::string json_string(const std::string& v) {
+    std::string o = "\"";
+    const size_t n = v.size();
+    for (size_t i = 0; i < n;) {
+        const unsigned char c = static_cast<unsigned char>(v[i]);
+        if (c < 0x80) {
+            switch (c) {
+                case '"': o += "\\\""; break;
+                case '\\': o += "\\\\"; break;
+                case '\n': o += "\\n"; break;
+                case '\t': o += "\\t"; break;
+                case '\r': o += "\\r"; break;
+                default:
+                    if (c < 0x20) {
+                        char buf[8];
+                        std::snprintf(buf, sizeof buf, "\\u%04x", c);
+                        o += buf;
+                    } else {
+                        o += static_cast<char>(c);
+                    }
+            }
+            ++i;
+            continue;
+        }
+        const size_t len = (c >= 0xC2 && c <= 0xDF) ? 2 : (c >= 0xE0 && c <= 0xEF) ? 3 : (c >= 0xF0 && c <= 0xF4) ? 4 : 0;
+        bool ok = len > 0 && i + len <= n;
+        for (size_t j = 1; ok && j < len; ++j) ok = (static_cast<unsigned char>(v[i + j]) & 0xC0) == 0x80;
+        if (ok) {  // no overlong forms, surrogates or code points above U+10FFFF
+            const unsigned char c1 = static_cast<unsigned char>(v[i + 1]);
+            ok = !(c == 0xE0 && c1 < 0xA0) && !(c == 0xED && c1 > 0x9F) && !(c == 0xF0 && c1 < 0x90) &&
+                 !(c == 0xF4 && c1 > 0x8F);
+        }
+        if (ok) {
+            o.append(v, i, len);
+            i += len;
+        } else {
+            o += "\xEF\xBF\xBD";
+            ++i;
+        }
+    }
+    return o + "\"";
+}
+inline std::string json_double(double v) {
+    char buf[32];
+    std::snprintf(buf, sizeof buf, "%.17g", v);
+    return buf;
+}
+}  // namespace b200
+
+// engine.cpp:206-289
+inline DecodeResult decode_greedy(const std::vector<std::string>& prompts, const EngineConfig& config,
+                                  const Model& target) {
+    config.validate();
+    if (static_cast<int>(prompts.size()) != config.batch_size)
+        throw ContractError("prompt count does not match batch_size");
+    EngineConfig g = config;
+    g.mode = Mode::greedy;
+    return b200::run_decode(prompts, g, target, nullptr);
+}
+
+// engine.cpp:291-528
+inline DecodeResult decode_speculative(const std::vector<std::string>& prompts, const EngineConfig& config,
+                                       const Model& target, const Model* draft) {
+    config.validate();
+    if (config.mode != Mode::vanilla && config.mode != Mode::ems)
+        throw ConfigError("speculative decoding needs the vanilla or ems mode");
+    if (static_cast<int>(prompts.size()) != config.batch_size)
+        throw ContractError("prompt count does not match batch_size");
+    return b200::run_decode(prompts, config, target, draft);
+}
+
+// engine.cpp:531-587: config, outputs, metrics, steps and the write ledger.
+inline std::string results_json(const EngineConfig& config, const DecodeResult& result) {
+    using b200::json_double;
+    using b200::json_string;
+    const RunMetrics& m = result.metrics;
+    std::string o = "{\n  \"config\": {";
+    o += "\"mode\": " + json_string(to_string(config.mode)) + ", \"predictor\": " +
+         json_string(to_string(config.predictor)) + ", \"k\": " + std::to_string(config.k) +
+         ", \"match_len\": " + std::to_string(config.match_len) + ", \"copy_len\": " + std::to_string(config.copy_len) +
+         ", \"batch_size\": " + std::to_string(config.batch_size) +
+         ", \"max_new_tokens\": " + std::to_string(config.max_new_tokens) +
+         ", \"stop_on_eos\": " + (config.stop_on_eos ? "true" : "false") + ", \"seed\": " + std::to_string(config.seed) +
+         ", \"synthetic_accuracy\": " + json_double(config.synthetic_accuracy) + "},\n  \"outputs\": [";
+    for (size_t s = 0; s < result.generated_tokens.size(); ++s) {
+        o += std::string(s ? ", " : "") + "{\"tokens\": [";
+        for (size_t j = 0; j < result.generated_tokens[s].size(); ++j)
+            o += std::string(j ? ", " : "") + std::to_string(result.generated_tokens[s][j]);
+        o += "], \"text\": " + json_string(s < result.texts.size() ? result.texts[s] : std::string()) + "}";
+    }
+    o += "],\n  \"metrics\": {\"decode_steps\": " + std::to_string(m.decode_steps) + ", \"tokens_generated\": [";
+    for (size_t s = 0; s < m.tokens_generated.size(); ++s)
+        o += std::string(s ? ", " : "") + std::to_string(m.tokens_generated[s]);
+    o += "], \"total_tokens_generated\": " + std::to_string(m.total_tokens_generated) +
+         ", \"avg_acceptance_length\": " + json_double(m.avg_acceptance_length) +
+         ", \"avg_padding_ratio\": " + json_double(m.avg_padding_ratio) +
+         ", \"total_input_padding\": " + std::to_string(m.total_input_padding) +
+         ", \"total_kv_padding\": " + std::to_string(m.total_kv_padding) +
+         ", \"useful_kv_writes\": " + std::to_string(m.useful_kv_writes) +
+         ", \"padding_kv_writes\": " + std::to_string(m.padding_kv_writes) +
+         ", \"real_tokens_processed\": " + std::to_string(m.real_tokens_processed) +
+         ", \"pad_tokens_processed\": " + std::to_string(m.pad_tokens_processed) +
+         ", \"total_tokens_processed\": " + std::to_string(m.total_tokens_processed) +
+         ", \"prefill_seconds\": " + json_double(m.prefill_seconds) +
+         ", \"decode_seconds\": " + json_double(m.decode_seconds) +
+         ", \"tokens_per_second_decode\": " + json_double(m.tokens_per_second_decode) +
+         ", \"tokens_per_second_total\": " + json_double(m.tokens_per_second_total) + "},\n  \"steps\": [";
+    for (size_t i = 0; i < result.steps.size(); ++i) {
+        const StepRecord& r = result.steps[i];
+        o += std::string(i ? ", " : "") + "{\"samples\": [";
+        for (size_t j = 0; j < r.samples.size(); ++j) {
+            const SampleStep& x = r.samples[j];
+            o += std::string(j ? ", " : "") + "{\"sample\": " + std::to_string(x.sample) + ", \"k\": " +
+                 std::to_string(x.k) + ", \"input_padding\": " + std::to_string(x.input_padding) +
+                 ", \"tau\": " + std::to_string(x.tau) + ", \"kv_padding\": " + std::to_string(x.kv_padding) +
+                 ", \"clipped\": " + (x.clipped ? "true" : "false") + "}";
+        }
+        o += "], \"tau_max\": " + std::to_string(r.tau_max) + ", \"delta_bar\": " + json_double(r.delta_bar) +
+             ", \"r_bar\": " + json_double(r.r_bar) + "}";
+    }
+    o += "],\n  \"ledger\": " + (result.ledger_json.empty() ? std::string("[]") : result.ledger_json) + "\n}";
+    return o;
 }
 
 }  // namespace specdec

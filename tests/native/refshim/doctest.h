@@ -2,7 +2,7 @@
 // reference's hot-path unit tests (/root/reference/proj/tests/test_ragged.cpp,
 // test_kv_cache.cpp, test_model.cpp) recompile unmodified against
 // include/specdec_b200.hpp.  Covers the subset those files use: TEST_CASE,
-// CHECK, CHECK_FALSE, REQUIRE, CHECK_THROWS_AS, doctest::Approx(...).epsilon().
+// CHECK, CHECK_FALSE, REQUIRE, REQUIRE_MESSAGE, CHECK_THROWS_AS, doctest::Approx(...).epsilon().
 // With DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN defined it also provides main(),
 // which runs every test case and exits non-zero on any failed assertion.
 #pragma once
@@ -81,6 +81,7 @@ private:
 #define CHECK_FALSE(...) \
     ::doctest::detail::report(!static_cast<bool>(__VA_ARGS__), "!(" #__VA_ARGS__ ")", __FILE__, __LINE__, false)
 #define REQUIRE(...) ::doctest::detail::report(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__, true)
+#define REQUIRE_MESSAGE(cond, msg) ::doctest::detail::report(static_cast<bool>(cond), msg, __FILE__, __LINE__, true)
 #define CHECK_THROWS_AS(expr, ...)                                                              \
     do {                                                                                        \
         bool doctest_ok_ = false;                                                               \

@@ -1,10 +1,11 @@
 """The reference's own hot-path unit suites (proj/tests/test_ragged.cpp,
-test_kv_cache.cpp, test_model.cpp + support/naive_model.cpp), recompiled
+test_kv_cache.cpp, test_model.cpp, test_engine.cpp + support/naive_model.cpp), recompiled
 unmodified against our C++ layer include/specdec_b200.hpp with a
 doctest-compatible harness (tests/native/Makefile, binaries in
 tests/native/_reftests/, built by __graft_entry__.build() where the reference
 sources exist).  Every TEST_CASE must pass on the B200; the host-only cases
-(ragged batching, the WriteLedger protocol) also run here without a GPU."""
+(ragged batching, the WriteLedger protocol, verify / step records / metric
+aggregation) also run here without a GPU."""
 import os
 import subprocess
 
@@ -39,8 +40,17 @@ def test_kv_cache_ledger_cases_pass_without_gpu(sd):
         assert cases.get(name), name
 
 
+def test_engine_host_cases_pass_without_gpu(sd):
+    _, cases = run_suite("test_engine")
+    for name in ("verification accepts the longest matching prefix plus one",
+                 "step records turn k and tau lists into alignment shortfalls",
+                 "metric aggregation matches an independent accumulation"):
+        assert cases.get(name), name
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite,n_cases", [("test_ragged", 7), ("test_kv_cache", 18), ("test_model", 15)])
+@pytest.mark.parametrize("suite,n_cases", [("test_ragged", 7), ("test_kv_cache", 18), ("test_model", 15),
+                                           ("test_engine", 13)])
 def test_reference_suite_passes_on_b200(sd, suite, n_cases):
     r, cases = run_suite(suite)
     assert len(cases) == n_cases, r.stdout
