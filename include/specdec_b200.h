@@ -240,6 +240,21 @@ int sd_verify_step_wait(sd_cache* c, int32_t* tau, int32_t* accepted, int32_t* c
  * restores the model's internal stream). */
 int sd_cache_set_stream(sd_cache* c, void* stream);
 
+/* ---- predictors (predictors.hpp:13-20, predictors.cpp) ------------------- */
+/* draft_predict: greedy k-token rollout of `draft` after `context` (a fresh
+ * one-sample arena per call); out[k].  ContractError for k < 1 or an empty
+ * context, CapacityError when context + k exceeds max_positions. */
+int sd_draft_predict(sd_model* draft, const int32_t* context, int n, int k, int32_t* out);
+/* retrieval_predict (LLMA prompt lookup): copy <= copy_len tokens that followed
+ * the rightmost earlier occurrence of the last match_len tokens; out[copy_len],
+ * *n_out tokens written (0 when nothing matches). */
+int sd_retrieval_predict(const int32_t* context, int n, int match_len, int copy_len, int32_t* out, int32_t* n_out);
+/* synthetic_predict: the target's greedy rollout with each position replaced by
+ * (id + 1) % vocab unless a SplitMix64(step_seed) coin lands below accuracy;
+ * ConfigError unless 0 <= accuracy < 1; out[k]. */
+int sd_synthetic_predict(sd_model* target, const int32_t* context, int n, int k, double accuracy, uint64_t step_seed,
+                         int32_t* out);
+
 /* ---- engine (decode_speculative / decode_greedy, engine.cpp:206-489) ------ */
 /* prompts: concatenated token ids (BOS included), prompt_lens[B].
  * gen_tokens[B][max_new_tokens], gen_counts[B]; step records as rows of

@@ -10,6 +10,7 @@
 //   specdec::ModelConfig, TokenPlan, greedy_next, Model                       model.hpp:14-103
 //   specdec::CacheArena, UnpadArena, PaddedGrid                               kv_cache.hpp:68-168
 //   specdec::VerifyResult, verify                                             engine.hpp:82-90
+//   specdec::draft_predict, retrieval_predict, synthetic_predict              predictors.hpp:13-20
 //   specdec::Mode, PredictorKind, EngineConfig, SampleStep, StepRecord,
 //     RunMetrics, DecodeResult, make_step_record, compute_metrics,
 //     decode_greedy, decode_speculative, results_json                         engine.hpp:15-110
@@ -548,6 +549,29 @@ inline VerifyResult verify(const std::vector<LogitsRow>& rows, const TokenSequen
     }
     r.tau = static_cast<int>(r.accepted.size());
     return r;
+}
+
+// ------------------------------------------------------------ predictors (predictors.hpp:13-20)
+// Draft / synthetic rollouts run on the GPU through the given Model.
+inline TokenSequence draft_predict(const TokenSequence& context, int k, const Model& draft) {
+    TokenSequence out(static_cast<size_t>(std::max(k, 0)));
+    b200::check(sd_draft_predict(draft.handle(), context.data(), static_cast<int>(context.size()), k, out.data()));
+    return out;
+}
+inline TokenSequence retrieval_predict(const TokenSequence& context, int match_len, int copy_len) {
+    TokenSequence out(static_cast<size_t>(std::max(copy_len, 0)));
+    int32_t n = 0;
+    b200::check(sd_retrieval_predict(context.data(), static_cast<int>(context.size()), match_len, copy_len, out.data(),
+                                     &n));
+    out.resize(static_cast<size_t>(n));
+    return out;
+}
+inline TokenSequence synthetic_predict(const TokenSequence& context, int k, const Model& target, double accuracy,
+                                       uint64_t step_seed) {
+    TokenSequence out(static_cast<size_t>(std::max(k, 0)));
+    b200::check(sd_synthetic_predict(target.handle(), context.data(), static_cast<int>(context.size()), k, accuracy,
+                                     step_seed, out.data()));
+    return out;
 }
 
 // ------------------------------------------------------------ engine (engine.hpp:15-110)

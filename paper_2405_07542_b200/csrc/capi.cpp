@@ -1283,6 +1283,31 @@ int sd_decode(const sd_engine_config* cfg, sd_model* target, sd_model* draft, co
     });
 }
 
+int sd_draft_predict(sd_model* draft, const int32_t* context, int n, int k, int32_t* out) {
+    return guarded([&] {
+        SD_CHECK(n >= 0 && (n == 0 || context), CONTRACT, "draft prediction needs a context");
+        const std::vector<int32_t> d = draft_predict_fresh(draft, std::vector<int32_t>(context, context + n), k);
+        std::copy(d.begin(), d.end(), out);
+    });
+}
+
+int sd_retrieval_predict(const int32_t* context, int n, int match_len, int copy_len, int32_t* out, int32_t* n_out) {
+    return guarded([&] {
+        const std::vector<int32_t> d = retrieval_predict(std::vector<int32_t>(context, context + n), match_len, copy_len);
+        std::copy(d.begin(), d.end(), out);
+        *n_out = (int32_t)d.size();
+    });
+}
+
+int sd_synthetic_predict(sd_model* target, const int32_t* context, int n, int k, double accuracy, uint64_t step_seed,
+                         int32_t* out) {
+    return guarded([&] {
+        const std::vector<int32_t> d =
+            synthetic_predict_fresh(target, std::vector<int32_t>(context, context + n), k, accuracy, step_seed);
+        std::copy(d.begin(), d.end(), out);
+    });
+}
+
 int sd_verify_step(sd_model* m, sd_cache* c, const int32_t* last, const int32_t* counts, const int32_t* drafts,
                    const int32_t* budget, const int32_t* active, int stop_on_eos, int32_t* tau,
                    int32_t* accepted, int32_t* clipped, float* logits) {

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "handles.h"
@@ -79,7 +80,36 @@ struct State {
     bool finished = false;
 };
 
+// predictors.cpp:61-72: the target's own greedy rollout, each position kept
+// with probability `accuracy` (SplitMix64 coins from the step seed) and
+// otherwise replaced by the next id
+void corrupt_rollout(std::vector<int32_t>& d, double accuracy, uint64_t step_seed, int vocab) {
+    uint64_t rs = step_seed;
+    for (int32_t& t : d) {
+        const double u = (double)(splitmix_next(rs) >> 11) * 0x1.0p-53;
+        if (u >= accuracy) t = (t + 1) % vocab;
+    }
+}
+
 }  // namespace
+
+// Stand-alone predictors (predictors.hpp:13-20) for the C ABI: a fresh
+// one-sample arena per draft rollout, as the reference allocates one per call.
+std::vector<int32_t> draft_predict_fresh(sd_model* draft, const std::vector<int32_t>& ctx, int k) {
+    SD_CHECK(k >= 1, CONTRACT, "draft length must be >= 1");
+    SD_CHECK(!ctx.empty(), CONTRACT, "draft prediction needs a context");
+    SD_CHECK((int)ctx.size() + k <= draft->m.cfg.max_positions, CAPACITY,
+             "context plus draft length exceeds max_positions");
+    std::unique_ptr<sd_cache> scratch(create_cache(draft, 1, draft->m.cfg.max_positions, UNPAD));
+    return draft_predict(draft, scratch.get(), ctx, k);
+}
+std::vector<int32_t> synthetic_predict_fresh(sd_model* target, const std::vector<int32_t>& ctx, int k,
+                                             double accuracy, uint64_t step_seed) {
+    SD_CHECK(accuracy >= 0.0 && accuracy < 1.0, CONFIG, "predictor accuracy must lie in [0, 1)");
+    std::vector<int32_t> d = draft_predict_fresh(target, ctx, k);
+    corrupt_rollout(d, accuracy, step_seed, target->m.cfg.vocab_size);
+    return d;
+}
 
 struct Decoder {
     const sd_engine_config& e;
@@ -94,12 +124,8 @@ struct Decoder {
         SD_CHECK(e.synthetic_accuracy >= 0.0 && e.synthetic_accuracy < 1.0, CONFIG,
                  "predictor accuracy must lie in [0, 1)");
         std::vector<int32_t> d = draft_predict(target, target_scratch, st.tokens, e.k);  // predictors.cpp:61-72
-        uint64_t rs = mix_seed(e.seed, (uint64_t)step, (uint64_t)(e.sample_id_base + s));
-        int V = target->m.cfg.vocab_size;
-        for (int32_t& t : d) {
-            double u = (double)(splitmix_next(rs) >> 11) * 0x1.0p-53;
-            if (u >= e.synthetic_accuracy) t = (t + 1) % V;
-        }
+        corrupt_rollout(d, e.synthetic_accuracy, mix_seed(e.seed, (uint64_t)step, (uint64_t)(e.sample_id_base + s)),
+                        target->m.cfg.vocab_size);
         return d;
     }
     ~Decoder() {

@@ -88,6 +88,9 @@ int decode_impl(const sd_engine_config& e, sd_model* target, sd_model* draft, co
                 int64_t rec_cap, int64_t* n_rec, int64_t* ledger, double* timing);
 void reset_cache(sd_cache* c);  // back to an empty arena (fresh-cache semantics)
 std::vector<int32_t> retrieval_predict(const std::vector<int32_t>& ctx, int match_len, int copy_len);
+std::vector<int32_t> draft_predict_fresh(sd_model* draft, const std::vector<int32_t>& ctx, int k);
+std::vector<int32_t> synthetic_predict_fresh(sd_model* target, const std::vector<int32_t>& ctx, int k, double accuracy,
+                                             uint64_t step_seed);
 
 sd_model* create_model(const Config& cfg, int device, int precision, const float* host_weights);
 sd_cache* create_cache(sd_model* m, int batch, int capacity, int layout);

@@ -1,5 +1,5 @@
 """The reference's own hot-path unit suites (proj/tests/test_ragged.cpp,
-test_kv_cache.cpp, test_model.cpp, test_engine.cpp + support/naive_model.cpp), recompiled
+test_kv_cache.cpp, test_model.cpp, test_engine.cpp, test_predictors.cpp + support/naive_model.cpp), recompiled
 unmodified against our C++ layer include/specdec_b200.hpp with a
 doctest-compatible harness (tests/native/Makefile, binaries in
 tests/native/_reftests/, built by __graft_entry__.build() where the reference
@@ -48,9 +48,16 @@ def test_engine_host_cases_pass_without_gpu(sd):
         assert cases.get(name), name
 
 
+def test_predictor_lookup_cases_pass_without_gpu(sd):
+    _, cases = run_suite("test_predictors")
+    lookup = [n for n in cases if n.startswith("prompt lookup")]
+    assert len(lookup) == 5, cases
+    assert all(cases[n] for n in lookup), cases
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("suite,n_cases", [("test_ragged", 7), ("test_kv_cache", 18), ("test_model", 15),
-                                           ("test_engine", 13)])
+                                           ("test_engine", 13), ("test_predictors", 12)])
 def test_reference_suite_passes_on_b200(sd, suite, n_cases):
     r, cases = run_suite(suite)
     assert len(cases) == n_cases, r.stdout
