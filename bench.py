@@ -174,13 +174,10 @@ def trace_launches(rec):
     return out
 
 
-def in_graph_attention(session, hbm, cap=4_000_000):
-    """Attention roofline inside the replayed CUDA graph (PDL chain intact):
-    %globaltimer records of every CTA (sd_debug_trace_*) give each launch's
-    span; its exposed time is from the moment its last predecessor finished
-    (the QKV reduction) to its last CTA's exit, and its algorithmic K/V bytes
-    are the sum of the per-CTA TK_ATTN_BYTES trace points.  Only the first
-    ~80% of the trace window is used (the ring may cut the tail)."""
+def in_graph_trace(session, cap=4_000_000):
+    """One EMS generation replayed from its CUDA graph (PDL chain intact) with
+    per-CTA %globaltimer records (sd_debug_trace_*): (records, launches, the
+    first ~80% of the trace window -- the ring may cut the tail)."""
     import ctypes as C
     from paper_2405_07542_b200 import specdec as sd
     L = sd.lib()
@@ -198,7 +195,15 @@ def in_graph_attention(session, hbm, cap=4_000_000):
     ls = trace_launches(rec)
     if not ls:
         return None
-    t_lo, t_hi = ls[0][1], ls[0][1] + 0.8 * (max(l[2] for l in ls) - ls[0][1])
+    return rec, ls, (ls[0][1], ls[0][1] + 0.8 * (max(l[2] for l in ls) - ls[0][1]))
+
+
+def in_graph_attention(tr, hbm):
+    """Attention roofline inside the replayed graph: each launch's exposed time
+    is from the moment its last predecessor finished (the QKV reduction) to its
+    last CTA's exit; its algorithmic K/V bytes are the sum of the per-CTA
+    TK_ATTN_BYTES trace points."""
+    rec, ls, (t_lo, t_hi) = tr
     pts = rec[rec["kid"] == 110]
     ready, tot_ns, tot_b, nl = 0, 0, 0, 0
     for kid, t0, t1, ctas, sms in ls:
@@ -215,6 +220,50 @@ def in_graph_attention(session, hbm, cap=4_000_000):
             "us_per_launch": round(tot_ns / nl / 1e3, 2), "mb_per_launch": round(tot_b / nl / 1e6, 2),
             "method": "graph replay with per-CTA %globaltimer records; exposed time = last CTA exit - "
                       "max(first CTA entry, predecessor exit); bytes = per-CTA algorithmic K/V bytes"}
+
+
+def in_graph_gemm_stage(tr, hbm, h, vocab):
+    """The dominant kernel's stage inside the replayed graph: every k_gemm
+    launch together with the split-K reduction / epilogue / LayerNorm launches
+    that follow it, timed from the end of the stage's predecessor (attention or
+    the previous stage) to the exit of its last CTA; bytes = the GEMM's weights
+    (>= 97% of its algorithmic bytes at T <= 192; the token operand and outputs
+    are left out, so the figure is conservative)."""
+    _, ls, (t_lo, t_hi) = tr
+    red = {2, 3, 4, 5, 6, 7}  # reductions (store / GELU / QKV / residual), LayerNorm rows, argmax
+    m = 4 * h
+    weights = {"qkv": 3 * h * h * 2, "o": h * h * 2, "fc": m * h * 2, "proj": h * m * 2, "lm": vocab * h * 2}
+    acc = {k: [0, 0, 0] for k in weights}  # ns, bytes, stages
+    prev_end, prev_kid, i = 0, None, 0
+    while i < len(ls):
+        kid, t0, t1 = ls[i][:3]
+        if kid != 1:
+            prev_end, prev_kid, i = max(prev_end, t1), kid, i + 1
+            continue
+        j, end, kinds = i + 1, t1, []
+        while j < len(ls) and ls[j][0] in red:
+            end = max(end, ls[j][2])
+            kinds.append(ls[j][0])
+            j += 1
+        cls = ("qkv" if 4 in kinds else "fc" if 3 in kinds else "lm" if 7 in kinds
+               else "o" if prev_kid == 9 else "proj" if 5 in kinds else None)
+        if cls and t0 > t_lo and end < t_hi:
+            a = acc[cls]
+            a[0] += end - max(t0, prev_end)
+            a[1] += weights[cls]
+            a[2] += 1
+        prev_end, prev_kid, i = max(prev_end, end), kinds[-1] if kinds else 1, j
+    ns = sum(v[0] for v in acc.values())
+    b = sum(v[1] for v in acc.values())
+    if not ns:
+        return None
+    gbs = b / ns
+    return {"achieved": round(gbs, 1), "frac": round(gbs / hbm, 4), "stages": sum(v[2] for v in acc.values()),
+            "per_gemm": {k: {"us_per_stage": round(v[0] / v[2] / 1e3, 2), "gbs": round(v[1] / v[0], 1),
+                             "frac": round(v[1] / v[0] / hbm, 4)} for k, v in acc.items() if v[2]},
+            "method": "graph replay with per-CTA %globaltimer records; stage = k_gemm + its reduction / LayerNorm "
+                      "launches, exposed time = last CTA exit - max(k_gemm entry, predecessor exit); "
+                      "bytes = weights only"}
 
 
 def step_stats(log_k, log_tau):
@@ -779,7 +828,9 @@ def main():
             roof["traffic_over_algorithmic"] = round(nc["traffic_mb_per_launch"] * 1e6 / (sum(alg) / len(alg)), 3)
             roof["ncu_step"] = {"T": mt["T"], "launches": nc["launches"]}
     try:
-        roof["attention_in_graph"] = in_graph_attention(ems, hbm)
+        tr = in_graph_trace(ems)
+        roof["attention_in_graph"] = in_graph_attention(tr, hbm) if tr else None
+        roof["gemm_stage_in_graph"] = in_graph_gemm_stage(tr, hbm, h, V) if tr else None
     except Exception as exc:  # diagnostics only
         roof["attention_in_graph"] = {"error": str(exc)[:200]}
     roof["all_gemms_gbs"] = round(stage_gbs, 1)

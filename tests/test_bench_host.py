@@ -106,3 +106,22 @@ def test_reference_bench_checks_follow_specdec_main():
     assert not chk["aligned_output_matches_greedy"] and not chk["aligned_and_unpad_step_records_agree"]
     assert not chk["useful_writes_agree_across_layouts"]
     assert chk["unpad_output_matches_greedy"] and chk["unpad_wrote_zero_padding_slots"]
+
+
+def test_in_graph_gemm_stage_classifies_and_times_each_stage():
+    # one layer in program order: QKV stage, attention, O stage (+ LN), FC, PROJ (+ LN), then the LM head
+    ls = [(1, 0, 100, 148, 148), (4, 90, 110, 1, 1),                     # QKV: 0 -> 110
+          (9, 105, 170, 148, 148),                                        # attention ends at 170
+          (1, 150, 240, 148, 148), (5, 235, 250, 1, 1), (6, 248, 260, 1, 1),  # O: 170 -> 260
+          (1, 255, 400, 148, 148), (3, 395, 410, 1, 1),                   # FC: 260 -> 410
+          (1, 405, 600, 148, 148), (5, 590, 615, 1, 1), (6, 612, 620, 1, 1),  # PROJ: 410 -> 620
+          (1, 615, 700, 148, 148), (7, 690, 705, 1, 1),                   # LM head: 620 -> 705
+          (12, 2000, 2001, 1, 1)]                                         # keeps the window open
+    h, V = 64, 256
+    r = bench.in_graph_gemm_stage((None, ls, (-1, 10_000)), hbm=1.0, h=h, vocab=V)
+    pg = r["per_gemm"]
+    assert set(pg) == {"qkv", "o", "fc", "proj", "lm"} and r["stages"] == 5
+    assert pg["qkv"]["us_per_stage"] == 0.11 and pg["o"]["us_per_stage"] == 0.09
+    assert pg["fc"]["us_per_stage"] == 0.15 and pg["proj"]["us_per_stage"] == 0.21
+    assert pg["lm"]["us_per_stage"] == round(85 / 1e3, 2)
+    assert pg["o"]["gbs"] == round(h * h * 2 / 90, 1)
