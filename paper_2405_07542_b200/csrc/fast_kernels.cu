@@ -332,6 +332,11 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
             // item's chunks below its new tokens stream during the QKV reduction.
             // (A smaller GEMM grid, e.g. a draft model's, leaves SMs free and this
             // CTA could run next to an unfinished k_pack: no early reads then.)
+            // In layers >= 1 the host sets a.pre_ok regardless: layer 0's
+            // attention either waited before its pdl_trigger() (a.pre_ok == 0) or
+            // ran only after an exited QKV CTA, so every later kernel of the
+            // forward -- launched downstream of that trigger -- starts after
+            // k_pack and the embedding completed.
             int pre_item = -1, pre_chunks = 0;
             // rows: keys left in the extent; <= 32 / <= 64 -> the 32- / 64-row boxes (no
             // over-read of a whole 128-key chunk past the extent; the rest of the stage
@@ -1170,7 +1175,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         PROF(PK_QKV, cl_launch(EPI_QKV, g, mp, n, st));
         at.layer = l;
         at.work = f->attn_work + l;
-        at.pre_ok = 0;
+        at.pre_ok = l > 0 ? 1 : 0;  // layer 0's attention anchors the step (see the producer)
         PROF(PK_ATTN, launch_attention(at, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, hd, qtiles, db.max_kv_upper,
                                        st));
         if (db.max_wide_q > 0) {  // prompt runs of >= kWideMin queries: the 128-query prefill kernel
@@ -1242,7 +1247,7 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
         // attention
         at.layer = l;
         at.work = f->attn_work + l;
-        at.pre_ok = g.grid == sms ? 1 : 0;  // the QKV GEMM above held every SM
+        at.pre_ok = (g.grid == sms || l > 0) ? 1 : 0;  // the QKV GEMM above held every SM, or layer >= 1
         PROF(PK_ATTN, launch_attention(at, f->kv_map, f->kv_map64, f->kv_map32, f->q_map, hd, qtiles, db.max_kv_upper,
                                        st));
         if (db.max_wide_q > 0) {  // prompt runs of >= kWideMin queries: the 128-query prefill kernel
