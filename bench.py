@@ -837,6 +837,11 @@ def main():
     roof["whole_step_gbs"] = round(step_b / (total_ms / 1000) / 1e9, 1) if total_ms else None
     # the generation's algorithmic bytes over the GRAPH-timed generation (the value's clock)
     roof["generation_hbm_roof_frac"] = round(step_b / (r_ems["ms"] / a.steps / 1000.0) / (hbm * 1e9), 4)
+    # the same fractions on north_star's nominal ~8 TB/s basis
+    gs = roof.get("gemm_stage_in_graph") or {}
+    roof["nominal_8tbs"] = {"generation_frac": round(step_b / (r_ems["ms"] / a.steps / 1000.0) / 8.0e12, 4),
+                            "gemm_stage_in_graph_frac": round(gs["achieved"] / 8000.0, 4) if "achieved" in gs else None,
+                            "peak_gbs": 8000.0}
 
     # the whole "batch 8-24" range: EMS and padded per batch, same generations
     per_batch = {B: {"ems": r_ems, "padded": r_pad, "roof": roof["generation_hbm_roof_frac"],
