@@ -839,6 +839,9 @@ def main():
     roof["generation_hbm_roof_frac"] = round(step_b / (r_ems["ms"] / a.steps / 1000.0) / (hbm * 1e9), 4)
     # the same fractions on north_star's nominal ~8 TB/s basis
     gs = roof.get("gemm_stage_in_graph") or {}
+    # next to the eager CUDA-event `frac`: the same k_gemm stage inside the
+    # replayed graph with its PDL overlap (per-CTA %globaltimer, weights-only bytes)
+    roof["frac_in_graph"] = gs.get("frac")
     roof["nominal_8tbs"] = {"generation_frac": round(step_b / (r_ems["ms"] / a.steps / 1000.0) / 8.0e12, 4),
                             "gemm_stage_in_graph_frac": round(gs["achieved"] / 8000.0, 4) if "achieved" in gs else None,
                             "peak_gbs": 8000.0}
