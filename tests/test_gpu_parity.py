@@ -210,6 +210,20 @@ def test_c3_layer_truncated_forward_vs_float64(sd):
     assert st["token_agree"] >= 0.75  # greedy streams, position-wise
 
 
+def test_c5_layer_truncated_forward_vs_float64(sd):
+    """(c') The C5 width (OPT-6.7B shape: h = 4096, 32 heads of 128) truncated
+    to L = 2, with ~4k-token prompts: prefill through the 128-query kernel in
+    256-token chunks, then one ragged verify forward over ~4.1k keys per
+    sample, against the float64 reference; plus greedy decoding."""
+    cfg = dict(num_layers=2, num_heads=32, head_dim=128, vocab_size=50272, max_positions=4480, init_seed=0xD5EED)
+    st = c3_truncated_parity(sd, cfg=cfg, B=2, seed=3, greedy_tokens=6, lo=3968, hi=4224, cap=4352)
+    print("C5 L=2 bf16 vs float64:", st)
+    assert st["max_abs_over_std"] <= 0.15
+    assert st["mean_abs_over_std"] <= 0.03
+    assert st["argmax_agree"] >= 0.9
+    assert st["token_agree"] >= 0.75
+
+
 # ------------------------------------------------------------------ (d)
 def test_long_prompt_prefill_vs_float64(sd):
     """(d) Prefill of 600-700-token prompts (forward chunks of <= 256 tokens cut

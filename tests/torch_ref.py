@@ -120,7 +120,7 @@ def parity_stats(ours: np.ndarray, ref: np.ndarray) -> dict:
 C3_L2 = dict(num_layers=2, num_heads=40, head_dim=128, vocab_size=50272, max_positions=2048, init_seed=0xD5EED)
 
 
-def c3_truncated_parity(sd, cfg=C3_L2, B=4, seed=1, greedy_tokens=0) -> dict:
+def c3_truncated_parity(sd, cfg=C3_L2, B=4, seed=1, greedy_tokens=0, lo=600, hi=660, cap=1024) -> dict:
     """bf16 verify-step logits of a layer-truncated C3 model (the library's
     public API: prefill + one ragged verify forward) against this float64
     reference on the fp32 weights of the same seed (an FP32_CHECK model of the
@@ -131,13 +131,13 @@ def c3_truncated_parity(sd, cfg=C3_L2, B=4, seed=1, greedy_tokens=0) -> dict:
 
     rng = np.random.default_rng(seed)
     V = cfg["vocab_size"]
-    prompts = [[0] + rng.integers(3, V, size=int(rng.integers(600, 660))).tolist() for _ in range(B)]
+    prompts = [[0] + rng.integers(3, V, size=int(rng.integers(lo, hi))).tolist() for _ in range(B)]
     drafts = [rng.integers(3, V, size=1 + (3 * s) % 8).tolist() for s in range(B)]
     m32 = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.FP32_CHECK)
     ref = TorchRef(cfg, m32.tensors(), device="cuda", dtype=torch.float64)
     m32.close()
     m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.BF16)
-    c = sd.UnpadArena(m, B, 1024)
+    c = sd.UnpadArena(m, B, cap)
     slots = [sd.TokenSlot(s, i) for s in range(B) for i in range(len(prompts[s]))]
     _, am = m.forward(sd.concatenate_inputs(prompts), c, slots, want_logits=False)
     for s in range(B):
@@ -151,7 +151,8 @@ def c3_truncated_parity(sd, cfg=C3_L2, B=4, seed=1, greedy_tokens=0) -> dict:
             for s in range(B)]
     c.close()
     out = parity_stats(lg, np.concatenate(rows))
-    out["config"] = "C3 shape truncated to L=%d, B=%d, ~600-token contexts, drafts 1-8" % (cfg["num_layers"], B)
+    out["config"] = "h=%d shape truncated to L=%d, B=%d, %d-%d-token contexts, drafts 1-8" % (
+        cfg["num_heads"] * cfg["head_dim"], cfg["num_layers"], B, lo, hi)
     if greedy_tokens:
         g = sd.decode(sd.EngineConfig(mode="greedy", batch_size=B, max_new_tokens=greedy_tokens, stop_on_eos=False),
                       m, prompts).generated_tokens
