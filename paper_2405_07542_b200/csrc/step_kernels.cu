@@ -11,6 +11,8 @@
 //   k_pad_fill   the vanilla layout's zero filler rows (kv_cache.cpp:295-307)
 #include <cuda_bf16.h>
 
+#include <climits>
+
 #include "common.h"
 #include "pdl.cuh"
 #include "step.h"
@@ -27,48 +29,114 @@ __device__ __forceinline__ int32_t draft_at(const StepArgs& a, int s, int doff, 
     return a.draft_stride ? a.drafts[(size_t)s * a.draft_stride + j] : a.drafts[doff + j];
 }
 
-// One block.  Thread 0 runs the O(B) prefix sums (B <= a few hundred), then
-// every thread fills token/plan rows in parallel.
-__global__ void k_pack(StepArgs a) {
+// Block-wide reductions / exclusive scan over one value per thread (256
+// threads): warp shuffles, then the 8 warp results through shared memory.
+constexpr int kStepThreads = 256;
+__device__ __forceinline__ int block_reduce_max(int v, int* sw) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = __reduce_max_sync(0xffffffffu, v);
+    if (lane == 0) sw[warp] = v;
+    __syncthreads();
+    int r = sw[0];
+#pragma unroll
+    for (int w = 1; w < kStepThreads / 32; ++w) r = max(r, sw[w]);
+    __syncthreads();
+    return r;
+}
+__device__ __forceinline__ int block_reduce_min(int v, int* sw) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = __reduce_min_sync(0xffffffffu, v);
+    if (lane == 0) sw[warp] = v;
+    __syncthreads();
+    int r = sw[0];
+#pragma unroll
+    for (int w = 1; w < kStepThreads / 32; ++w) r = min(r, sw[w]);
+    __syncthreads();
+    return r;
+}
+// exclusive prefix sums of two values at once; `tot` receives the block totals
+__device__ __forceinline__ int2 block_excl_scan2(int2 v, int2* sw, int2& tot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int2 x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int yx = __shfl_up_sync(0xffffffffu, x.x, o), yy = __shfl_up_sync(0xffffffffu, x.y, o);
+        if (lane >= o) {
+            x.x += yx;
+            x.y += yy;
+        }
+    }
+    if (lane == 31) sw[warp] = x;
+    __syncthreads();
+    int2 off = make_int2(0, 0);
+    tot = make_int2(0, 0);
+#pragma unroll
+    for (int w = 0; w < kStepThreads / 32; ++w) {
+        if (w < warp) {
+            off.x += sw[w].x;
+            off.y += sw[w].y;
+        }
+        tot.x += sw[w].x;
+        tot.y += sw[w].y;
+    }
+    __syncthreads();
+    return make_int2(off.x + x.x - v.x, off.y + x.y - v.y);
+}
+
+// One block of 256 threads.  The prefix sums of Algorithm 1 (ragged.cpp:6-17)
+// run as block scans over the samples (no serial per-sample loop), then every
+// thread fills the token / plan rows of its samples.
+__global__ void __launch_bounds__(kStepThreads) k_pack(StepArgs a) {
     CtaTrace trace__(TK_PACK);
     pdl_trigger();
     pdl_wait();
+    __shared__ int s_red[kStepThreads / 32];
+    __shared__ int2 s_scan[kStepThreads / 32];
     const int B = a.B;
     // padded input rows (1 + k_max per sample)?  The layout's own choice unless
     // an ablation mode decouples input padding from KV padding.
     const bool pad_in = a.layout == PADDED ? a.ablation != 1 : a.ablation == 2;
-    if (threadIdx.x == 0) {
-        int t = 0, d = 0, kmax = 0;
-        for (int s = 0; s < B; ++s)
-            if (a.active[s] && a.counts[s] > kmax) kmax = a.counts[s];
-        int base = -1;
-        for (int s = 0; s < B; ++s) {
-            a.draft_off[s] = d;
-            d += a.active[s] ? a.counts[s] : 0;
-            a.first_row[s] = t;
-            if (!a.active[s]) continue;
-            if (a.layout == PADDED && base < 0) base = a.committed[s];
-            t += 1 + (pad_in ? kmax : a.counts[s]);
+    int km = 0, first = INT_MAX;
+    for (int s = threadIdx.x; s < B; s += kStepThreads)
+        if (a.active[s]) {
+            km = max(km, a.counts[s]);
+            first = min(first, s);
+        }
+    const int kmax = block_reduce_max(km, s_red);
+    first = block_reduce_min(first, s_red);
+    const int base = a.layout == PADDED && first < B ? a.committed[first] : -1;
+    // draft_off / first_row: exclusive prefix sums over the active samples
+    int2 carry = make_int2(0, 0);  // (drafts, rows) before this chunk of samples
+    bool over = false;
+    for (int c0 = 0; c0 < B; c0 += kStepThreads) {
+        const int s = c0 + threadIdx.x;
+        const bool act = s < B && a.active[s];
+        const int ks = act ? a.counts[s] : 0;
+        int2 tot;
+        const int2 ex = block_excl_scan2(make_int2(ks, act ? 1 + (pad_in ? kmax : ks) : 0), s_scan, tot);
+        if (s < B) {
+            a.draft_off[s] = carry.x + ex.x;
+            a.first_row[s] = carry.y + ex.y;
         }
         // Capacity guard for the device-resident loop (the host-driven step
         // checks on the host first): never write past a sample's extent.
-        bool over = false;
-        for (int s = 0; s < B; ++s) {
-            if (!a.active[s]) continue;
-            int last = a.layout == PADDED ? base + kmax : a.committed[s] + (pad_in ? kmax : a.counts[s]);
+        if (act) {
+            const int last = a.layout == PADDED ? base + kmax : a.committed[s] + (pad_in ? kmax : ks);
             if (last >= a.cap) over = true;
         }
-        if (over) {
-            a.scalars[4] = 2;  // CapacityError, reported by the host
-            for (int s = 0; s < B; ++s) a.active[s] = 0;
-            t = 0;
-        }
-        a.scalars[0] = t;     // T
-        a.scalars[1] = kmax;  // k_max
-        a.scalars[2] = base;  // padded grid base row
+        carry.x += tot.x;
+        carry.y += tot.y;
     }
-    __syncthreads();
-    const int kmax = a.scalars[1], base = a.scalars[2];
+    over = __syncthreads_or(over);
+    if (over)
+        for (int s = threadIdx.x; s < B; s += kStepThreads) a.active[s] = 0;
+    if (threadIdx.x == 0) {
+        if (over) a.scalars[4] = 2;       // CapacityError, reported by the host
+        a.scalars[0] = over ? 0 : carry.y;  // T
+        a.scalars[1] = kmax;              // k_max
+        a.scalars[2] = base;              // padded grid base row
+    }
+    __syncthreads();  // active flags cleared on overflow
     for (int s = threadIdx.x; s < B; s += blockDim.x) {
         const int row0 = a.first_row[s];
         if (!a.active[s]) {
@@ -130,23 +198,44 @@ __global__ void k_accept(StepArgs a) {
         }
         int ks = a.counts[s], row0 = a.first_row[s], d0 = a.draft_off[s];
         int vt = ks + 1;
-        for (int j = 0; j <= ks; ++j) {
+        // picks and drafts of up to kAccBatch positions loaded before the
+        // first comparison (one round trip instead of one per position); the
+        // verification itself is the reference's first-mismatch scan
+        constexpr int kAccBatch = 16;
+        int pick[kAccBatch], drf[kAccBatch];
+#pragma unroll
+        for (int j = 0; j < kAccBatch; ++j) {
+            pick[j] = j <= ks ? a.argmax[row0 + j] : 0;
+            drf[j] = j < ks ? draft_at(a, s, d0, j) : -1;
+        }
+        bool hit = false;
+#pragma unroll
+        for (int j = 0; j < kAccBatch; ++j) {
+            if (hit || j > ks) break;
+            a.accepted[s * W + j] = pick[j];
+            if (j < ks && pick[j] != drf[j]) {
+                vt = j + 1;
+                hit = true;
+            }
+        }
+        for (int j = kAccBatch; !hit && j <= ks; ++j) {  // k > 15 only
             int x = a.argmax[row0 + j];
             a.accepted[s * W + j] = x;
             if (j < ks && x != draft_at(a, s, d0, j)) {
                 vt = j + 1;
-                break;
+                hit = true;
             }
         }
         int budget = a.budget ? a.budget[s] : a.max_new - a.gen[s];
         int tau = vt < budget ? vt : budget;
-        if (a.stop_on_eos) {
-            for (int j = 0; j < tau; ++j) {
-                if (a.accepted[s * W + j] == 1 /* tok::kEos */) {
-                    tau = j + 1;
-                    break;
-                }
-            }
+        if (a.stop_on_eos) {  // first EOS among the accepted tokens ends the sample
+            int eos = -1;
+#pragma unroll
+            for (int j = 0; j < kAccBatch; ++j)
+                if (eos < 0 && j < tau && pick[j] == 1 /* tok::kEos */) eos = j;
+            for (int j = kAccBatch; eos < 0 && j < tau; ++j)
+                if (a.accepted[s * W + j] == 1) eos = j;
+            if (eos >= 0) tau = eos + 1;
         }
         a.tau[s] = tau;
         a.clipped[s] = tau < vt ? 1 : 0;
@@ -154,11 +243,22 @@ __global__ void k_accept(StepArgs a) {
         if (a.layout == UNPAD) a.committed[s] += tau;  // kv_cache.cpp:158
         if (a.ctx) {  // device-resident loop: append, advance, finish (engine.cpp:465-470)
             int len = a.ctx_len[s];
-            for (int j = 0; j < tau; ++j) a.ctx[(size_t)s * a.ctx_cap + len + j] = a.accepted[s * W + j];
+            int last_tok = 0;
+            int32_t* cp = a.ctx + (size_t)s * a.ctx_cap + len;
+#pragma unroll
+            for (int j = 0; j < kAccBatch; ++j)
+                if (j < tau) {
+                    cp[j] = pick[j];
+                    last_tok = pick[j];
+                }
+            for (int j = kAccBatch; j < tau; ++j) {
+                last_tok = a.accepted[s * W + j];
+                cp[j] = last_tok;
+            }
             a.ctx_len[s] = len + tau;
             int g = a.gen[s] + tau;
             a.gen[s] = g;
-            bool done = g >= a.max_new || (a.stop_on_eos && a.accepted[s * W + tau - 1] == 1);
+            bool done = g >= a.max_new || (a.stop_on_eos && last_tok == 1);
             if (done) a.active[s] = 0;
             else atomicAdd(&s_active, 1);
         }
@@ -365,7 +465,7 @@ void launch_draft_take(const DraftArgs& d, int j, cudaStream_t st) {
 }
 void launch_draft_commit(const DraftArgs& d, cudaStream_t st) { launch_k(k_draft_commit, dim3(1), dim3(256), 0, st, d); }
 
-void launch_pack(const StepArgs& a, cudaStream_t st) { launch_k(k_pack, dim3(1), dim3(256), 0, st, a); }
+void launch_pack(const StepArgs& a, cudaStream_t st) { launch_k(k_pack, dim3(1), dim3(kStepThreads), 0, st, a); }
 void launch_accept(const StepArgs& a, cudaStream_t st) { launch_k(k_accept, dim3(1), dim3(256), 0, st, a); }
 void launch_pad_fill(const StepArgs& a, const Cache& c, cudaStream_t st) {
     dim3 grid(c.L * 2, c.B);
