@@ -49,7 +49,7 @@ struct FastWorkspace {
     CUtensorMap kv_map32;      // ... with box {64, 32}
     CUtensorMap q_map;         // TMA view of the queries [256][h], one-row boxes {64, 1}
     CUtensorMap q_map128;      // ... with 128-row boxes (prefill kernel)
-    int* attn_work = nullptr;  // persistent attention item counters [2][num_layers], zeroed per forward
+    int* attn_work = nullptr;  // persistent attention item counters [2][num_layers], zeroed by each forward's k_embed_ln
     std::vector<void*> allocs;
 };
 
@@ -145,10 +145,17 @@ __global__ void __launch_bounds__(kRowThreads) k_embed_ln(const __nv_bfloat16* _
                                                           const Plan* __restrict__ plans, int h,
                                                           float* __restrict__ resid, const float* __restrict__ g,
                                                           const float* __restrict__ b, __nv_bfloat16* __restrict__ y,
-                                                          const int* __restrict__ dT, float2* __restrict__ stats) {
+                                                          const int* __restrict__ dT, float2* __restrict__ stats,
+                                                          int* __restrict__ zero_work, int n_zero) {
     CtaTrace trace__(TK_EMBED_LN);
     pdl_trigger();
     pdl_wait();
+    // this forward's attention item counters: every attention launch is
+    // downstream of this kernel's completion when it first touches its counter
+    // (layer 0 takes its first item after griddepcontrol.wait unless a.pre_ok;
+    // see the attention producer), so no memset node has to break the PDL chain
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < n_zero; i += kRowThreads) zero_work[i] = 0;
     __shared__ float scratch[32];
     int t = blockIdx.x;
     if (t >= *dT) return;
@@ -277,11 +284,16 @@ __global__ void __launch_bounds__(kPThreads, HD == 64 ? 2 : 1)
     // the producer); otherwise every warp waits first.
     __shared__ int s_order[256];
     const bool lpt = a.B <= 256;
-    // the producer's first work item: the counter is zeroed before the forward
-    // (not by a predecessor kernel), so its round trip overlaps the dependency wait
+    // the producer's first work item.  The counter is zeroed by the forward's
+    // k_embed_ln: under a.pre_ok every kernel up to it has completed (see the
+    // producer), so the round trip overlaps the dependency wait; otherwise the
+    // item is taken after the wait.
     int first_item = 0;
-    if (tid == 128) first_item = atomicAdd(a.work, 1);
-    if (!a.pre_ok) pdl_wait();
+    if (tid == 128 && a.pre_ok) first_item = atomicAdd(a.work, 1);
+    if (!a.pre_ok) {
+        pdl_wait();
+        if (tid == 128) first_item = atomicAdd(a.work, 1);
+    }
     if (lpt)
         for (int x = tid; x < a.B; x += kPThreads) {
             const int lx = a.segs[x].kv_len;
@@ -1115,11 +1127,10 @@ void forward_fast_dev(const Model& m, Cache& c, Workspace& ws, const DeviceBatch
     base.plans = dplans;
     base.kv = (__nv_bfloat16*)c.kv;
 
-    CUDA_OK(cudaMemsetAsync(f->attn_work, 0, sizeof(int) * 2 * (size_t)cfg.num_layers, st));
     PROF(PK_ROW, launch_k(k_embed_ln, dim3(n), dim3(kRowThreads), 0, st, (const __nv_bfloat16*)m.tok16,
                           (const __nv_bfloat16*)m.pos16, tokens, dplans, h, resid, (const float*)m.layers[0].ln1_g,
                           (const float*)m.layers[0].ln1_b, f->xb, (const int*)db.dT,
-                          m.fast->compact ? f->stats : nullptr));
+                          m.fast->compact ? f->stats : nullptr, f->attn_work, 2 * (int)cfg.num_layers));
     launches++;
     AttnArgs at{};
     at.q = f->q;
