@@ -260,3 +260,42 @@ def test_nccl_gather_of_session_outputs(sd):
     comm.close()
     s.close()
     m.close()
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_verify_step_with_more_samples_than_one_pack_block(sd, precision):
+    """k_pack's block scans walk the samples in chunks of 256 threads: a
+    300-sample verify step (some samples inactive, draft counts 0-7) gives
+    exactly the taus, accepted tokens and committed lengths of the same samples
+    verified in three batches of 100 (a sample's result does not depend on the
+    batch; test_engine.cpp:307-320)."""
+    cfg = dict(num_layers=2, num_heads=2, head_dim=64, vocab_size=300, max_positions=128, init_seed=0x51)
+    m = sd.Model.init(sd.ModelConfig(**cfg), precision=sd.FP32_CHECK if precision == "fp32" else sd.BF16)
+    rng = np.random.default_rng(11)
+    B = 300
+    prompts = [[0] + rng.integers(3, 300, size=int(rng.integers(3, 12))).tolist() for _ in range(B)]
+    active = [int(s % 7 != 3) for s in range(B)]
+    counts = [int(k) * a for k, a in zip(rng.integers(0, 8, size=B), active)]  # finished samples bring no drafts
+    drafts = [rng.integers(3, 300, size=k).tolist() for k in counts]
+
+    def run(ids):
+        c = sd.UnpadArena(m, len(ids), 64)
+        ps = [prompts[s] for s in ids]
+        _, am = m.forward(sd.concatenate_inputs(ps), c,
+                          [sd.TokenSlot(i, j) for i, p in enumerate(ps) for j in range(len(p))], want_logits=False)
+        for i, p in enumerate(ps):
+            c.commit_accepted(i, len(p))
+        ends = np.cumsum([len(p) for p in ps]) - 1
+        last = [int(am[e]) for e in ends]
+        tau, acc, clip, _ = c.verify_step(last, [counts[s] for s in ids], [t for s in ids for t in drafts[s]],
+                                          [20] * len(ids), [active[s] for s in ids], False)
+        out = [(int(tau[i]), acc[i][: tau[i]].tolist(), c.committed_len(i)) for i in range(len(ids))]
+        c.close()
+        return out
+
+    whole = run(list(range(B)))
+    parts = run(list(range(0, 100))) + run(list(range(100, 200))) + run(list(range(200, 300)))
+    assert whole == parts
+    assert all(t == 0 for (t, _, _), a in zip(whole, active) if not a)
+    assert any(t > 1 for t, _, _ in whole) or precision == "bf16"
+    m.close()
